@@ -1,0 +1,52 @@
+"""Shared helpers for the tests: golden-fixture parsing and small seeded cases."""
+import os
+
+import numpy as np
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def load_fig2c():
+    """Parse tests/golden/fig2c_mask.txt -> (n_s, n_r, n_c, ts int64 [L], mask uint8 [L][L])."""
+    ts = None
+    rows = []
+    n_s = n_r = n_c = None
+    with open(os.path.join(GOLDEN, "fig2c_mask.txt")) as f:
+        for line in f:
+            s = line.strip()
+            if s.startswith("# layout:"):
+                kv = dict(t.split("=") for t in s[len("# layout:"):].split())
+                n_s, n_r, n_c = int(kv["n_static"]), int(kv["n_rt"]), int(kv["n_cand"])
+            elif s.startswith("# ts:"):
+                ts = np.array([int(t) for t in s[len("# ts:"):].split()], dtype=np.int64)
+            elif s and not s.startswith("#"):
+                rows.append([1 if t == "1" else 0 for t in s.split()[1:]])
+    return n_s, n_r, n_c, ts, np.array(rows, dtype=np.uint8)
+
+
+def tiny_user(rng, n_s, n_r, n_c, d, G=4, ts_span=50):
+    """Random tiny user: x [L][d], gid [L], ts [L] (ties likely among rt/candidates)."""
+    L = n_s + n_r + n_c
+    x = rng.standard_normal((L, d))
+    gid = np.array([0] * (n_s // 2) + [1] * (n_s - n_s // 2) + [2] * n_r + [3] * n_c)
+    gid = np.minimum(gid, G - 1)
+    ts = np.concatenate([np.zeros(n_s, np.int64),
+                         np.sort(rng.integers(0, ts_span, n_r))[::-1],
+                         np.sort(rng.integers(0, ts_span, n_c))[::-1]]).astype(np.int64)
+    return x, gid, ts
+
+
+def tiny_params(rng, d, H, G=4, rab_buckets=0, scale=1.0):
+    p = {
+        "W1": rng.standard_normal((4 * d, d)) * scale / np.sqrt(d),
+        "b1": rng.standard_normal(4 * d) * 0.1,
+        "W2": rng.standard_normal((d, d)) * scale / np.sqrt(d),
+        "b2": rng.standard_normal(d) * 0.1,
+        "gamma1": 1 + 0.2 * rng.standard_normal((G, d)),
+        "beta1": 0.2 * rng.standard_normal((G, d)),
+        "gamma2": 1 + 0.2 * rng.standard_normal((G, d)),
+        "beta2": 0.2 * rng.standard_normal((G, d)),
+    }
+    if rab_buckets:
+        p["rab_w"] = 0.3 * rng.standard_normal((H, rab_buckets))
+    return p
