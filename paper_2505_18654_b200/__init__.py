@@ -1,0 +1,15 @@
+"""B200-native MTGR hot path: jagged Group-Layer-Norm + HSTU encoder layer (arXiv 2505.18654).
+
+The compute lives in libmtgr.so (hand-written sm_100a CUDA behind the C ABI of
+include/mtgr.h); this package is the thin ctypes binding with the same names.
+"""
+from ._lib import MtgrError, LIB_PATH, lib, SIGNATURES
+from .api import (JaggedBatch, HstuStack, layer_cfg, build_jagged, balance_lpt, validate_jagged,
+                  mask_dense, gln_fwd, gln_bwd, attn_fwd, attn_bwd, hstu_layer_fwd,
+                  hstu_layer_bwd, layer_saved_bytes, layer_workspace_bytes, params_to_device,
+                  alloc_grads, scale_, gemm)
+
+__all__ = ["MtgrError", "LIB_PATH", "lib", "SIGNATURES", "JaggedBatch", "HstuStack", "layer_cfg",
+           "build_jagged", "balance_lpt", "validate_jagged", "mask_dense", "gln_fwd", "gln_bwd",
+           "attn_fwd", "attn_bwd", "hstu_layer_fwd", "hstu_layer_bwd", "layer_saved_bytes",
+           "layer_workspace_bytes", "params_to_device", "alloc_grads", "scale_", "gemm"]

@@ -1,0 +1,102 @@
+"""ctypes declarations of include/mtgr.h and the loader of the in-tree libmtgr.so.
+
+Argument marshalling only: every step of the hot path runs inside libmtgr.  There is no
+fallback — if the shared library is missing the import of the operations fails loudly.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from ctypes import POINTER, c_float, c_int32, c_int64, c_size_t, c_void_p, c_char_p, c_uint8
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libmtgr.so")
+
+MTGR_F32, MTGR_BF16 = 0, 1
+STATUS = {0: "MTGR_OK", 1: "MTGR_E_ARG", 2: "MTGR_E_SHAPE", 3: "MTGR_E_LAYOUT", 4: "MTGR_E_DTYPE",
+          5: "MTGR_E_WORKSPACE", 6: "MTGR_E_BUDGET", 7: "MTGR_E_UNSUPPORTED", 8: "MTGR_E_CUDA",
+          9: "MTGR_E_INVALID"}
+
+
+class MtgrError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class Jagged(ctypes.Structure):
+    _fields_ = [("num_users", c_int32), ("total_tokens", c_int32), ("max_len", c_int32),
+                ("offsets", c_void_p), ("n_static", c_void_p), ("n_rt", c_void_p),
+                ("n_cand", c_void_p), ("group_id", c_void_p), ("ts", c_void_p),
+                ("inv_norm", c_void_p)]
+
+
+class LayerCfg(ctypes.Structure):
+    _fields_ = [("d_model", c_int32), ("n_heads", c_int32), ("num_groups", c_int32),
+                ("rab_buckets", c_int32), ("eps", c_float), ("qkvu_silu", c_int32)]
+
+
+_PNAMES = ("w1", "b1", "w2", "b2", "gamma1", "beta1", "gamma2", "beta2", "rab_w")
+
+
+class LayerParams(ctypes.Structure):
+    _fields_ = [(n, c_void_p) for n in _PNAMES]
+
+
+class LayerGrads(ctypes.Structure):
+    _fields_ = [(n, c_void_p) for n in _PNAMES]
+
+
+# name -> (restype, argtypes); mirrors include/mtgr.h
+_S = c_int32  # mtgr_status_t
+_P = c_void_p
+SIGNATURES = {
+    "mtgr_status_str": (c_char_p, [c_int32]),
+    "mtgr_last_error": (c_char_p, []),
+    "mtgr_version": (c_int32, []),
+    "mtgr_build_jagged": (_S, [_P, c_int32, _P, c_int32, _P, _P, _P, _P, _P]),
+    "mtgr_balance_lpt": (_S, [_P, c_int32, c_int32, c_int64, _P, _P]),
+    "mtgr_validate_jagged": (_S, [POINTER(Jagged), c_int32, _P]),
+    "mtgr_mask_dense": (_S, [POINTER(Jagged), c_int32, _P, _P]),
+    "mtgr_gln_fwd": (_S, [POINTER(LayerCfg), POINTER(Jagged), c_int32, _P, _P, _P, _P, _P, _P, _P]),
+    "mtgr_gln_bwd_workspace_bytes": (c_size_t, [POINTER(LayerCfg), POINTER(Jagged)]),
+    "mtgr_gln_bwd": (_S, [POINTER(LayerCfg), POINTER(Jagged), c_int32, _P, _P, _P, _P, _P, _P, _P,
+                          _P, _P, c_size_t, _P]),
+    "mtgr_attn_workspace_bytes": (c_size_t, [POINTER(LayerCfg), POINTER(Jagged), c_int32]),
+    "mtgr_hstu_attn_fwd": (_S, [POINTER(LayerCfg), POINTER(Jagged), c_int32, _P, _P, _P, c_int64,
+                                _P, _P, _P, _P, _P, c_size_t, _P]),
+    "mtgr_hstu_attn_bwd": (_S, [POINTER(LayerCfg), POINTER(Jagged), c_int32, _P, _P, _P, _P,
+                                c_int64, _P, _P, _P, _P, _P, c_int64, _P, _P, c_size_t, _P]),
+    "mtgr_layer_saved_bytes": (c_size_t, [POINTER(LayerCfg), c_int32, c_int32]),
+    "mtgr_layer_workspace_bytes": (c_size_t, [POINTER(LayerCfg), POINTER(Jagged), c_int32]),
+    "mtgr_hstu_layer_fwd": (_S, [POINTER(LayerCfg), POINTER(Jagged), c_int32, POINTER(LayerParams),
+                                 _P, _P, _P, _P, c_size_t, _P]),
+    "mtgr_hstu_layer_bwd": (_S, [POINTER(LayerCfg), POINTER(Jagged), c_int32, POINTER(LayerParams),
+                                 _P, _P, _P, _P, POINTER(LayerGrads), c_int32, _P, c_size_t, _P]),
+    "mtgr_scale_f32": (_S, [_P, c_int64, c_float, _P]),
+    "mtgr_gemm": (_S, [c_int32, c_int32, c_int32, c_int32, _P, c_int64, c_int32, _P, c_int64,
+                       c_int32, _P, c_int64, c_int32, _P, c_int32, _P, c_size_t, _P]),
+    "mtgr_gemm_workspace_bytes": (c_size_t, [c_int32, c_int32, c_int32, c_int32, c_int32]),
+}
+
+_lib = None
+
+
+def lib():
+    """Load libmtgr.so (built in-tree by __graft_entry__.build()).  Raises if absent."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"libmtgr.so not found at {LIB_PATH}; run __graft_entry__.build()")
+        L = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def check(status: int):
+    if status != 0:
+        msg = lib().mtgr_last_error().decode(errors="replace")
+        raise MtgrError(status, msg)

@@ -1,0 +1,326 @@
+// Group-Layer Norm forward / backward (Eq.6; readings R#13, R#14).
+//
+// HBM-bound: one warp per token, 16-byte vector loads (8 elements per lane per chunk),
+// warp-shuffle reductions, statistics kept in registers.  The backward optionally fuses
+//  * MODE_GATE: the gate backward of Eq.6 (dO = dY (.) U, dU = dY (.) O) and the SiLU'
+//    of the U projection (R#5), writing dO and dp_U directly, and
+//  * MODE_RESID: the residual of Eq.6 (dx = GLN1_bwd(dX~) + dZ).
+// Parameter gradients are per-block partial sums (smem) reduced in block order by a second
+// kernel.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace mtgr {
+
+constexpr int GLN_MAXC = 4;  // chunks of 8 per lane -> d <= 1024
+
+__device__ __forceinline__ void load8(const float* p, float* v) {
+  float4 a = reinterpret_cast<const float4*>(p)[0];
+  float4 b = reinterpret_cast<const float4*>(p)[1];
+  v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+}
+__device__ __forceinline__ void load8(const __nv_bfloat16* p, float* v) {
+  uint4 a = *reinterpret_cast<const uint4*>(p);
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&a);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    float2 f = __bfloat1622float2(h[i]);
+    v[2 * i] = f.x; v[2 * i + 1] = f.y;
+  }
+}
+__device__ __forceinline__ void store8(float* p, const float* v) {
+  reinterpret_cast<float4*>(p)[0] = make_float4(v[0], v[1], v[2], v[3]);
+  reinterpret_cast<float4*>(p)[1] = make_float4(v[4], v[5], v[6], v[7]);
+}
+__device__ __forceinline__ void store8(__nv_bfloat16* p, const float* v) {
+  uint4 a;
+  __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&a);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+  *reinterpret_cast<uint4*>(p) = a;
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+template <class T>
+__global__ void __launch_bounds__(256) gln_fwd_kernel(const T* __restrict__ x,
+                                                      const uint8_t* __restrict__ gid,
+                                                      const float* __restrict__ gamma,
+                                                      const float* __restrict__ beta,
+                                                      T* __restrict__ y, float* __restrict__ mean,
+                                                      float* __restrict__ rstd, int ntok, int d,
+                                                      float eps) {
+  const int lane = threadIdx.x & 31;
+  const int nwarps = gridDim.x * (blockDim.x >> 5);
+  const int nch = d >> 3;
+  const float inv_d = 1.0f / (float)d;
+  for (int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); t < ntok; t += nwarps) {
+    float v[GLN_MAXC][8];
+    float s = 0.f;
+    const T* xr = x + (int64_t)t * d;
+#pragma unroll
+    for (int k = 0; k < GLN_MAXC; ++k) {
+      int c = lane + 32 * k;
+      if (c < nch) {
+        load8(xr + c * 8, v[k]);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) s += v[k][e];
+      }
+    }
+    const float mu = warp_sum(s) * inv_d;
+    float q = 0.f;
+#pragma unroll
+    for (int k = 0; k < GLN_MAXC; ++k)
+      if (lane + 32 * k < nch) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          float dlt = v[k][e] - mu;
+          q += dlt * dlt;
+        }
+      }
+    const float var = warp_sum(q) * inv_d;
+    const float r = 1.0f / sqrtf(var + eps);
+    const int g = gid[t];
+    const float* gr = gamma + (int64_t)g * d;
+    const float* br = beta + (int64_t)g * d;
+    T* yr = y + (int64_t)t * d;
+#pragma unroll
+    for (int k = 0; k < GLN_MAXC; ++k) {
+      int c = lane + 32 * k;
+      if (c < nch) {
+        float gg[8], bb[8], o[8];
+        load8(gr + c * 8, gg);
+        load8(br + c * 8, bb);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) o[e] = gg[e] * ((v[k][e] - mu) * r) + bb[e];
+        store8(yr + c * 8, o);
+      }
+    }
+    if (lane == 0) {
+      if (mean) mean[t] = mu;
+      if (rstd) rstd[t] = r;
+    }
+  }
+}
+
+enum { GLN_PLAIN = 0, GLN_GATE = 1, GLN_RESID = 2 };
+
+template <class T>
+struct GlnBwdArgs {
+  const T* dy;
+  const T* x;
+  const float* mean;
+  const float* rstd;
+  const float* gamma;
+  const uint8_t* gid;
+  T* dx;          // GLN_GATE: dO
+  float* part;    // [nblocks][G][2][d]
+  int ntok, d, G, tok_per_block;
+  // GLN_GATE
+  const T* o;     // [T][d]
+  const T* u;     // rows ld_a
+  const T* pre_u; // rows ld_a (pre-activation of U) or NULL (linear)
+  int64_t ld_a;
+  T* dpu;         // rows ld_dp
+  int64_t ld_dp;
+  // GLN_RESID
+  const T* dz;
+};
+
+template <class T, int MODE>
+__global__ void __launch_bounds__(256) gln_bwd_kernel(GlnBwdArgs<T> a) {
+  extern __shared__ float sacc[];  // [G][2][d]
+  const int d = a.d, G = a.G;
+  for (int i = threadIdx.x; i < G * 2 * d; i += blockDim.x) sacc[i] = 0.f;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int nch = d >> 3;
+  const float inv_d = 1.0f / (float)d;
+  const int t_begin = blockIdx.x * a.tok_per_block;
+  const int t_end = min(a.ntok, t_begin + a.tok_per_block);
+  // each warp owns a contiguous token sub-range; running per-group partials in registers
+  const int per_w = (a.tok_per_block + nw - 1) / nw;
+  const int w_begin = t_begin + warp * per_w;
+  const int w_end = min(t_end, w_begin + per_w);
+  float pg[GLN_MAXC][8], pb[GLN_MAXC][8];
+  int cur_g = -1;
+  auto flush = [&]() {
+    if (cur_g < 0) return;
+#pragma unroll
+    for (int k = 0; k < GLN_MAXC; ++k) {
+      int c = lane + 32 * k;
+      if (c < nch) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          atomicAdd(&sacc[(cur_g * 2 + 0) * d + c * 8 + e], pg[k][e]);
+          atomicAdd(&sacc[(cur_g * 2 + 1) * d + c * 8 + e], pb[k][e]);
+        }
+      }
+    }
+  };
+  for (int t = w_begin; t < w_end; ++t) {
+    const int g = a.gid[t];
+    if (g != cur_g) {
+      flush();
+      cur_g = g;
+#pragma unroll
+      for (int k = 0; k < GLN_MAXC; ++k)
+#pragma unroll
+        for (int e = 0; e < 8; ++e) pg[k][e] = pb[k][e] = 0.f;
+    }
+    const float mu = a.mean[t], r = a.rstd[t];
+    const float* gr = a.gamma + (int64_t)g * d;
+    float xh[GLN_MAXC][8], dxh[GLN_MAXC][8];
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int k = 0; k < GLN_MAXC; ++k) {
+      int c = lane + 32 * k;
+      if (c < nch) {
+        float xv[8], dyv[8], gg[8];
+        load8(a.x + (int64_t)t * d + c * 8, xv);
+        load8(a.dy + (int64_t)t * d + c * 8, dyv);
+        load8(gr + c * 8, gg);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          xh[k][e] = (xv[e] - mu) * r;
+          dxh[k][e] = dyv[e] * gg[e];
+          pg[k][e] += dyv[e] * xh[k][e];
+          pb[k][e] += dyv[e];
+          s1 += dxh[k][e];
+          s2 += dxh[k][e] * xh[k][e];
+        }
+      }
+    }
+    const float m1 = warp_sum(s1) * inv_d, m2 = warp_sum(s2) * inv_d;
+#pragma unroll
+    for (int k = 0; k < GLN_MAXC; ++k) {
+      int c = lane + 32 * k;
+      if (c < nch) {
+        float o[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) o[e] = r * (dxh[k][e] - m1 - xh[k][e] * m2);
+        if (MODE == GLN_RESID) {
+          float z[8];
+          load8(a.dz + (int64_t)t * d + c * 8, z);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) o[e] += z[e];
+          store8(a.dx + (int64_t)t * d + c * 8, o);
+        } else if (MODE == GLN_GATE) {
+          // o[] = dY; dO = dY * U;  dp_U = dY * O * silu'(p_U)
+          float uu[8], oo[8], dO[8], du[8];
+          load8(a.u + (int64_t)t * a.ld_a + c * 8, uu);
+          load8(a.o + (int64_t)t * d + c * 8, oo);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            dO[e] = o[e] * uu[e];
+            du[e] = o[e] * oo[e];
+          }
+          if (a.pre_u) {
+            float pp[8];
+            load8(a.pre_u + (int64_t)t * a.ld_a + c * 8, pp);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) du[e] *= dsilu_f(pp[e]);
+          }
+          store8(a.dx + (int64_t)t * d + c * 8, dO);
+          store8(a.dpu + (int64_t)t * a.ld_dp + c * 8, du);
+        } else {
+          store8(a.dx + (int64_t)t * d + c * 8, o);
+        }
+      }
+    }
+  }
+  flush();
+  __syncthreads();
+  float* dst = a.part + (int64_t)blockIdx.x * G * 2 * d;
+  for (int i = threadIdx.x; i < G * 2 * d; i += blockDim.x) dst[i] = sacc[i];
+}
+
+// dgamma/dbeta[g][c] = sum over blocks (fixed order) of the partials
+__global__ void gln_param_reduce_kernel(const float* __restrict__ part, int nblocks, int G, int d,
+                                        float* __restrict__ dgamma, float* __restrict__ dbeta,
+                                        int accumulate) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;  // over G*2*d
+  if (i >= G * 2 * d) return;
+  float s = 0.f;
+  for (int b = 0; b < nblocks; ++b) s += part[(int64_t)b * G * 2 * d + i];
+  int g = i / (2 * d), w = (i / d) & 1, c = i % d;
+  float* out = (w == 0 ? dgamma : dbeta) + g * d + c;
+  *out = accumulate ? *out + s : s;
+}
+
+// ------------------------------------------------------------------ host launchers
+
+static int gln_bwd_blocks(int ntok) {
+  int nb = 2 * num_sms();
+  int per = ceil_div(ntok > 0 ? ntok : 1, nb);
+  if (per < 64) {
+    per = 64;
+    nb = ceil_div(ntok > 0 ? ntok : 1, per);
+  }
+  return nb;
+}
+
+size_t gln_bwd_ws_bytes(int ntok, int d, int G) {
+  return align_up((size_t)gln_bwd_blocks(ntok) * G * 2 * d * sizeof(float), 256);
+}
+
+template <class T>
+mtgr_status_t gln_fwd_launch(const T* x, const uint8_t* gid, const float* gamma,
+                             const float* beta, T* y, float* mean, float* rstd, int ntok, int d,
+                             float eps, cudaStream_t st) {
+  if (ntok == 0) return MTGR_OK;
+  int blocks = min(ceil_div(ntok, 8), 8 * num_sms());
+  gln_fwd_kernel<T><<<blocks, 256, 0, st>>>(x, gid, gamma, beta, y, mean, rstd, ntok, d, eps);
+  return check_launch("gln_fwd");
+}
+
+template <class T>
+mtgr_status_t gln_bwd_launch(const GlnBwdIO& io, int mode, float* part, float* dgamma,
+                             float* dbeta, int accumulate, cudaStream_t st) {
+  GlnBwdArgs<T> a{};
+  a.dy = (const T*)io.dy; a.x = (const T*)io.x; a.mean = io.mean; a.rstd = io.rstd;
+  a.gamma = io.gamma; a.gid = io.gid; a.dx = (T*)io.dx; a.part = part;
+  a.ntok = io.ntok; a.d = io.d; a.G = io.G;
+  a.o = (const T*)io.o; a.u = (const T*)io.u; a.pre_u = (const T*)io.pre_u; a.ld_a = io.ld_a;
+  a.dpu = (T*)io.dpu; a.ld_dp = io.ld_dp; a.dz = (const T*)io.dz;
+  int nb = gln_bwd_blocks(io.ntok);
+  a.tok_per_block = ceil_div(io.ntok > 0 ? io.ntok : 1, nb);
+  size_t smem = (size_t)io.G * 2 * io.d * sizeof(float);
+  if (io.ntok > 0) {
+    if (mode == GLN_GATE) {
+      cudaFuncSetAttribute(gln_bwd_kernel<T, GLN_GATE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      gln_bwd_kernel<T, GLN_GATE><<<nb, 256, smem, st>>>(a);
+    } else if (mode == GLN_RESID) {
+      cudaFuncSetAttribute(gln_bwd_kernel<T, GLN_RESID>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      gln_bwd_kernel<T, GLN_RESID><<<nb, 256, smem, st>>>(a);
+    } else {
+      cudaFuncSetAttribute(gln_bwd_kernel<T, GLN_PLAIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      gln_bwd_kernel<T, GLN_PLAIN><<<nb, 256, smem, st>>>(a);
+    }
+    MTGR_TRY(check_launch("gln_bwd"));
+  } else {
+    nb = 0;
+  }
+  int n = io.G * 2 * io.d;
+  gln_param_reduce_kernel<<<ceil_div(n, 256), 256, 0, st>>>(part, nb, io.G, io.d, dgamma, dbeta,
+                                                            accumulate);
+  return check_launch("gln_param_reduce");
+}
+
+template mtgr_status_t gln_fwd_launch<float>(const float*, const uint8_t*, const float*,
+                                             const float*, float*, float*, float*, int, int,
+                                             float, cudaStream_t);
+template mtgr_status_t gln_fwd_launch<__nv_bfloat16>(const __nv_bfloat16*, const uint8_t*,
+                                                     const float*, const float*, __nv_bfloat16*,
+                                                     float*, float*, int, int, float,
+                                                     cudaStream_t);
+template mtgr_status_t gln_bwd_launch<float>(const GlnBwdIO&, int, float*, float*, float*, int,
+                                             cudaStream_t);
+template mtgr_status_t gln_bwd_launch<__nv_bfloat16>(const GlnBwdIO&, int, float*, float*,
+                                                     float*, int, cudaStream_t);
+
+}  // namespace mtgr

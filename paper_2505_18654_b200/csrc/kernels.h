@@ -1,0 +1,82 @@
+// Internal launcher declarations of libmtgr (not part of the public ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+#include "../../include/mtgr.h"
+
+namespace mtgr {
+
+// ------------------------------------------------------------------ GLN
+enum { GLNB_PLAIN = 0, GLNB_GATE = 1, GLNB_RESID = 2 };
+struct GlnBwdIO {
+  const void* dy; const void* x; const float* mean; const float* rstd; const float* gamma;
+  const uint8_t* gid; void* dx; int ntok, d, G;
+  const void* o; const void* u; const void* pre_u; int64_t ld_a; void* dpu; int64_t ld_dp;
+  const void* dz;
+};
+size_t gln_bwd_ws_bytes(int ntok, int d, int G);
+template <class T>
+mtgr_status_t gln_fwd_launch(const T* x, const uint8_t* gid, const float* gamma,
+                             const float* beta, T* y, float* mean, float* rstd, int ntok, int d,
+                             float eps, cudaStream_t st);
+template <class T>
+mtgr_status_t gln_bwd_launch(const GlnBwdIO& io, int mode, float* part, float* dgamma,
+                             float* dbeta, int accumulate, cudaStream_t st);
+
+// ------------------------------------------------------------------ GEMM
+enum { EPI_STORE = 0, EPI_QKVU = 1, EPI_RESID = 2, EPI_F32 = 3 };
+struct GemmIO {
+  int M, N, K;
+  const void* A; int64_t lda; int a_kmajor;
+  const void* B; int64_t ldb; int b_kmajor;
+  void* C; int64_t ldc;        // EPI_F32: float
+  void* C2;                    // EPI_QKVU: activated output (same ld as C)
+  const float* bias;           // [N] or NULL
+  const void* R; int64_t ldr;  // EPI_RESID residual
+  int accumulate;              // EPI_F32
+  int silu;                    // EPI_QKVU: 1 = C2 = silu(C), 0 = C2 = C
+};
+template <class T>
+mtgr_status_t gemm_simt_launch(const GemmIO& g, int epi, cudaStream_t st);
+size_t gemm_ws_bytes(int M, int N, int K, int epi, bool bf16);
+mtgr_status_t gemm_bf16_launch(const GemmIO& g, int epi, void* ws, size_t ws_bytes,
+                               cudaStream_t st);
+
+// ------------------------------------------------------------------ attention
+struct AttnIO {
+  mtgr_jagged_t jag;
+  int H, dh, d, nb;            // heads, head dim, d_model, rab buckets (0 = off)
+  const void* q; const void* k; const void* v; int64_t ld;
+  const void* u;               // gate or NULL
+  void* o; void* y;            // fwd outputs [T][d]
+  const void* dO;              // bwd input [T][d]
+  const void* pre; int64_t ld_pre;  // silu' source (points at Q block) or NULL
+  void* dq; void* dk; void* dv; int64_t ld_out;
+  const float* diag_a;         // [T][H]  nu*silu(s_ii) for non-static tokens, 0 otherwise
+  const float* diag_ds;        // [T][H]  nu*silu'(s_ii)*(dO_i . v_i)
+  const float* rab_w; float* drab;
+};
+size_t attn_ws_bytes(int ntok, int H);
+template <class T>
+mtgr_status_t attn_diag_launch(const AttnIO& a, bool bwd, float* diag_a, float* diag_ds,
+                               cudaStream_t st);
+template <class T>
+mtgr_status_t attn_simt_fwd_launch(const AttnIO& a, cudaStream_t st);
+template <class T>
+mtgr_status_t attn_simt_bwd_launch(const AttnIO& a, cudaStream_t st);
+mtgr_status_t attn_tc_fwd_launch(const AttnIO& a, cudaStream_t st);
+mtgr_status_t attn_tc_bwd_launch(const AttnIO& a, cudaStream_t st);
+bool attn_tc_supported(int dh);
+
+// ------------------------------------------------------------------ misc
+template <class T>
+mtgr_status_t colsum_launch(const T* X, int64_t ld, int ntok, int n, float* out, float* part,
+                            int accumulate, cudaStream_t st);
+size_t colsum_ws_bytes(int ntok, int n);
+mtgr_status_t scale_launch(float* g, int64_t n, float s, cudaStream_t st);
+mtgr_status_t mask_dense_launch(const mtgr_jagged_t& j, int user, uint8_t* out, cudaStream_t st);
+mtgr_status_t validate_launch(const mtgr_jagged_t& j, int G, cudaStream_t st);
+
+}  // namespace mtgr

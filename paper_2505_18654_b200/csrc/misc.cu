@@ -1,0 +1,117 @@
+// Small HBM-bound kernels: bias-gradient column sums, gradient scaling (P:360 aggregation),
+// the dense mask export and the jagged metadata validator.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace mtgr {
+
+// ------------------------------------------------------------------ column sums (db = sum_t dY)
+constexpr int CS_ROWS = 256;  // tokens per partial
+
+template <class T>
+__global__ void colsum_part_kernel(const T* __restrict__ X, int64_t ld, int ntok, int n,
+                                   float* __restrict__ part) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  const int r0 = blockIdx.y * CS_ROWS, r1 = min(ntok, r0 + CS_ROWS);
+  float s = 0.f;
+  for (int r = r0; r < r1; ++r) s += to_f(X[(int64_t)r * ld + c]);
+  part[(int64_t)blockIdx.y * n + c] = s;
+}
+
+__global__ void colsum_reduce_kernel(const float* __restrict__ part, int nparts, int n,
+                                     float* __restrict__ out, int accumulate) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  float s = 0.f;
+  for (int p = 0; p < nparts; ++p) s += part[(int64_t)p * n + c];
+  out[c] = accumulate ? out[c] + s : s;
+}
+
+size_t colsum_ws_bytes(int ntok, int n) {
+  return align_up((size_t)ceil_div(ntok > 0 ? ntok : 1, CS_ROWS) * n * sizeof(float), 256);
+}
+
+template <class T>
+mtgr_status_t colsum_launch(const T* X, int64_t ld, int ntok, int n, float* out, float* part,
+                            int accumulate, cudaStream_t st) {
+  int nparts = ntok > 0 ? ceil_div(ntok, CS_ROWS) : 0;
+  if (nparts > 0) {
+    colsum_part_kernel<T><<<dim3(ceil_div(n, 128), nparts), 128, 0, st>>>(X, ld, ntok, n, part);
+    MTGR_TRY(check_launch("colsum_part"));
+  }
+  colsum_reduce_kernel<<<ceil_div(n, 128), 128, 0, st>>>(part, nparts, n, out, accumulate);
+  return check_launch("colsum_reduce");
+}
+template mtgr_status_t colsum_launch<float>(const float*, int64_t, int, int, float*, float*, int,
+                                            cudaStream_t);
+template mtgr_status_t colsum_launch<__nv_bfloat16>(const __nv_bfloat16*, int64_t, int, int,
+                                                    float*, float*, int, cudaStream_t);
+
+// ------------------------------------------------------------------ scale
+__global__ void scale_kernel(float* g, int64_t n, float s) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    g[i] *= s;
+}
+mtgr_status_t scale_launch(float* g, int64_t n, float s, cudaStream_t st) {
+  if (n == 0) return MTGR_OK;
+  int64_t nb64 = ceil_div64(n, 256); int blocks = (int)(nb64 < 4 * num_sms() ? nb64 : 4 * num_sms());
+  scale_kernel<<<blocks, 256, 0, st>>>(g, n, s);
+  return check_launch("scale");
+}
+
+// ------------------------------------------------------------------ dense mask export
+// The exact composition the attention kernels use: the off-diagonal predicate on the key range
+// [0, n_static + n_rt) plus the diagonal of non-static rows (R#8-R#12).
+__global__ void mask_dense_kernel(mtgr_jagged_t j, int user, uint8_t* out) {
+  UserSpan us = load_user(j, user);
+  const int64_t n = (int64_t)us.L * us.L;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int r = (int)(e / us.L), c = (int)(e % us.L);
+    long long tr = j.ts ? j.ts[us.off + r] : 0, tc = j.ts ? j.ts[us.off + c] : 0;
+    bool v = (c < us.ns + us.nr && visible_offdiag(r, c, us.ns, tr, tc)) || (r >= us.ns && r == c);
+    out[e] = v ? 1 : 0;
+  }
+}
+mtgr_status_t mask_dense_launch(const mtgr_jagged_t& j, int user, uint8_t* out, cudaStream_t st) {
+  int blocks = 2 * num_sms();
+  mask_dense_kernel<<<blocks, 256, 0, st>>>(j, user, out);
+  return check_launch("mask_dense");
+}
+
+// ------------------------------------------------------------------ validation
+__device__ int g_validate_flag;
+__global__ void validate_kernel(mtgr_jagged_t j, int G) {
+  int bad = 0;
+  const int B = j.num_users;
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    if (j.offsets[0] != 0) bad |= 1;
+    if (j.offsets[B] != j.total_tokens) bad |= 2;
+  }
+  for (int u = blockIdx.x * blockDim.x + threadIdx.x; u < B; u += gridDim.x * blockDim.x) {
+    int L = j.offsets[u + 1] - j.offsets[u];
+    if (L < 0) bad |= 4;
+    if (L > j.max_len) bad |= 8;
+    if (j.n_static[u] < 0 || j.n_rt[u] < 0 || j.n_cand[u] < 0) bad |= 16;
+    if (j.n_static[u] + j.n_rt[u] + j.n_cand[u] != L) bad |= 32;
+    if (j.n_rt[u] > 0 && !j.ts) bad |= 64;
+  }
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < j.total_tokens; t += gridDim.x * blockDim.x)
+    if (j.group_id && j.group_id[t] >= G) bad |= 128;
+  if (bad) atomicOr(&g_validate_flag, bad);
+}
+mtgr_status_t validate_launch(const mtgr_jagged_t& j, int G, cudaStream_t st) {
+  int zero = 0, flag = 0;
+  cudaMemcpyToSymbolAsync(g_validate_flag, &zero, sizeof(int), 0, cudaMemcpyHostToDevice, st);
+  validate_kernel<<<num_sms(), 256, 0, st>>>(j, G);
+  MTGR_TRY(check_launch("validate"));
+  cudaMemcpyFromSymbolAsync(&flag, g_validate_flag, sizeof(int), 0, cudaMemcpyDeviceToHost, st);
+  cudaError_t e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return set_error(MTGR_E_CUDA, "validate: %s", cudaGetErrorString(e));
+  if (flag) return set_error(MTGR_E_INVALID, "mtgr_validate_jagged: metadata check failed (flags 0x%x)", flag);
+  return MTGR_OK;
+}
+
+}  // namespace mtgr

@@ -50,3 +50,28 @@ def tiny_params(rng, d, H, G=4, rab_buckets=0, scale=1.0):
     if rab_buckets:
         p["rab_w"] = 0.3 * rng.standard_normal((H, rab_buckets))
     return p
+
+
+def make_batch(cfg_name, n_users=None, seg=None, **over):
+    """Seeded batch from synth: (cfg, seg [B][4], ts [T], X [T][d], dZ [T][d], params)."""
+    import synth
+    cfg = synth.config(cfg_name, **over)
+    if seg is None:
+        seg = synth.gen_segments(cfg, n_users)
+    seg = np.asarray(seg, dtype=np.int32)
+    L = seg.astype(np.int64).sum(1)
+    ts = np.concatenate([synth.gen_user_ts(cfg, u, seg[u]) for u in range(len(seg))] + [np.zeros(0, np.int64)])
+    X = np.concatenate([synth.gen_user_x(cfg, u, int(L[u])) for u in range(len(seg))] +
+                       [np.zeros((0, cfg["d"]), np.float32)])
+    dZ = np.concatenate([synth.gen_user_dz(cfg, u, int(L[u])) for u in range(len(seg))] +
+                        [np.zeros((0, cfg["d"]), np.float32)])
+    P = synth.gen_layer_params(cfg, 0, cfg.get("rab_buckets", 0))
+    return cfg, seg, ts, X, dZ, P
+
+
+def rel_err(got, ref):
+    got = np.asarray(got, dtype=np.float64)
+    ref = np.asarray(ref, dtype=np.float64)
+    if ref.size == 0:
+        return 0.0
+    return float(np.abs(got - ref).max() / max(np.abs(ref).max(), 1e-30))
