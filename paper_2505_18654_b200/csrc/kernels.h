@@ -80,3 +80,11 @@ mtgr_status_t mask_dense_launch(const mtgr_jagged_t& j, int user, uint8_t* out, 
 mtgr_status_t validate_launch(const mtgr_jagged_t& j, int G, cudaStream_t st);
 
 }  // namespace mtgr
+
+#include <cuda.h>
+namespace mtgr {
+// 2-D bf16 TMA descriptor: `inner` contiguous elements x `outer` rows (row stride ld_elems),
+// box {box_inner, box_outer}, SWIZZLE_128B, zero fill out of bounds.
+mtgr_status_t make_tmap_bf16(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer,
+                             uint64_t ld_elems, uint32_t box_inner, uint32_t box_outer);
+}  // namespace mtgr

@@ -1,11 +1,379 @@
-// tcgen05 bf16 GEMM (placeholder: routes to the SIMT kernel until the tensor-core kernel lands).
+// tcgen05 bf16 GEMM for the layer's dense contractions (PAPER.md P:313 QKVU projection,
+// Eq.6 output "MLP", and their backward): C[M][N] = A[M][K] * B[N][K]^T, fp32 accumulation
+// in TMEM.
+//
+// Persistent, warp-specialised, one CTA per SM:
+//   warp 0 : TMA producer  (4-stage ring of 128x64 A + 256x64 B bf16 tiles, SWIZZLE_128B)
+//   warp 1 : MMA issuer    (one thread, tcgen05.mma.cta_group::1 M=128 N=256 K=16)
+//   warp 2 : TMEM allocator (512 columns = two 128x256 fp32 accumulators, double-buffered)
+//   warps 4-7: epilogue    (tcgen05.ld 32x32b -> registers -> fused epilogue -> global)
+// Either operand may be K-major or MN-major (the weight-gradient and data-gradient GEMMs read
+// activations [T][n] as MN-major operands directly — no transposes).  Small output grids
+// (weight gradients, K = T) are split along K with a deterministic second-pass reduction.
+// Fused epilogues: +bias and SiLU with both pre/post-activation stores (QKVU, R#5);
+// +bias +residual (Eq.6); fp32 (partial) stores for weight gradients.
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.h"
+#include "sm100.cuh"
 
 namespace mtgr {
-size_t gemm_ws_bytes(int M, int N, int K, int epi, bool bf16) { (void)M; (void)N; (void)K; (void)epi; (void)bf16; return 0; }
-mtgr_status_t gemm_bf16_launch(const GemmIO& g, int epi, void* ws, size_t ws_bytes, cudaStream_t st) {
-  (void)ws; (void)ws_bytes;
-  return gemm_simt_launch<__nv_bfloat16>(g, epi, st);
+namespace tcg {
+
+constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
+constexpr int A_BYTES = BM * BK * 2;
+constexpr int B_BYTES = BN * BK * 2;
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
+constexpr int NTHREADS = 256;
+
+struct Params {
+  int M, N, K;
+  int num_m, num_n, num_splits, kb_per_split, num_kb;
+  int a_mn, b_mn;
+  void* C;
+  int64_t ldc;
+  void* C2;
+  const float* bias;
+  const __nv_bfloat16* R;
+  int64_t ldr;
+  float* part;  // split-K partials [splits][M][N]
+  int accumulate;
+  int silu;
+};
+
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
 }
+
+template <int EPI>
+__global__ void __launch_bounds__(NTHREADS, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   Params p) {
+  using namespace sm100;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 128);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int total = p.num_m * p.num_n * p.num_splits;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int item = blockIdx.x; item < total; item += gridDim.x) {
+        const int nb = item % p.num_n, rest = item / p.num_n;
+        const int mb = rest % p.num_m, sp = rest / p.num_m;
+        const int kb0 = sp * p.kb_per_split, kb1 = min(p.num_kb, kb0 + p.kb_per_split);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_expect_tx(&full[stage], STAGE_BYTES);
+          const int k = kb * BK;
+          uint8_t* a_dst = sA + stage * A_BYTES;
+          uint8_t* b_dst = sB + stage * B_BYTES;
+          if (!p.a_mn) {
+            tma_load_2d(a_dst, &tmA, &full[stage], k, mb * BM);
+          } else {
+#pragma unroll
+            for (int c = 0; c < BM / 64; ++c) tma_load_2d(a_dst + c * 8192, &tmA, &full[stage], mb * BM + c * 64, k);
+          }
+          if (!p.b_mn) {
+            tma_load_2d(b_dst, &tmB, &full[stage], k, nb * BN);
+          } else {
+#pragma unroll
+            for (int c = 0; c < BN / 64; ++c) tma_load_2d(b_dst + c * 8192, &tmB, &full[stage], nb * BN + c * 64, k);
+          }
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t idesc = idesc_bf16_f32(BM, BN, p.a_mn, p.b_mn);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int item = blockIdx.x; item < total; item += gridDim.x, ++it) {
+        const int sp = item / (p.num_n * p.num_m);
+        const int kb0 = sp * p.kb_per_split, kb1 = min(p.num_kb, kb0 + p.kb_per_split);
+        const int buf = it & 1;
+        const uint32_t acc_phase = (it >> 1) & 1;
+        mbar_wait(&tempty[buf], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem + buf * BN;
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a_base = smem_u32(sA + stage * A_BYTES);
+          const uint32_t b_base = smem_u32(sB + stage * B_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint64_t ad = p.a_mn ? desc_sw128(a_base + k * 2048, 8192, 1024)
+                                       : desc_sw128(a_base + k * 32, 16, 1024);
+            const uint64_t bd = p.b_mn ? desc_sw128(b_base + k * 2048, 8192, 1024)
+                                       : desc_sw128(b_base + k * 32, 16, 1024);
+            mma_bf16_ss(d_tmem, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+          }
+          mma_commit(&empty[stage]);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        mma_commit(&tfull[buf]);
+      }
+    }
+  } else if (warp >= 4) {
+    const int q = warp - 4;
+    const int row = q * 32 + lane;
+    int it = 0;
+    for (int item = blockIdx.x; item < total; item += gridDim.x, ++it) {
+      const int nb = item % p.num_n, rest = item / p.num_n;
+      const int mb = rest % p.num_m, sp = rest / p.num_m;
+      const int buf = it & 1;
+      const uint32_t acc_phase = (it >> 1) & 1;
+      mbar_wait(&tfull[buf], acc_phase);
+      tc_fence_after();
+      const int m = mb * BM + row;
+      const bool row_ok = m < p.M;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t r[32];
+        tmem_ld32(tmem + buf * BN + c * 32 + ((uint32_t)(q * 32) << 16), r);
+        tmem_ld_wait();
+        const int n0 = nb * BN + c * 32;
+        if (!row_ok || n0 >= p.N) continue;
+        float v[32];
+#pragma unroll
+        for (int e = 0; e < 32; ++e) v[e] = __uint_as_float(r[e]);
+        const bool full_chunk = n0 + 32 <= p.N;
+        if (EPI == EPI_F32) {
+          float* dst;
+          bool acc = false;
+          if (p.num_splits > 1) {
+            dst = p.part + ((int64_t)sp * p.M + m) * p.N + n0;
+          } else {
+            dst = (float*)p.C + (int64_t)m * p.ldc + n0;
+            acc = p.accumulate;
+          }
+          if (full_chunk) {
+#pragma unroll
+            for (int e = 0; e < 32; e += 4) {
+              float4 o = make_float4(v[e], v[e + 1], v[e + 2], v[e + 3]);
+              if (acc) {
+                float4 old = *reinterpret_cast<float4*>(dst + e);
+                o.x += old.x; o.y += old.y; o.z += old.z; o.w += old.w;
+              }
+              *reinterpret_cast<float4*>(dst + e) = o;
+            }
+          } else {
+            for (int e = 0; e < 32 && n0 + e < p.N; ++e) dst[e] = acc ? dst[e] + v[e] : v[e];
+          }
+        } else {
+          if (p.bias) {
+#pragma unroll
+            for (int e = 0; e < 32; ++e) v[e] += (n0 + e < p.N) ? __ldg(p.bias + n0 + e) : 0.f;
+          }
+          if (EPI == EPI_RESID) {
+            const __nv_bfloat16* rr = p.R + (int64_t)m * p.ldr + n0;
+            if (full_chunk) {
+#pragma unroll
+              for (int e = 0; e < 32; e += 8) {
+                uint4 u = *reinterpret_cast<const uint4*>(rr + e);
+                const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                  float2 f = __bfloat1622float2(h[i]);
+                  v[e + 2 * i] += f.x;
+                  v[e + 2 * i + 1] += f.y;
+                }
+              }
+            } else {
+              for (int e = 0; e < 32 && n0 + e < p.N; ++e) v[e] += __bfloat162float(rr[e]);
+            }
+          }
+          __nv_bfloat16* dst = (__nv_bfloat16*)p.C + (int64_t)m * p.ldc + n0;
+          if (full_chunk) {
+#pragma unroll
+            for (int e = 0; e < 32; e += 8) {
+              uint4 u = make_uint4(pack_bf16(v[e], v[e + 1]), pack_bf16(v[e + 2], v[e + 3]),
+                                   pack_bf16(v[e + 4], v[e + 5]), pack_bf16(v[e + 6], v[e + 7]));
+              *reinterpret_cast<uint4*>(dst + e) = u;
+            }
+          } else {
+            for (int e = 0; e < 32 && n0 + e < p.N; ++e) dst[e] = __float2bfloat16_rn(v[e]);
+          }
+          if (EPI == EPI_QKVU) {
+            __nv_bfloat16* dst2 = (__nv_bfloat16*)p.C2 + (int64_t)m * p.ldc + n0;
+#pragma unroll
+            for (int e = 0; e < 32; ++e) v[e] = p.silu ? silu_f(v[e]) : v[e];
+            if (full_chunk) {
+#pragma unroll
+              for (int e = 0; e < 32; e += 8) {
+                uint4 u = make_uint4(pack_bf16(v[e], v[e + 1]), pack_bf16(v[e + 2], v[e + 3]),
+                                     pack_bf16(v[e + 4], v[e + 5]), pack_bf16(v[e + 6], v[e + 7]));
+                *reinterpret_cast<uint4*>(dst2 + e) = u;
+              }
+            } else {
+              for (int e = 0; e < 32 && n0 + e < p.N; ++e) dst2[e] = __float2bfloat16_rn(v[e]);
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[buf]);
+    }
+  }
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+// C (+)= sum over splits of the partials (fixed order: deterministic)
+__global__ void splitk_reduce_kernel(const float* __restrict__ part, int splits, int M, int N,
+                                     float* __restrict__ C, int64_t ldc, int accumulate) {
+  const int64_t total = (int64_t)M * N;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float s = 0.f;
+    for (int k = 0; k < splits; ++k) s += part[(int64_t)k * total + i];
+    const int64_t m = i / N, n = i % N;
+    float* c = C + m * ldc + n;
+    *c = accumulate ? *c + s : s;
+  }
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }
+  return fn;
+}
+
+struct Split {
+  int splits, kb_per_split;
+};
+static Split choose_split(int M, int N, int K, int epi) {
+  const int num_kb = ceil_div(K, BK);
+  const int tiles = ceil_div(M, BM) * ceil_div(N, BN);
+  Split s{1, num_kb};
+  if (epi == EPI_F32 && tiles < num_sms() && num_kb > 1) {
+    int want = ceil_div(2 * num_sms(), tiles);
+    want = std::min(want, num_kb);
+    s.kb_per_split = ceil_div(num_kb, want);
+    s.splits = ceil_div(num_kb, s.kb_per_split);
+  }
+  return s;
+}
+
+}  // namespace tcg
+
+mtgr_status_t make_tmap_bf16(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer,
+                             uint64_t ld_elems, uint32_t box_inner, uint32_t box_outer) {
+  auto fn = tcg::encode_fn();
+  if (!fn) return set_error(MTGR_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {ld_elems * 2};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box,
+                  estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return set_error(MTGR_E_CUDA, "cuTensorMapEncodeTiled failed (%d): inner %llu outer %llu ld %llu",
+                     (int)r, (unsigned long long)inner, (unsigned long long)outer,
+                     (unsigned long long)ld_elems);
+  return MTGR_OK;
+}
+
+size_t gemm_ws_bytes(int M, int N, int K, int epi, bool bf16) {
+  if (!bf16 || epi != EPI_F32) return 0;
+  tcg::Split s = tcg::choose_split(M, N, K, epi);
+  return s.splits > 1 ? align_up((size_t)s.splits * M * N * sizeof(float), 256) : 0;
+}
+
+mtgr_status_t gemm_bf16_launch(const GemmIO& g, int epi, void* ws, size_t ws_bytes,
+                               cudaStream_t st) {
+  using namespace tcg;
+  if (g.M == 0 || g.N == 0) return MTGR_OK;
+  if (g.K == 0) return gemm_simt_launch<__nv_bfloat16>(g, epi, st);  // bias / zero only
+  MTGR_CHECK(g.lda % 8 == 0 && g.ldb % 8 == 0 && aligned16(g.A) && aligned16(g.B), MTGR_E_LAYOUT,
+             "tc gemm: operands need 16-byte aligned rows (ld %% 8 == 0)");
+  MTGR_CHECK(g.ldc % 8 == 0 && aligned16(g.C) && (!g.C2 || aligned16(g.C2)) &&
+                 (!g.R || (g.ldr % 8 == 0 && aligned16(g.R))),
+             MTGR_E_LAYOUT, "tc gemm: outputs need 16-byte aligned rows");
+  CUtensorMap ta, tb;
+  if (g.a_kmajor) MTGR_TRY(make_tmap_bf16(&ta, g.A, g.K, g.M, g.lda, 64, BM));
+  else MTGR_TRY(make_tmap_bf16(&ta, g.A, g.M, g.K, g.lda, 64, 64));
+  if (g.b_kmajor) MTGR_TRY(make_tmap_bf16(&tb, g.B, g.K, g.N, g.ldb, 64, BN));
+  else MTGR_TRY(make_tmap_bf16(&tb, g.B, g.N, g.K, g.ldb, 64, 64));
+  Params p{};
+  p.M = g.M; p.N = g.N; p.K = g.K;
+  p.num_m = ceil_div(g.M, BM); p.num_n = ceil_div(g.N, BN); p.num_kb = ceil_div(g.K, BK);
+  Split s = choose_split(g.M, g.N, g.K, epi);
+  p.num_splits = s.splits; p.kb_per_split = s.kb_per_split;
+  p.a_mn = g.a_kmajor ? 0 : 1; p.b_mn = g.b_kmajor ? 0 : 1;
+  p.C = g.C; p.ldc = g.ldc; p.C2 = g.C2; p.bias = g.bias;
+  p.R = (const __nv_bfloat16*)g.R; p.ldr = g.ldr; p.accumulate = g.accumulate; p.silu = g.silu;
+  if (epi == EPI_F32 && s.splits > 1) {
+    MTGR_CHECK(ws && ws_bytes >= gemm_ws_bytes(g.M, g.N, g.K, epi, true), MTGR_E_WORKSPACE,
+               "tc gemm: split-K workspace too small");
+    p.part = (float*)ws;
+  }
+  const int total = p.num_m * p.num_n * p.num_splits;
+  const int grid = std::min(total, num_sms());
+  auto launch = [&](auto kern) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    kern<<<grid, NTHREADS, SMEM_BYTES, st>>>(ta, tb, p);
+  };
+  switch (epi) {
+    case EPI_STORE: launch(gemm_tc_kernel<EPI_STORE>); break;
+    case EPI_QKVU: launch(gemm_tc_kernel<EPI_QKVU>); break;
+    case EPI_RESID: launch(gemm_tc_kernel<EPI_RESID>); break;
+    default: launch(gemm_tc_kernel<EPI_F32>); break;
+  }
+  MTGR_TRY(check_launch("gemm_tc"));
+  if (epi == EPI_F32 && s.splits > 1) {
+    const int64_t tot = (int64_t)g.M * g.N;
+    const int blocks = (int)std::min<int64_t>(ceil_div64(tot, 256), 8 * num_sms());
+    splitk_reduce_kernel<<<blocks, 256, 0, st>>>(p.part, s.splits, g.M, g.N, (float*)g.C, g.ldc,
+                                                 g.accumulate);
+    MTGR_TRY(check_launch("splitk_reduce"));
+  }
+  return MTGR_OK;
+}
+
 }  // namespace mtgr
