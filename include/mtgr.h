@@ -233,6 +233,19 @@ mtgr_status_t mtgr_gemm(mtgr_dtype_t dtype, int32_t M, int32_t N, int32_t K, con
 size_t mtgr_gemm_workspace_bytes(mtgr_dtype_t dtype, int32_t M, int32_t N, int32_t K,
                                  int32_t c_f32);
 
+/* ---------------------------------------------------------------- tracing */
+
+/* Number of CUDA kernels libmtgr has launched in this process (all streams). */
+int64_t mtgr_launch_count(void);
+/* Per-kernel-kind CUDA-event timing: when enabled, each instrumented launch records an event
+ * pair on its own stream.  query() synchronises on the recorded events and returns the number
+ * of launches and the summed device time (ms) of `kind` since the last reset. */
+void mtgr_prof_enable(int32_t on);
+void mtgr_prof_reset(void);
+int32_t mtgr_prof_num_kinds(void);
+const char* mtgr_prof_kind_name(int32_t kind);
+mtgr_status_t mtgr_prof_query(int32_t kind, int64_t* launches, double* total_ms);
+
 #ifdef __cplusplus
 }
 #endif

@@ -7,9 +7,11 @@ from ._lib import MtgrError, LIB_PATH, lib, SIGNATURES
 from .api import (JaggedBatch, HstuStack, layer_cfg, build_jagged, balance_lpt, validate_jagged,
                   mask_dense, gln_fwd, gln_bwd, attn_fwd, attn_bwd, hstu_layer_fwd,
                   hstu_layer_bwd, layer_saved_bytes, layer_workspace_bytes, params_to_device,
-                  alloc_grads, scale_, gemm)
+                  alloc_grads, grad_numel, scale_, gemm, launch_count, prof_enable, prof_reset,
+                  prof_query)
 
 __all__ = ["MtgrError", "LIB_PATH", "lib", "SIGNATURES", "JaggedBatch", "HstuStack", "layer_cfg",
            "build_jagged", "balance_lpt", "validate_jagged", "mask_dense", "gln_fwd", "gln_bwd",
            "attn_fwd", "attn_bwd", "hstu_layer_fwd", "hstu_layer_bwd", "layer_saved_bytes",
-           "layer_workspace_bytes", "params_to_device", "alloc_grads", "scale_", "gemm"]
+           "layer_workspace_bytes", "params_to_device", "alloc_grads", "grad_numel", "scale_", "gemm", "launch_count", "prof_enable",
+           "prof_reset", "prof_query"]

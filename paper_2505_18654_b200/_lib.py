@@ -76,6 +76,12 @@ SIGNATURES = {
     "mtgr_gemm": (_S, [c_int32, c_int32, c_int32, c_int32, _P, c_int64, c_int32, _P, c_int64,
                        c_int32, _P, c_int64, c_int32, _P, c_int32, _P, c_size_t, _P]),
     "mtgr_gemm_workspace_bytes": (c_size_t, [c_int32, c_int32, c_int32, c_int32, c_int32]),
+    "mtgr_launch_count": (c_int64, []),
+    "mtgr_prof_enable": (None, [c_int32]),
+    "mtgr_prof_reset": (None, []),
+    "mtgr_prof_num_kinds": (c_int32, []),
+    "mtgr_prof_kind_name": (c_char_p, [c_int32]),
+    "mtgr_prof_query": (_S, [c_int32, POINTER(c_int64), POINTER(ctypes.c_double)]),
 }
 
 _lib = None

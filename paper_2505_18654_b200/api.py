@@ -202,17 +202,31 @@ def _cparams(p: dict) -> LayerParams:
     return LayerParams(*[(p[k].data_ptr() if p.get(k) is not None else None) for k in PARAM_KEYS])
 
 
-def alloc_grads(cfg: LayerCfg, device) -> dict:
+def grad_numel(cfg: LayerCfg) -> int:
     d, G = cfg.d_model, cfg.num_groups
-    f = lambda *s: torch.zeros(*s, dtype=torch.float32, device=device)
-    g = dict(W1=f(4 * d, d), b1=f(4 * d), W2=f(d, d), b2=f(d), gamma1=f(G, d), beta1=f(G, d),
-             gamma2=f(G, d), beta2=f(G, d))
+    return 5 * d * d + 5 * d + 4 * G * d + (cfg.n_heads * cfg.rab_buckets if cfg.rab_buckets > 0 else 0)
+
+
+def alloc_grads(cfg: LayerCfg, device, flat: torch.Tensor | None = None) -> dict:
+    """fp32 gradient views (mtgr_layer_grads_t) carved from one flat bucket (all-reduce unit)."""
+    d, G = cfg.d_model, cfg.num_groups
+    if flat is None:
+        flat = torch.zeros(grad_numel(cfg), dtype=torch.float32, device=device)
+    shapes = dict(W1=(4 * d, d), b1=(4 * d,), W2=(d, d), b2=(d,), gamma1=(G, d), beta1=(G, d),
+                  gamma2=(G, d), beta2=(G, d))
     if cfg.rab_buckets > 0:
-        g["rab_w"] = f(cfg.n_heads, cfg.rab_buckets)
+        shapes["rab_w"] = (cfg.n_heads, cfg.rab_buckets)
+    g, off = {}, 0
+    for k, shp in shapes.items():
+        n = int(np.prod(shp))
+        g[k] = flat[off:off + n].view(*shp)
+        off += n
+    assert off == flat.numel()
+    g["_flat"] = flat
     return g
 
 
-def _cgrads(g: dict) -> LayerGrads:
+def _cgrads(g: dict) -> LayerGrads:  # noqa: E302
     return LayerGrads(*[(g[k].data_ptr() if g.get(k) is not None else None) for k in PARAM_KEYS])
 
 
@@ -279,7 +293,11 @@ class HstuStack:
 
     def __init__(self, cfg: LayerCfg, params: list, dtype: torch.dtype, device):
         self.cfg, self.params, self.dtype, self.device = cfg, params, dtype, device
-        self.grads = [alloc_grads(cfg, device) for _ in params]
+        n = grad_numel(cfg)
+        # one flat fp32 buffer holding every layer's gradients; per-layer slices are the
+        # all-reduce buckets of data-parallel training
+        self.grad_flat = torch.zeros(n * len(params), dtype=torch.float32, device=device)
+        self.grads = [alloc_grads(cfg, device, self.grad_flat[i * n:(i + 1) * n]) for i in range(len(params))]
         self._jb = None
 
     def bind(self, jb: JaggedBatch):
@@ -291,23 +309,55 @@ class HstuStack:
         T, d = max(jb.total_tokens, 1), self.cfg.d_model
         sb = layer_saved_bytes(self.cfg, jb.total_tokens, self.dtype)
         self.saved = [_ws(sb, self.device) for _ in self.params]
-        self.xs = [torch.empty(T, d, dtype=self.dtype, device=self.device) for _ in range(len(self.params) + 1)]
+        self.xs = [None] + [torch.empty(T, d, dtype=self.dtype, device=self.device) for _ in self.params]
         self.dbuf = [torch.empty(T, d, dtype=self.dtype, device=self.device) for _ in range(2)]
         self.ws = _ws(layer_workspace_bytes(self.cfg, jb, self.dtype), self.device)
 
     def forward(self, x: torch.Tensor) -> torch.Tensor:
         jb = self._jb
-        self.xs[0][:jb.total_tokens].copy_(x)
+        assert x.is_contiguous() and x.dtype == self.dtype
+        self.xs[0] = x  # layer-0 input is read in place (kept alive for the backward)
         for li, P in enumerate(self.params):
             hstu_layer_fwd(self.cfg, jb, P, self.xs[li], self.xs[li + 1], self.saved[li], self.ws)
         return self.xs[-1][:jb.total_tokens]
 
-    def backward(self, dz: torch.Tensor, accumulate=False) -> torch.Tensor:
+    def backward(self, dz: torch.Tensor, accumulate=False, on_layer_done=None) -> torch.Tensor:
+        """Backward through the stack.  on_layer_done(li, grad_bucket) is called right after
+        layer li's backward is enqueued (hook for overlapping its all-reduce)."""
         jb = self._jb
         cur = dz
         for li in range(len(self.params) - 1, -1, -1):
             out = self.dbuf[li % 2]
             hstu_layer_bwd(self.cfg, jb, self.params[li], self.xs[li], self.saved[li], cur,
                            self.grads[li], dx=out, accumulate=accumulate, ws=self.ws)
+            if on_layer_done is not None:
+                on_layer_done(li, self.grads[li]["_flat"])
             cur = out
         return cur[:jb.total_tokens]
+
+
+# ------------------------------------------------------------------ tracing
+
+def launch_count() -> int:
+    """Kernels libmtgr has launched in this process."""
+    return int(lib().mtgr_launch_count())
+
+
+def prof_enable(on: bool = True):
+    lib().mtgr_prof_enable(1 if on else 0)
+
+
+def prof_reset():
+    lib().mtgr_prof_reset()
+
+
+def prof_query() -> dict:
+    """{kind: (launches, total_ms)} of CUDA-event-timed kernels since the last reset."""
+    out = {}
+    for k in range(lib().mtgr_prof_num_kinds()):
+        n = ctypes.c_int64()
+        ms = ctypes.c_double()
+        check(lib().mtgr_prof_query(k, ctypes.byref(n), ctypes.byref(ms)))
+        if n.value:
+            out[lib().mtgr_prof_kind_name(k).decode()] = (int(n.value), float(ms.value))
+    return out

@@ -9,6 +9,7 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "prof.h"
 
 namespace mtgr {
 
@@ -23,6 +24,7 @@ mtgr_status_t set_error(mtgr_status_t s, const char* fmt, ...) {
 }
 
 mtgr_status_t check_launch(const char* what) {
+  count_launch();
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_error(MTGR_E_CUDA, "%s: %s", what, cudaGetErrorString(e));
   return MTGR_OK;
@@ -135,7 +137,7 @@ static mtgr_status_t run_attn_fwd(const AttnIO& a, float* diag, cudaStream_t st)
   MTGR_TRY(attn_diag_launch<T>(a, false, diag, nullptr, st));
   AttnIO b = a;
   b.diag_a = diag;
-  if (std::is_same<T, __nv_bfloat16>::value && a.nb == 0 && attn_tc_supported(a.dh))
+  if (std::is_same<T, __nv_bfloat16>::value && a.nb == 0 && a.u && attn_tc_supported(a.dh))
     return attn_tc_fwd_launch(b, st);
   return attn_simt_fwd_launch<T>(b, st);
 }
@@ -228,7 +230,8 @@ static mtgr_status_t layer_bwd_t(const mtgr_layer_cfg_t* c, const mtgr_jagged_t*
       for (float* q : {G->gamma1, G->beta1, G->gamma2, G->beta2})
         cudaMemsetAsync(q, 0, sizeof(float) * c->num_groups * d, st);
     }
-    return check_launch("layer_bwd(empty)");
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? MTGR_OK : set_error(MTGR_E_CUDA, "layer_bwd: %s", cudaGetErrorString(e));
   }
   // dW2 = dZ^T Y~, db2 = sum dZ, dY~ = dZ W2
   GemmIO g{};

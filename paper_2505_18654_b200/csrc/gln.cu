@@ -9,6 +9,7 @@
 // kernel.
 #include "common.cuh"
 #include "kernels.h"
+#include "prof.h"
 
 namespace mtgr {
 
@@ -273,6 +274,7 @@ mtgr_status_t gln_fwd_launch(const T* x, const uint8_t* gid, const float* gamma,
                              const float* beta, T* y, float* mean, float* rstd, int ntok, int d,
                              float eps, cudaStream_t st) {
   if (ntok == 0) return MTGR_OK;
+  ProfScope ps(PROF_GLN_FWD, st);
   int blocks = min(ceil_div(ntok, 8), 8 * num_sms());
   gln_fwd_kernel<T><<<blocks, 256, 0, st>>>(x, gid, gamma, beta, y, mean, rstd, ntok, d, eps);
   return check_launch("gln_fwd");
@@ -281,6 +283,7 @@ mtgr_status_t gln_fwd_launch(const T* x, const uint8_t* gid, const float* gamma,
 template <class T>
 mtgr_status_t gln_bwd_launch(const GlnBwdIO& io, int mode, float* part, float* dgamma,
                              float* dbeta, int accumulate, cudaStream_t st) {
+  ProfScope ps(PROF_GLN_BWD, st);
   GlnBwdArgs<T> a{};
   a.dy = (const T*)io.dy; a.x = (const T*)io.x; a.mean = io.mean; a.rstd = io.rstd;
   a.gamma = io.gamma; a.gid = io.gid; a.dx = (T*)io.dx; a.part = part;

@@ -2,6 +2,7 @@
 // the dense mask export and the jagged metadata validator.
 #include "common.cuh"
 #include "kernels.h"
+#include "prof.h"
 
 namespace mtgr {
 
@@ -35,6 +36,7 @@ size_t colsum_ws_bytes(int ntok, int n) {
 template <class T>
 mtgr_status_t colsum_launch(const T* X, int64_t ld, int ntok, int n, float* out, float* part,
                             int accumulate, cudaStream_t st) {
+  ProfScope ps(PROF_COLSUM, st);
   int nparts = ntok > 0 ? ceil_div(ntok, CS_ROWS) : 0;
   if (nparts > 0) {
     colsum_part_kernel<T><<<dim3(ceil_div(n, 128), nparts), 128, 0, st>>>(X, ld, ntok, n, part);

@@ -8,6 +8,7 @@
 //    visible only to themselves, rule 3 P:338, and enter through the diagonal term).
 #include "common.cuh"
 #include "kernels.h"
+#include "prof.h"
 
 namespace mtgr {
 
@@ -83,6 +84,8 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmIO g) {
 template <class T>
 mtgr_status_t gemm_simt_launch(const GemmIO& g, int epi, cudaStream_t st) {
   if (g.M == 0 || g.N == 0) return MTGR_OK;
+  ProfScope ps(epi == EPI_QKVU ? PROF_GEMM_QKVU : epi == EPI_RESID ? PROF_GEMM_OUT
+               : epi == EPI_STORE ? PROF_GEMM_DGRAD : PROF_GEMM_WGRAD, st);
   dim3 grid(ceil_div(g.N, SG_BN), ceil_div(g.M, SG_BM));
   switch (epi) {
     case EPI_STORE: gemm_simt_kernel<T, EPI_STORE><<<grid, 256, 0, st>>>(g); break;
@@ -150,6 +153,7 @@ mtgr_status_t attn_diag_launch(const AttnIO& a, bool bwd, float* diag_a, float* 
                                cudaStream_t st) {
   int ntok = a.jag.total_tokens;
   if (ntok == 0) return MTGR_OK;
+  ProfScope ps(PROF_ATTN_DIAG, st);
   int blocks = min(ceil_div(ntok, 8), 8 * num_sms());
   attn_diag_kernel<T><<<blocks, 256, 0, st>>>(a, bwd ? 1 : 0, diag_a, diag_ds);
   return check_launch("attn_diag");
@@ -402,6 +406,7 @@ template <class T>
 mtgr_status_t attn_simt_fwd_launch(const AttnIO& a, cudaStream_t st) {
   if (a.jag.num_users == 0 || a.jag.max_len == 0) return MTGR_OK;
   dim3 grid(ceil_div(a.jag.max_len, SA_B), a.H, a.jag.num_users);
+  ProfScope ps(PROF_ATTN_FWD, st);
   size_t smem = (3 * SA_B * a.dh + SA_B * (SA_B + 1)) * sizeof(float) + SA_B * sizeof(long long);
   cudaFuncSetAttribute(attn_simt_fwd_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   attn_simt_fwd_kernel<T><<<grid, 256, smem, st>>>(a);
@@ -414,9 +419,13 @@ mtgr_status_t attn_simt_bwd_launch(const AttnIO& a, cudaStream_t st) {
   dim3 grid(ceil_div(a.jag.max_len, SA_B), a.H, a.jag.num_users);
   size_t smem_kv = (4 * SA_B * a.dh + 2 * SA_B * (SA_B + 1)) * sizeof(float) +
                    SA_B * sizeof(long long) + (size_t)(a.nb > 0 ? a.nb : 1) * sizeof(float);
-  cudaFuncSetAttribute(attn_simt_dkv_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_kv);
-  attn_simt_dkv_kernel<T><<<grid, 256, smem_kv, st>>>(a);
-  MTGR_TRY(check_launch("attn_simt_dkv"));
+  {
+    ProfScope ps(PROF_ATTN_DV, st);
+    cudaFuncSetAttribute(attn_simt_dkv_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_kv);
+    attn_simt_dkv_kernel<T><<<grid, 256, smem_kv, st>>>(a);
+    MTGR_TRY(check_launch("attn_simt_dkv"));
+  }
+  ProfScope ps(PROF_ATTN_DQ, st);
   size_t smem_q = (4 * SA_B * a.dh + SA_B * (SA_B + 1)) * sizeof(float) + SA_B * sizeof(long long);
   cudaFuncSetAttribute(attn_simt_dq_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_q);
   attn_simt_dq_kernel<T><<<grid, 256, smem_q, st>>>(a);

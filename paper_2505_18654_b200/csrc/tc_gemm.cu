@@ -18,6 +18,7 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "prof.h"
 #include "sm100.cuh"
 
 namespace mtgr {
@@ -355,6 +356,8 @@ mtgr_status_t gemm_bf16_launch(const GemmIO& g, int epi, void* ws, size_t ws_byt
   }
   const int total = p.num_m * p.num_n * p.num_splits;
   const int grid = std::min(total, num_sms());
+  ProfScope ps(epi == EPI_QKVU ? PROF_GEMM_QKVU : epi == EPI_RESID ? PROF_GEMM_OUT
+               : epi == EPI_STORE ? PROF_GEMM_DGRAD : PROF_GEMM_WGRAD, st);
   auto launch = [&](auto kern) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     kern<<<grid, NTHREADS, SMEM_BYTES, st>>>(ta, tb, p);
