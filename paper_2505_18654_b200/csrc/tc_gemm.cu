@@ -24,12 +24,16 @@
 namespace mtgr {
 namespace tcg {
 
-constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
+constexpr int BM = 128, BN = 256, BK = 64, STAGES = 3;
 constexpr int A_BYTES = BM * BK * 2;
 constexpr int B_BYTES = BN * BK * 2;
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
-constexpr int NTHREADS = 256;
+constexpr int NUM_EPI_WARPS = 8;                     // 2 per TMEM lane quadrant
+constexpr int STG_BYTES = 2 * 32 * 128;              // per epilogue warp: 2 x [32 rows][64 bf16]
+constexpr int OFF_STG = STAGES * STAGE_BYTES;
+constexpr int OFF_BAR = OFF_STG + NUM_EPI_WARPS * STG_BYTES;
+constexpr int SMEM_BYTES = OFF_BAR + 512 + 1024;
+constexpr int NTHREADS = 128 + 32 * NUM_EPI_WARPS;
 
 struct Params {
   int M, N, K;
@@ -37,10 +41,7 @@ struct Params {
   int a_mn, b_mn;
   void* C;
   int64_t ldc;
-  void* C2;
   const float* bias;
-  const __nv_bfloat16* R;
-  int64_t ldr;
   float* part;  // split-K partials [splits][M][N]
   int accumulate;
   int silu;
@@ -50,34 +51,48 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&h);
 }
+__device__ __forceinline__ float silu_tanh(float x) {
+  const float h = 0.5f * x;
+  return fmaf(h, sm100::tanh_approx(h), h);
+}
 
+// Epilogue layout: epilogue warp ew (warps 4..11) owns TMEM lane quadrant q = warp % 4 (rows
+// q*32..q*32+31 of the tile) and column half ew / 4; it drains two 64-column chunks per tile:
+// tcgen05.ld -> fused math -> bf16 into a SWIZZLE_128B smem staging tile [32][64] ->
+// TMA store (bulk group).  The residual tile is TMA-loaded into the same staging buffer.
 template <int EPI>
 __global__ void __launch_bounds__(NTHREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   Params p) {
+                   const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmC2,
+                   const __grid_constant__ CUtensorMap tmR, Params p) {
   using namespace sm100;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* rbar = tempty + 2;  // [NUM_EPI_WARPS]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rbar + NUM_EPI_WARPS);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
+    if (EPI != EPI_F32) tma_prefetch(&tmC);
+    if (EPI == EPI_QKVU) tma_prefetch(&tmC2);
+    if (EPI == EPI_RESID) tma_prefetch(&tmR);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], 128);
+      mbar_init(&tempty[b], 32 * NUM_EPI_WARPS);
     }
+    for (int w = 0; w < NUM_EPI_WARPS; ++w) mbar_init(&rbar[w], 1);
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc<512>(tmem_slot);
@@ -151,8 +166,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       }
     }
   } else if (warp >= 4) {
-    const int q = warp - 4;
-    const int row = q * 32 + lane;
+    const int ew = warp - 4;
+    const int q = warp & 3;
+    const int hf = ew >> 2;
+    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+    uint8_t* stg = smem + OFF_STG + ew * STG_BYTES;
+    uint8_t* srow = stg + lane * 128;
+    uint32_t rphase = 0;
     int it = 0;
     for (int item = blockIdx.x; item < total; item += gridDim.x, ++it) {
       const int nb = item % p.num_n, rest = item / p.num_n;
@@ -161,95 +181,118 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       const uint32_t acc_phase = (it >> 1) & 1;
       mbar_wait(&tfull[buf], acc_phase);
       tc_fence_after();
-      const int m = mb * BM + row;
-      const bool row_ok = m < p.M;
+      const int m0 = mb * BM + q * 32;
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
-        uint32_t r[32];
-        tmem_ld32(tmem + buf * BN + c * 32 + ((uint32_t)(q * 32) << 16), r);
+      for (int c = 0; c < 2; ++c) {
+        const int col = hf * 128 + c * 64;
+        const int n0 = nb * BN + col;
+        uint32_t r0[32], r1[32];
+        tmem_ld32(tmem + buf * BN + col + lane_off, r0);
+        tmem_ld32(tmem + buf * BN + col + 32 + lane_off, r1);
         tmem_ld_wait();
-        const int n0 = nb * BN + c * 32;
-        if (!row_ok || n0 >= p.N) continue;
-        float v[32];
+        if (c == 1) {
+          tc_fence_before();
+          mbar_arrive(&tempty[buf]);
+        }
+        if (n0 >= p.N || m0 >= p.M) continue;  // warp-uniform
+        float v[64];
 #pragma unroll
-        for (int e = 0; e < 32; ++e) v[e] = __uint_as_float(r[e]);
-        const bool full_chunk = n0 + 32 <= p.N;
+        for (int e = 0; e < 32; ++e) {
+          v[e] = __uint_as_float(r0[e]);
+          v[32 + e] = __uint_as_float(r1[e]);
+        }
         if (EPI == EPI_F32) {
-          float* dst;
-          bool acc = false;
-          if (p.num_splits > 1) {
-            dst = p.part + ((int64_t)sp * p.M + m) * p.N + n0;
-          } else {
-            dst = (float*)p.C + (int64_t)m * p.ldc + n0;
-            acc = p.accumulate;
-          }
-          if (full_chunk) {
-#pragma unroll
-            for (int e = 0; e < 32; e += 4) {
-              float4 o = make_float4(v[e], v[e + 1], v[e + 2], v[e + 3]);
-              if (acc) {
-                float4 old = *reinterpret_cast<float4*>(dst + e);
-                o.x += old.x; o.y += old.y; o.z += old.z; o.w += old.w;
-              }
-              *reinterpret_cast<float4*>(dst + e) = o;
+          const int m = m0 + lane;
+          if (m < p.M) {
+            float* dst;
+            bool acc = false;
+            if (p.num_splits > 1) {
+              dst = p.part + ((int64_t)sp * p.M + m) * p.N + n0;
+            } else {
+              dst = (float*)p.C + (int64_t)m * p.ldc + n0;
+              acc = p.accumulate;
             }
-          } else {
-            for (int e = 0; e < 32 && n0 + e < p.N; ++e) dst[e] = acc ? dst[e] + v[e] : v[e];
-          }
-        } else {
-          if (p.bias) {
+            if (n0 + 64 <= p.N) {
 #pragma unroll
-            for (int e = 0; e < 32; ++e) v[e] += (n0 + e < p.N) ? __ldg(p.bias + n0 + e) : 0.f;
-          }
-          if (EPI == EPI_RESID) {
-            const __nv_bfloat16* rr = p.R + (int64_t)m * p.ldr + n0;
-            if (full_chunk) {
-#pragma unroll
-              for (int e = 0; e < 32; e += 8) {
-                uint4 u = *reinterpret_cast<const uint4*>(rr + e);
-                const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                  float2 f = __bfloat1622float2(h[i]);
-                  v[e + 2 * i] += f.x;
-                  v[e + 2 * i + 1] += f.y;
+              for (int e = 0; e < 64; e += 4) {
+                float4 o = make_float4(v[e], v[e + 1], v[e + 2], v[e + 3]);
+                if (acc) {
+                  const float4 old = *reinterpret_cast<const float4*>(dst + e);
+                  o.x += old.x; o.y += old.y; o.z += old.z; o.w += old.w;
                 }
+                *reinterpret_cast<float4*>(dst + e) = o;
               }
             } else {
-              for (int e = 0; e < 32 && n0 + e < p.N; ++e) v[e] += __bfloat162float(rr[e]);
+#pragma unroll
+              for (int e = 0; e < 64; ++e)
+                if (n0 + e < p.N) dst[e] = acc ? dst[e] + v[e] : v[e];
             }
           }
-          __nv_bfloat16* dst = (__nv_bfloat16*)p.C + (int64_t)m * p.ldc + n0;
-          if (full_chunk) {
+          continue;
+        }
+        if (p.bias) {
+          if (n0 + 64 <= p.N) {
+            const float4* b4 = reinterpret_cast<const float4*>(p.bias + n0);
 #pragma unroll
-            for (int e = 0; e < 32; e += 8) {
-              uint4 u = make_uint4(pack_bf16(v[e], v[e + 1]), pack_bf16(v[e + 2], v[e + 3]),
-                                   pack_bf16(v[e + 4], v[e + 5]), pack_bf16(v[e + 6], v[e + 7]));
-              *reinterpret_cast<uint4*>(dst + e) = u;
+            for (int e = 0; e < 16; ++e) {
+              const float4 b = __ldg(b4 + e);
+              v[4 * e] += b.x; v[4 * e + 1] += b.y; v[4 * e + 2] += b.z; v[4 * e + 3] += b.w;
             }
           } else {
-            for (int e = 0; e < 32 && n0 + e < p.N; ++e) dst[e] = __float2bfloat16_rn(v[e]);
+#pragma unroll
+            for (int e = 0; e < 64; ++e) v[e] += (n0 + e < p.N) ? __ldg(p.bias + n0 + e) : 0.f;
           }
-          if (EPI == EPI_QKVU) {
-            __nv_bfloat16* dst2 = (__nv_bfloat16*)p.C2 + (int64_t)m * p.ldc + n0;
+        }
+        // the previous TMA store of this warp must have finished reading the staging tile
+        if (lane == 0) tma_store_wait_read<0>();
+        __syncwarp();
+        if (EPI == EPI_RESID) {
+          if (lane == 0) {
+            mbar_expect_tx(&rbar[ew], 32 * 128);
+            tma_load_2d(stg, &tmR, &rbar[ew], n0, m0);
+          }
+          mbar_wait(&rbar[ew], rphase);
+          rphase ^= 1;
 #pragma unroll
-            for (int e = 0; e < 32; ++e) v[e] = p.silu ? silu_f(v[e]) : v[e];
-            if (full_chunk) {
+          for (int j = 0; j < 8; ++j) {
+            const uint4 w = *reinterpret_cast<const uint4*>(srow + ((j ^ (lane & 7)) << 4));
+            const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&w);
 #pragma unroll
-              for (int e = 0; e < 32; e += 8) {
-                uint4 u = make_uint4(pack_bf16(v[e], v[e + 1]), pack_bf16(v[e + 2], v[e + 3]),
-                                     pack_bf16(v[e + 4], v[e + 5]), pack_bf16(v[e + 6], v[e + 7]));
-                *reinterpret_cast<uint4*>(dst2 + e) = u;
-              }
-            } else {
-              for (int e = 0; e < 32 && n0 + e < p.N; ++e) dst2[e] = __float2bfloat16_rn(v[e]);
+            for (int k = 0; k < 4; ++k) {
+              const float2 f = __bfloat1622float2(h2[k]);
+              v[8 * j + 2 * k] += f.x;
+              v[8 * j + 2 * k + 1] += f.y;
             }
           }
         }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const uint4 w = make_uint4(pack_bf16(v[8 * j], v[8 * j + 1]), pack_bf16(v[8 * j + 2], v[8 * j + 3]),
+                                     pack_bf16(v[8 * j + 4], v[8 * j + 5]), pack_bf16(v[8 * j + 6], v[8 * j + 7]));
+          *reinterpret_cast<uint4*>(srow + ((j ^ (lane & 7)) << 4)) = w;
+        }
+        if (EPI == EPI_QKVU) {
+          uint8_t* srow2 = srow + 32 * 128;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            float a[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) a[k] = p.silu ? silu_tanh(v[8 * j + k]) : v[8 * j + k];
+            const uint4 w = make_uint4(pack_bf16(a[0], a[1]), pack_bf16(a[2], a[3]),
+                                       pack_bf16(a[4], a[5]), pack_bf16(a[6], a[7]));
+            *reinterpret_cast<uint4*>(srow2 + ((j ^ (lane & 7)) << 4)) = w;
+          }
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_2d(&tmC, stg, n0, m0);
+          if (EPI == EPI_QKVU) tma_store_2d(&tmC2, stg + 32 * 128, n0, m0);
+          tma_store_commit();
+        }
       }
-      tc_fence_before();
-      mbar_arrive(&tempty[buf]);
     }
+    if (lane == 0) tma_store_wait<0>();
   }
   __syncthreads();
   if (warp == 2) {
@@ -334,21 +377,25 @@ mtgr_status_t gemm_bf16_launch(const GemmIO& g, int epi, void* ws, size_t ws_byt
   MTGR_CHECK(g.lda % 8 == 0 && g.ldb % 8 == 0 && aligned16(g.A) && aligned16(g.B), MTGR_E_LAYOUT,
              "tc gemm: operands need 16-byte aligned rows (ld %% 8 == 0)");
   MTGR_CHECK(g.ldc % 8 == 0 && aligned16(g.C) && (!g.C2 || aligned16(g.C2)) &&
-                 (!g.R || (g.ldr % 8 == 0 && aligned16(g.R))),
+                 (!g.R || (g.ldr % 8 == 0 && aligned16(g.R))) && (!g.bias || aligned16(g.bias)),
              MTGR_E_LAYOUT, "tc gemm: outputs need 16-byte aligned rows");
   CUtensorMap ta, tb;
   if (g.a_kmajor) MTGR_TRY(make_tmap_bf16(&ta, g.A, g.K, g.M, g.lda, 64, BM));
   else MTGR_TRY(make_tmap_bf16(&ta, g.A, g.M, g.K, g.lda, 64, 64));
   if (g.b_kmajor) MTGR_TRY(make_tmap_bf16(&tb, g.B, g.K, g.N, g.ldb, 64, BN));
   else MTGR_TRY(make_tmap_bf16(&tb, g.B, g.N, g.K, g.ldb, 64, 64));
+  CUtensorMap tc = ta, tc2 = ta, tr = ta;
+  if (epi != EPI_F32) MTGR_TRY(make_tmap_bf16(&tc, g.C, g.N, g.M, g.ldc, 64, 32));
+  if (epi == EPI_QKVU) MTGR_TRY(make_tmap_bf16(&tc2, g.C2, g.N, g.M, g.ldc, 64, 32));
+  if (epi == EPI_RESID) MTGR_TRY(make_tmap_bf16(&tr, g.R, g.N, g.M, g.ldr, 64, 32));
   Params p{};
   p.M = g.M; p.N = g.N; p.K = g.K;
   p.num_m = ceil_div(g.M, BM); p.num_n = ceil_div(g.N, BN); p.num_kb = ceil_div(g.K, BK);
   Split s = choose_split(g.M, g.N, g.K, epi);
   p.num_splits = s.splits; p.kb_per_split = s.kb_per_split;
   p.a_mn = g.a_kmajor ? 0 : 1; p.b_mn = g.b_kmajor ? 0 : 1;
-  p.C = g.C; p.ldc = g.ldc; p.C2 = g.C2; p.bias = g.bias;
-  p.R = (const __nv_bfloat16*)g.R; p.ldr = g.ldr; p.accumulate = g.accumulate; p.silu = g.silu;
+  p.C = g.C; p.ldc = g.ldc; p.bias = g.bias;
+  p.accumulate = g.accumulate; p.silu = g.silu;
   if (epi == EPI_F32 && s.splits > 1) {
     MTGR_CHECK(ws && ws_bytes >= gemm_ws_bytes(g.M, g.N, g.K, epi, true), MTGR_E_WORKSPACE,
                "tc gemm: split-K workspace too small");
@@ -360,7 +407,7 @@ mtgr_status_t gemm_bf16_launch(const GemmIO& g, int epi, void* ws, size_t ws_byt
                : epi == EPI_STORE ? PROF_GEMM_DGRAD : PROF_GEMM_WGRAD, st);
   auto launch = [&](auto kern) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-    kern<<<grid, NTHREADS, SMEM_BYTES, st>>>(ta, tb, p);
+    kern<<<grid, NTHREADS, SMEM_BYTES, st>>>(ta, tb, tc, tc2, tr, p);
   };
   switch (epi) {
     case EPI_STORE: launch(gemm_tc_kernel<EPI_STORE>); break;
