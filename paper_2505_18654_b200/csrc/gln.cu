@@ -7,13 +7,13 @@
 //  * MODE_RESID: the residual of Eq.6 (dx = GLN1_bwd(dX~) + dZ).
 // Parameter gradients are per-block partial sums (smem) reduced in block order by a second
 // kernel.
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.h"
 #include "prof.h"
 
 namespace mtgr {
-
-constexpr int GLN_MAXC = 4;  // chunks of 8 per lane -> d <= 1024
 
 __device__ __forceinline__ void load8(const float* p, float* v) {
   float4 a = reinterpret_cast<const float4*>(p)[0];
@@ -47,7 +47,7 @@ __device__ __forceinline__ float warp_sum(float v) {
   return v;
 }
 
-template <class T>
+template <class T, int NC>
 __global__ void __launch_bounds__(256) gln_fwd_kernel(const T* __restrict__ x,
                                                       const uint8_t* __restrict__ gid,
                                                       const float* __restrict__ gamma,
@@ -60,11 +60,11 @@ __global__ void __launch_bounds__(256) gln_fwd_kernel(const T* __restrict__ x,
   const int nch = d >> 3;
   const float inv_d = 1.0f / (float)d;
   for (int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); t < ntok; t += nwarps) {
-    float v[GLN_MAXC][8];
+    float v[NC][8];
     float s = 0.f;
     const T* xr = x + (int64_t)t * d;
 #pragma unroll
-    for (int k = 0; k < GLN_MAXC; ++k) {
+    for (int k = 0; k < NC; ++k) {
       int c = lane + 32 * k;
       if (c < nch) {
         load8(xr + c * 8, v[k]);
@@ -75,7 +75,7 @@ __global__ void __launch_bounds__(256) gln_fwd_kernel(const T* __restrict__ x,
     const float mu = warp_sum(s) * inv_d;
     float q = 0.f;
 #pragma unroll
-    for (int k = 0; k < GLN_MAXC; ++k)
+    for (int k = 0; k < NC; ++k)
       if (lane + 32 * k < nch) {
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
@@ -90,7 +90,7 @@ __global__ void __launch_bounds__(256) gln_fwd_kernel(const T* __restrict__ x,
     const float* br = beta + (int64_t)g * d;
     T* yr = y + (int64_t)t * d;
 #pragma unroll
-    for (int k = 0; k < GLN_MAXC; ++k) {
+    for (int k = 0; k < NC; ++k) {
       int c = lane + 32 * k;
       if (c < nch) {
         float gg[8], bb[8], o[8];
@@ -119,8 +119,8 @@ struct GlnBwdArgs {
   const float* gamma;
   const uint8_t* gid;
   T* dx;          // GLN_GATE: dO
-  float* part;    // [nblocks][G][2][d]
-  int ntok, d, G, tok_per_block;
+  float* part;    // [G][2][d] fp32 accumulators (zeroed by the launcher)
+  int ntok, d, G, tok_per_warp;
   // GLN_GATE
   const T* o;     // [T][d]
   const T* u;     // rows ld_a
@@ -132,78 +132,61 @@ struct GlnBwdArgs {
   const T* dz;
 };
 
-template <class T, int MODE>
-__global__ void __launch_bounds__(256) gln_bwd_kernel(GlnBwdArgs<T> a) {
+constexpr int GLNB_WARPS = 4;
+
+// One warp per token (contiguous token range per warp).  Parameter-gradient contributions
+// dgamma[g] += dy*xhat, dbeta[g] += dy go to the block's smem accumulator [G][2][d]
+// (shared-memory reductions), written out as a per-block partial.
+template <class T, int MODE, int NC>
+__global__ void __launch_bounds__(32 * GLNB_WARPS, (NC <= 2 ? 6 : 4)) gln_bwd_kernel(GlnBwdArgs<T> a) {
   extern __shared__ float sacc[];  // [G][2][d]
   const int d = a.d, G = a.G;
   for (int i = threadIdx.x; i < G * 2 * d; i += blockDim.x) sacc[i] = 0.f;
   __syncthreads();
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nch = d >> 3;
   const float inv_d = 1.0f / (float)d;
-  const int t_begin = blockIdx.x * a.tok_per_block;
-  const int t_end = min(a.ntok, t_begin + a.tok_per_block);
-  // each warp owns a contiguous token sub-range; running per-group partials in registers
-  const int per_w = (a.tok_per_block + nw - 1) / nw;
-  const int w_begin = t_begin + warp * per_w;
-  const int w_end = min(t_end, w_begin + per_w);
-  float pg[GLN_MAXC][8], pb[GLN_MAXC][8];
-  int cur_g = -1;
-  auto flush = [&]() {
-    if (cur_g < 0) return;
-#pragma unroll
-    for (int k = 0; k < GLN_MAXC; ++k) {
-      int c = lane + 32 * k;
-      if (c < nch) {
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          atomicAdd(&sacc[(cur_g * 2 + 0) * d + c * 8 + e], pg[k][e]);
-          atomicAdd(&sacc[(cur_g * 2 + 1) * d + c * 8 + e], pb[k][e]);
-        }
-      }
-    }
-  };
+  const int w_begin = (blockIdx.x * GLNB_WARPS + warp) * a.tok_per_warp;
+  const int w_end = min(a.ntok, w_begin + a.tok_per_warp);
+#pragma unroll 2
   for (int t = w_begin; t < w_end; ++t) {
     const int g = a.gid[t];
-    if (g != cur_g) {
-      flush();
-      cur_g = g;
-#pragma unroll
-      for (int k = 0; k < GLN_MAXC; ++k)
-#pragma unroll
-        for (int e = 0; e < 8; ++e) pg[k][e] = pb[k][e] = 0.f;
-    }
     const float mu = a.mean[t], r = a.rstd[t];
     const float* gr = a.gamma + (int64_t)g * d;
-    float xh[GLN_MAXC][8], dxh[GLN_MAXC][8];
+    float xh[NC][8], dyv[NC][8];
     float s1 = 0.f, s2 = 0.f;
 #pragma unroll
-    for (int k = 0; k < GLN_MAXC; ++k) {
-      int c = lane + 32 * k;
+    for (int k = 0; k < NC; ++k) {
+      const int c = lane + 32 * k;
       if (c < nch) {
-        float xv[8], dyv[8], gg[8];
+        float xv[8], gg[8];
         load8(a.x + (int64_t)t * d + c * 8, xv);
-        load8(a.dy + (int64_t)t * d + c * 8, dyv);
+        load8(a.dy + (int64_t)t * d + c * 8, dyv[k]);
         load8(gr + c * 8, gg);
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
           xh[k][e] = (xv[e] - mu) * r;
-          dxh[k][e] = dyv[e] * gg[e];
-          pg[k][e] += dyv[e] * xh[k][e];
-          pb[k][e] += dyv[e];
-          s1 += dxh[k][e];
-          s2 += dxh[k][e] * xh[k][e];
+          const float dxh = dyv[k][e] * gg[e];
+          s1 += dxh;
+          s2 += dxh * xh[k][e];
         }
       }
     }
     const float m1 = warp_sum(s1) * inv_d, m2 = warp_sum(s2) * inv_d;
 #pragma unroll
-    for (int k = 0; k < GLN_MAXC; ++k) {
-      int c = lane + 32 * k;
+    for (int k = 0; k < NC; ++k) {
+      const int c = lane + 32 * k;
       if (c < nch) {
-        float o[8];
+        float gg[8], o[8];
+        load8(gr + c * 8, gg);
+        float* accg = sacc + (g * 2 + 0) * d + c * 8;
+        float* accb = sacc + (g * 2 + 1) * d + c * 8;
 #pragma unroll
-        for (int e = 0; e < 8; ++e) o[e] = r * (dxh[k][e] - m1 - xh[k][e] * m2);
+        for (int e = 0; e < 8; ++e) {
+          atomicAdd(accg + e, dyv[k][e] * xh[k][e]);
+          atomicAdd(accb + e, dyv[k][e]);
+          o[e] = r * (dyv[k][e] * gg[e] - m1 - xh[k][e] * m2);
+        }
         if (MODE == GLN_RESID) {
           float z[8];
           load8(a.dz + (int64_t)t * d + c * 8, z);
@@ -234,39 +217,48 @@ __global__ void __launch_bounds__(256) gln_bwd_kernel(GlnBwdArgs<T> a) {
       }
     }
   }
-  flush();
   __syncthreads();
-  float* dst = a.part + (int64_t)blockIdx.x * G * 2 * d;
-  for (int i = threadIdx.x; i < G * 2 * d; i += blockDim.x) dst[i] = sacc[i];
+  // block partial -> global accumulators [G][2][d] (red.global.add; order not deterministic)
+  for (int i = threadIdx.x; i < G * 2 * d; i += blockDim.x) {
+    const float v = sacc[i];
+    if (v != 0.f) atomicAdd(a.part + i, v);
+  }
 }
 
-// dgamma/dbeta[g][c] = sum over blocks (fixed order) of the partials
-__global__ void gln_param_reduce_kernel(const float* __restrict__ part, int nblocks, int G, int d,
+// dgamma/dbeta (+)= accumulators
+__global__ void gln_param_finish_kernel(const float* __restrict__ acc, int G, int d,
                                         float* __restrict__ dgamma, float* __restrict__ dbeta,
                                         int accumulate) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;  // over G*2*d
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= G * 2 * d) return;
-  float s = 0.f;
-  for (int b = 0; b < nblocks; ++b) s += part[(int64_t)b * G * 2 * d + i];
-  int g = i / (2 * d), w = (i / d) & 1, c = i % d;
+  const int g = i / (2 * d), w = (i / d) & 1, c = i % d;
   float* out = (w == 0 ? dgamma : dbeta) + g * d + c;
-  *out = accumulate ? *out + s : s;
+  *out = accumulate ? *out + acc[i] : acc[i];
 }
 
 // ------------------------------------------------------------------ host launchers
 
+static int gln_nc(int d) { return (d + 255) / 256; }  // 8-element chunks per lane
+
+static int gln_bwd_tok_per_warp(int ntok) {
+  const int warps_wanted = 16 * num_sms() * GLNB_WARPS;  // ~16 blocks per SM worth of work
+  int tpw = ceil_div(ntok > 0 ? ntok : 1, warps_wanted);
+  return std::max(tpw, 32);
+}
 static int gln_bwd_blocks(int ntok) {
-  int nb = 2 * num_sms();
-  int per = ceil_div(ntok > 0 ? ntok : 1, nb);
-  if (per < 64) {
-    per = 64;
-    nb = ceil_div(ntok > 0 ? ntok : 1, per);
-  }
-  return nb;
+  return ceil_div(ceil_div(ntok > 0 ? ntok : 1, gln_bwd_tok_per_warp(ntok)), GLNB_WARPS);
 }
 
 size_t gln_bwd_ws_bytes(int ntok, int d, int G) {
-  return align_up((size_t)gln_bwd_blocks(ntok) * G * 2 * d * sizeof(float), 256);
+  (void)ntok;
+  return align_up((size_t)G * 2 * d * sizeof(float), 256);
+}
+
+template <class T, int NC>
+static void gln_fwd_go(const T* x, const uint8_t* gid, const float* gamma, const float* beta, T* y,
+                       float* mean, float* rstd, int ntok, int d, float eps, cudaStream_t st) {
+  int blocks = min(ceil_div(ntok, 8), 16 * num_sms());
+  gln_fwd_kernel<T, NC><<<blocks, 256, 0, st>>>(x, gid, gamma, beta, y, mean, rstd, ntok, d, eps);
 }
 
 template <class T>
@@ -275,9 +267,29 @@ mtgr_status_t gln_fwd_launch(const T* x, const uint8_t* gid, const float* gamma,
                              float eps, cudaStream_t st) {
   if (ntok == 0) return MTGR_OK;
   ProfScope ps(PROF_GLN_FWD, st);
-  int blocks = min(ceil_div(ntok, 8), 8 * num_sms());
-  gln_fwd_kernel<T><<<blocks, 256, 0, st>>>(x, gid, gamma, beta, y, mean, rstd, ntok, d, eps);
+  switch (gln_nc(d)) {
+    case 1: gln_fwd_go<T, 1>(x, gid, gamma, beta, y, mean, rstd, ntok, d, eps, st); break;
+    case 2: gln_fwd_go<T, 2>(x, gid, gamma, beta, y, mean, rstd, ntok, d, eps, st); break;
+    case 3: gln_fwd_go<T, 3>(x, gid, gamma, beta, y, mean, rstd, ntok, d, eps, st); break;
+    default: gln_fwd_go<T, 4>(x, gid, gamma, beta, y, mean, rstd, ntok, d, eps, st); break;
+  }
   return check_launch("gln_fwd");
+}
+
+template <class T, int MODE, int NC>
+static void gln_bwd_go(const GlnBwdArgs<T>& a, int nb, size_t smem, cudaStream_t st) {
+  cudaFuncSetAttribute(gln_bwd_kernel<T, MODE, NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  gln_bwd_kernel<T, MODE, NC><<<nb, 32 * GLNB_WARPS, smem, st>>>(a);
+}
+
+template <class T, int MODE>
+static void gln_bwd_mode(const GlnBwdArgs<T>& a, int nb, size_t smem, cudaStream_t st) {
+  switch (gln_nc(a.d)) {
+    case 1: gln_bwd_go<T, MODE, 1>(a, nb, smem, st); break;
+    case 2: gln_bwd_go<T, MODE, 2>(a, nb, smem, st); break;
+    case 3: gln_bwd_go<T, MODE, 3>(a, nb, smem, st); break;
+    default: gln_bwd_go<T, MODE, 4>(a, nb, smem, st); break;
+  }
 }
 
 template <class T>
@@ -290,28 +302,20 @@ mtgr_status_t gln_bwd_launch(const GlnBwdIO& io, int mode, float* part, float* d
   a.ntok = io.ntok; a.d = io.d; a.G = io.G;
   a.o = (const T*)io.o; a.u = (const T*)io.u; a.pre_u = (const T*)io.pre_u; a.ld_a = io.ld_a;
   a.dpu = (T*)io.dpu; a.ld_dp = io.ld_dp; a.dz = (const T*)io.dz;
-  int nb = gln_bwd_blocks(io.ntok);
-  a.tok_per_block = ceil_div(io.ntok > 0 ? io.ntok : 1, nb);
+  a.tok_per_warp = gln_bwd_tok_per_warp(io.ntok);
+  int nb = io.ntok > 0 ? gln_bwd_blocks(io.ntok) : 0;
   size_t smem = (size_t)io.G * 2 * io.d * sizeof(float);
-  if (io.ntok > 0) {
-    if (mode == GLN_GATE) {
-      cudaFuncSetAttribute(gln_bwd_kernel<T, GLN_GATE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      gln_bwd_kernel<T, GLN_GATE><<<nb, 256, smem, st>>>(a);
-    } else if (mode == GLN_RESID) {
-      cudaFuncSetAttribute(gln_bwd_kernel<T, GLN_RESID>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      gln_bwd_kernel<T, GLN_RESID><<<nb, 256, smem, st>>>(a);
-    } else {
-      cudaFuncSetAttribute(gln_bwd_kernel<T, GLN_PLAIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      gln_bwd_kernel<T, GLN_PLAIN><<<nb, 256, smem, st>>>(a);
-    }
+  cudaMemsetAsync(part, 0, smem, st);
+  if (nb > 0) {
+    if (mode == GLN_GATE) gln_bwd_mode<T, GLN_GATE>(a, nb, smem, st);
+    else if (mode == GLN_RESID) gln_bwd_mode<T, GLN_RESID>(a, nb, smem, st);
+    else gln_bwd_mode<T, GLN_PLAIN>(a, nb, smem, st);
     MTGR_TRY(check_launch("gln_bwd"));
-  } else {
-    nb = 0;
   }
   int n = io.G * 2 * io.d;
-  gln_param_reduce_kernel<<<ceil_div(n, 256), 256, 0, st>>>(part, nb, io.G, io.d, dgamma, dbeta,
+  gln_param_finish_kernel<<<ceil_div(n, 256), 256, 0, st>>>(part, io.G, io.d, dgamma, dbeta,
                                                             accumulate);
-  return check_launch("gln_param_reduce");
+  return check_launch("gln_param_finish");
 }
 
 template mtgr_status_t gln_fwd_launch<float>(const float*, const uint8_t*, const float*,

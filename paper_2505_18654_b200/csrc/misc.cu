@@ -7,26 +7,60 @@
 namespace mtgr {
 
 // ------------------------------------------------------------------ column sums (db = sum_t dY)
-constexpr int CS_ROWS = 256;  // tokens per partial
+constexpr int CS_ROWS = 128;  // tokens per partial
 
-template <class T>
-__global__ void colsum_part_kernel(const T* __restrict__ X, int64_t ld, int ntok, int n,
-                                   float* __restrict__ part) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= n) return;
-  const int r0 = blockIdx.y * CS_ROWS, r1 = min(ntok, r0 + CS_ROWS);
-  float s = 0.f;
-  for (int r = r0; r < r1; ++r) s += to_f(X[(int64_t)r * ld + c]);
-  part[(int64_t)blockIdx.y * n + c] = s;
+__device__ __forceinline__ void cs_load8(const float* p, float* v) {
+  const float4 a = reinterpret_cast<const float4*>(p)[0], b = reinterpret_cast<const float4*>(p)[1];
+  v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+}
+__device__ __forceinline__ void cs_load8(const __nv_bfloat16* p, float* v) {
+  const uint4 a = *reinterpret_cast<const uint4*>(p);
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&a);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 f = __bfloat1622float2(h[i]);
+    v[2 * i] = f.x; v[2 * i + 1] = f.y;
+  }
 }
 
-__global__ void colsum_reduce_kernel(const float* __restrict__ part, int nparts, int n,
-                                     float* __restrict__ out, int accumulate) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= n) return;
+// thread = 8 consecutive columns (16-byte loads), block.y = CS_ROWS tokens
+template <class T>
+__global__ void __launch_bounds__(256) colsum_part_kernel(const T* __restrict__ X, int64_t ld,
+                                                          int ntok, int n, float* __restrict__ part) {
+  const int c0 = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
+  if (c0 >= n) return;
+  const int r0 = blockIdx.y * CS_ROWS, r1 = min(ntok, r0 + CS_ROWS);
+  float s[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll 8
+  for (int r = r0; r < r1; ++r) {
+    float v[8];
+    cs_load8(X + (int64_t)r * ld + c0, v);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) s[e] += v[e];
+  }
+  float* dst = part + (int64_t)blockIdx.y * n + c0;
+  reinterpret_cast<float4*>(dst)[0] = make_float4(s[0], s[1], s[2], s[3]);
+  reinterpret_cast<float4*>(dst)[1] = make_float4(s[4], s[5], s[6], s[7]);
+}
+
+// fixed-order two-level sum of the partials (deterministic)
+__global__ void __launch_bounds__(256) colsum_reduce_kernel(const float* __restrict__ part,
+                                                            int nparts, int n,
+                                                            float* __restrict__ out, int accumulate) {
+  __shared__ float red[8][33];
+  const int col = blockIdx.x * 32 + (threadIdx.x & 31);
+  const int rg = threadIdx.x >> 5;
   float s = 0.f;
-  for (int p = 0; p < nparts; ++p) s += part[(int64_t)p * n + c];
-  out[c] = accumulate ? out[c] + s : s;
+  if (col < n)
+    for (int p = rg; p < nparts; p += 8) s += part[(int64_t)p * n + col];
+  red[rg][threadIdx.x & 31] = s;
+  __syncthreads();
+  if (rg == 0 && col < n) {
+    float t = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) t += red[k][threadIdx.x];
+    out[col] = accumulate ? out[col] + t : t;
+  }
 }
 
 size_t colsum_ws_bytes(int ntok, int n) {
@@ -37,12 +71,13 @@ template <class T>
 mtgr_status_t colsum_launch(const T* X, int64_t ld, int ntok, int n, float* out, float* part,
                             int accumulate, cudaStream_t st) {
   ProfScope ps(PROF_COLSUM, st);
+  MTGR_CHECK(n % 8 == 0 && ld % 8 == 0, MTGR_E_LAYOUT, "colsum: n and ld must be multiples of 8");
   int nparts = ntok > 0 ? ceil_div(ntok, CS_ROWS) : 0;
   if (nparts > 0) {
-    colsum_part_kernel<T><<<dim3(ceil_div(n, 128), nparts), 128, 0, st>>>(X, ld, ntok, n, part);
+    colsum_part_kernel<T><<<dim3(ceil_div(n, 8 * 256), nparts), 256, 0, st>>>(X, ld, ntok, n, part);
     MTGR_TRY(check_launch("colsum_part"));
   }
-  colsum_reduce_kernel<<<ceil_div(n, 128), 128, 0, st>>>(part, nparts, n, out, accumulate);
+  colsum_reduce_kernel<<<ceil_div(n, 32), 256, 0, st>>>(part, nparts, n, out, accumulate);
   return check_launch("colsum_reduce");
 }
 template mtgr_status_t colsum_launch<float>(const float*, int64_t, int, int, float*, float*, int,

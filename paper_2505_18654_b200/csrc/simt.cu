@@ -6,6 +6,8 @@
 //  * attention fwd / bwd (Eq.5) per (user, head, 32-row tile): exact mask predicate
 //    in registers (R#8-R#12), keys restricted to [0, n_static + n_rt) (candidate columns are
 //    visible only to themselves, rule 3 P:338, and enter through the diagonal term).
+#include <type_traits>
+
 #include "common.cuh"
 #include "kernels.h"
 #include "prof.h"
@@ -104,6 +106,23 @@ constexpr int SA_B = 32;  // rows per tile (queries or keys)
 // diagonal terms of non-static tokens (R#9): a_ii = nu*silu(s_ii), ds_ii = nu*silu'(s_ii)*(dO_i.v_i)
 // with s_ii = q_i.k_i (+ rab_w[h][0], the bucket of |dt| = 0).  One warp per token.
 template <class T>
+__device__ __forceinline__ void ld8f(const T* p, float* v) {
+  if constexpr (std::is_same<T, float>::value) {
+    const float4 a = reinterpret_cast<const float4*>(p)[0], b = reinterpret_cast<const float4*>(p)[1];
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+  } else {
+    const uint4 a = *reinterpret_cast<const uint4*>(p);
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&a);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float2 f = __bfloat1622float2(h[i]);
+      v[2 * i] = f.x; v[2 * i + 1] = f.y;
+    }
+  }
+}
+
+// one warp per token; lane c handles 8-element chunks c, c+32, ... of each head (16-byte loads)
+template <class T>
 __global__ void attn_diag_kernel(AttnIO a, int bwd, float* __restrict__ diag_a,
                                  float* __restrict__ diag_ds) {
   const int lane = threadIdx.x & 31;
@@ -112,6 +131,7 @@ __global__ void attn_diag_kernel(AttnIO a, int bwd, float* __restrict__ diag_a,
   const int nwarps = gridDim.x * (blockDim.x >> 5);
   const T* q = (const T*)a.q; const T* k = (const T*)a.k; const T* v = (const T*)a.v;
   const T* dO = (const T*)a.dO;
+  const int nch = a.dh >> 3;
   for (int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); t < ntok; t += nwarps) {
     // user of token t: last u with offsets[u] <= t
     int lo = 0, hi = B - 1;
@@ -119,15 +139,25 @@ __global__ void attn_diag_kernel(AttnIO a, int bwd, float* __restrict__ diag_a,
       int mid = (lo + hi + 1) >> 1;
       if (a.jag.offsets[mid] <= t) lo = mid; else hi = mid - 1;
     }
-    UserSpan us = load_user(a.jag, lo);
+    const UserSpan us = load_user(a.jag, lo);
     const bool nonstatic = (t - us.off) >= us.ns;
     for (int h = 0; h < a.H; ++h) {
       float s = 0.f, pv = 0.f;
       if (nonstatic) {
-        for (int c = lane; c < a.dh; c += 32) {
-          int64_t col = (int64_t)h * a.dh + c;
-          s += to_f(q[(int64_t)t * a.ld + col]) * to_f(k[(int64_t)t * a.ld + col]);
-          if (bwd) pv += to_f(dO[(int64_t)t * a.d + col]) * to_f(v[(int64_t)t * a.ld + col]);
+        for (int c = lane; c < nch; c += 32) {
+          const int64_t col = (int64_t)h * a.dh + c * 8;
+          float qa[8], ka[8];
+          ld8f(q + (int64_t)t * a.ld + col, qa);
+          ld8f(k + (int64_t)t * a.ld + col, ka);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) s = fmaf(qa[e], ka[e], s);
+          if (bwd) {
+            float da[8], va[8];
+            ld8f(dO + (int64_t)t * a.d + col, da);
+            ld8f(v + (int64_t)t * a.ld + col, va);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) pv = fmaf(da[e], va[e], pv);
+          }
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {

@@ -20,8 +20,8 @@
 // to themselves, rule 3 P:338) and to [0, n_static) when every row of the tile is static
 // (R#8), so fully masked tiles are never loaded.
 //
-// Warp roles (256 threads): w0 TMA producer, w1 MMA issuer, w2 TMEM allocator,
-// w4-w7 softmax/epilogue (thread = row = TMEM lane).  TMEM: R1 [0,128) (bf16 pairs),
+// Warp roles (384 threads): w0 TMA producer, w1 MMA issuer, w2 TMEM allocator,
+// w4-w11 softmax/epilogue (two warps per TMEM lane quadrant, thread = row = TMEM lane).  TMEM: R1 [0,128) (bf16 pairs),
 // acc [128,384), S buffers [384,512).
 #include <algorithm>
 
@@ -73,7 +73,7 @@ __device__ __forceinline__ uint32_t pack2(float a, float b) {
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(384, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tmC1, const __grid_constant__ CUtensorMap tmC2,
                    const __grid_constant__ CUtensorMap tmR2, Args a) {
   using namespace sm100;
@@ -120,10 +120,10 @@ __global__ void __launch_bounds__(256, 1)
     if (TWO) tma_prefetch(&tmR2);
     for (int s = 0; s < 3; ++s) { mbar_init(&kv_full[s], 1); mbar_init(&kv_empty[s], 1); }
     for (int b = 0; b < 2; ++b) {
-      mbar_init(&s_full[b], 1); mbar_init(&s_free[b], 128);
-      mbar_init(&t_full[b], 128); mbar_init(&t_free[b], 1);
+      mbar_init(&s_full[b], 1); mbar_init(&s_free[b], 256);
+      mbar_init(&t_full[b], 256); mbar_init(&t_free[b], 1);
     }
-    mbar_init(r1_ready, 128);
+    mbar_init(r1_ready, 256);
     mbar_init(r2_full, 1);
     mbar_init(o_full, 1);
     fence_barrier_init();
@@ -213,18 +213,21 @@ __global__ void __launch_bounds__(256, 1)
     }
   } else if (warp >= 4) {
     // ---------------------------------------------------------------- softmax + epilogue
-    const int q = warp - 4;
+    // 8 warps: quadrant q = warp % 4 owns TMEM lanes (rows) q*32..q*32+31; half = which 32 of the
+    // 64 tile columns (and which 128 of the 256 accumulator columns) the warp handles.
+    const int q = warp & 3;
+    const int half = (warp - 4) >> 2;
     const int row = q * 32 + lane;
     const int my = r0 + row;                 // user-local index of this thread's row
     const int64_t g = (int64_t)us.off + my;  // global token index
     const int T = a.jag.total_tokens;
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
-    // R1 row -> TMEM (bf16 pairs)
+    // R1 row (this warp's 128 head-dim columns) -> TMEM as bf16 pairs
 #pragma unroll 1
-    for (int cc = 0; cc < 4; ++cc) {
+    for (int cc = 0; cc < 2; ++cc) {
       uint32_t w[32];
       if (g < T) {
-        const uint4* src = reinterpret_cast<const uint4*>(a.r1 + g * a.ld_r1 + hcol + cc * 64);
+        const uint4* src = reinterpret_cast<const uint4*>(a.r1 + g * a.ld_r1 + hcol + half * 128 + cc * 64);
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
           uint4 v = __ldg(src + i);
@@ -234,7 +237,7 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
         for (int i = 0; i < 32; ++i) w[i] = 0u;
       }
-      tmem_st32(tmem + COL_R1 + cc * 32 + lane_off, w);
+      tmem_st32(tmem + COL_R1 + half * 64 + cc * 32 + lane_off, w);
     }
     tmem_st_wait();
     tc_fence_before();
@@ -242,87 +245,91 @@ __global__ void __launch_bounds__(256, 1)
 
     const long long my_ts = (my < us.L && a.jag.ts) ? a.jag.ts[g] : 0;
     const bool need_ts_rows = TRANS && (r0 + BR > us.ns) && (r0 < kv_end);
+    const int j_half = half * 32;
 #pragma unroll 1
     for (int t = 0; t < ntiles; ++t) {
       const int c0 = c_begin + t * BC;
       const bool need_ts = TRANS ? need_ts_rows : (c0 + BC > us.ns && c0 < kv_end);
       long long* tsb = sTs;
-      if (need_ts) {  // uniform over the 4 softmax warps
+      if (need_ts) {  // uniform over the 8 softmax warps
         const int i = threadIdx.x - 128;
-        named_bar_sync(1, 128);  // everyone is done reading the previous tile's times
+        named_bar_sync(1, 256);  // everyone is done reading the previous tile's times
         if (i < BC) tsb[i] = (c0 + i < us.L && a.jag.ts) ? a.jag.ts[us.off + c0 + i] : 0;
-        named_bar_sync(1, 128);
+        named_bar_sync(1, 256);
       }
       const int sb = TWO ? 0 : (t & 1);
       const int use = TWO ? t : (t >> 1);
       mbar_wait(&s_full[sb], use & 1);
       tc_fence_after();
-      uint32_t s[64];
-      uint32_t dp[TWO ? 64 : 1];
-      {
-        uint32_t (&s0)[32] = *reinterpret_cast<uint32_t(*)[32]>(&s[0]);
-        uint32_t (&s1)[32] = *reinterpret_cast<uint32_t(*)[32]>(&s[32]);
-        tmem_ld32(tmem + COL_S + sb * BC + lane_off, s0);
-        tmem_ld32(tmem + COL_S + sb * BC + 32 + lane_off, s1);
-        if constexpr (TWO) {
-          uint32_t (&d0)[32] = *reinterpret_cast<uint32_t(*)[32]>(&dp[0]);
-          uint32_t (&d1)[32] = *reinterpret_cast<uint32_t(*)[32]>(&dp[TWO ? 32 : 0]);
-          tmem_ld32(tmem + COL_S + BC + lane_off, d0);
-          tmem_ld32(tmem + COL_S + BC + 32 + lane_off, d1);
-        }
+      uint32_t s[32];
+      uint32_t dp[TWO ? 32 : 1];
+      tmem_ld32(tmem + COL_S + sb * BC + j_half + lane_off, s);
+      if constexpr (TWO) {
+        uint32_t (&d0)[32] = *reinterpret_cast<uint32_t(*)[32]>(&dp[0]);
+        tmem_ld32(tmem + COL_S + BC + j_half + lane_off, d0);
       }
       tmem_ld_wait();
       tc_fence_before();
       mbar_arrive(&s_free[sb]);
-      // visibility of the 64 columns for this row (dynamic mask, R#8-R#12)
-      uint64_t vis;
+      // visibility of this warp's 32 columns for this row (dynamic mask, R#8-R#12)
+      const int cb = c0 + j_half;
+      uint32_t vis;
       if (!TRANS) {
-        if (c0 + BC <= us.ns) {
-          vis = ~0ull;
+        if (cb + 32 <= us.ns) {
+          vis = 0xffffffffu;
         } else {
           vis = 0;
           const bool rs = my < us.ns;
 #pragma unroll 8
-          for (int jj = 0; jj < BC; ++jj) {
-            const int j = c0 + jj;
-            const bool v = j < kv_end && (j < us.ns || (!rs && tsb[jj] < my_ts));
-            vis |= (uint64_t)v << jj;
+          for (int jj = 0; jj < 32; ++jj) {
+            const int j = cb + jj;
+            const bool v = j < kv_end && (j < us.ns || (!rs && tsb[j_half + jj] < my_ts));
+            vis |= (uint32_t)v << jj;
           }
         }
       } else {
         if (my < us.ns) {
-          const int nvalid = us.L - c0;
-          vis = nvalid >= BC ? ~0ull : (nvalid <= 0 ? 0ull : ((1ull << nvalid) - 1));
+          const int nvalid = us.L - cb;
+          vis = nvalid >= 32 ? 0xffffffffu : (nvalid <= 0 ? 0u : ((1u << nvalid) - 1u));
         } else if (my < kv_end) {
           vis = 0;
 #pragma unroll 8
-          for (int jj = 0; jj < BC; ++jj) {
-            const int i = c0 + jj;
-            const bool v = i < us.L && i >= us.ns && my_ts < tsb[jj];
-            vis |= (uint64_t)v << jj;
+          for (int jj = 0; jj < 32; ++jj) {
+            const int i = cb + jj;
+            const bool v = i < us.L && i >= us.ns && my_ts < tsb[j_half + jj];
+            vis |= (uint32_t)v << jj;
           }
         } else {
           vis = 0;
         }
       }
-      // T tile values -> bf16 -> swizzled smem (row = 128 B, 16-byte chunk c at c ^ (row & 7))
+      // T values -> bf16 -> swizzled smem (row = 128 B, 16-byte chunk c at c ^ (row & 7))
+      uint32_t pk[16];
+#pragma unroll
+      for (int e = 0; e < 32; e += 2) {
+        const float s0 = __uint_as_float(s[e]), s1 = __uint_as_float(s[e + 1]);
+        float v0, v1;
+        if constexpr (TWO) {
+          v0 = __uint_as_float(dp[e]) * dsilu_fast(s0);
+          v1 = __uint_as_float(dp[e + 1]) * dsilu_fast(s1);
+        } else {
+          v0 = silu_fast(s0);
+          v1 = silu_fast(s1);
+        }
+        if (vis != 0xffffffffu) {
+          v0 = ((vis >> e) & 1u) ? v0 : 0.f;
+          v1 = ((vis >> (e + 1)) & 1u) ? v1 : 0.f;
+        }
+        pk[e >> 1] = pack2(v0, v1);
+      }
       const int tb = t & 1;
       mbar_wait(&t_free[tb], ((t >> 1) & 1) ^ 1);
       uint8_t* trow = sT + tb * T_BYTES + row * 128;
 #pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        float v[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const int jj = c * 8 + e;
-          const float sv = __uint_as_float(s[jj]);
-          float val;
-          if constexpr (TWO) val = __uint_as_float(dp[jj]) * dsilu_fast(sv);
-          else val = silu_fast(sv);
-          v[e] = ((vis >> jj) & 1ull) ? val : 0.f;
-        }
-        uint4 pk = make_uint4(pack2(v[0], v[1]), pack2(v[2], v[3]), pack2(v[4], v[5]), pack2(v[6], v[7]));
-        *reinterpret_cast<uint4*>(trow + ((c ^ (row & 7)) << 4)) = pk;
+      for (int c = 0; c < 4; ++c) {
+        const int chunk = half * 4 + c;
+        *reinterpret_cast<uint4*>(trow + ((chunk ^ (row & 7)) << 4)) =
+            make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
       }
       fence_proxy_async_smem();
       mbar_arrive(&t_full[tb]);
@@ -334,17 +341,18 @@ __global__ void __launch_bounds__(256, 1)
     const bool row_ok = my < us.L;
     const float dg = row_ok ? a.diag[g * a.H + h] : 0.f;
 #pragma unroll 1
-    for (int cc = 0; cc < DH / 32; ++cc) {
+    for (int cc = 0; cc < 4; ++cc) {
+      const int acol = half * 128 + cc * 32;
       uint32_t r[32];
       if (ntiles > 0) {
-        tmem_ld32(tmem + COL_ACC + cc * 32 + lane_off, r);
+        tmem_ld32(tmem + COL_ACC + acol + lane_off, r);
         tmem_ld_wait();
       } else {
 #pragma unroll
         for (int i = 0; i < 32; ++i) r[i] = 0u;
       }
       if (!row_ok) continue;
-      const int col = hcol + cc * 32;
+      const int col = hcol + acol;
       float v[32];
       const uint4* ep = reinterpret_cast<const uint4*>(a.e + g * a.ld_e + col);
 #pragma unroll
@@ -422,7 +430,7 @@ static mtgr_status_t launch_mode(const AttnIO& io, const void* c1, int64_t ld_c1
   dim3 grid(ceil_div(io.jag.max_len, BR), io.H, io.jag.num_users);
   ProfScope ps(MODE == FWD ? PROF_ATTN_FWD : MODE == DV ? PROF_ATTN_DV : MODE == DK ? PROF_ATTN_DK : PROF_ATTN_DQ, st);
   cudaFuncSetAttribute(attn_tc_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-  attn_tc_kernel<MODE><<<grid, 256, SMEM_BYTES, st>>>(m1, m2, m3, args);
+  attn_tc_kernel<MODE><<<grid, 384, SMEM_BYTES, st>>>(m1, m2, m3, args);
   return check_launch("attn_tc");
 }
 
