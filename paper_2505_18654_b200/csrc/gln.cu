@@ -134,11 +134,13 @@ struct GlnBwdArgs {
 
 constexpr int GLNB_WARPS = 4;
 
-// One warp per token (contiguous token range per warp).  Parameter-gradient contributions
-// dgamma[g] += dy*xhat, dbeta[g] += dy go to the block's smem accumulator [G][2][d]
-// (shared-memory reductions), written out as a per-block partial.
+// One warp per token, a contiguous token range per warp.  All of a token's loads are issued
+// before any reduction (memory-level parallelism); the parameter-gradient contributions
+// dgamma[g] += dy*xhat, dbeta[g] += dy are accumulated in registers while the group id stays
+// the same (tokens of a group are contiguous within a user) and flushed to the block's smem
+// accumulator [G][2][d] on a group change; block partials go to global with red.add.
 template <class T, int MODE, int NC>
-__global__ void __launch_bounds__(32 * GLNB_WARPS, (NC <= 2 ? 6 : 4)) gln_bwd_kernel(GlnBwdArgs<T> a) {
+__global__ void __launch_bounds__(32 * GLNB_WARPS, (NC <= 2 ? 3 : 2)) gln_bwd_kernel(GlnBwdArgs<T> a) {
   extern __shared__ float sacc[];  // [G][2][d]
   const int d = a.d, G = a.G;
   for (int i = threadIdx.x; i < G * 2 * d; i += blockDim.x) sacc[i] = 0.f;
@@ -148,27 +150,65 @@ __global__ void __launch_bounds__(32 * GLNB_WARPS, (NC <= 2 ? 6 : 4)) gln_bwd_ke
   const float inv_d = 1.0f / (float)d;
   const int w_begin = (blockIdx.x * GLNB_WARPS + warp) * a.tok_per_warp;
   const int w_end = min(a.ntok, w_begin + a.tok_per_warp);
-#pragma unroll 2
+  float pg[NC][8], pb[NC][8];
+#pragma unroll
+  for (int k = 0; k < NC; ++k)
+#pragma unroll
+    for (int e = 0; e < 8; ++e) pg[k][e] = pb[k][e] = 0.f;
+  int cur_g = w_begin < w_end ? a.gid[w_begin] : 0;
+  auto flush = [&]() {
+#pragma unroll
+    for (int k = 0; k < NC; ++k) {
+      const int c = lane + 32 * k;
+      if (c < nch) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          atomicAdd(&sacc[(cur_g * 2 + 0) * d + c * 8 + e], pg[k][e]);
+          atomicAdd(&sacc[(cur_g * 2 + 1) * d + c * 8 + e], pb[k][e]);
+          pg[k][e] = pb[k][e] = 0.f;
+        }
+      }
+    }
+  };
+#pragma unroll 1
   for (int t = w_begin; t < w_end; ++t) {
     const int g = a.gid[t];
     const float mu = a.mean[t], r = a.rstd[t];
+    float xv[NC][8], dyv[NC][8], e1[NC][8], e2[NC][8], e3[NC][8];
+#pragma unroll
+    for (int k = 0; k < NC; ++k) {
+      const int c = lane + 32 * k;
+      if (c < nch) {
+        load8(a.x + (int64_t)t * d + c * 8, xv[k]);
+        load8(a.dy + (int64_t)t * d + c * 8, dyv[k]);
+        if (MODE == GLN_RESID) load8(a.dz + (int64_t)t * d + c * 8, e1[k]);
+        if (MODE == GLN_GATE) {
+          load8(a.u + (int64_t)t * a.ld_a + c * 8, e1[k]);
+          load8(a.o + (int64_t)t * d + c * 8, e2[k]);
+          if (a.pre_u) load8(a.pre_u + (int64_t)t * a.ld_a + c * 8, e3[k]);
+        }
+      }
+    }
+    if (g != cur_g) {
+      flush();
+      cur_g = g;
+    }
     const float* gr = a.gamma + (int64_t)g * d;
-    float xh[NC][8], dyv[NC][8];
+    float gg[NC][8];
     float s1 = 0.f, s2 = 0.f;
 #pragma unroll
     for (int k = 0; k < NC; ++k) {
       const int c = lane + 32 * k;
       if (c < nch) {
-        float xv[8], gg[8];
-        load8(a.x + (int64_t)t * d + c * 8, xv);
-        load8(a.dy + (int64_t)t * d + c * 8, dyv[k]);
-        load8(gr + c * 8, gg);
+        load8(gr + c * 8, gg[k]);
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
-          xh[k][e] = (xv[e] - mu) * r;
-          const float dxh = dyv[k][e] * gg[e];
+          xv[k][e] = (xv[k][e] - mu) * r;  // xhat
+          const float dxh = dyv[k][e] * gg[k][e];
+          pg[k][e] = fmaf(dyv[k][e], xv[k][e], pg[k][e]);
+          pb[k][e] += dyv[k][e];
           s1 += dxh;
-          s2 += dxh * xh[k][e];
+          s2 = fmaf(dxh, xv[k][e], s2);
         }
       }
     }
@@ -177,37 +217,21 @@ __global__ void __launch_bounds__(32 * GLNB_WARPS, (NC <= 2 ? 6 : 4)) gln_bwd_ke
     for (int k = 0; k < NC; ++k) {
       const int c = lane + 32 * k;
       if (c < nch) {
-        float gg[8], o[8];
-        load8(gr + c * 8, gg);
-        float* accg = sacc + (g * 2 + 0) * d + c * 8;
-        float* accb = sacc + (g * 2 + 1) * d + c * 8;
+        float o[8];
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          atomicAdd(accg + e, dyv[k][e] * xh[k][e]);
-          atomicAdd(accb + e, dyv[k][e]);
-          o[e] = r * (dyv[k][e] * gg[e] - m1 - xh[k][e] * m2);
-        }
+        for (int e = 0; e < 8; ++e) o[e] = r * (dyv[k][e] * gg[k][e] - m1 - xv[k][e] * m2);
         if (MODE == GLN_RESID) {
-          float z[8];
-          load8(a.dz + (int64_t)t * d + c * 8, z);
 #pragma unroll
-          for (int e = 0; e < 8; ++e) o[e] += z[e];
+          for (int e = 0; e < 8; ++e) o[e] += e1[k][e];
           store8(a.dx + (int64_t)t * d + c * 8, o);
         } else if (MODE == GLN_GATE) {
           // o[] = dY; dO = dY * U;  dp_U = dY * O * silu'(p_U)
-          float uu[8], oo[8], dO[8], du[8];
-          load8(a.u + (int64_t)t * a.ld_a + c * 8, uu);
-          load8(a.o + (int64_t)t * d + c * 8, oo);
+          float dO[8], du[8];
 #pragma unroll
           for (int e = 0; e < 8; ++e) {
-            dO[e] = o[e] * uu[e];
-            du[e] = o[e] * oo[e];
-          }
-          if (a.pre_u) {
-            float pp[8];
-            load8(a.pre_u + (int64_t)t * a.ld_a + c * 8, pp);
-#pragma unroll
-            for (int e = 0; e < 8; ++e) du[e] *= dsilu_f(pp[e]);
+            dO[e] = o[e] * e1[k][e];
+            du[e] = o[e] * e2[k][e];
+            if (a.pre_u) du[e] *= dsilu_f(e3[k][e]);
           }
           store8(a.dx + (int64_t)t * d + c * 8, dO);
           store8(a.dpu + (int64_t)t * a.ld_dp + c * 8, du);
@@ -217,6 +241,7 @@ __global__ void __launch_bounds__(32 * GLNB_WARPS, (NC <= 2 ? 6 : 4)) gln_bwd_ke
       }
     }
   }
+  if (w_begin < w_end) flush();
   __syncthreads();
   // block partial -> global accumulators [G][2][d] (red.global.add; order not deterministic)
   for (int i = threadIdx.x; i < G * 2 * d; i += blockDim.x) {

@@ -24,6 +24,8 @@
 // w4-w11 softmax/epilogue (two warps per TMEM lane quadrant, thread = row = TMEM lane).  TMEM: R1 [0,128) (bf16 pairs),
 // acc [128,384), S buffers [384,512).
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -57,7 +59,12 @@ struct Args {
   __nv_bfloat16* out; int64_t ld_out;
   __nv_bfloat16* out2;                      // FWD y (ld_out)
   const float* diag;                        // [T][H]
+  long long* dbg;                           // debug timestamps (MTGR_ATTN_TRACE) or NULL
 };
+
+// debug tracing of one CTA (MTGR_ATTN_TRACE=1): slot layout [role][event][tile]
+#define DBG_ON (a.dbg != nullptr && blockIdx.x == 2 && blockIdx.y == 0 && blockIdx.z == 0)
+#define DBG(slot) do { if (DBG_ON) a.dbg[(slot)] = clock64(); } while (0)
 
 __device__ __forceinline__ float silu_fast(float s) {
   const float h = 0.5f * s;
@@ -114,6 +121,7 @@ __global__ void __launch_bounds__(384, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 17);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) DBG(10 * 64 + 4);
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmC1);
     tma_prefetch(&tmC2);
@@ -172,10 +180,13 @@ __global__ void __launch_bounds__(384, 1)
         for (int t = 0; t <= ntiles; ++t) {
           if (t < ntiles) {
             const int stage = t % STAGES;
+            if (t < 64) DBG(0 * 64 + t);
             mbar_wait(&kv_full[stage], (t / STAGES) & 1);
+            if (t < 64) DBG(1 * 64 + t);
             const int sb = TWO ? 0 : (t & 1);
             const int use = TWO ? t : (t >> 1);
             mbar_wait(&s_free[sb], (use & 1) ^ 1);
+            if (t < 64) DBG(2 * 64 + t);
             tc_fence_after();
             const uint32_t c1 = smem_u32(sStage + stage * STAGE_BYTES);
             const uint32_t s_col = tmem + COL_S + sb * BC;
@@ -197,7 +208,9 @@ __global__ void __launch_bounds__(384, 1)
           }
           if (t >= 1) {
             const int tp = t - 1, tb = tp & 1, sp = tp % STAGES;
+            if (tp < 64) DBG(3 * 64 + tp);
             mbar_wait(&t_full[tb], (tp >> 1) & 1);
+            if (tp < 64) DBG(4 * 64 + tp);
             tc_fence_after();
             const uint32_t x = smem_u32(sStage + sp * STAGE_BYTES) + (TWO ? 0 : CT_BYTES);
 #pragma unroll
@@ -242,6 +255,7 @@ __global__ void __launch_bounds__(384, 1)
     tmem_st_wait();
     tc_fence_before();
     mbar_arrive(r1_ready);
+    if (warp == 4 && lane == 0) DBG(10 * 64 + 3);
 
     const long long my_ts = (my < us.L && a.jag.ts) ? a.jag.ts[g] : 0;
     const bool need_ts_rows = TRANS && (r0 + BR > us.ns) && (r0 < kv_end);
@@ -259,7 +273,10 @@ __global__ void __launch_bounds__(384, 1)
       }
       const int sb = TWO ? 0 : (t & 1);
       const int use = TWO ? t : (t >> 1);
+      const bool dbgt = warp == 4 && lane == 0 && t < 64;
+      if (dbgt) DBG(5 * 64 + t);
       mbar_wait(&s_full[sb], use & 1);
+      if (dbgt) DBG(6 * 64 + t);
       tc_fence_after();
       uint32_t s[32];
       uint32_t dp[TWO ? 32 : 1];
@@ -323,7 +340,9 @@ __global__ void __launch_bounds__(384, 1)
         pk[e >> 1] = pack2(v0, v1);
       }
       const int tb = t & 1;
+      if (dbgt) DBG(7 * 64 + t);
       mbar_wait(&t_free[tb], ((t >> 1) & 1) ^ 1);
+      if (dbgt) DBG(8 * 64 + t);
       uint8_t* trow = sT + tb * T_BYTES + row * 128;
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
@@ -333,10 +352,13 @@ __global__ void __launch_bounds__(384, 1)
       }
       fence_proxy_async_smem();
       mbar_arrive(&t_full[tb]);
+      if (dbgt) DBG(9 * 64 + t);
     }
 
     // ---------------------------------------------------------------- epilogue
+    if (warp == 4 && lane == 0) DBG(10 * 64 + 0);
     mbar_wait(o_full, 0);
+    if (warp == 4 && lane == 0) DBG(10 * 64 + 1);
     tc_fence_after();
     const bool row_ok = my < us.L;
     const float dg = row_ok ? a.diag[g * a.H + h] : 0.f;
@@ -409,6 +431,7 @@ __global__ void __launch_bounds__(384, 1)
       }
     }
   }
+  if (warp == 4 && lane == 0) DBG(10 * 64 + 2);
   tc_fence_before();
   __syncthreads();
   if (warp == 2) {
@@ -430,7 +453,22 @@ static mtgr_status_t launch_mode(const AttnIO& io, const void* c1, int64_t ld_c1
   dim3 grid(ceil_div(io.jag.max_len, BR), io.H, io.jag.num_users);
   ProfScope ps(MODE == FWD ? PROF_ATTN_FWD : MODE == DV ? PROF_ATTN_DV : MODE == DK ? PROF_ATTN_DK : PROF_ATTN_DQ, st);
   cudaFuncSetAttribute(attn_tc_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-  attn_tc_kernel<MODE><<<grid, 384, SMEM_BYTES, st>>>(m1, m2, m3, args);
+  static const bool trace = getenv("MTGR_ATTN_TRACE") != nullptr;
+  Args a2 = args;
+  if (trace) {  // debug only: time-stamp one CTA's pipeline events
+    cudaMalloc(&a2.dbg, 11 * 64 * sizeof(long long));
+    cudaMemsetAsync(a2.dbg, 0, 11 * 64 * sizeof(long long), st);
+  }
+  attn_tc_kernel<MODE><<<grid, 384, SMEM_BYTES, st>>>(m1, m2, m3, a2);
+  if (trace) {
+    long long h[11 * 64];
+    cudaMemcpyAsync(h, a2.dbg, sizeof(h), cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    cudaFree(a2.dbg);
+    fprintf(stderr, "ATTN_TRACE mode=%d", MODE);
+    for (int i = 0; i < 11 * 64; ++i) fprintf(stderr, " %lld", h[i]);
+    fprintf(stderr, "\n");
+  }
   return check_launch("attn_tc");
 }
 
