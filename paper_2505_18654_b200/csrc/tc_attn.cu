@@ -3,26 +3,31 @@
 //
 // One CTA = (128-row tile, head, user); rows never cross users.  Four modes share one kernel:
 //
-//   mode | rows (R1, in TMEM) | R2 (smem) | column tile C1 | C2 / X     | T tile          | acc
-//   FWD  | Q                  |  -        | K (64 keys)    | X = V      | P  = silu(S)*m  | O
-//   DV   | K                  |  -        | Q (64 queries) | X = dO     | P^T             | dV
-//   DQ   | Q                  | dO        | K              | C2 = V     | dS = dP*silu'(S)*m | dQ (X = C1)
-//   DK   | K                  | V         | Q              | C2 = dO    | dS^T            | dK (X = C1)
+//   mode | rows (R1, in TMEM) | R2 (smem) | column tile C1 | X (acc B)  | T tile            | acc
+//   FWD  | Q                  |  -        | K (64 keys)    | V          | P  = silu(S)*m    | O
+//   DV   | K                  |  -        | Q (64 queries) | dO         | P^T               | dV
+//   DQ   | Q                  | dO        | K              | K  (= C1)  | dS = dP*silu'(S)*m| dQ
+//   DK   | K                  | V         | Q              | Q  (= C1)  | dS^T              | dK
+//   (DQ/DK also stream C2 = V / dO for dP = R2 C2^T.)
 //
 // Per column tile:  S = R1 C1^T (tcgen05.mma, A from TMEM, B = C1 K-major smem, M=128 N=64
-// K=256) [and dP = R2 C2^T, SS];  4 "softmax" warps tcgen05.ld S (and dP), apply the mask
+// K=256) [and dP = R2 C2^T, SS];  8 "softmax" warps tcgen05.ld S (and dP), apply the mask
 // predicate in registers and SiLU / SiLU' (tanh.approx), write the bf16 T tile into a
 // SWIZZLE_128B smem buffer;  acc += T X (M=128 N=256 K=64, B = X MN-major — the same
-// TMA-loaded tile read with an MN-major descriptor).  The 1/N factor, the diagonal term of
-// non-static tokens (R#9: candidates and real-time tokens see themselves), the gate
-// (FWD: y = o*u) and the QKV activation backward (silu'(p)) are fused into the epilogue.
-// Keys of a query tile are restricted to [0, n_static + n_rt) (candidate keys are visible only
-// to themselves, rule 3 P:338) and to [0, n_static) when every row of the tile is static
-// (R#8), so fully masked tiles are never loaded.
+// TMA-loaded tile read with an MN-major descriptor).  Dependent N=64 MMA chains are
+// latency-bound, so two independent chains are always interleaved: S of two column tiles
+// (FWD/DV) or S and dP of one tile (DQ/DK).
+// The 1/N factor, the diagonal term of non-static tokens (R#9: candidates and real-time tokens
+// see themselves), the gate (FWD: y = o*u) and the QKV activation backward (silu'(p)) are fused
+// into the epilogue, which stages E/U tiles and the outputs in shared memory (TMA in, coalesced
+// row stores out).  Keys of a query tile are restricted to [0, n_static + n_rt) (candidate keys
+// are visible only to themselves, rule 3 P:338) and to [0, n_static) when every row of the tile
+// is static (R#8), so fully masked tiles are never loaded.
 //
-// Warp roles (384 threads): w0 TMA producer, w1 MMA issuer, w2 TMEM allocator,
-// w4-w11 softmax/epilogue (two warps per TMEM lane quadrant, thread = row = TMEM lane).  TMEM: R1 [0,128) (bf16 pairs),
-// acc [128,384), S buffers [384,512).
+// Warp roles (384 threads): w0 TMA producer (R1, R2, C1, E), w1 MMA issuer, w2 TMEM allocator,
+// w3 TMA producer (X or C2, U), w4-w11 softmax/epilogue (two warps per TMEM lane quadrant,
+// thread = row = TMEM lane).  TMEM: R1 [0,128) (bf16 pairs), acc [128,384), S [384,448),
+// S' / dP [448,512).
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
@@ -38,31 +43,30 @@ namespace tca {
 constexpr int DH = 256;
 constexpr int BR = 128;                 // rows per CTA
 constexpr int BC = 64;                  // columns per iterated tile
+constexpr int KB = 1024;
 constexpr int CT_BYTES = BC * DH * 2;   // 32 KB: 4 boxes {64 dh, 64 rows}
-constexpr int R2_BYTES = BR * DH * 2;   // 64 KB: 4 boxes {64 dh, 128 rows}
+constexpr int RT_BYTES = BR * DH * 2;   // 64 KB: 4 boxes {64 dh, 128 rows}
 constexpr int T_BYTES = BR * BC * 2;    // 16 KB
-constexpr int OFF_T = 192 * 1024;
+constexpr int OFF_T = 192 * KB;
 constexpr int OFF_TS = OFF_T + 2 * T_BYTES;
-constexpr int OFF_BAR = OFF_TS + 2 * BC * 8;
-constexpr int SMEM_BYTES = OFF_BAR + 256 + 1024;
+constexpr int OFF_BAR = OFF_TS + BC * 8;
+constexpr int SMEM_BYTES = OFF_BAR + 512 + 1024;
 constexpr uint32_t COL_R1 = 0, COL_ACC = 128, COL_S = 384;
+constexpr int NSM = 8;  // softmax/epilogue warps
 
 enum { FWD = 0, DV = 1, DQ = 2, DK = 3 };
 
 struct Args {
   mtgr_jagged_t jag;
   int H, d;
-  const __nv_bfloat16* r1; int64_t ld_r1;   // row operand 1 (block start)
-  const __nv_bfloat16* e; int64_t ld_e;     // epilogue diagonal vector
-  const __nv_bfloat16* u; int64_t ld_u;     // FWD gate
-  const __nv_bfloat16* pre; int64_t ld_pre; // silu' source block or NULL
   __nv_bfloat16* out; int64_t ld_out;
   __nv_bfloat16* out2;                      // FWD y (ld_out)
   const float* diag;                        // [T][H]
+  int has_u;                                // U / pre tile present
   long long* dbg;                           // debug timestamps (MTGR_ATTN_TRACE) or NULL
 };
 
-// debug tracing of one CTA (MTGR_ATTN_TRACE=1): slot layout [role][event][tile]
+// debug tracing of one CTA (MTGR_ATTN_TRACE=1): slot layout [event][tile]
 #define DBG_ON (a.dbg != nullptr && blockIdx.x == 2 && blockIdx.y == 0 && blockIdx.z == 0)
 #define DBG(slot) do { if (DBG_ON) a.dbg[(slot)] = clock64(); } while (0)
 
@@ -78,16 +82,25 @@ __device__ __forceinline__ uint32_t pack2(float a, float b) {
   __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&h);
 }
+// 16-byte chunk j (0..7) of row r inside a SWIZZLE_128B box of 128-byte rows
+__device__ __forceinline__ uint32_t sw128(int r, int j) { return r * 128 + ((j ^ (r & 7)) << 4); }
 
 template <int MODE>
 __global__ void __launch_bounds__(384, 1)
-    attn_tc_kernel(const __grid_constant__ CUtensorMap tmC1, const __grid_constant__ CUtensorMap tmC2,
-                   const __grid_constant__ CUtensorMap tmR2, Args a) {
+    attn_tc_kernel(const __grid_constant__ CUtensorMap tmC1, const __grid_constant__ CUtensorMap tmX,
+                   const __grid_constant__ CUtensorMap tmR1, const __grid_constant__ CUtensorMap tmR2,
+                   const __grid_constant__ CUtensorMap tmE, const __grid_constant__ CUtensorMap tmU,
+                   Args a) {
   using namespace sm100;
   constexpr bool TWO = (MODE == DQ || MODE == DK);
   constexpr bool TRANS = (MODE == DV || MODE == DK);
-  constexpr int STAGES = TWO ? 2 : 3;
-  constexpr int STAGE_BYTES = 2 * CT_BYTES;
+  // smem regions (see header)
+  constexpr int OFF_C1 = TWO ? 64 * KB : 0;           // C1 ring, 3 slots
+  constexpr int OFF_X = TWO ? 160 * KB : 96 * KB;     // X ring (3 slots) or C2 slot (1)
+  constexpr int NX = TWO ? 1 : 3;
+  constexpr int OFF_R1STAGE = TWO ? 128 * KB : 96 * KB;
+  constexpr int OFF_E = 0;                            // free after the last score MMA
+  constexpr int OFF_U = TWO ? 64 * KB : 96 * KB;      // free after the last acc MMA
 
   const int u = blockIdx.z, h = blockIdx.y, r0 = blockIdx.x * BR;
   const UserSpan us = load_user(a.jag, u);
@@ -104,36 +117,47 @@ __global__ void __launch_bounds__(384, 1)
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sR2 = smem;                              // TWO only (64 KB)
-  uint8_t* sStage = smem + (TWO ? R2_BYTES : 0);    // STAGES x 64 KB
-  uint8_t* sT = smem + OFF_T;                       // 2 x 16 KB
-  long long* sTs = reinterpret_cast<long long*>(smem + OFF_TS);  // [2][64]
+  uint8_t* sT = smem + OFF_T;
+  long long* sTs = reinterpret_cast<long long*>(smem + OFF_TS);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
-  uint64_t* kv_full = bars;            // [3]
-  uint64_t* kv_empty = bars + 3;       // [3]
-  uint64_t* s_full = bars + 6;         // [2]
-  uint64_t* s_free = bars + 8;         // [2]
-  uint64_t* t_full = bars + 10;        // [2]
-  uint64_t* t_free = bars + 12;        // [2]
-  uint64_t* r1_ready = bars + 14;
-  uint64_t* r2_full = bars + 15;
-  uint64_t* o_full = bars + 16;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 17);
+  uint64_t* c1_full = bars;           // [3]
+  uint64_t* c1_empty = bars + 3;      // [3]
+  uint64_t* x_full = bars + 6;        // [3]
+  uint64_t* x_empty = bars + 9;       // [3]
+  uint64_t* s_full = bars + 12;       // [2]
+  uint64_t* s_free = bars + 14;       // [2]
+  uint64_t* t_full = bars + 16;       // [2]
+  uint64_t* t_free = bars + 18;       // [2]
+  uint64_t* r1_full = bars + 20;
+  uint64_t* r1_done = bars + 21;
+  uint64_t* r2_full = bars + 22;
+  uint64_t* e_full = bars + 23;
+  uint64_t* u_full = bars + 24;
+  uint64_t* o_full = bars + 25;
+  uint64_t* sc_done = bars + 26;      // every score MMA (S, dP) has completed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 27);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) DBG(10 * 64 + 4);
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmC1);
-    tma_prefetch(&tmC2);
-    if (TWO) tma_prefetch(&tmR2);
-    for (int s = 0; s < 3; ++s) { mbar_init(&kv_full[s], 1); mbar_init(&kv_empty[s], 1); }
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(&s_full[b], 1); mbar_init(&s_free[b], 256);
-      mbar_init(&t_full[b], 256); mbar_init(&t_free[b], 1);
+    tma_prefetch(&tmX);
+    tma_prefetch(&tmR1);
+    for (int s = 0; s < 3; ++s) {
+      mbar_init(&c1_full[s], 1); mbar_init(&c1_empty[s], 1);
+      mbar_init(&x_full[s], 1); mbar_init(&x_empty[s], 1);
     }
-    mbar_init(r1_ready, 256);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&s_full[b], 1); mbar_init(&s_free[b], 32 * NSM);
+      mbar_init(&t_full[b], 32 * NSM); mbar_init(&t_free[b], 1);
+    }
+    mbar_init(r1_full, 1);
+    mbar_init(r1_done, 32 * NSM);
     mbar_init(r2_full, 1);
+    mbar_init(e_full, 1);
+    mbar_init(u_full, 1);
     mbar_init(o_full, 1);
+    mbar_init(sc_done, 1);
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc<512>(tmem_slot);
@@ -142,26 +166,57 @@ __global__ void __launch_bounds__(384, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const int hcol = h * DH;
+  const int row0 = us.off + r0;  // global row of the tile's first row
 
   if (warp == 0) {
-    // ---------------------------------------------------------------- TMA producer
-    if (lane == 0 && ntiles > 0) {
-      if (TWO) {
-        mbar_expect_tx(r2_full, R2_BYTES);
+    // ---------------------------------------------------------------- producer A: R1, R2, C1, E
+    if (lane == 0) {
+      mbar_expect_tx(r1_full, RT_BYTES);
 #pragma unroll
-        for (int c = 0; c < 4; ++c) tma_load_2d(sR2 + c * (R2_BYTES / 4), &tmR2, r2_full, hcol + c * 64, us.off + r0);
+      for (int c = 0; c < 4; ++c) tma_load_2d(smem + OFF_R1STAGE + c * (RT_BYTES / 4), &tmR1, r1_full, hcol + c * 64, row0);
+      if (ntiles > 0) {
+        if (TWO) {
+          mbar_expect_tx(r2_full, RT_BYTES);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) tma_load_2d(smem + c * (RT_BYTES / 4), &tmR2, r2_full, hcol + c * 64, row0);
+        }
+        for (int t = 0; t < ntiles; ++t) {
+          const int slot = t % 3;
+          if (TWO && t == 2) mbar_wait(r1_done, 0);  // slot 2 overlaps the R1 staging area
+          mbar_wait(&c1_empty[slot], ((t / 3) & 1) ^ 1);
+          mbar_expect_tx(&c1_full[slot], CT_BYTES);
+          const int row = us.off + c_begin + t * BC;
+          uint8_t* dst = smem + OFF_C1 + slot * CT_BYTES;
+#pragma unroll
+          for (int c = 0; c < 4; ++c) tma_load_2d(dst + c * (CT_BYTES / 4), &tmC1, &c1_full[slot], hcol + c * 64, row);
+        }
+        // E tile once every score MMA is done (the C1 ring / R2 region is then free)
+        mbar_wait(sc_done, 0);
+      } else {
+        mbar_wait(r1_done, 0);  // E overlaps the R1 staging area when there is no mainloop
       }
+      mbar_expect_tx(e_full, RT_BYTES);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) tma_load_2d(smem + OFF_E + c * (RT_BYTES / 4), &tmE, e_full, hcol + c * 64, row0);
+    }
+  } else if (warp == 3) {
+    // ---------------------------------------------------------------- producer B: X / C2, U
+    if (lane == 0) {
+      mbar_wait(r1_done, 0);  // the R1 staging area overlaps this ring
       for (int t = 0; t < ntiles; ++t) {
-        const int stage = t % STAGES;
-        mbar_wait(&kv_empty[stage], ((t / STAGES) & 1) ^ 1);
-        mbar_expect_tx(&kv_full[stage], STAGE_BYTES);
+        const int slot = t % NX;
+        mbar_wait(&x_empty[slot], ((t / NX) & 1) ^ 1);
+        mbar_expect_tx(&x_full[slot], CT_BYTES);
         const int row = us.off + c_begin + t * BC;
-        uint8_t* c1 = sStage + stage * STAGE_BYTES;
+        uint8_t* dst = smem + OFF_X + slot * CT_BYTES;
 #pragma unroll
-        for (int c = 0; c < 4; ++c) tma_load_2d(c1 + c * (CT_BYTES / 4), &tmC1, &kv_full[stage], hcol + c * 64, row);
+        for (int c = 0; c < 4; ++c) tma_load_2d(dst + c * (CT_BYTES / 4), &tmX, &x_full[slot], hcol + c * 64, row);
+      }
+      if (a.has_u) {
+        mbar_wait(o_full, 0);
+        mbar_expect_tx(u_full, RT_BYTES);
 #pragma unroll
-        for (int c = 0; c < 4; ++c)
-          tma_load_2d(c1 + CT_BYTES + c * (CT_BYTES / 4), &tmC2, &kv_full[stage], hcol + c * 64, row);
+        for (int c = 0; c < 4; ++c) tma_load_2d(smem + OFF_U + c * (RT_BYTES / 4), &tmU, u_full, hcol + c * 64, row0);
       }
     }
   } else if (warp == 1) {
@@ -172,89 +227,125 @@ __global__ void __launch_bounds__(384, 1)
       } else {
         constexpr uint32_t idesc_s = idesc_bf16_f32(BR, BC, 0, 0);
         constexpr uint32_t idesc_acc = idesc_bf16_f32(BR, DH, 0, 1);
-        mbar_wait(r1_ready, 0);
+        const uint32_t t_base = smem_u32(sT);
+        const uint32_t c1_base = smem_u32(smem + OFF_C1);
+        const uint32_t x_base = smem_u32(smem + OFF_X);
+        const uint32_t r2_base = smem_u32(smem);
+        mbar_wait(r1_done, 0);
         if (TWO) mbar_wait(r2_full, 0);
         tc_fence_after();
-        const uint32_t t_base = smem_u32(sT);
-        const uint32_t r2_base = smem_u32(sR2);
-        for (int t = 0; t <= ntiles; ++t) {
-          if (t < ntiles) {
-            const int stage = t % STAGES;
+        // acc += T_j X_j
+        auto acc = [&](int j) {
+          const int tb = j & 1;
+          if (j < 64) DBG(3 * 64 + j);
+          mbar_wait(&t_full[tb], (j >> 1) & 1);
+          if (j < 64) DBG(4 * 64 + j);
+          uint32_t x;
+          if (TWO) {
+            x = c1_base + (j % 3) * CT_BYTES;  // X = C1 (held in the C1 ring until here)
+          } else {
+            mbar_wait(&x_full[j % 3], (j / 3) & 1);
+            x = x_base + (j % 3) * CT_BYTES;
+          }
+          tc_fence_after();
+#pragma unroll
+          for (int k = 0; k < BC / 16; ++k)
+            mma_bf16_ss(tmem + COL_ACC, desc_sw128(t_base + tb * T_BYTES + k * 32, 16, 1024),
+                        desc_sw128(x + k * 2048, CT_BYTES / 4, 1024), idesc_acc, (j > 0 || k > 0));
+          mma_commit(&t_free[tb]);
+          if (TWO) mma_commit(&c1_empty[j % 3]);
+          else mma_commit(&x_empty[j % 3]);
+        };
+        if (!TWO) {
+          // two independent S chains (tiles t, t+1) interleaved, then the accs of the previous pair
+          for (int t = 0; t < ntiles; t += 2) {
+            const bool b = t + 1 < ntiles;
             if (t < 64) DBG(0 * 64 + t);
-            mbar_wait(&kv_full[stage], (t / STAGES) & 1);
+            mbar_wait(&c1_full[t % 3], (t / 3) & 1);
+            if (b) mbar_wait(&c1_full[(t + 1) % 3], ((t + 1) / 3) & 1);
             if (t < 64) DBG(1 * 64 + t);
-            const int sb = TWO ? 0 : (t & 1);
-            const int use = TWO ? t : (t >> 1);
-            mbar_wait(&s_free[sb], (use & 1) ^ 1);
+            mbar_wait(&s_free[0], ((t >> 1) & 1) ^ 1);
+            if (b) mbar_wait(&s_free[1], ((t >> 1) & 1) ^ 1);
             if (t < 64) DBG(2 * 64 + t);
             tc_fence_after();
-            const uint32_t c1 = smem_u32(sStage + stage * STAGE_BYTES);
-            const uint32_t s_col = tmem + COL_S + sb * BC;
+            const uint32_t ka = c1_base + (t % 3) * CT_BYTES;
+            const uint32_t kb = c1_base + ((t + 1) % 3) * CT_BYTES;
 #pragma unroll
-            for (int k = 0; k < DH / 16; ++k)
-              mma_bf16_ts(s_col, tmem + COL_R1 + k * 8,
-                          desc_sw128(c1 + (k >> 2) * (CT_BYTES / 4) + (k & 3) * 32, 16, 1024), idesc_s,
-                          k > 0);
-            if (TWO) {
-              const uint32_t c2 = c1 + CT_BYTES;
-#pragma unroll
-              for (int k = 0; k < DH / 16; ++k)
-                mma_bf16_ss(tmem + COL_S + BC,
-                            desc_sw128(r2_base + (k >> 2) * (R2_BYTES / 4) + (k & 3) * 32, 16, 1024),
-                            desc_sw128(c2 + (k >> 2) * (CT_BYTES / 4) + (k & 3) * 32, 16, 1024),
-                            idesc_s, k > 0);
+            for (int k = 0; k < DH / 16; ++k) {
+              const uint32_t off = (k >> 2) * (CT_BYTES / 4) + (k & 3) * 32;
+              mma_bf16_ts(tmem + COL_S, tmem + COL_R1 + k * 8, desc_sw128(ka + off, 16, 1024), idesc_s, k > 0);
+              if (b) mma_bf16_ts(tmem + COL_S + BC, tmem + COL_R1 + k * 8, desc_sw128(kb + off, 16, 1024), idesc_s, k > 0);
             }
-            mma_commit(&s_full[sb]);
+            mma_commit(&s_full[0]);
+            mma_commit(&c1_empty[t % 3]);
+            if (b) {
+              mma_commit(&s_full[1]);
+              mma_commit(&c1_empty[(t + 1) % 3]);
+            }
+            if (t + 2 >= ntiles) mma_commit(sc_done);
+            if (t >= 2) {
+              acc(t - 2);
+              acc(t - 1);
+            }
           }
-          if (t >= 1) {
-            const int tp = t - 1, tb = tp & 1, sp = tp % STAGES;
-            if (tp < 64) DBG(3 * 64 + tp);
-            mbar_wait(&t_full[tb], (tp >> 1) & 1);
-            if (tp < 64) DBG(4 * 64 + tp);
+          const int tl = (ntiles - 1) & ~1;  // first tile of the last pair
+          acc(tl);
+          if (tl + 1 < ntiles) acc(tl + 1);
+        } else {
+          // S and dP of one tile interleaved (independent chains), then the acc of the previous tile
+          for (int t = 0; t < ntiles; ++t) {
+            if (t < 64) DBG(0 * 64 + t);
+            mbar_wait(&c1_full[t % 3], (t / 3) & 1);
+            mbar_wait(&x_full[0], t & 1);
+            if (t < 64) DBG(1 * 64 + t);
+            mbar_wait(&s_free[0], (t & 1) ^ 1);
+            if (t < 64) DBG(2 * 64 + t);
             tc_fence_after();
-            const uint32_t x = smem_u32(sStage + sp * STAGE_BYTES) + (TWO ? 0 : CT_BYTES);
+            const uint32_t c1 = c1_base + (t % 3) * CT_BYTES;
 #pragma unroll
-            for (int k = 0; k < BC / 16; ++k)
-              mma_bf16_ss(tmem + COL_ACC, desc_sw128(t_base + tb * T_BYTES + k * 32, 16, 1024),
-                          desc_sw128(x + k * 2048, CT_BYTES / 4, 1024), idesc_acc, (tp > 0 || k > 0));
-            mma_commit(&t_free[tb]);
-            mma_commit(&kv_empty[sp]);
+            for (int k = 0; k < DH / 16; ++k) {
+              const uint32_t off = (k >> 2) * (CT_BYTES / 4) + (k & 3) * 32;
+              mma_bf16_ts(tmem + COL_S, tmem + COL_R1 + k * 8, desc_sw128(c1 + off, 16, 1024), idesc_s, k > 0);
+              mma_bf16_ss(tmem + COL_S + BC,
+                          desc_sw128(r2_base + (k >> 2) * (RT_BYTES / 4) + (k & 3) * 32, 16, 1024),
+                          desc_sw128(x_base + off, 16, 1024), idesc_s, k > 0);
+            }
+            mma_commit(&s_full[0]);
+            mma_commit(&x_empty[0]);
+            if (t + 1 == ntiles) mma_commit(sc_done);
+            if (t >= 1) acc(t - 1);
           }
+          acc(ntiles - 1);
         }
         mma_commit(o_full);
       }
     }
   } else if (warp >= 4) {
     // ---------------------------------------------------------------- softmax + epilogue
-    // 8 warps: quadrant q = warp % 4 owns TMEM lanes (rows) q*32..q*32+31; half = which 32 of the
-    // 64 tile columns (and which 128 of the 256 accumulator columns) the warp handles.
+    // quadrant q = warp % 4 owns TMEM lanes (rows) q*32..q*32+31; half = which 32 of the 64 tile
+    // columns (and which 128 of the 256 head-dim columns) the warp handles.
     const int q = warp & 3;
     const int half = (warp - 4) >> 2;
     const int row = q * 32 + lane;
     const int my = r0 + row;                 // user-local index of this thread's row
-    const int64_t g = (int64_t)us.off + my;  // global token index
-    const int T = a.jag.total_tokens;
+    const int64_t g = (int64_t)row0 + row;   // global token index
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
-    // R1 row (this warp's 128 head-dim columns) -> TMEM as bf16 pairs
+    // R1 row (this warp's 128 head-dim columns) smem -> TMEM as bf16 pairs
+    mbar_wait(r1_full, 0);
 #pragma unroll 1
     for (int cc = 0; cc < 2; ++cc) {
+      const uint8_t* box = smem + OFF_R1STAGE + (half * 2 + cc) * (RT_BYTES / 4);
       uint32_t w[32];
-      if (g < T) {
-        const uint4* src = reinterpret_cast<const uint4*>(a.r1 + g * a.ld_r1 + hcol + half * 128 + cc * 64);
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          uint4 v = __ldg(src + i);
-          w[4 * i] = v.x; w[4 * i + 1] = v.y; w[4 * i + 2] = v.z; w[4 * i + 3] = v.w;
-        }
-      } else {
-#pragma unroll
-        for (int i = 0; i < 32; ++i) w[i] = 0u;
+      for (int j = 0; j < 8; ++j) {
+        const uint4 v = *reinterpret_cast<const uint4*>(box + sw128(row, j));
+        w[4 * j] = v.x; w[4 * j + 1] = v.y; w[4 * j + 2] = v.z; w[4 * j + 3] = v.w;
       }
       tmem_st32(tmem + COL_R1 + half * 64 + cc * 32 + lane_off, w);
     }
     tmem_st_wait();
     tc_fence_before();
-    mbar_arrive(r1_ready);
+    mbar_arrive(r1_done);
     if (warp == 4 && lane == 0) DBG(10 * 64 + 3);
 
     const long long my_ts = (my < us.L && a.jag.ts) ? a.jag.ts[g] : 0;
@@ -267,9 +358,9 @@ __global__ void __launch_bounds__(384, 1)
       long long* tsb = sTs;
       if (need_ts) {  // uniform over the 8 softmax warps
         const int i = threadIdx.x - 128;
-        named_bar_sync(1, 256);  // everyone is done reading the previous tile's times
+        named_bar_sync(1, 32 * NSM);  // everyone is done reading the previous tile's times
         if (i < BC) tsb[i] = (c0 + i < us.L && a.jag.ts) ? a.jag.ts[us.off + c0 + i] : 0;
-        named_bar_sync(1, 256);
+        named_bar_sync(1, 32 * NSM);
       }
       const int sb = TWO ? 0 : (t & 1);
       const int use = TWO ? t : (t >> 1);
@@ -343,13 +434,11 @@ __global__ void __launch_bounds__(384, 1)
       if (dbgt) DBG(7 * 64 + t);
       mbar_wait(&t_free[tb], ((t >> 1) & 1) ^ 1);
       if (dbgt) DBG(8 * 64 + t);
-      uint8_t* trow = sT + tb * T_BYTES + row * 128;
+      uint8_t* tbuf = sT + tb * T_BYTES;
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const int chunk = half * 4 + c;
-        *reinterpret_cast<uint4*>(trow + ((chunk ^ (row & 7)) << 4)) =
+      for (int c = 0; c < 4; ++c)
+        *reinterpret_cast<uint4*>(tbuf + sw128(row, half * 4 + c)) =
             make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
-      }
       fence_proxy_async_smem();
       mbar_arrive(&t_full[tb]);
       if (dbgt) DBG(9 * 64 + t);
@@ -360,11 +449,15 @@ __global__ void __launch_bounds__(384, 1)
     mbar_wait(o_full, 0);
     if (warp == 4 && lane == 0) DBG(10 * 64 + 1);
     tc_fence_after();
+    mbar_wait(e_full, 0);
+    if (a.has_u) mbar_wait(u_full, 0);
     const bool row_ok = my < us.L;
     const float dg = row_ok ? a.diag[g * a.H + h] : 0.f;
+    uint8_t* sE = smem + OFF_E;
+    uint8_t* sU = smem + OFF_U;
 #pragma unroll 1
     for (int cc = 0; cc < 4; ++cc) {
-      const int acol = half * 128 + cc * 32;
+      const int acol = half * 128 + cc * 32;  // head-dim column of this chunk
       uint32_t r[32];
       if (ntiles > 0) {
         tmem_ld32(tmem + COL_ACC + acol + lane_off, r);
@@ -373,62 +466,57 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
         for (int i = 0; i < 32; ++i) r[i] = 0u;
       }
-      if (!row_ok) continue;
-      const int col = hcol + acol;
-      float v[32];
-      const uint4* ep = reinterpret_cast<const uint4*>(a.e + g * a.ld_e + col);
+      const int bx = acol >> 6, j0 = (acol & 63) >> 3;
+      uint8_t* ebox = sE + bx * (RT_BYTES / 4);
+      uint8_t* ubox = sU + bx * (RT_BYTES / 4);
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
-        uint4 w = __ldg(ep + i);
+        const uint32_t off = sw128(row, j0 + i);
+        uint4 w = *reinterpret_cast<const uint4*>(ebox + off);
         const __nv_bfloat162* hh = reinterpret_cast<const __nv_bfloat162*>(&w);
+        float v[8];
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-          float2 f = __bfloat1622float2(hh[k]);
-          v[8 * i + 2 * k] = fmaf(us.nu, __uint_as_float(r[8 * i + 2 * k]), dg * f.x);
-          v[8 * i + 2 * k + 1] = fmaf(us.nu, __uint_as_float(r[8 * i + 2 * k + 1]), dg * f.y);
+          const float2 f = __bfloat1622float2(hh[k]);
+          v[2 * k] = fmaf(us.nu, __uint_as_float(r[8 * i + 2 * k]), dg * f.x);
+          v[2 * k + 1] = fmaf(us.nu, __uint_as_float(r[8 * i + 2 * k + 1]), dg * f.y);
         }
-      }
-      uint4* op = reinterpret_cast<uint4*>(a.out + g * a.ld_out + col);
-      if (MODE == FWD) {
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-          op[i] = make_uint4(pack2(v[8 * i], v[8 * i + 1]), pack2(v[8 * i + 2], v[8 * i + 3]),
-                             pack2(v[8 * i + 4], v[8 * i + 5]), pack2(v[8 * i + 6], v[8 * i + 7]));
-        const uint4* up = reinterpret_cast<const uint4*>(a.u + g * a.ld_u + col);
-        uint4* yp = reinterpret_cast<uint4*>(a.out2 + g * a.ld_out + col);
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          uint4 w = __ldg(up + i);
-          const __nv_bfloat162* hh = reinterpret_cast<const __nv_bfloat162*>(&w);
+        if (MODE == FWD) {
+          const uint4 uw = *reinterpret_cast<const uint4*>(ubox + off);
+          const __nv_bfloat162* uh = reinterpret_cast<const __nv_bfloat162*>(&uw);
           float y[8];
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
-            float2 f = __bfloat1622float2(hh[k]);
-            y[2 * k] = v[8 * i + 2 * k] * f.x;
-            y[2 * k + 1] = v[8 * i + 2 * k + 1] * f.y;
+            const float2 f = __bfloat1622float2(uh[k]);
+            y[2 * k] = v[2 * k] * f.x;
+            y[2 * k + 1] = v[2 * k + 1] * f.y;
           }
-          yp[i] = make_uint4(pack2(y[0], y[1]), pack2(y[2], y[3]), pack2(y[4], y[5]), pack2(y[6], y[7]));
-        }
-      } else {
-        if (a.pre) {
-          const uint4* pp = reinterpret_cast<const uint4*>(a.pre + g * a.ld_pre + col);
+          *reinterpret_cast<uint4*>(ubox + off) =
+              make_uint4(pack2(y[0], y[1]), pack2(y[2], y[3]), pack2(y[4], y[5]), pack2(y[6], y[7]));
+        } else if (a.has_u) {
+          const uint4 pw = *reinterpret_cast<const uint4*>(ubox + off);
+          const __nv_bfloat162* ph = reinterpret_cast<const __nv_bfloat162*>(&pw);
 #pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            uint4 w = __ldg(pp + i);
-            const __nv_bfloat162* hh = reinterpret_cast<const __nv_bfloat162*>(&w);
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              float2 f = __bfloat1622float2(hh[k]);
-              v[8 * i + 2 * k] *= dsilu_f(f.x);
-              v[8 * i + 2 * k + 1] *= dsilu_f(f.y);
-            }
+          for (int k = 0; k < 4; ++k) {
+            const float2 f = __bfloat1622float2(ph[k]);
+            v[2 * k] *= dsilu_f(f.x);
+            v[2 * k + 1] *= dsilu_f(f.y);
           }
         }
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-          op[i] = make_uint4(pack2(v[8 * i], v[8 * i + 1]), pack2(v[8 * i + 2], v[8 * i + 3]),
-                             pack2(v[8 * i + 4], v[8 * i + 5]), pack2(v[8 * i + 6], v[8 * i + 7]));
+        *reinterpret_cast<uint4*>(ebox + off) =
+            make_uint4(pack2(v[0], v[1]), pack2(v[2], v[3]), pack2(v[4], v[5]), pack2(v[6], v[7]));
       }
+    }
+    named_bar_sync(1, 32 * NSM);
+    // coalesced row stores: warp w writes rows w, w+8, ...; lane l covers head-dim columns l*8..+7
+    const int sw = warp - 4;
+    const int nrows = min(BR, us.L - r0);
+    const int bx = lane >> 3, jj = lane & 7;
+    for (int rr = sw; rr < nrows; rr += NSM) {
+      const uint32_t off = bx * (RT_BYTES / 4) + sw128(rr, jj);
+      const int64_t go = (int64_t)(row0 + rr) * a.ld_out + hcol + lane * 8;
+      *reinterpret_cast<uint4*>(a.out + go) = *reinterpret_cast<const uint4*>(sE + off);
+      if (MODE == FWD) *reinterpret_cast<uint4*>(a.out2 + go) = *reinterpret_cast<const uint4*>(sU + off);
     }
   }
   if (warp == 4 && lane == 0) DBG(10 * 64 + 2);
@@ -440,33 +528,41 @@ __global__ void __launch_bounds__(384, 1)
   }
 }
 
+struct Maps {
+  CUtensorMap c1, x, r1, r2, e, u;
+};
+
 template <int MODE>
-static mtgr_status_t launch_mode(const AttnIO& io, const void* c1, int64_t ld_c1, const void* c2,
-                                 int64_t ld_c2, const void* r2, int64_t ld_r2, const Args& args,
-                                 cudaStream_t st) {
+static mtgr_status_t launch_mode(const AttnIO& io, const void* c1, int64_t ld_c1, const void* x,
+                                 int64_t ld_x, const void* r1, int64_t ld_r1, const void* r2,
+                                 int64_t ld_r2, const void* e, int64_t ld_e, const void* uu,
+                                 int64_t ld_u, const Args& args, cudaStream_t st) {
   const int T = io.jag.total_tokens, d = io.d;
-  CUtensorMap m1, m2, m3;
-  MTGR_TRY(make_tmap_bf16(&m1, c1, d, T, ld_c1, 64, BC));
-  MTGR_TRY(make_tmap_bf16(&m2, c2, d, T, ld_c2, 64, BC));
-  if (r2) MTGR_TRY(make_tmap_bf16(&m3, r2, d, T, ld_r2, 64, BR));
-  else m3 = m1;
+  Maps m;
+  MTGR_TRY(make_tmap_bf16(&m.c1, c1, d, T, ld_c1, 64, BC));
+  MTGR_TRY(make_tmap_bf16(&m.x, x, d, T, ld_x, 64, BC));
+  MTGR_TRY(make_tmap_bf16(&m.r1, r1, d, T, ld_r1, 64, BR));
+  if (r2) MTGR_TRY(make_tmap_bf16(&m.r2, r2, d, T, ld_r2, 64, BR)); else m.r2 = m.r1;
+  MTGR_TRY(make_tmap_bf16(&m.e, e, d, T, ld_e, 64, BR));
+  if (uu) MTGR_TRY(make_tmap_bf16(&m.u, uu, d, T, ld_u, 64, BR)); else m.u = m.e;
+  Args a2 = args;
+  a2.has_u = uu != nullptr;
   dim3 grid(ceil_div(io.jag.max_len, BR), io.H, io.jag.num_users);
   ProfScope ps(MODE == FWD ? PROF_ATTN_FWD : MODE == DV ? PROF_ATTN_DV : MODE == DK ? PROF_ATTN_DK : PROF_ATTN_DQ, st);
   cudaFuncSetAttribute(attn_tc_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
   static const bool trace = getenv("MTGR_ATTN_TRACE") != nullptr;
-  Args a2 = args;
   if (trace) {  // debug only: time-stamp one CTA's pipeline events
     cudaMalloc(&a2.dbg, 11 * 64 * sizeof(long long));
     cudaMemsetAsync(a2.dbg, 0, 11 * 64 * sizeof(long long), st);
   }
-  attn_tc_kernel<MODE><<<grid, 384, SMEM_BYTES, st>>>(m1, m2, m3, a2);
+  attn_tc_kernel<MODE><<<grid, 384, SMEM_BYTES, st>>>(m.c1, m.x, m.r1, m.r2, m.e, m.u, a2);
   if (trace) {
-    long long h[11 * 64];
-    cudaMemcpyAsync(h, a2.dbg, sizeof(h), cudaMemcpyDeviceToHost, st);
+    long long hb[11 * 64];
+    cudaMemcpyAsync(hb, a2.dbg, sizeof(hb), cudaMemcpyDeviceToHost, st);
     cudaStreamSynchronize(st);
     cudaFree(a2.dbg);
     fprintf(stderr, "ATTN_TRACE mode=%d", MODE);
-    for (int i = 0; i < 11 * 64; ++i) fprintf(stderr, " %lld", h[i]);
+    for (int i = 0; i < 11 * 64; ++i) fprintf(stderr, " %lld", hb[i]);
     fprintf(stderr, "\n");
   }
   return check_launch("attn_tc");
@@ -480,15 +576,14 @@ mtgr_status_t attn_tc_fwd_launch(const AttnIO& io, cudaStream_t st) {
   using namespace tca;
   if (io.jag.num_users == 0 || io.jag.max_len == 0 || io.jag.total_tokens == 0) return MTGR_OK;
   MTGR_CHECK(io.u && io.y, MTGR_E_UNSUPPORTED, "tc attention forward needs the gate (u, y)");
-  typedef __nv_bfloat16 bf;
+  MTGR_CHECK(io.d % 8 == 0, MTGR_E_LAYOUT, "d_model must be a multiple of 8");
   Args a{};
   a.jag = io.jag; a.H = io.H; a.d = io.d;
-  a.r1 = (const bf*)io.q; a.ld_r1 = io.ld;
-  a.e = (const bf*)io.v; a.ld_e = io.ld;
-  a.u = (const bf*)io.u; a.ld_u = io.ld;
-  a.out = (bf*)io.o; a.out2 = (bf*)io.y; a.ld_out = io.d;
+  a.out = (__nv_bfloat16*)io.o; a.out2 = (__nv_bfloat16*)io.y; a.ld_out = io.d;
   a.diag = io.diag_a;
-  return launch_mode<FWD>(io, io.k, io.ld, io.v, io.ld, nullptr, 0, a, st);
+  // C1 = K, X = V, R1 = Q, E = V, U = U
+  return launch_mode<FWD>(io, io.k, io.ld, io.v, io.ld, io.q, io.ld, nullptr, 0, io.v, io.ld, io.u,
+                          io.ld, a, st);
 }
 
 mtgr_status_t attn_tc_bwd_launch(const AttnIO& io, cudaStream_t st) {
@@ -496,35 +591,27 @@ mtgr_status_t attn_tc_bwd_launch(const AttnIO& io, cudaStream_t st) {
   if (io.jag.num_users == 0 || io.jag.max_len == 0 || io.jag.total_tokens == 0) return MTGR_OK;
   typedef __nv_bfloat16 bf;
   const bf* pre = (const bf*)io.pre;
-  {  // dV = nu P^T dO (+ diag a_jj dO_j), * silu'(p_V)
+  const int64_t D = io.d;
+  {  // dV = nu P^T dO (+ diag a_jj dO_j), * silu'(p_V): C1 = Q, X = dO, R1 = K, E = dO, U = p_V
     Args a{};
     a.jag = io.jag; a.H = io.H; a.d = io.d;
-    a.r1 = (const bf*)io.k; a.ld_r1 = io.ld;
-    a.e = (const bf*)io.dO; a.ld_e = io.d;
-    a.pre = pre ? pre + 2 * (int64_t)io.d : nullptr; a.ld_pre = io.ld_pre;
-    a.out = (bf*)io.dv; a.ld_out = io.ld_out;
-    a.diag = io.diag_a;
-    MTGR_TRY(launch_mode<DV>(io, io.q, io.ld, io.dO, io.d, nullptr, 0, a, st));
+    a.out = (bf*)io.dv; a.ld_out = io.ld_out; a.diag = io.diag_a;
+    MTGR_TRY(launch_mode<DV>(io, io.q, io.ld, io.dO, D, io.k, io.ld, nullptr, 0, io.dO, D,
+                             pre ? pre + 2 * D : nullptr, io.ld_pre, a, st));
   }
-  {  // dK = nu dS^T Q (+ diag ds_jj q_j), * silu'(p_K)
+  {  // dK = nu dS^T Q (+ diag ds_jj q_j), * silu'(p_K): C1 = Q, C2 = dO, R1 = K, R2 = V, E = Q
     Args a{};
     a.jag = io.jag; a.H = io.H; a.d = io.d;
-    a.r1 = (const bf*)io.k; a.ld_r1 = io.ld;
-    a.e = (const bf*)io.q; a.ld_e = io.ld;
-    a.pre = pre ? pre + (int64_t)io.d : nullptr; a.ld_pre = io.ld_pre;
-    a.out = (bf*)io.dk; a.ld_out = io.ld_out;
-    a.diag = io.diag_ds;
-    MTGR_TRY(launch_mode<DK>(io, io.q, io.ld, io.dO, io.d, io.v, io.ld, a, st));
+    a.out = (bf*)io.dk; a.ld_out = io.ld_out; a.diag = io.diag_ds;
+    MTGR_TRY(launch_mode<DK>(io, io.q, io.ld, io.dO, D, io.k, io.ld, io.v, io.ld, io.q, io.ld,
+                             pre ? pre + D : nullptr, io.ld_pre, a, st));
   }
-  {  // dQ = nu dS K (+ diag ds_ii k_i), * silu'(p_Q)
+  {  // dQ = nu dS K (+ diag ds_ii k_i), * silu'(p_Q): C1 = K, C2 = V, R1 = Q, R2 = dO, E = K
     Args a{};
     a.jag = io.jag; a.H = io.H; a.d = io.d;
-    a.r1 = (const bf*)io.q; a.ld_r1 = io.ld;
-    a.e = (const bf*)io.k; a.ld_e = io.ld;
-    a.pre = pre; a.ld_pre = io.ld_pre;
-    a.out = (bf*)io.dq; a.ld_out = io.ld_out;
-    a.diag = io.diag_ds;
-    MTGR_TRY(launch_mode<DQ>(io, io.k, io.ld, io.v, io.ld, io.dO, io.d, a, st));
+    a.out = (bf*)io.dq; a.ld_out = io.ld_out; a.diag = io.diag_ds;
+    MTGR_TRY(launch_mode<DQ>(io, io.k, io.ld, io.v, io.ld, io.q, io.ld, io.dO, D, io.k, io.ld, pre,
+                             io.ld_pre, a, st));
   }
   return MTGR_OK;
 }
