@@ -10,13 +10,13 @@
 //   DK   | K                  | V         | Q              | Q  (= C1)  | dS^T              | dK
 //   (DQ/DK also stream C2 = V / dO for dP = R2 C2^T.)
 //
-// Per column tile:  S = R1 C1^T (tcgen05.mma, A from TMEM, B = C1 K-major smem, M=128 N=64
-// K=256) [and dP = R2 C2^T, SS];  8 "softmax" warps tcgen05.ld S (and dP), apply the mask
-// predicate in registers and SiLU / SiLU' (tanh.approx), write the bf16 T tile into a
-// SWIZZLE_128B smem buffer;  acc += T X (M=128 N=256 K=64, B = X MN-major — the same
-// TMA-loaded tile read with an MN-major descriptor).  Dependent N=64 MMA chains are
-// latency-bound, so two independent chains are always interleaved: S of two column tiles
-// (FWD/DV) or S and dP of one tile (DQ/DK).
+// Per column tile:  S = R1 C1^T (tcgen05.mma SS: A = R1 resident in smem, B = C1 K-major,
+// M=128 N=64 K=256) [and dP = R2 C2^T];  8 "softmax" warps tcgen05.ld S (and dP), apply the
+// mask predicate in registers and SiLU / SiLU' (tanh.approx), and tcgen05.st the bf16 T tile
+// into TMEM;  acc += T X (A = T from TMEM, B = X MN-major — the same TMA-loaded tile read with
+// an MN-major descriptor, M=128 N=256 K=64).  (Measured: with A from TMEM an N=64 MMA is bound
+// by the TMEM A-operand read, ~70 cycles instead of 32, so the N=64 score MMAs read A from smem
+// and only the N=256 accumulate MMAs read A from TMEM.)
 // The 1/N factor, the diagonal term of non-static tokens (R#9: candidates and real-time tokens
 // see themselves), the gate (FWD: y = o*u) and the QKV activation backward (silu'(p)) are fused
 // into the epilogue, which stages E/U tiles and the outputs in shared memory (TMA in, coalesced
@@ -24,10 +24,10 @@
 // are visible only to themselves, rule 3 P:338) and to [0, n_static) when every row of the tile
 // is static (R#8), so fully masked tiles are never loaded.
 //
-// Warp roles (384 threads): w0 TMA producer (R1, R2, C1, E), w1 MMA issuer, w2 TMEM allocator,
-// w3 TMA producer (X or C2, U), w4-w11 softmax/epilogue (two warps per TMEM lane quadrant,
-// thread = row = TMEM lane).  TMEM: R1 [0,128) (bf16 pairs), acc [128,384), S [384,448),
-// S' / dP [448,512).
+// Warp roles (384 threads): w0 TMA producer (R1, R2, C1, E, U), w1 MMA issuer, w2 TMEM allocator,
+// w3 TMA producer (X or C2), w4-w11 softmax/epilogue (two warps per TMEM lane quadrant,
+// thread = row = TMEM lane).  TMEM: acc [0,256), S [256,384) (two buffers, or S and dP),
+// T [384,448) (two buffers of bf16 pairs).
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
@@ -51,7 +51,6 @@ constexpr int OFF_T = 192 * KB;
 constexpr int OFF_TS = OFF_T + 2 * T_BYTES;
 constexpr int OFF_BAR = OFF_TS + BC * 8;
 constexpr int SMEM_BYTES = OFF_BAR + 512 + 1024;
-constexpr uint32_t COL_R1 = 0, COL_ACC = 128, COL_S = 384;
 constexpr int NSM = 8;  // softmax/epilogue warps
 
 enum { FWD = 0, DV = 1, DQ = 2, DK = 3 };
@@ -94,13 +93,18 @@ __global__ void __launch_bounds__(384, 1)
   using namespace sm100;
   constexpr bool TWO = (MODE == DQ || MODE == DK);
   constexpr bool TRANS = (MODE == DV || MODE == DK);
-  // smem regions (see header)
-  constexpr int OFF_C1 = TWO ? 64 * KB : 0;           // C1 ring, 3 slots
-  constexpr int OFF_X = TWO ? 160 * KB : 96 * KB;     // X ring (3 slots) or C2 slot (1)
-  constexpr int NX = TWO ? 1 : 3;
-  constexpr int OFF_R1STAGE = TWO ? 128 * KB : 96 * KB;
-  constexpr int OFF_E = 0;                            // free after the last score MMA
-  constexpr int OFF_U = TWO ? 64 * KB : 96 * KB;      // free after the last acc MMA
+  // smem map (KB):         !TWO                        TWO
+  //   [0,64)    R1 (S A operand)  -> E            R1 -> E
+  //   [64,128)  C1 slots 0,1      -> U            R2 (dP A operand) -> U
+  //   [128,192) X slots 0,1                        C1 slots 0,1
+  //   [192,224) C1 slot 2                          C2 slot
+  // E and U are loaded once every score MMA has completed (their regions are then free).
+  constexpr int OFF_R1 = 0, OFF_R2 = 64 * KB, OFF_E = 0, OFF_U = 64 * KB;
+  constexpr int NC1 = TWO ? 2 : 3;
+  constexpr int NX = TWO ? 1 : 2;
+  constexpr int OFF_X = TWO ? 192 * KB : 128 * KB;
+  // TMEM columns: acc [0,256) | S buffers [256,384) (TWO: S, dP) | P buffers [384,448)
+  constexpr uint32_t T_ACC = 0, T_S = 256, T_P = 384;
 
   const int u = blockIdx.z, h = blockIdx.y, r0 = blockIdx.x * BR;
   const UserSpan us = load_user(a.jag, u);
@@ -117,7 +121,6 @@ __global__ void __launch_bounds__(384, 1)
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sT = smem + OFF_T;
   long long* sTs = reinterpret_cast<long long*>(smem + OFF_TS);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
   uint64_t* c1_full = bars;           // [3]
@@ -126,16 +129,19 @@ __global__ void __launch_bounds__(384, 1)
   uint64_t* x_empty = bars + 9;       // [3]
   uint64_t* s_full = bars + 12;       // [2]
   uint64_t* s_free = bars + 14;       // [2]
-  uint64_t* t_full = bars + 16;       // [2]
-  uint64_t* t_free = bars + 18;       // [2]
+  uint64_t* t_full = bars + 16;       // [2]  P buffer written
+  uint64_t* t_free = bars + 18;       // [2]  P buffer consumed by its acc MMAs
   uint64_t* r1_full = bars + 20;
-  uint64_t* r1_done = bars + 21;
   uint64_t* r2_full = bars + 22;
   uint64_t* e_full = bars + 23;
   uint64_t* u_full = bars + 24;
   uint64_t* o_full = bars + 25;
   uint64_t* sc_done = bars + 26;      // every score MMA (S, dP) has completed
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 27);
+  auto c1_slot = [&](int t) -> uint8_t* {
+    const int sl = t % NC1;
+    return TWO ? smem + 128 * KB + sl * CT_BYTES : (sl < 2 ? smem + 64 * KB + sl * CT_BYTES : smem + 192 * KB);
+  };
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) DBG(10 * 64 + 4);
@@ -152,7 +158,6 @@ __global__ void __launch_bounds__(384, 1)
       mbar_init(&t_full[b], 32 * NSM); mbar_init(&t_free[b], 1);
     }
     mbar_init(r1_full, 1);
-    mbar_init(r1_done, 32 * NSM);
     mbar_init(r2_full, 1);
     mbar_init(e_full, 1);
     mbar_init(u_full, 1);
@@ -169,40 +174,40 @@ __global__ void __launch_bounds__(384, 1)
   const int row0 = us.off + r0;  // global row of the tile's first row
 
   if (warp == 0) {
-    // ---------------------------------------------------------------- producer A: R1, R2, C1, E
+    // ---------------------------------------------------------------- producer A: R1, R2, C1, E, U
     if (lane == 0) {
-      mbar_expect_tx(r1_full, RT_BYTES);
-#pragma unroll
-      for (int c = 0; c < 4; ++c) tma_load_2d(smem + OFF_R1STAGE + c * (RT_BYTES / 4), &tmR1, r1_full, hcol + c * 64, row0);
       if (ntiles > 0) {
+        mbar_expect_tx(r1_full, RT_BYTES);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) tma_load_2d(smem + OFF_R1 + c * (RT_BYTES / 4), &tmR1, r1_full, hcol + c * 64, row0);
         if (TWO) {
           mbar_expect_tx(r2_full, RT_BYTES);
 #pragma unroll
-          for (int c = 0; c < 4; ++c) tma_load_2d(smem + c * (RT_BYTES / 4), &tmR2, r2_full, hcol + c * 64, row0);
+          for (int c = 0; c < 4; ++c) tma_load_2d(smem + OFF_R2 + c * (RT_BYTES / 4), &tmR2, r2_full, hcol + c * 64, row0);
         }
         for (int t = 0; t < ntiles; ++t) {
-          const int slot = t % 3;
-          if (TWO && t == 2) mbar_wait(r1_done, 0);  // slot 2 overlaps the R1 staging area
-          mbar_wait(&c1_empty[slot], ((t / 3) & 1) ^ 1);
+          const int slot = t % NC1;
+          mbar_wait(&c1_empty[slot], ((t / NC1) & 1) ^ 1);
           mbar_expect_tx(&c1_full[slot], CT_BYTES);
           const int row = us.off + c_begin + t * BC;
-          uint8_t* dst = smem + OFF_C1 + slot * CT_BYTES;
+          uint8_t* dst = c1_slot(t);
 #pragma unroll
           for (int c = 0; c < 4; ++c) tma_load_2d(dst + c * (CT_BYTES / 4), &tmC1, &c1_full[slot], hcol + c * 64, row);
         }
-        // E tile once every score MMA is done (the C1 ring / R2 region is then free)
-        mbar_wait(sc_done, 0);
-      } else {
-        mbar_wait(r1_done, 0);  // E overlaps the R1 staging area when there is no mainloop
+        mbar_wait(sc_done, 0);  // R1 / R2 / C1 slots 0,1 are free from here on
       }
       mbar_expect_tx(e_full, RT_BYTES);
 #pragma unroll
       for (int c = 0; c < 4; ++c) tma_load_2d(smem + OFF_E + c * (RT_BYTES / 4), &tmE, e_full, hcol + c * 64, row0);
+      if (a.has_u) {
+        mbar_expect_tx(u_full, RT_BYTES);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) tma_load_2d(smem + OFF_U + c * (RT_BYTES / 4), &tmU, u_full, hcol + c * 64, row0);
+      }
     }
   } else if (warp == 3) {
-    // ---------------------------------------------------------------- producer B: X / C2, U
+    // ---------------------------------------------------------------- producer B: X or C2
     if (lane == 0) {
-      mbar_wait(r1_done, 0);  // the R1 staging area overlaps this ring
       for (int t = 0; t < ntiles; ++t) {
         const int slot = t % NX;
         mbar_wait(&x_empty[slot], ((t / NX) & 1) ^ 1);
@@ -212,113 +217,81 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
         for (int c = 0; c < 4; ++c) tma_load_2d(dst + c * (CT_BYTES / 4), &tmX, &x_full[slot], hcol + c * 64, row);
       }
-      if (a.has_u) {
-        mbar_wait(o_full, 0);
-        mbar_expect_tx(u_full, RT_BYTES);
-#pragma unroll
-        for (int c = 0; c < 4; ++c) tma_load_2d(smem + OFF_U + c * (RT_BYTES / 4), &tmU, u_full, hcol + c * 64, row0);
-      }
     }
   } else if (warp == 1) {
     // ---------------------------------------------------------------- MMA issuer
-    if (lane == 0) {
-      if (ntiles == 0) {
-        mbar_arrive(o_full);
-      } else {
-        constexpr uint32_t idesc_s = idesc_bf16_f32(BR, BC, 0, 0);
-        constexpr uint32_t idesc_acc = idesc_bf16_f32(BR, DH, 0, 1);
-        const uint32_t t_base = smem_u32(sT);
-        const uint32_t c1_base = smem_u32(smem + OFF_C1);
-        const uint32_t x_base = smem_u32(smem + OFF_X);
-        const uint32_t r2_base = smem_u32(smem);
-        mbar_wait(r1_done, 0);
-        if (TWO) mbar_wait(r2_full, 0);
+    // The whole warp walks the schedule so every operand is warp-uniform (uniform registers, no
+    // per-instruction waterfall); one elected lane issues the tcgen05 instructions.
+    const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
+    const int nt = __shfl_sync(0xffffffffu, ntiles, 0);
+    if (nt == 0) {
+      if (lane == 0) mbar_arrive(o_full);
+    } else {
+      constexpr uint32_t idesc_s = idesc_bf16_f32(BR, BC, 0, 0);
+      constexpr uint32_t idesc_acc = idesc_bf16_f32(BR, DH, 0, 1);
+      const uint32_t r1_base = smem_u32(smem + OFF_R1);
+      const uint32_t r2_base = smem_u32(smem + OFF_R2);
+      const uint32_t x_base = smem_u32(smem + OFF_X);
+      mbar_wait(r1_full, 0);
+      if (TWO) mbar_wait(r2_full, 0);
+      // acc += P_j X_j  (A = P from TMEM, B = X MN-major)
+      auto acc = [&](int j) {
+        const int tb = j & 1;
+        if (j < 64 && lane == 0) DBG(3 * 64 + j);
+        mbar_wait(&t_full[tb], (j >> 1) & 1);
+        if (j < 64 && lane == 0) DBG(4 * 64 + j);
+        uint32_t x;
+        if (TWO) {
+          x = smem_u32(c1_slot(j));  // X = C1 (held in the C1 ring until here)
+        } else {
+          mbar_wait(&x_full[j % NX], (j / NX) & 1);
+          x = x_base + (j % NX) * CT_BYTES;
+        }
         tc_fence_after();
-        // acc += T_j X_j
-        auto acc = [&](int j) {
-          const int tb = j & 1;
-          if (j < 64) DBG(3 * 64 + j);
-          mbar_wait(&t_full[tb], (j >> 1) & 1);
-          if (j < 64) DBG(4 * 64 + j);
-          uint32_t x;
-          if (TWO) {
-            x = c1_base + (j % 3) * CT_BYTES;  // X = C1 (held in the C1 ring until here)
-          } else {
-            mbar_wait(&x_full[j % 3], (j / 3) & 1);
-            x = x_base + (j % 3) * CT_BYTES;
-          }
-          tc_fence_after();
+        if (elect_one()) {
 #pragma unroll
           for (int k = 0; k < BC / 16; ++k)
-            mma_bf16_ss(tmem + COL_ACC, desc_sw128(t_base + tb * T_BYTES + k * 32, 16, 1024),
+            mma_bf16_ts(tm + T_ACC, tm + T_P + tb * 32 + k * 8,
                         desc_sw128(x + k * 2048, CT_BYTES / 4, 1024), idesc_acc, (j > 0 || k > 0));
           mma_commit(&t_free[tb]);
-          if (TWO) mma_commit(&c1_empty[j % 3]);
-          else mma_commit(&x_empty[j % 3]);
-        };
-        if (!TWO) {
-          // two independent S chains (tiles t, t+1) interleaved, then the accs of the previous pair
-          for (int t = 0; t < ntiles; t += 2) {
-            const bool b = t + 1 < ntiles;
-            if (t < 64) DBG(0 * 64 + t);
-            mbar_wait(&c1_full[t % 3], (t / 3) & 1);
-            if (b) mbar_wait(&c1_full[(t + 1) % 3], ((t + 1) / 3) & 1);
-            if (t < 64) DBG(1 * 64 + t);
-            mbar_wait(&s_free[0], ((t >> 1) & 1) ^ 1);
-            if (b) mbar_wait(&s_free[1], ((t >> 1) & 1) ^ 1);
-            if (t < 64) DBG(2 * 64 + t);
-            tc_fence_after();
-            const uint32_t ka = c1_base + (t % 3) * CT_BYTES;
-            const uint32_t kb = c1_base + ((t + 1) % 3) * CT_BYTES;
-#pragma unroll
-            for (int k = 0; k < DH / 16; ++k) {
-              const uint32_t off = (k >> 2) * (CT_BYTES / 4) + (k & 3) * 32;
-              mma_bf16_ts(tmem + COL_S, tmem + COL_R1 + k * 8, desc_sw128(ka + off, 16, 1024), idesc_s, k > 0);
-              if (b) mma_bf16_ts(tmem + COL_S + BC, tmem + COL_R1 + k * 8, desc_sw128(kb + off, 16, 1024), idesc_s, k > 0);
-            }
-            mma_commit(&s_full[0]);
-            mma_commit(&c1_empty[t % 3]);
-            if (b) {
-              mma_commit(&s_full[1]);
-              mma_commit(&c1_empty[(t + 1) % 3]);
-            }
-            if (t + 2 >= ntiles) mma_commit(sc_done);
-            if (t >= 2) {
-              acc(t - 2);
-              acc(t - 1);
-            }
-          }
-          const int tl = (ntiles - 1) & ~1;  // first tile of the last pair
-          acc(tl);
-          if (tl + 1 < ntiles) acc(tl + 1);
-        } else {
-          // S and dP of one tile interleaved (independent chains), then the acc of the previous tile
-          for (int t = 0; t < ntiles; ++t) {
-            if (t < 64) DBG(0 * 64 + t);
-            mbar_wait(&c1_full[t % 3], (t / 3) & 1);
-            mbar_wait(&x_full[0], t & 1);
-            if (t < 64) DBG(1 * 64 + t);
-            mbar_wait(&s_free[0], (t & 1) ^ 1);
-            if (t < 64) DBG(2 * 64 + t);
-            tc_fence_after();
-            const uint32_t c1 = c1_base + (t % 3) * CT_BYTES;
-#pragma unroll
-            for (int k = 0; k < DH / 16; ++k) {
-              const uint32_t off = (k >> 2) * (CT_BYTES / 4) + (k & 3) * 32;
-              mma_bf16_ts(tmem + COL_S, tmem + COL_R1 + k * 8, desc_sw128(c1 + off, 16, 1024), idesc_s, k > 0);
-              mma_bf16_ss(tmem + COL_S + BC,
-                          desc_sw128(r2_base + (k >> 2) * (RT_BYTES / 4) + (k & 3) * 32, 16, 1024),
-                          desc_sw128(x_base + off, 16, 1024), idesc_s, k > 0);
-            }
-            mma_commit(&s_full[0]);
-            mma_commit(&x_empty[0]);
-            if (t + 1 == ntiles) mma_commit(sc_done);
-            if (t >= 1) acc(t - 1);
-          }
-          acc(ntiles - 1);
+          if (TWO) mma_commit(&c1_empty[j % NC1]);
+          else mma_commit(&x_empty[j % NX]);
         }
-        mma_commit(o_full);
+        __syncwarp();
+      };
+      for (int t = 0; t < nt; ++t) {
+        const int sb = TWO ? 0 : (t & 1);
+        const int use = TWO ? t : (t >> 1);
+        if (t < 64 && lane == 0) DBG(0 * 64 + t);
+        mbar_wait(&c1_full[t % NC1], (t / NC1) & 1);
+        if (TWO) mbar_wait(&x_full[0], t & 1);
+        if (t < 64 && lane == 0) DBG(1 * 64 + t);
+        mbar_wait(&s_free[sb], (use & 1) ^ 1);
+        if (t < 64 && lane == 0) DBG(2 * 64 + t);
+        tc_fence_after();
+        const uint32_t c1 = smem_u32(c1_slot(t));
+        if (elect_one()) {
+#pragma unroll
+          for (int k = 0; k < DH / 16; ++k) {
+            const uint32_t aoff = (k >> 2) * (RT_BYTES / 4) + (k & 3) * 32;
+            const uint32_t boff = (k >> 2) * (CT_BYTES / 4) + (k & 3) * 32;
+            mma_bf16_ss(tm + T_S + sb * BC, desc_sw128(r1_base + aoff, 16, 1024),
+                        desc_sw128(c1 + boff, 16, 1024), idesc_s, k > 0);
+            if (TWO)
+              mma_bf16_ss(tm + T_S + BC, desc_sw128(r2_base + aoff, 16, 1024),
+                          desc_sw128(x_base + boff, 16, 1024), idesc_s, k > 0);
+          }
+          mma_commit(&s_full[sb]);
+          if (TWO) mma_commit(&x_empty[0]);
+          else mma_commit(&c1_empty[t % NC1]);
+          if (t + 1 == nt) mma_commit(sc_done);
+        }
+        __syncwarp();
+        if (t >= 1) acc(t - 1);
       }
+      acc(nt - 1);
+      if (elect_one()) mma_commit(o_full);
+      __syncwarp();
     }
   } else if (warp >= 4) {
     // ---------------------------------------------------------------- softmax + epilogue
@@ -330,22 +303,6 @@ __global__ void __launch_bounds__(384, 1)
     const int my = r0 + row;                 // user-local index of this thread's row
     const int64_t g = (int64_t)row0 + row;   // global token index
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
-    // R1 row (this warp's 128 head-dim columns) smem -> TMEM as bf16 pairs
-    mbar_wait(r1_full, 0);
-#pragma unroll 1
-    for (int cc = 0; cc < 2; ++cc) {
-      const uint8_t* box = smem + OFF_R1STAGE + (half * 2 + cc) * (RT_BYTES / 4);
-      uint32_t w[32];
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const uint4 v = *reinterpret_cast<const uint4*>(box + sw128(row, j));
-        w[4 * j] = v.x; w[4 * j + 1] = v.y; w[4 * j + 2] = v.z; w[4 * j + 3] = v.w;
-      }
-      tmem_st32(tmem + COL_R1 + half * 64 + cc * 32 + lane_off, w);
-    }
-    tmem_st_wait();
-    tc_fence_before();
-    mbar_arrive(r1_done);
     if (warp == 4 && lane == 0) DBG(10 * 64 + 3);
 
     const long long my_ts = (my < us.L && a.jag.ts) ? a.jag.ts[g] : 0;
@@ -371,10 +328,10 @@ __global__ void __launch_bounds__(384, 1)
       tc_fence_after();
       uint32_t s[32];
       uint32_t dp[TWO ? 32 : 1];
-      tmem_ld32(tmem + COL_S + sb * BC + j_half + lane_off, s);
+      tmem_ld32(tmem + T_S + sb * BC + j_half + lane_off, s);
       if constexpr (TWO) {
         uint32_t (&d0)[32] = *reinterpret_cast<uint32_t(*)[32]>(&dp[0]);
-        tmem_ld32(tmem + COL_S + BC + j_half + lane_off, d0);
+        tmem_ld32(tmem + T_S + BC + j_half + lane_off, d0);
       }
       tmem_ld_wait();
       tc_fence_before();
@@ -411,7 +368,7 @@ __global__ void __launch_bounds__(384, 1)
           vis = 0;
         }
       }
-      // T values -> bf16 -> swizzled smem (row = 128 B, 16-byte chunk c at c ^ (row & 7))
+      // P (T) values -> bf16 pairs -> TMEM P buffer (A operand of the acc MMA)
       uint32_t pk[16];
 #pragma unroll
       for (int e = 0; e < 32; e += 2) {
@@ -434,12 +391,10 @@ __global__ void __launch_bounds__(384, 1)
       if (dbgt) DBG(7 * 64 + t);
       mbar_wait(&t_free[tb], ((t >> 1) & 1) ^ 1);
       if (dbgt) DBG(8 * 64 + t);
-      uint8_t* tbuf = sT + tb * T_BYTES;
-#pragma unroll
-      for (int c = 0; c < 4; ++c)
-        *reinterpret_cast<uint4*>(tbuf + sw128(row, half * 4 + c)) =
-            make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
-      fence_proxy_async_smem();
+      tc_fence_after();
+      tmem_st16(tmem + T_P + tb * 32 + half * 16 + lane_off, pk);
+      tmem_st_wait();
+      tc_fence_before();
       mbar_arrive(&t_full[tb]);
       if (dbgt) DBG(9 * 64 + t);
     }
@@ -460,7 +415,7 @@ __global__ void __launch_bounds__(384, 1)
       const int acol = half * 128 + cc * 32;  // head-dim column of this chunk
       uint32_t r[32];
       if (ntiles > 0) {
-        tmem_ld32(tmem + COL_ACC + acol + lane_off, r);
+        tmem_ld32(tmem + T_ACC + acol + lane_off, r);
         tmem_ld_wait();
       } else {
 #pragma unroll

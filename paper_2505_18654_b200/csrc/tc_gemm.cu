@@ -133,37 +133,42 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      const uint32_t idesc = idesc_bf16_f32(BM, BN, p.a_mn, p.b_mn);
-      int stage = 0;
-      uint32_t phase = 0;
-      int it = 0;
-      for (int item = blockIdx.x; item < total; item += gridDim.x, ++it) {
-        const int sp = item / (p.num_n * p.num_m);
-        const int kb0 = sp * p.kb_per_split, kb1 = min(p.num_kb, kb0 + p.kb_per_split);
-        const int buf = it & 1;
-        const uint32_t acc_phase = (it >> 1) & 1;
-        mbar_wait(&tempty[buf], acc_phase ^ 1);
+    // the whole warp walks the schedule (warp-uniform operands); one elected lane issues
+    const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
+    const int a_mn = __shfl_sync(0xffffffffu, p.a_mn, 0), b_mn = __shfl_sync(0xffffffffu, p.b_mn, 0);
+    const uint32_t idesc = idesc_bf16_f32(BM, BN, a_mn, b_mn);
+    int stage = 0;
+    uint32_t phase = 0;
+    int it = 0;
+    for (int item = blockIdx.x; item < total; item += gridDim.x, ++it) {
+      const int sp = item / (p.num_n * p.num_m);
+      const int kb0 = sp * p.kb_per_split, kb1 = min(p.num_kb, kb0 + p.kb_per_split);
+      const int buf = it & 1;
+      const uint32_t acc_phase = (it >> 1) & 1;
+      mbar_wait(&tempty[buf], acc_phase ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tm + buf * BN;
+      for (int kb = kb0; kb < kb1; ++kb) {
+        mbar_wait(&full[stage], phase);
         tc_fence_after();
-        const uint32_t d_tmem = tmem + buf * BN;
-        for (int kb = kb0; kb < kb1; ++kb) {
-          mbar_wait(&full[stage], phase);
-          tc_fence_after();
-          const uint32_t a_base = smem_u32(sA + stage * A_BYTES);
-          const uint32_t b_base = smem_u32(sB + stage * B_BYTES);
+        const uint32_t a_base = smem_u32(sA + stage * A_BYTES);
+        const uint32_t b_base = smem_u32(sB + stage * B_BYTES);
+        if (elect_one()) {
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) {
-            const uint64_t ad = p.a_mn ? desc_sw128(a_base + k * 2048, 8192, 1024)
-                                       : desc_sw128(a_base + k * 32, 16, 1024);
-            const uint64_t bd = p.b_mn ? desc_sw128(b_base + k * 2048, 8192, 1024)
-                                       : desc_sw128(b_base + k * 32, 16, 1024);
+            const uint64_t ad = a_mn ? desc_sw128(a_base + k * 2048, 8192, 1024)
+                                     : desc_sw128(a_base + k * 32, 16, 1024);
+            const uint64_t bd = b_mn ? desc_sw128(b_base + k * 2048, 8192, 1024)
+                                     : desc_sw128(b_base + k * 32, 16, 1024);
             mma_bf16_ss(d_tmem, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
           }
           mma_commit(&empty[stage]);
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
-        mma_commit(&tfull[buf]);
+        __syncwarp();
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
+      if (elect_one()) mma_commit(&tfull[buf]);
+      __syncwarp();
     }
   } else if (warp >= 4) {
     const int ew = warp - 4;
