@@ -265,19 +265,13 @@ def run_mtgr(args, cfg, rank, world, local_rank):
     stack.bind(jb)
     x_dev = torch.from_numpy(X).to(dev, dt)
     dz_dev = torch.from_numpy(dZ).to(dev, dt)
-    inv_B = 1.0 / wl["B_g"]
-    works = []
-
-    def allreduce_hook(li, bucket):
-        if world > 1:
-            works.append(dist.all_reduce(bucket, async_op=True))
+    from paper_2505_18654_b200.dp import GradAggregator
+    agg = GradAggregator(wl["B_g"])  # per-layer bucket all-reduce (NCCL) + 1/B_global
 
     def step(xin=x_dev, dzin=dz_dev):
         stack.forward(xin)
-        stack.backward(dzin, on_layer_done=allreduce_hook)
-        while works:
-            works.pop(0).wait()
-        m.scale_(stack.grad_flat, inv_B)
+        stack.backward(dzin, on_layer_done=agg.on_layer_done)
+        agg.finish(stack.grad_flat)
 
     def barrier():
         if world > 1:
