@@ -85,7 +85,7 @@ __device__ __forceinline__ uint32_t pack2(float a, float b) {
 __device__ __forceinline__ uint32_t sw128(int r, int j) { return r * 128 + ((j ^ (r & 7)) << 4); }
 
 template <int MODE>
-__global__ void __launch_bounds__(384, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tmC1, const __grid_constant__ CUtensorMap tmX,
                    const __grid_constant__ CUtensorMap tmR1, const __grid_constant__ CUtensorMap tmR2,
                    const __grid_constant__ CUtensorMap tmE, const __grid_constant__ CUtensorMap tmU,
@@ -106,15 +106,23 @@ __global__ void __launch_bounds__(384, 1)
   // TMEM columns: acc [0,256) | S buffers [256,384) (TWO: S, dP) | P buffers [384,448)
   constexpr uint32_t T_ACC = 0, T_S = 256, T_P = 384;
 
+  // A cluster = two consecutive row tiles of the same (user, head): the column tiles they both
+  // stream are loaded once from L2 and multicast into both CTAs (each CTA issues half of the
+  // boxes), halving L2->SM traffic.  The column range is the union over the pair (the mask
+  // predicate makes the extra tiles exact zeros).  The second CTA of a user with an odd number
+  // of row tiles runs the pipeline on masked rows and stores nothing.
   const int u = blockIdx.z, h = blockIdx.y, r0 = blockIdx.x * BR;
+  const uint16_t crank = (uint16_t)sm100::cluster_ctarank();
   const UserSpan us = load_user(a.jag, u);
-  if (r0 >= us.L) return;
+  const int pr0 = (blockIdx.x & ~1) * BR;
+  if (pr0 >= us.L) return;  // uniform over the cluster
+  const int pair_end = min(us.L, pr0 + 2 * BR);
   const int kv_end = us.ns + us.nr;
   int c_begin = 0, c_end = 0;
   if (!TRANS) {
-    c_end = (min(BR, us.L - r0) + r0 > us.ns) ? kv_end : us.ns;
-  } else if (r0 < kv_end) {
-    c_begin = (r0 < us.ns) ? 0 : us.ns;
+    c_end = (pair_end > us.ns) ? kv_end : us.ns;
+  } else if (pr0 < kv_end) {
+    c_begin = (pr0 < us.ns) ? 0 : us.ns;
     c_end = us.L;
   }
   const int ntiles = c_end > c_begin ? (c_end - c_begin + BC - 1) / BC : 0;
@@ -150,8 +158,8 @@ __global__ void __launch_bounds__(384, 1)
     tma_prefetch(&tmX);
     tma_prefetch(&tmR1);
     for (int s = 0; s < 3; ++s) {
-      mbar_init(&c1_full[s], 1); mbar_init(&c1_empty[s], 1);
-      mbar_init(&x_full[s], 1); mbar_init(&x_empty[s], 1);
+      mbar_init(&c1_full[s], 1); mbar_init(&c1_empty[s], 2);  // empties: released by both CTAs
+      mbar_init(&x_full[s], 1); mbar_init(&x_empty[s], 2);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&s_full[b], 1); mbar_init(&s_free[b], 32 * NSM);
@@ -167,7 +175,7 @@ __global__ void __launch_bounds__(384, 1)
   }
   if (warp == 2) tmem_alloc<512>(tmem_slot);
   tc_fence_before();
-  __syncthreads();
+  cluster_sync();  // barriers of both CTAs initialised before any multicast traffic
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const int hcol = h * DH;
@@ -192,7 +200,8 @@ __global__ void __launch_bounds__(384, 1)
           const int row = us.off + c_begin + t * BC;
           uint8_t* dst = c1_slot(t);
 #pragma unroll
-          for (int c = 0; c < 4; ++c) tma_load_2d(dst + c * (CT_BYTES / 4), &tmC1, &c1_full[slot], hcol + c * 64, row);
+          for (int c = crank * 2; c < crank * 2 + 2; ++c)
+            tma_load_2d_mc(dst + c * (CT_BYTES / 4), &tmC1, &c1_full[slot], hcol + c * 64, row, 0x3);
         }
         mbar_wait(sc_done, 0);  // R1 / R2 / C1 slots 0,1 are free from here on
       }
@@ -215,7 +224,8 @@ __global__ void __launch_bounds__(384, 1)
         const int row = us.off + c_begin + t * BC;
         uint8_t* dst = smem + OFF_X + slot * CT_BYTES;
 #pragma unroll
-        for (int c = 0; c < 4; ++c) tma_load_2d(dst + c * (CT_BYTES / 4), &tmX, &x_full[slot], hcol + c * 64, row);
+        for (int c = crank * 2; c < crank * 2 + 2; ++c)
+          tma_load_2d_mc(dst + c * (CT_BYTES / 4), &tmX, &x_full[slot], hcol + c * 64, row, 0x3);
       }
     }
   } else if (warp == 1) {
@@ -254,8 +264,8 @@ __global__ void __launch_bounds__(384, 1)
             mma_bf16_ts(tm + T_ACC, tm + T_P + tb * 32 + k * 8,
                         desc_sw128(x + k * 2048, CT_BYTES / 4, 1024), idesc_acc, (j > 0 || k > 0));
           mma_commit(&t_free[tb]);
-          if (TWO) mma_commit(&c1_empty[j % NC1]);
-          else mma_commit(&x_empty[j % NX]);
+          if (TWO) mma_commit_mc(&c1_empty[j % NC1], 0x3);
+          else mma_commit_mc(&x_empty[j % NX], 0x3);
         }
         __syncwarp();
       };
@@ -282,8 +292,8 @@ __global__ void __launch_bounds__(384, 1)
                           desc_sw128(x_base + boff, 16, 1024), idesc_s, k > 0);
           }
           mma_commit(&s_full[sb]);
-          if (TWO) mma_commit(&x_empty[0]);
-          else mma_commit(&c1_empty[t % NC1]);
+          if (TWO) mma_commit_mc(&x_empty[0], 0x3);
+          else mma_commit_mc(&c1_empty[t % NC1], 0x3);
           if (t + 1 == nt) mma_commit(sc_done);
         }
         __syncwarp();
@@ -476,7 +486,7 @@ __global__ void __launch_bounds__(384, 1)
   }
   if (warp == 4 && lane == 0) DBG(10 * 64 + 2);
   tc_fence_before();
-  __syncthreads();
+  cluster_sync();  // no CTA leaves while its peer may still signal its barriers
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc<512>(tmem);
@@ -502,7 +512,7 @@ static mtgr_status_t launch_mode(const AttnIO& io, const void* c1, int64_t ld_c1
   if (uu) MTGR_TRY(make_tmap_bf16(&m.u, uu, d, T, ld_u, 64, BR)); else m.u = m.e;
   Args a2 = args;
   a2.has_u = uu != nullptr;
-  dim3 grid(ceil_div(io.jag.max_len, BR), io.H, io.jag.num_users);
+  dim3 grid(2 * ceil_div(io.jag.max_len, 2 * BR), io.H, io.jag.num_users);  // cluster pairs
   ProfScope ps(MODE == FWD ? PROF_ATTN_FWD : MODE == DV ? PROF_ATTN_DV : MODE == DK ? PROF_ATTN_DK : PROF_ATTN_DQ, st);
   cudaFuncSetAttribute(attn_tc_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
   static const bool trace = getenv("MTGR_ATTN_TRACE") != nullptr;

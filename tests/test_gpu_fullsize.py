@@ -1,0 +1,87 @@
+"""Parity at the benchmark's full size and launch configuration (BASELINE configs[1] 'small':
+3 layers, d=512, 256 users, T~264k, bf16) on outputs the oracle can compute user by user, plus
+properties that hold at any size; and the MTGR-large shape (d=768, L=4484) on one layer."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_2505_18654_b200 as m
+import synth
+from tests.fixtures import rel_err
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def dev():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch.device("cuda:0")
+
+
+def _batch(cfg, users=None):
+    seg = synth.gen_segments(cfg)
+    users = np.arange(len(seg)) if users is None else np.asarray(users)
+    L = seg.astype(np.int64).sum(1)
+    ts = np.concatenate([synth.gen_user_ts(cfg, int(u), seg[u]) for u in users])
+    X = np.concatenate([synth.gen_user_x(cfg, int(u), int(L[u])) for u in users])
+    dZ = np.concatenate([synth.gen_user_dz(cfg, int(u), int(L[u])) for u in users])
+    return seg, users, ts, X, dZ
+
+
+def _run(dev, cfg, seg, users, ts, X, dZ, Ps):
+    jb = m.JaggedBatch.build(seg, ts, dev, users=users.astype(np.int32))
+    lc = m.layer_cfg(cfg["d"], cfg["H"], cfg["groups"])
+    stack = m.HstuStack(lc, [m.params_to_device(P, torch.bfloat16, dev) for P in Ps], torch.bfloat16, dev)
+    stack.bind(jb)
+    z = stack.forward(torch.from_numpy(X).to(dev, torch.bfloat16))
+    dx = stack.backward(torch.from_numpy(dZ).to(dev, torch.bfloat16))
+    torch.cuda.synchronize()
+    return jb, z.float().cpu().numpy(), dx.float().cpu().numpy(), [g["_flat"].clone() for g in stack.grads]
+
+
+def _oracle_user(cfg, seg, u, ts_u, X_u, dZ_u, Ps):
+    ocfg = dict(d=cfg["d"], H=cfg["H"])
+    gid = oracle.build_jagged(seg[u:u + 1])["group_id"]
+    nU, nS, nR, K = (int(v) for v in seg[u])
+    z, caches = oracle.stack_fwd_user(X_u, gid, nU + nS, nR, K, ts_u, Ps, ocfg)
+    dx, _ = oracle.stack_bwd_user(dZ_u, caches, Ps, ocfg)
+    return z, dx
+
+
+def test_small_config_sampled_users_and_additivity(dev):
+    cfg = synth.config("small")
+    Ps = [synth.gen_layer_params(cfg, li) for li in range(cfg["n_layers"])]
+    seg, users, ts, X, dZ = _batch(cfg)
+    jb, z, dx, grads = _run(dev, cfg, seg, users, ts, X, dZ, Ps)
+    off = jb.host["offsets"]
+    L = seg.astype(np.int64).sum(1)
+    for u in (0, int(np.argmax(L)), int(np.argmin(L))):
+        a, b = int(off[u]), int(off[u + 1])
+        zo, dxo = _oracle_user(cfg, seg, u, ts[a:b], X[a:b], dZ[a:b], Ps)
+        assert rel_err(z[a:b], zo) <= 2e-2, ("Z", u)
+        assert rel_err(dx[a:b], dxo) <= 2e-2, ("dX", u)
+    # parameter gradients are sums over users: full batch == first half + second half
+    h = len(seg) // 2
+    parts = []
+    for us_ in (np.arange(h), np.arange(h, len(seg))):
+        s2, u2, ts2, X2, dZ2 = _batch(cfg, us_)
+        parts.append(_run(dev, cfg, s2, u2, ts2, X2, dZ2, Ps)[3])
+    for li in range(cfg["n_layers"]):
+        full = grads[li].cpu().numpy()
+        summed = (parts[0][li] + parts[1][li]).cpu().numpy()
+        assert rel_err(full, summed) <= 1e-3, li
+
+
+def test_large_shape_one_layer(dev):
+    cfg = synth.config("large", users=2, n_layers=1)
+    Ps = [synth.gen_layer_params(cfg, 0)]
+    seg, users, ts, X, dZ = _batch(cfg)
+    jb, z, dx, grads = _run(dev, cfg, seg, users, ts, X, dZ, Ps)
+    off = jb.host["offsets"]
+    u = 1
+    a, b = int(off[u]), int(off[u + 1])
+    zo, dxo = _oracle_user(cfg, seg, u, ts[a:b], X[a:b], dZ[a:b], Ps)
+    assert rel_err(z[a:b], zo) <= 2e-2
+    assert rel_err(dx[a:b], dxo) <= 2e-2
