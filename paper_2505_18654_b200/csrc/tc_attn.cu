@@ -93,18 +93,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
   using namespace sm100;
   constexpr bool TWO = (MODE == DQ || MODE == DK);
   constexpr bool TRANS = (MODE == DV || MODE == DK);
-  // smem map (KB):         !TWO                        TWO
-  //   [0,64)    R1 (S A operand)  -> E            R1 -> E
-  //   [64,128)  C1 slots 0,1      -> U            R2 (dP A operand) -> U
-  //   [128,192) X slots 0,1                        C1 slots 0,1
-  //   [192,224) C1 slot 2                          C2 slot
-  // E and U are loaded once every score MMA has completed (their regions are then free).
-  constexpr int OFF_R1 = 0, OFF_R2 = 64 * KB, OFF_E = 0, OFF_U = 64 * KB;
+  // smem map (KB):      !TWO (FWD, DV)                      TWO (DQ, DK)
+  //   [0,64)     C1 slots 0,1 -> E (after last S)        R1 (S A operand) -> E
+  //   [64,96)    C1 slot 2                                R2 (dP A operand) -> U
+  //   [96,128)   X slot 0                                 R2
+  //   [128,160)  X slot 1                                 C1 slot 0
+  //   [160,224)  R1 staging, then U (prefetched early)    C1 slot 1, C2 slot
+  // (The rings receive multicast data from the peer CTA, so nothing CTA-private may alias them
+  //  while the peer can still be filling them.)
+  // TMEM columns:  !TWO: R1 [0,128) (TS A operand), acc [128,384), S [384,448), P [448,512)
+  //                 TWO: acc [0,256), S [256,320), dP [320,384), P [384,448)
+  // (Measured, tools/microbench: an SS M=128 N=64 MMA is smem-bound at 48 cycles, a TS one
+  //  runs at its 32-cycle floor; so FWD/DV keep R1 in TMEM; DQ/DK need both row operands
+  //  and keep them in smem.)
   constexpr int NC1 = TWO ? 2 : 3;
   constexpr int NX = TWO ? 1 : 2;
-  constexpr int OFF_X = TWO ? 192 * KB : 128 * KB;
-  // TMEM columns: acc [0,256) | S buffers [256,384) (TWO: S, dP) | P buffers [384,448)
-  constexpr uint32_t T_ACC = 0, T_S = 256, T_P = 384;
+  constexpr int OFF_R1 = 0, OFF_R2 = 64 * KB;
+  constexpr int OFF_R1STAGE = 160 * KB;
+  constexpr int OFF_E = 0;
+  constexpr int OFF_U = TWO ? 64 * KB : 160 * KB;
+  constexpr int OFF_X = TWO ? 192 * KB : 96 * KB;
+  constexpr int OFF_C1 = TWO ? 128 * KB : 0;
+  constexpr uint32_t T_R1 = 0;
+  constexpr uint32_t T_ACC = TWO ? 0 : 128;
+  constexpr uint32_t T_S = TWO ? 256 : 384;
+  constexpr uint32_t T_DP = 320;
+  constexpr uint32_t T_P = TWO ? 384 : 448;
 
   // A cluster = two consecutive row tiles of the same (user, head): the column tiles they both
   // stream are loaded once from L2 and multicast into both CTAs (each CTA issues half of the
@@ -140,16 +154,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
   uint64_t* t_full = bars + 16;       // [2]  P buffer written
   uint64_t* t_free = bars + 18;       // [2]  P buffer consumed by its acc MMAs
   uint64_t* r1_full = bars + 20;
+  uint64_t* r1_done = bars + 21;      // R1 copied into TMEM (FWD/DV)
   uint64_t* r2_full = bars + 22;
   uint64_t* e_full = bars + 23;
   uint64_t* u_full = bars + 24;
   uint64_t* o_full = bars + 25;
   uint64_t* sc_done = bars + 26;      // every score MMA (S, dP) has completed
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 27);
-  auto c1_slot = [&](int t) -> uint8_t* {
-    const int sl = t % NC1;
-    return TWO ? smem + 128 * KB + sl * CT_BYTES : (sl < 2 ? smem + 64 * KB + sl * CT_BYTES : smem + 192 * KB);
-  };
+  auto c1_slot = [&](int t) -> uint8_t* { return smem + OFF_C1 + (t % NC1) * CT_BYTES; };
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) DBG(10 * 64 + 4);
@@ -166,6 +178,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       mbar_init(&t_full[b], 32 * NSM); mbar_init(&t_free[b], 1);
     }
     mbar_init(r1_full, 1);
+    mbar_init(r1_done, 32 * NSM);
     mbar_init(r2_full, 1);
     mbar_init(e_full, 1);
     mbar_init(u_full, 1);
@@ -182,12 +195,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
   const int row0 = us.off + r0;  // global row of the tile's first row
 
   if (warp == 0) {
-    // ---------------------------------------------------------------- producer A: R1, R2, C1, E, U
+    // ---------------------------------------------------------------- producer A: R1, R2, C1, E (, U)
     if (lane == 0) {
-      if (ntiles > 0) {
+      if (ntiles > 0 || !TWO) {
         mbar_expect_tx(r1_full, RT_BYTES);
+        uint8_t* r1dst = smem + (TWO ? OFF_R1 : OFF_R1STAGE);
 #pragma unroll
-        for (int c = 0; c < 4; ++c) tma_load_2d(smem + OFF_R1 + c * (RT_BYTES / 4), &tmR1, r1_full, hcol + c * 64, row0);
+        for (int c = 0; c < 4; ++c) tma_load_2d(r1dst + c * (RT_BYTES / 4), &tmR1, r1_full, hcol + c * 64, row0);
+      }
+      if (ntiles > 0) {
         if (TWO) {
           mbar_expect_tx(r2_full, RT_BYTES);
 #pragma unroll
@@ -203,20 +219,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
           for (int c = crank * 2; c < crank * 2 + 2; ++c)
             tma_load_2d_mc(dst + c * (CT_BYTES / 4), &tmC1, &c1_full[slot], hcol + c * 64, row, 0x3);
         }
-        mbar_wait(sc_done, 0);  // R1 / R2 / C1 slots 0,1 are free from here on
+        mbar_wait(sc_done, 0);  // the E (and TWO: U) regions are free from here on
       }
       mbar_expect_tx(e_full, RT_BYTES);
 #pragma unroll
       for (int c = 0; c < 4; ++c) tma_load_2d(smem + OFF_E + c * (RT_BYTES / 4), &tmE, e_full, hcol + c * 64, row0);
-      if (a.has_u) {
+      if (TWO && a.has_u) {
         mbar_expect_tx(u_full, RT_BYTES);
 #pragma unroll
         for (int c = 0; c < 4; ++c) tma_load_2d(smem + OFF_U + c * (RT_BYTES / 4), &tmU, u_full, hcol + c * 64, row0);
       }
     }
   } else if (warp == 3) {
-    // ---------------------------------------------------------------- producer B: X or C2
+    // ---------------------------------------------------------------- producer B: X or C2 (, U)
     if (lane == 0) {
+      if (!TWO && a.has_u) {
+        mbar_wait(r1_done, 0);  // U replaces the (CTA-private) R1 staging area
+        mbar_expect_tx(u_full, RT_BYTES);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) tma_load_2d(smem + OFF_U + c * (RT_BYTES / 4), &tmU, u_full, hcol + c * 64, row0);
+      }
       for (int t = 0; t < ntiles; ++t) {
         const int slot = t % NX;
         mbar_wait(&x_empty[slot], ((t / NX) & 1) ^ 1);
@@ -242,8 +264,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       const uint32_t r1_base = smem_u32(smem + OFF_R1);
       const uint32_t r2_base = smem_u32(smem + OFF_R2);
       const uint32_t x_base = smem_u32(smem + OFF_X);
-      mbar_wait(r1_full, 0);
-      if (TWO) mbar_wait(r2_full, 0);
+      if (TWO) {
+        mbar_wait(r1_full, 0);
+        mbar_wait(r2_full, 0);
+      } else {
+        mbar_wait(r1_done, 0);  // R1 copied into TMEM by the softmax warps
+      }
       // acc += P_j X_j  (A = P from TMEM, B = X MN-major)
       auto acc = [&](int j) {
         const int tb = j & 1;
@@ -270,30 +296,35 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
         __syncwarp();
       };
       for (int t = 0; t < nt; ++t) {
-        const int sb = TWO ? 0 : (t & 1);
-        const int use = TWO ? t : (t >> 1);
         if (t < 64 && lane == 0) DBG(0 * 64 + t);
         mbar_wait(&c1_full[t % NC1], (t / NC1) & 1);
         if (TWO) mbar_wait(&x_full[0], t & 1);
         if (t < 64 && lane == 0) DBG(1 * 64 + t);
-        mbar_wait(&s_free[sb], (use & 1) ^ 1);
+        mbar_wait(&s_free[0], (t & 1) ^ 1);  // single S (and dP) buffer, released on tcgen05.ld
         if (t < 64 && lane == 0) DBG(2 * 64 + t);
         tc_fence_after();
         const uint32_t c1 = smem_u32(c1_slot(t));
         if (elect_one()) {
+          if (TWO) {
+            // dP first so its C2 slot is released (and refilled) as early as possible
 #pragma unroll
-          for (int k = 0; k < DH / 16; ++k) {
-            const uint32_t aoff = (k >> 2) * (RT_BYTES / 4) + (k & 3) * 32;
-            const uint32_t boff = (k >> 2) * (CT_BYTES / 4) + (k & 3) * 32;
-            mma_bf16_ss(tm + T_S + sb * BC, desc_sw128(r1_base + aoff, 16, 1024),
-                        desc_sw128(c1 + boff, 16, 1024), idesc_s, k > 0);
-            if (TWO)
-              mma_bf16_ss(tm + T_S + BC, desc_sw128(r2_base + aoff, 16, 1024),
-                          desc_sw128(x_base + boff, 16, 1024), idesc_s, k > 0);
+            for (int k = 0; k < DH / 16; ++k)
+              mma_bf16_ss(tm + T_DP, desc_sw128(r2_base + (k >> 2) * (RT_BYTES / 4) + (k & 3) * 32, 16, 1024),
+                          desc_sw128(x_base + (k >> 2) * (CT_BYTES / 4) + (k & 3) * 32, 16, 1024), idesc_s, k > 0);
+            mma_commit_mc(&x_empty[0], 0x3);
+#pragma unroll
+            for (int k = 0; k < DH / 16; ++k)
+              mma_bf16_ss(tm + T_S, desc_sw128(r1_base + (k >> 2) * (RT_BYTES / 4) + (k & 3) * 32, 16, 1024),
+                          desc_sw128(c1 + (k >> 2) * (CT_BYTES / 4) + (k & 3) * 32, 16, 1024), idesc_s, k > 0);
+            mma_commit(&s_full[0]);
+          } else {
+#pragma unroll
+            for (int k = 0; k < DH / 16; ++k)
+              mma_bf16_ts(tm + T_S, tm + T_R1 + k * 8,
+                          desc_sw128(c1 + (k >> 2) * (CT_BYTES / 4) + (k & 3) * 32, 16, 1024), idesc_s, k > 0);
+            mma_commit(&s_full[0]);
+            mma_commit_mc(&c1_empty[t % NC1], 0x3);
           }
-          mma_commit(&s_full[sb]);
-          if (TWO) mma_commit_mc(&x_empty[0], 0x3);
-          else mma_commit_mc(&c1_empty[t % NC1], 0x3);
           if (t + 1 == nt) mma_commit(sc_done);
         }
         __syncwarp();
@@ -313,6 +344,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     const int my = r0 + row;                 // user-local index of this thread's row
     const int64_t g = (int64_t)row0 + row;   // global token index
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+    if (!TWO) {
+      // R1 row (this warp's 128 head-dim columns): smem staging -> TMEM as bf16 pairs
+      mbar_wait(r1_full, 0);
+#pragma unroll 1
+      for (int cc = 0; cc < 2; ++cc) {
+        const uint8_t* box = smem + OFF_R1STAGE + (half * 2 + cc) * (RT_BYTES / 4);
+        uint32_t w[32];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const uint4 v = *reinterpret_cast<const uint4*>(box + sw128(row, j));
+          w[4 * j] = v.x; w[4 * j + 1] = v.y; w[4 * j + 2] = v.z; w[4 * j + 3] = v.w;
+        }
+        tmem_st32(tmem + T_R1 + half * 64 + cc * 32 + lane_off, w);
+      }
+      tmem_st_wait();
+      tc_fence_before();
+      mbar_arrive(r1_done);
+    }
     if (warp == 4 && lane == 0) DBG(10 * 64 + 3);
 
     const long long my_ts = (my < us.L && a.jag.ts) ? a.jag.ts[g] : 0;
@@ -329,8 +378,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
         if (i < BC) tsb[i] = (c0 + i < us.L && a.jag.ts) ? a.jag.ts[us.off + c0 + i] : 0;
         named_bar_sync(1, 32 * NSM);
       }
-      const int sb = TWO ? 0 : (t & 1);
-      const int use = TWO ? t : (t >> 1);
+      const int sb = 0, use = t;  // single S (and dP) buffer
       const bool dbgt = warp == 4 && lane == 0 && t < 64;
       if (dbgt) DBG(5 * 64 + t);
       mbar_wait(&s_full[sb], use & 1);
@@ -338,10 +386,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       tc_fence_after();
       uint32_t s[32];
       uint32_t dp[TWO ? 32 : 1];
-      tmem_ld32(tmem + T_S + sb * BC + j_half + lane_off, s);
+      tmem_ld32(tmem + T_S + j_half + lane_off, s);
       if constexpr (TWO) {
         uint32_t (&d0)[32] = *reinterpret_cast<uint32_t(*)[32]>(&dp[0]);
-        tmem_ld32(tmem + T_S + BC + j_half + lane_off, d0);
+        tmem_ld32(tmem + T_DP + j_half + lane_off, d0);
       }
       tmem_ld_wait();
       tc_fence_before();
@@ -464,8 +512,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
             const float2 f = __bfloat1622float2(ph[k]);
-            v[2 * k] *= dsilu_f(f.x);
-            v[2 * k + 1] *= dsilu_f(f.y);
+            v[2 * k] *= dsilu_fast(f.x);
+            v[2 * k + 1] *= dsilu_fast(f.y);
           }
         }
         *reinterpret_cast<uint4*>(ebox + off) =
