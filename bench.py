@@ -205,10 +205,19 @@ def time_oracle(cfg, wl, n_users, start=0):
     return tok, secs
 
 
+def _seg_desc(spec):
+    if spec[0] == "fixed":
+        return str(spec[1])
+    if spec[0] == "uniform":
+        return f"U{{{spec[1]}..{spec[2]}}}"
+    return f"min({spec[3]}, {spec[1]}*u^(-1/{spec[2]}))"
+
+
 def workload_desc(cfg, wl, world):
     return {"workload": f"MTGR-{cfg['name']} shape: {cfg['n_layers']} layers, d={cfg['d']}, "
-                        f"{cfg['H']} heads (d_h={cfg['d'] // cfg['H']}), {cfg['users']} users/rank, "
-                        f"n_U={cfg['nU']}, n_S={cfg['nS']}, n_r={cfg['nR']}, K={cfg['K']}",
+                        f"{cfg['H']} heads (d_h={cfg['d'] // cfg['H']}), {cfg['users']} users/rank x "
+                        f"(n_U={_seg_desc(cfg['nU'])}, n_S={_seg_desc(cfg['nS'])}, "
+                        f"n_r={_seg_desc(cfg['nR'])}, K={_seg_desc(cfg['K'])})",
             "users_per_rank": cfg["users"], "global_batch_users": wl["B_g"],
             "tokens_global": wl["tokens_global"], "mean_len": round(wl["tokens_global"] / wl["B_g"], 1),
             "parallelism": f"dp{world}", "balancer": "token-count LPT",

@@ -220,6 +220,13 @@ static mtgr_status_t layer_bwd_t(const mtgr_layer_cfg_t* c, const mtgr_jagged_t*
   size_t scratch_bytes = cw.cap > cw.used ? cw.cap - align_up(cw.used, 256) : 0;
   if (c->rab_buckets > 0 && G->rab_w && !acc)
     cudaMemsetAsync(G->rab_w, 0, sizeof(float) * H * c->rab_buckets, st);
+  // bias gradients are accumulated by the producing kernels (red.add): start from zero
+  if (!acc && ntok > 0) {
+    cudaMemsetAsync(G->b1, 0, sizeof(float) * 4 * d, st);
+    cudaMemsetAsync(G->b2, 0, sizeof(float) * d, st);
+  }
+  const bool tc_attn = std::is_same<T, __nv_bfloat16>::value && c->rab_buckets == 0 &&
+                       attn_tc_supported(d / H);
   if (ntok == 0) {
     // gradients of an empty batch are zero
     if (!acc) {
@@ -240,7 +247,6 @@ static mtgr_status_t layer_bwd_t(const mtgr_layer_cfg_t* c, const mtgr_jagged_t*
   g.B = yt; g.ldb = d; g.b_kmajor = 0;
   g.C = G->w2; g.ldc = d; g.accumulate = acc;
   MTGR_TRY(run_gemm<T>(g, EPI_F32, scratch, scratch_bytes, st));
-  MTGR_TRY(colsum_launch<T>(dz, d, ntok, d, G->b2, (float*)scratch, acc, st));
   GemmIO h{};
   h.M = ntok; h.N = d; h.K = d;
   h.A = dz; h.lda = d; h.a_kmajor = 1;
@@ -252,7 +258,7 @@ static mtgr_status_t layer_bwd_t(const mtgr_layer_cfg_t* c, const mtgr_jagged_t*
   gi.dy = buf; gi.x = y; gi.mean = mu2; gi.rstd = r2; gi.gamma = P->gamma2; gi.gid = j->group_id;
   gi.dx = dO; gi.ntok = ntok; gi.d = d; gi.G = c->num_groups;
   gi.o = o; gi.u = a + 3 * d; gi.pre_u = c->qkvu_silu ? p + 3 * d : nullptr; gi.ld_a = 4 * d;
-  gi.dpu = dp + 3 * d; gi.ld_dp = 4 * d;
+  gi.dpu = dp + 3 * d; gi.ld_dp = 4 * d; gi.dcol = G->b1 + 3 * d;  // db1 of the U block
   MTGR_TRY(gln_bwd_launch<T>(gi, GLNB_GATE, (float*)scratch, G->gamma2, G->beta2, acc, st));
   // attention backward (+ silu' of Q, K, V) into dp[:, 0:3d]
   AttnIO at{};
@@ -261,7 +267,9 @@ static mtgr_status_t layer_bwd_t(const mtgr_layer_cfg_t* c, const mtgr_jagged_t*
   at.dO = dO; at.pre = c->qkvu_silu ? p : nullptr; at.ld_pre = 4 * d;
   at.dq = dp; at.dk = dp + d; at.dv = dp + 2 * d; at.ld_out = 4 * d;
   at.rab_w = P->rab_w; at.drab = c->rab_buckets > 0 ? G->rab_w : nullptr;
+  at.dbias = tc_attn ? G->b1 : nullptr;  // db1 of the Q|K|V blocks fused into the epilogues
   MTGR_TRY(run_attn_bwd<T>(at, diag_a, diag_ds, st));
+  if (!tc_attn) MTGR_TRY(colsum_launch<T>(dp, 4 * d, ntok, 3 * d, G->b1, (float*)scratch, 1, st));
   // dW1 = dp^T X~, db1 = sum dp, dX~ = dp W1
   GemmIO k{};
   k.M = 4 * d; k.N = d; k.K = ntok;
@@ -269,7 +277,6 @@ static mtgr_status_t layer_bwd_t(const mtgr_layer_cfg_t* c, const mtgr_jagged_t*
   k.B = xt; k.ldb = d; k.b_kmajor = 0;
   k.C = G->w1; k.ldc = d; k.accumulate = acc;
   MTGR_TRY(run_gemm<T>(k, EPI_F32, scratch, scratch_bytes, st));
-  MTGR_TRY(colsum_launch<T>(dp, 4 * d, ntok, 4 * d, G->b1, (float*)scratch, acc, st));
   GemmIO m{};
   m.M = ntok; m.N = d; m.K = 4 * d;
   m.A = dp; m.lda = 4 * d; m.a_kmajor = 1;
@@ -280,6 +287,7 @@ static mtgr_status_t layer_bwd_t(const mtgr_layer_cfg_t* c, const mtgr_jagged_t*
   GlnBwdIO gj{};
   gj.dy = buf; gj.x = x; gj.mean = mu1; gj.rstd = r1; gj.gamma = P->gamma1; gj.gid = j->group_id;
   gj.dx = dx; gj.ntok = ntok; gj.d = d; gj.G = c->num_groups; gj.dz = dz;
+  gj.dcol = G->b2;  // db2 = sum_t dZ fused into the GLN1 backward (which reads dZ anyway)
   return gln_bwd_launch<T>(gj, GLNB_RESID, (float*)scratch, G->gamma1, G->beta1, acc, st);
 }
 

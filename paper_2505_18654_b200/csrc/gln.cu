@@ -130,6 +130,7 @@ struct GlnBwdArgs {
   int64_t ld_dp;
   // GLN_RESID
   const T* dz;
+  float* dcol;    // [d] column-sum accumulator (red.add): sum of dz (RESID) / dp_U (GATE), or NULL
 };
 
 constexpr int GLNB_WARPS = 4;
@@ -141,20 +142,21 @@ constexpr int GLNB_WARPS = 4;
 // accumulator [G][2][d] on a group change; block partials go to global with red.add.
 template <class T, int MODE, int NC>
 __global__ void __launch_bounds__(32 * GLNB_WARPS, (NC <= 2 ? 3 : 2)) gln_bwd_kernel(GlnBwdArgs<T> a) {
-  extern __shared__ float sacc[];  // [G][2][d]
+  extern __shared__ float sacc[];  // [G][2][d] (+ [d] column sums)
   const int d = a.d, G = a.G;
-  for (int i = threadIdx.x; i < G * 2 * d; i += blockDim.x) sacc[i] = 0.f;
+  const bool csum = MODE != GLN_PLAIN && a.dcol != nullptr;
+  for (int i = threadIdx.x; i < G * 2 * d + d; i += blockDim.x) sacc[i] = 0.f;
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nch = d >> 3;
   const float inv_d = 1.0f / (float)d;
   const int w_begin = (blockIdx.x * GLNB_WARPS + warp) * a.tok_per_warp;
   const int w_end = min(a.ntok, w_begin + a.tok_per_warp);
-  float pg[NC][8], pb[NC][8];
+  float pg[NC][8], pb[NC][8], pc[NC][8];
 #pragma unroll
   for (int k = 0; k < NC; ++k)
 #pragma unroll
-    for (int e = 0; e < 8; ++e) pg[k][e] = pb[k][e] = 0.f;
+    for (int e = 0; e < 8; ++e) pg[k][e] = pb[k][e] = pc[k][e] = 0.f;
   int cur_g = w_begin < w_end ? a.gid[w_begin] : 0;
   auto flush = [&]() {
 #pragma unroll
@@ -222,7 +224,10 @@ __global__ void __launch_bounds__(32 * GLNB_WARPS, (NC <= 2 ? 3 : 2)) gln_bwd_ke
         for (int e = 0; e < 8; ++e) o[e] = r * (dyv[k][e] * gg[k][e] - m1 - xv[k][e] * m2);
         if (MODE == GLN_RESID) {
 #pragma unroll
-          for (int e = 0; e < 8; ++e) o[e] += e1[k][e];
+          for (int e = 0; e < 8; ++e) {
+            o[e] += e1[k][e];
+            pc[k][e] += e1[k][e];
+          }
           store8(a.dx + (int64_t)t * d + c * 8, o);
         } else if (MODE == GLN_GATE) {
           // o[] = dY; dO = dY * U;  dp_U = dY * O * silu'(p_U)
@@ -232,6 +237,7 @@ __global__ void __launch_bounds__(32 * GLNB_WARPS, (NC <= 2 ? 3 : 2)) gln_bwd_ke
             dO[e] = o[e] * e1[k][e];
             du[e] = o[e] * e2[k][e];
             if (a.pre_u) du[e] *= dsilu_f(e3[k][e]);
+            pc[k][e] += du[e];
           }
           store8(a.dx + (int64_t)t * d + c * 8, dO);
           store8(a.dpu + (int64_t)t * a.ld_dp + c * 8, du);
@@ -242,7 +248,18 @@ __global__ void __launch_bounds__(32 * GLNB_WARPS, (NC <= 2 ? 3 : 2)) gln_bwd_ke
     }
   }
   if (w_begin < w_end) flush();
+  if (csum) {
+#pragma unroll
+    for (int k = 0; k < NC; ++k) {
+      const int c = lane + 32 * k;
+      if (c < nch)
+#pragma unroll
+        for (int e = 0; e < 8; ++e) atomicAdd(&sacc[G * 2 * d + c * 8 + e], pc[k][e]);
+    }
+  }
   __syncthreads();
+  if (csum)
+    for (int i = threadIdx.x; i < d; i += blockDim.x) atomicAdd(a.dcol + i, sacc[G * 2 * d + i]);
   // block partial -> global accumulators [G][2][d] (red.global.add; order not deterministic)
   for (int i = threadIdx.x; i < G * 2 * d; i += blockDim.x) {
     const float v = sacc[i];
@@ -326,11 +343,11 @@ mtgr_status_t gln_bwd_launch(const GlnBwdIO& io, int mode, float* part, float* d
   a.gamma = io.gamma; a.gid = io.gid; a.dx = (T*)io.dx; a.part = part;
   a.ntok = io.ntok; a.d = io.d; a.G = io.G;
   a.o = (const T*)io.o; a.u = (const T*)io.u; a.pre_u = (const T*)io.pre_u; a.ld_a = io.ld_a;
-  a.dpu = (T*)io.dpu; a.ld_dp = io.ld_dp; a.dz = (const T*)io.dz;
+  a.dpu = (T*)io.dpu; a.ld_dp = io.ld_dp; a.dz = (const T*)io.dz; a.dcol = io.dcol;
   a.tok_per_warp = gln_bwd_tok_per_warp(io.ntok);
   int nb = io.ntok > 0 ? gln_bwd_blocks(io.ntok) : 0;
-  size_t smem = (size_t)io.G * 2 * io.d * sizeof(float);
-  cudaMemsetAsync(part, 0, smem, st);
+  size_t smem = ((size_t)io.G * 2 * io.d + io.d) * sizeof(float);
+  cudaMemsetAsync(part, 0, (size_t)io.G * 2 * io.d * sizeof(float), st);
   if (nb > 0) {
     if (mode == GLN_GATE) gln_bwd_mode<T, GLN_GATE>(a, nb, smem, st);
     else if (mode == GLN_RESID) gln_bwd_mode<T, GLN_RESID>(a, nb, smem, st);

@@ -15,6 +15,7 @@ struct GlnBwdIO {
   const uint8_t* gid; void* dx; int ntok, d, G;
   const void* o; const void* u; const void* pre_u; int64_t ld_a; void* dpu; int64_t ld_dp;
   const void* dz;
+  float* dcol;  // optional fused column sum (red.add): sum_t dz (RESID) or sum_t dp_U (GATE)
 };
 size_t gln_bwd_ws_bytes(int ntok, int d, int G);
 template <class T>
@@ -57,6 +58,8 @@ struct AttnIO {
   const float* diag_a;         // [T][H]  nu*silu(s_ii) for non-static tokens, 0 otherwise
   const float* diag_ds;        // [T][H]  nu*silu'(s_ii)*(dO_i . v_i)
   const float* rab_w; float* drab;
+  float* dbias;                // optional: column sums of the (bwd) outputs, red.add into
+                               // dbias[col] for the Q|K|V blocks (tensor-core path only)
 };
 size_t attn_ws_bytes(int ntok, int H);
 template <class T>

@@ -121,57 +121,48 @@ __device__ __forceinline__ void ld8f(const T* p, float* v) {
   }
 }
 
-// one warp per token; lane c handles 8-element chunks c, c+32, ... of each head (16-byte loads)
+// one block per user, one warp per NON-STATIC token of that user (static tokens have no diagonal
+// term: their self-visibility is inside the static block, R#8/R#9); lane c handles 8-element
+// chunks c, c+32, ... of each head (16-byte loads).  Entries of static tokens are never read.
 template <class T>
-__global__ void attn_diag_kernel(AttnIO a, int bwd, float* __restrict__ diag_a,
-                                 float* __restrict__ diag_ds) {
+__global__ void __launch_bounds__(256) attn_diag_kernel(AttnIO a, int bwd, float* __restrict__ diag_a,
+                                                        float* __restrict__ diag_ds) {
   const int lane = threadIdx.x & 31;
-  const int ntok = a.jag.total_tokens;
-  const int B = a.jag.num_users;
-  const int nwarps = gridDim.x * (blockDim.x >> 5);
+  const UserSpan us = load_user(a.jag, blockIdx.x);
   const T* q = (const T*)a.q; const T* k = (const T*)a.k; const T* v = (const T*)a.v;
   const T* dO = (const T*)a.dO;
   const int nch = a.dh >> 3;
-  for (int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); t < ntok; t += nwarps) {
-    // user of token t: last u with offsets[u] <= t
-    int lo = 0, hi = B - 1;
-    while (lo < hi) {
-      int mid = (lo + hi + 1) >> 1;
-      if (a.jag.offsets[mid] <= t) lo = mid; else hi = mid - 1;
-    }
-    const UserSpan us = load_user(a.jag, lo);
-    const bool nonstatic = (t - us.off) >= us.ns;
+  for (int li = us.ns + (threadIdx.x >> 5); li < us.L; li += blockDim.x >> 5) {
+    const int64_t t = us.off + li;
     for (int h = 0; h < a.H; ++h) {
       float s = 0.f, pv = 0.f;
-      if (nonstatic) {
-        for (int c = lane; c < nch; c += 32) {
-          const int64_t col = (int64_t)h * a.dh + c * 8;
-          float qa[8], ka[8];
-          ld8f(q + (int64_t)t * a.ld + col, qa);
-          ld8f(k + (int64_t)t * a.ld + col, ka);
+      for (int c = lane; c < nch; c += 32) {
+        const int64_t col = (int64_t)h * a.dh + c * 8;
+        float qa[8], ka[8];
+        ld8f(q + t * a.ld + col, qa);
+        ld8f(k + t * a.ld + col, ka);
 #pragma unroll
-          for (int e = 0; e < 8; ++e) s = fmaf(qa[e], ka[e], s);
-          if (bwd) {
-            float da[8], va[8];
-            ld8f(dO + (int64_t)t * a.d + col, da);
-            ld8f(v + (int64_t)t * a.ld + col, va);
-#pragma unroll
-            for (int e = 0; e < 8; ++e) pv = fmaf(da[e], va[e], pv);
-          }
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          s += __shfl_xor_sync(0xffffffffu, s, o);
-          pv += __shfl_xor_sync(0xffffffffu, pv, o);
-        }
-        if (a.nb > 0) s += a.rab_w[h * a.nb + 0];
-      }
-      if (lane == 0) {
-        diag_a[(int64_t)t * a.H + h] = nonstatic ? us.nu * silu_f(s) : 0.f;
+        for (int e = 0; e < 8; ++e) s = fmaf(qa[e], ka[e], s);
         if (bwd) {
-          float ds = nonstatic ? us.nu * dsilu_f(s) * pv : 0.f;
-          diag_ds[(int64_t)t * a.H + h] = ds;
-          if (a.nb > 0 && a.drab && nonstatic) atomicAdd(&a.drab[h * a.nb + 0], ds);
+          float da[8], va[8];
+          ld8f(dO + t * a.d + col, da);
+          ld8f(v + t * a.ld + col, va);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) pv = fmaf(da[e], va[e], pv);
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        s += __shfl_xor_sync(0xffffffffu, s, o);
+        pv += __shfl_xor_sync(0xffffffffu, pv, o);
+      }
+      if (a.nb > 0) s += a.rab_w[h * a.nb + 0];
+      if (lane == 0) {
+        diag_a[t * a.H + h] = us.nu * silu_f(s);
+        if (bwd) {
+          const float ds = us.nu * dsilu_f(s) * pv;
+          diag_ds[t * a.H + h] = ds;
+          if (a.nb > 0 && a.drab) atomicAdd(&a.drab[h * a.nb + 0], ds);
         }
       }
     }
@@ -181,11 +172,9 @@ __global__ void attn_diag_kernel(AttnIO a, int bwd, float* __restrict__ diag_a,
 template <class T>
 mtgr_status_t attn_diag_launch(const AttnIO& a, bool bwd, float* diag_a, float* diag_ds,
                                cudaStream_t st) {
-  int ntok = a.jag.total_tokens;
-  if (ntok == 0) return MTGR_OK;
+  if (a.jag.total_tokens == 0 || a.jag.num_users == 0) return MTGR_OK;
   ProfScope ps(PROF_ATTN_DIAG, st);
-  int blocks = min(ceil_div(ntok, 8), 8 * num_sms());
-  attn_diag_kernel<T><<<blocks, 256, 0, st>>>(a, bwd ? 1 : 0, diag_a, diag_ds);
+  attn_diag_kernel<T><<<a.jag.num_users, 256, 0, st>>>(a, bwd ? 1 : 0, diag_a, diag_ds);
   return check_launch("attn_diag");
 }
 template mtgr_status_t attn_diag_launch<float>(const AttnIO&, bool, float*, float*, cudaStream_t);
@@ -256,7 +245,7 @@ __global__ void __launch_bounds__(256) attn_simt_fwd_kernel(AttnIO a) {
   }
   if (i >= us.L) return;
   const int64_t t = us.off + i;
-  const float da = a.diag_a[t * a.H + h];
+  const float da = i >= us.ns ? a.diag_a[t * a.H + h] : 0.f;
 #pragma unroll
   for (int c = 0; c < 32; ++c) {
     if (c >= ncol) break;
@@ -343,7 +332,8 @@ __global__ void __launch_bounds__(256) attn_simt_dkv_kernel(AttnIO a) {
       if (rab_acc[e] != 0.f) atomicAdd(&a.drab[h * a.nb + e], us.nu * rab_acc[e]);
   if (j >= us.L) return;
   const int64_t t = us.off + j;
-  const float da = a.diag_a[t * a.H + h], dd = a.diag_ds[t * a.H + h];
+  const float da = j >= us.ns ? a.diag_a[t * a.H + h] : 0.f;
+  const float dd = j >= us.ns ? a.diag_ds[t * a.H + h] : 0.f;
   const T* pre = (const T*)a.pre;
 #pragma unroll
   for (int c = 0; c < 32; ++c) {
@@ -420,7 +410,7 @@ __global__ void __launch_bounds__(256) attn_simt_dq_kernel(AttnIO a) {
   }
   if (i >= us.L) return;
   const int64_t t = us.off + i;
-  const float dd = a.diag_ds[t * a.H + h];
+  const float dd = i >= us.ns ? a.diag_ds[t * a.H + h] : 0.f;
   const T* pre = (const T*)a.pre;
 #pragma unroll
   for (int c = 0; c < 32; ++c) {

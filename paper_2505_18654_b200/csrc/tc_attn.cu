@@ -62,6 +62,7 @@ struct Args {
   __nv_bfloat16* out2;                      // FWD y (ld_out)
   const float* diag;                        // [T][H]
   int has_u;                                // U / pre tile present
+  float* dbias;                             // bwd: red.add column sums of the outputs, or NULL
   long long* dbg;                           // debug timestamps (MTGR_ATTN_TRACE) or NULL
 };
 
@@ -465,7 +466,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     mbar_wait(e_full, 0);
     if (a.has_u) mbar_wait(u_full, 0);
     const bool row_ok = my < us.L;
-    const float dg = row_ok ? a.diag[g * a.H + h] : 0.f;
+    const float dg = (row_ok && my >= us.ns) ? a.diag[g * a.H + h] : 0.f;  // static rows: none
     uint8_t* sE = smem + OFF_E;
     uint8_t* sU = smem + OFF_U;
 #pragma unroll 1
@@ -525,11 +526,35 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     const int sw = warp - 4;
     const int nrows = min(BR, us.L - r0);
     const int bx = lane >> 3, jj = lane & 7;
+    float cs[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     for (int rr = sw; rr < nrows; rr += NSM) {
       const uint32_t off = bx * (RT_BYTES / 4) + sw128(rr, jj);
       const int64_t go = (int64_t)(row0 + rr) * a.ld_out + hcol + lane * 8;
-      *reinterpret_cast<uint4*>(a.out + go) = *reinterpret_cast<const uint4*>(sE + off);
+      const uint4 w = *reinterpret_cast<const uint4*>(sE + off);
+      *reinterpret_cast<uint4*>(a.out + go) = w;
       if (MODE == FWD) *reinterpret_cast<uint4*>(a.out2 + go) = *reinterpret_cast<const uint4*>(sU + off);
+      if (MODE != FWD) {
+        const __nv_bfloat162* hh = reinterpret_cast<const __nv_bfloat162*>(&w);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float2 f = __bfloat1622float2(hh[k]);
+          cs[2 * k] += f.x;
+          cs[2 * k + 1] += f.y;
+        }
+      }
+    }
+    if (MODE != FWD && a.dbias != nullptr) {
+      // bias gradient of this projection block: column sums over the tile's rows (fused, so
+      // the layer never re-reads dp for it); [8 warps][256 columns] partials in free smem
+      float* red = reinterpret_cast<float*>(smem + 192 * KB);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) red[sw * DH + lane * 8 + e] = cs[e];
+      named_bar_sync(1, 32 * NSM);
+      const int col = threadIdx.x - 128;
+      float sum = 0.f;
+#pragma unroll
+      for (int w2 = 0; w2 < NSM; ++w2) sum += red[w2 * DH + col];
+      if (sum != 0.f) atomicAdd(a.dbias + hcol + col, sum);
     }
   }
   if (warp == 4 && lane == 0) DBG(10 * 64 + 2);
@@ -609,6 +634,7 @@ mtgr_status_t attn_tc_bwd_launch(const AttnIO& io, cudaStream_t st) {
     Args a{};
     a.jag = io.jag; a.H = io.H; a.d = io.d;
     a.out = (bf*)io.dv; a.ld_out = io.ld_out; a.diag = io.diag_a;
+    a.dbias = io.dbias ? io.dbias + 2 * D : nullptr;
     MTGR_TRY(launch_mode<DV>(io, io.q, io.ld, io.dO, D, io.k, io.ld, nullptr, 0, io.dO, D,
                              pre ? pre + 2 * D : nullptr, io.ld_pre, a, st));
   }
@@ -616,6 +642,7 @@ mtgr_status_t attn_tc_bwd_launch(const AttnIO& io, cudaStream_t st) {
     Args a{};
     a.jag = io.jag; a.H = io.H; a.d = io.d;
     a.out = (bf*)io.dk; a.ld_out = io.ld_out; a.diag = io.diag_ds;
+    a.dbias = io.dbias ? io.dbias + D : nullptr;
     MTGR_TRY(launch_mode<DK>(io, io.q, io.ld, io.dO, D, io.k, io.ld, io.v, io.ld, io.q, io.ld,
                              pre ? pre + D : nullptr, io.ld_pre, a, st));
   }
@@ -623,6 +650,7 @@ mtgr_status_t attn_tc_bwd_launch(const AttnIO& io, cudaStream_t st) {
     Args a{};
     a.jag = io.jag; a.H = io.H; a.d = io.d;
     a.out = (bf*)io.dq; a.ld_out = io.ld_out; a.diag = io.diag_ds;
+    a.dbias = io.dbias;
     MTGR_TRY(launch_mode<DQ>(io, io.k, io.ld, io.v, io.ld, io.q, io.ld, io.dO, D, io.k, io.ld, pre,
                              io.ld_pre, a, st));
   }
