@@ -41,7 +41,7 @@ def parse():
     ap.add_argument("--impl", default="mtgr", choices=["mtgr", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-users", type=int, default=2, help="users in the CPU oracle sample")
+    ap.add_argument("--cpu-users", type=int, default=24, help="users in the CPU oracle sample (~10 s)")
     ap.add_argument("--backend", default="nccl")
     return ap.parse_args()
 
