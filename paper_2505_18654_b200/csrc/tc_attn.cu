@@ -241,14 +241,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
         for (int c = 0; c < 4; ++c) tma_load_2d(smem + OFF_U + c * (RT_BYTES / 4), &tmU, u_full, hcol + c * 64, row0);
       }
       for (int t = 0; t < ntiles; ++t) {
-        const int slot = t % NX;
-        mbar_wait(&x_empty[slot], ((t / NX) & 1) ^ 1);
-        mbar_expect_tx(&x_full[slot], CT_BYTES);
         const int row = us.off + c_begin + t * BC;
-        uint8_t* dst = smem + OFF_X + slot * CT_BYTES;
+        if (TWO) {
+          // C2: one slot split in two head-dim halves with their own barriers, so the first half
+          // of the next tile is refilled while the dP MMAs still read the second half
+          for (int hh = 0; hh < 2; ++hh) {
+            mbar_wait(&x_empty[hh], (t & 1) ^ 1);
+            mbar_expect_tx(&x_full[hh], CT_BYTES / 2);
+            const int c = 2 * hh + crank;
+            tma_load_2d_mc(smem + OFF_X + c * (CT_BYTES / 4), &tmX, &x_full[hh], hcol + c * 64, row, 0x3);
+          }
+        } else {
+          const int slot = t % NX;
+          mbar_wait(&x_empty[slot], ((t / NX) & 1) ^ 1);
+          mbar_expect_tx(&x_full[slot], CT_BYTES);
+          uint8_t* dst = smem + OFF_X + slot * CT_BYTES;
 #pragma unroll
-        for (int c = crank * 2; c < crank * 2 + 2; ++c)
-          tma_load_2d_mc(dst + c * (CT_BYTES / 4), &tmX, &x_full[slot], hcol + c * 64, row, 0x3);
+          for (int c = crank * 2; c < crank * 2 + 2; ++c)
+            tma_load_2d_mc(dst + c * (CT_BYTES / 4), &tmX, &x_full[slot], hcol + c * 64, row, 0x3);
+        }
       }
     }
   } else if (warp == 1) {
@@ -299,20 +310,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       for (int t = 0; t < nt; ++t) {
         if (t < 64 && lane == 0) DBG(0 * 64 + t);
         mbar_wait(&c1_full[t % NC1], (t / NC1) & 1);
-        if (TWO) mbar_wait(&x_full[0], t & 1);
         if (t < 64 && lane == 0) DBG(1 * 64 + t);
         mbar_wait(&s_free[0], (t & 1) ^ 1);  // single S (and dP) buffer, released on tcgen05.ld
         if (t < 64 && lane == 0) DBG(2 * 64 + t);
         tc_fence_after();
         const uint32_t c1 = smem_u32(c1_slot(t));
+        if (TWO) {
+          // dP first, per head-dim half, so each half of the C2 slot is released (and refilled)
+          // as early as possible
+          for (int hh = 0; hh < 2; ++hh) {
+            mbar_wait(&x_full[hh], t & 1);
+            tc_fence_after();
+            if (elect_one()) {
+#pragma unroll
+              for (int k = hh * 8; k < hh * 8 + 8; ++k)
+                mma_bf16_ss(tm + T_DP, desc_sw128(r2_base + (k >> 2) * (RT_BYTES / 4) + (k & 3) * 32, 16, 1024),
+                            desc_sw128(x_base + (k >> 2) * (CT_BYTES / 4) + (k & 3) * 32, 16, 1024), idesc_s, k > 0);
+              mma_commit_mc(&x_empty[hh], 0x3);
+            }
+            __syncwarp();
+          }
+        }
         if (elect_one()) {
           if (TWO) {
-            // dP first so its C2 slot is released (and refilled) as early as possible
-#pragma unroll
-            for (int k = 0; k < DH / 16; ++k)
-              mma_bf16_ss(tm + T_DP, desc_sw128(r2_base + (k >> 2) * (RT_BYTES / 4) + (k & 3) * 32, 16, 1024),
-                          desc_sw128(x_base + (k >> 2) * (CT_BYTES / 4) + (k & 3) * 32, 16, 1024), idesc_s, k > 0);
-            mma_commit_mc(&x_empty[0], 0x3);
 #pragma unroll
             for (int k = 0; k < DH / 16; ++k)
               mma_bf16_ss(tm + T_S, desc_sw128(r1_base + (k >> 2) * (RT_BYTES / 4) + (k & 3) * 32, 16, 1024),
