@@ -41,6 +41,29 @@ __device__ __forceinline__ void store8(__nv_bfloat16* p, const float* v) {
   *reinterpret_cast<uint4*>(p) = a;
 }
 
+// raw (still packed) 8-element vectors: 16 B for bf16, 32 B for fp32; unpacked only when used
+template <class T> struct Raw8;
+template <> struct Raw8<__nv_bfloat16> { uint4 v; };
+template <> struct Raw8<float> { float4 a, b; };
+__device__ __forceinline__ void rload(const __nv_bfloat16* p, Raw8<__nv_bfloat16>& r) {
+  r.v = *reinterpret_cast<const uint4*>(p);
+}
+__device__ __forceinline__ void rload(const float* p, Raw8<float>& r) {
+  r.a = reinterpret_cast<const float4*>(p)[0];
+  r.b = reinterpret_cast<const float4*>(p)[1];
+}
+__device__ __forceinline__ void unpack(const Raw8<__nv_bfloat16>& r, float* v) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&r.v);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 f = __bfloat1622float2(h[i]);
+    v[2 * i] = f.x; v[2 * i + 1] = f.y;
+  }
+}
+__device__ __forceinline__ void unpack(const Raw8<float>& r, float* v) {
+  v[0] = r.a.x; v[1] = r.a.y; v[2] = r.a.z; v[3] = r.a.w; v[4] = r.b.x; v[5] = r.b.y; v[6] = r.b.z; v[7] = r.b.w;
+}
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -141,7 +164,7 @@ constexpr int GLNB_WARPS = 4;
 // the same (tokens of a group are contiguous within a user) and flushed to the block's smem
 // accumulator [G][2][d] on a group change; block partials go to global with red.add.
 template <class T, int MODE, int NC>
-__global__ void __launch_bounds__(32 * GLNB_WARPS, (NC <= 2 ? 3 : 2)) gln_bwd_kernel(GlnBwdArgs<T> a) {
+__global__ void __launch_bounds__(32 * GLNB_WARPS, (NC <= 2 ? (MODE == GLN_GATE ? 3 : 4) : 3)) gln_bwd_kernel(GlnBwdArgs<T> a) {
   extern __shared__ float sacc[];  // [G][2][d] (+ [d] column sums)
   const int d = a.d, G = a.G;
   const bool csum = MODE != GLN_PLAIN && a.dcol != nullptr;
@@ -176,18 +199,18 @@ __global__ void __launch_bounds__(32 * GLNB_WARPS, (NC <= 2 ? 3 : 2)) gln_bwd_ke
   for (int t = w_begin; t < w_end; ++t) {
     const int g = a.gid[t];
     const float mu = a.mean[t], r = a.rstd[t];
-    float xv[NC][8], dyv[NC][8], e1[NC][8], e2[NC][8], e3[NC][8];
+    Raw8<T> xr[NC], dyr[NC], e1r[NC], e2r[NC], e3r[NC];
 #pragma unroll
     for (int k = 0; k < NC; ++k) {
       const int c = lane + 32 * k;
       if (c < nch) {
-        load8(a.x + (int64_t)t * d + c * 8, xv[k]);
-        load8(a.dy + (int64_t)t * d + c * 8, dyv[k]);
-        if (MODE == GLN_RESID) load8(a.dz + (int64_t)t * d + c * 8, e1[k]);
+        rload(a.x + (int64_t)t * d + c * 8, xr[k]);
+        rload(a.dy + (int64_t)t * d + c * 8, dyr[k]);
+        if (MODE == GLN_RESID) rload(a.dz + (int64_t)t * d + c * 8, e1r[k]);
         if (MODE == GLN_GATE) {
-          load8(a.u + (int64_t)t * a.ld_a + c * 8, e1[k]);
-          load8(a.o + (int64_t)t * d + c * 8, e2[k]);
-          if (a.pre_u) load8(a.pre_u + (int64_t)t * a.ld_a + c * 8, e3[k]);
+          rload(a.u + (int64_t)t * a.ld_a + c * 8, e1r[k]);
+          rload(a.o + (int64_t)t * d + c * 8, e2r[k]);
+          if (a.pre_u) rload(a.pre_u + (int64_t)t * a.ld_a + c * 8, e3r[k]);
         }
       }
     }
@@ -196,21 +219,23 @@ __global__ void __launch_bounds__(32 * GLNB_WARPS, (NC <= 2 ? 3 : 2)) gln_bwd_ke
       cur_g = g;
     }
     const float* gr = a.gamma + (int64_t)g * d;
-    float gg[NC][8];
     float s1 = 0.f, s2 = 0.f;
 #pragma unroll
     for (int k = 0; k < NC; ++k) {
       const int c = lane + 32 * k;
       if (c < nch) {
-        load8(gr + c * 8, gg[k]);
+        float xv[8], dyv[8], gg[8];
+        unpack(xr[k], xv);
+        unpack(dyr[k], dyv);
+        load8(gr + c * 8, gg);
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
-          xv[k][e] = (xv[k][e] - mu) * r;  // xhat
-          const float dxh = dyv[k][e] * gg[k][e];
-          pg[k][e] = fmaf(dyv[k][e], xv[k][e], pg[k][e]);
-          pb[k][e] += dyv[k][e];
+          const float xh = (xv[e] - mu) * r;
+          const float dxh = dyv[e] * gg[e];
+          pg[k][e] = fmaf(dyv[e], xh, pg[k][e]);
+          pb[k][e] += dyv[e];
           s1 += dxh;
-          s2 = fmaf(dxh, xv[k][e], s2);
+          s2 = fmaf(dxh, xh, s2);
         }
       }
     }
@@ -219,24 +244,33 @@ __global__ void __launch_bounds__(32 * GLNB_WARPS, (NC <= 2 ? 3 : 2)) gln_bwd_ke
     for (int k = 0; k < NC; ++k) {
       const int c = lane + 32 * k;
       if (c < nch) {
-        float o[8];
+        float xv[8], dyv[8], gg[8], o[8];
+        unpack(xr[k], xv);
+        unpack(dyr[k], dyv);
+        load8(gr + c * 8, gg);
 #pragma unroll
-        for (int e = 0; e < 8; ++e) o[e] = r * (dyv[k][e] * gg[k][e] - m1 - xv[k][e] * m2);
+        for (int e = 0; e < 8; ++e) o[e] = r * (dyv[e] * gg[e] - m1 - (xv[e] - mu) * r * m2);
         if (MODE == GLN_RESID) {
+          float z[8];
+          unpack(e1r[k], z);
 #pragma unroll
           for (int e = 0; e < 8; ++e) {
-            o[e] += e1[k][e];
-            pc[k][e] += e1[k][e];
+            o[e] += z[e];
+            pc[k][e] += z[e];
           }
           store8(a.dx + (int64_t)t * d + c * 8, o);
         } else if (MODE == GLN_GATE) {
           // o[] = dY; dO = dY * U;  dp_U = dY * O * silu'(p_U)
-          float dO[8], du[8];
+          float uu[8], oo[8], dO[8], du[8];
+          unpack(e1r[k], uu);
+          unpack(e2r[k], oo);
+          float pp[8];
+          if (a.pre_u) unpack(e3r[k], pp);
 #pragma unroll
           for (int e = 0; e < 8; ++e) {
-            dO[e] = o[e] * e1[k][e];
-            du[e] = o[e] * e2[k][e];
-            if (a.pre_u) du[e] *= dsilu_f(e3[k][e]);
+            dO[e] = o[e] * uu[e];
+            du[e] = o[e] * oo[e];
+            if (a.pre_u) du[e] *= dsilu_f(pp[e]);
             pc[k][e] += du[e];
           }
           store8(a.dx + (int64_t)t * d + c * 8, dO);

@@ -96,30 +96,33 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
   constexpr bool TRANS = (MODE == DV || MODE == DK);
   // smem map (KB):      !TWO (FWD, DV)                      TWO (DQ, DK)
   //   [0,64)     C1 slots 0,1 -> E (after last S)        R1 (S A operand) -> E
-  //   [64,96)    C1 slot 2                                R2 (dP A operand) -> U
-  //   [96,128)   X slot 0                                 R2
-  //   [128,160)  X slot 1                                 C1 slot 0
-  //   [160,224)  R1 staging, then U (prefetched early)    C1 slot 1, C2 slot
+  //   [64,96)    C1 slot 2                                R2 head-dim 128..255 (dP A, SS);
+  //                                                       prologue: staging of R2 0..127 -> U 0,1
+  //   [96,128)   X slot 0                                 C1 slot 0
+  //   [128,160)  X slot 1                                 C1 slot 1
+  //   [160,192)  R1 staging, then U (prefetched early)    C1 slot 2
+  //   [192,224)  R1 staging, then U                       C2 slot (two halves) -> U 2,3
   // (The rings receive multicast data from the peer CTA, so nothing CTA-private may alias them
   //  while the peer can still be filling them.)
   // TMEM columns:  !TWO: R1 [0,128) (TS A operand), acc [128,384), S [384,448), P [448,512)
-  //                 TWO: acc [0,256), S [256,320), dP [320,384), P [384,448)
+  //                 TWO: acc [0,256), S [256,320), dP [320,384), P [384,448),
+  //                      R2 head-dim 0..127 [448,512) (TS A operand of the first dP half)
   // (Measured, tools/microbench: an SS M=128 N=64 MMA is smem-bound at 48 cycles, a TS one
-  //  runs at its 32-cycle floor; so FWD/DV keep R1 in TMEM; DQ/DK need both row operands
-  //  and keep them in smem.)
-  constexpr int NC1 = TWO ? 2 : 3;
+  //  runs at its 32-cycle floor.  FWD/DV keep R1 in TMEM; DQ/DK cannot hold both row operands
+  //  in TMEM, so half of R2 lives in TMEM to free smem for a 3-slot C1 ring.)
+  constexpr int NC1 = 3;
   constexpr int NX = TWO ? 1 : 2;
-  constexpr int OFF_R1 = 0, OFF_R2 = 64 * KB;
+  constexpr int OFF_R1 = 0, OFF_R2B = 64 * KB;
   constexpr int OFF_R1STAGE = 160 * KB;
   constexpr int OFF_E = 0;
-  constexpr int OFF_U = TWO ? 64 * KB : 160 * KB;
   constexpr int OFF_X = TWO ? 192 * KB : 96 * KB;
-  constexpr int OFF_C1 = TWO ? 128 * KB : 0;
+  constexpr int OFF_C1 = TWO ? 96 * KB : 0;
   constexpr uint32_t T_R1 = 0;
   constexpr uint32_t T_ACC = TWO ? 0 : 128;
   constexpr uint32_t T_S = TWO ? 256 : 384;
   constexpr uint32_t T_DP = 320;
   constexpr uint32_t T_P = TWO ? 384 : 448;
+  constexpr uint32_t T_R2A = 448;
 
   // A cluster = two consecutive row tiles of the same (user, head): the column tiles they both
   // stream are loaded once from L2 and multicast into both CTAs (each CTA issues half of the
@@ -161,8 +164,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
   uint64_t* u_full = bars + 24;
   uint64_t* o_full = bars + 25;
   uint64_t* sc_done = bars + 26;      // every score MMA (S, dP) has completed
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 27);
+  uint64_t* r2a_full = bars + 27;     // TWO: R2 head-dim 0..127 staged in smem
+  uint64_t* r2a_done = bars + 28;     // TWO: ... and copied into TMEM
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 29);
   auto c1_slot = [&](int t) -> uint8_t* { return smem + OFF_C1 + (t % NC1) * CT_BYTES; };
+  auto u_box = [&](int b) -> uint8_t* {  // smem of U box b (16 KB each)
+    if (TWO) return b < 2 ? smem + 64 * KB + b * (RT_BYTES / 4) : smem + 192 * KB + (b - 2) * (RT_BYTES / 4);
+    return smem + 160 * KB + b * (RT_BYTES / 4);
+  };
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) DBG(10 * 64 + 4);
@@ -185,6 +194,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     mbar_init(u_full, 1);
     mbar_init(o_full, 1);
     mbar_init(sc_done, 1);
+    mbar_init(r2a_full, 1);
+    mbar_init(r2a_done, 32 * NSM);
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc<512>(tmem_slot);
@@ -205,12 +216,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
         for (int c = 0; c < 4; ++c) tma_load_2d(r1dst + c * (RT_BYTES / 4), &tmR1, r1_full, hcol + c * 64, row0);
       }
       if (ntiles > 0) {
-        if (TWO) {
-          mbar_expect_tx(r2_full, RT_BYTES);
+        if (TWO) {  // R2 head-dim 0..127 -> staging (copied to TMEM by the softmax warps)
+          mbar_expect_tx(r2a_full, RT_BYTES / 2);
 #pragma unroll
-          for (int c = 0; c < 4; ++c) tma_load_2d(smem + OFF_R2 + c * (RT_BYTES / 4), &tmR2, r2_full, hcol + c * 64, row0);
+          for (int c = 0; c < 2; ++c) tma_load_2d(smem + OFF_R2B + c * (RT_BYTES / 4), &tmR2, r2a_full, hcol + c * 64, row0);
         }
         for (int t = 0; t < ntiles; ++t) {
+          if (TWO && t == NC1) {
+            // R2 head-dim 128..255 replaces the staging once its first half sits in TMEM
+            mbar_wait(r2a_done, 0);
+            mbar_expect_tx(r2_full, RT_BYTES / 2);
+#pragma unroll
+            for (int c = 2; c < 4; ++c) tma_load_2d(smem + OFF_R2B + (c - 2) * (RT_BYTES / 4), &tmR2, r2_full, hcol + c * 64, row0);
+          }
           const int slot = t % NC1;
           mbar_wait(&c1_empty[slot], ((t / NC1) & 1) ^ 1);
           mbar_expect_tx(&c1_full[slot], CT_BYTES);
@@ -220,6 +238,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
           for (int c = crank * 2; c < crank * 2 + 2; ++c)
             tma_load_2d_mc(dst + c * (CT_BYTES / 4), &tmC1, &c1_full[slot], hcol + c * 64, row, 0x3);
         }
+        if (TWO && ntiles <= NC1) {
+          mbar_wait(r2a_done, 0);
+          mbar_expect_tx(r2_full, RT_BYTES / 2);
+#pragma unroll
+          for (int c = 2; c < 4; ++c) tma_load_2d(smem + OFF_R2B + (c - 2) * (RT_BYTES / 4), &tmR2, r2_full, hcol + c * 64, row0);
+        }
         mbar_wait(sc_done, 0);  // the E (and TWO: U) regions are free from here on
       }
       mbar_expect_tx(e_full, RT_BYTES);
@@ -228,7 +252,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       if (TWO && a.has_u) {
         mbar_expect_tx(u_full, RT_BYTES);
 #pragma unroll
-        for (int c = 0; c < 4; ++c) tma_load_2d(smem + OFF_U + c * (RT_BYTES / 4), &tmU, u_full, hcol + c * 64, row0);
+        for (int c = 0; c < 4; ++c) tma_load_2d(u_box(c), &tmU, u_full, hcol + c * 64, row0);
       }
     }
   } else if (warp == 3) {
@@ -238,7 +262,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
         mbar_wait(r1_done, 0);  // U replaces the (CTA-private) R1 staging area
         mbar_expect_tx(u_full, RT_BYTES);
 #pragma unroll
-        for (int c = 0; c < 4; ++c) tma_load_2d(smem + OFF_U + c * (RT_BYTES / 4), &tmU, u_full, hcol + c * 64, row0);
+        for (int c = 0; c < 4; ++c) tma_load_2d(u_box(c), &tmU, u_full, hcol + c * 64, row0);
       }
       for (int t = 0; t < ntiles; ++t) {
         const int row = us.off + c_begin + t * BC;
@@ -274,10 +298,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       constexpr uint32_t idesc_s = idesc_bf16_f32(BR, BC, 0, 0);
       constexpr uint32_t idesc_acc = idesc_bf16_f32(BR, DH, 0, 1);
       const uint32_t r1_base = smem_u32(smem + OFF_R1);
-      const uint32_t r2_base = smem_u32(smem + OFF_R2);
+      const uint32_t r2b_base = smem_u32(smem + OFF_R2B);
       const uint32_t x_base = smem_u32(smem + OFF_X);
       if (TWO) {
         mbar_wait(r1_full, 0);
+        mbar_wait(r2a_done, 0);
         mbar_wait(r2_full, 0);
       } else {
         mbar_wait(r1_done, 0);  // R1 copied into TMEM by the softmax warps
@@ -323,9 +348,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
             tc_fence_after();
             if (elect_one()) {
 #pragma unroll
-              for (int k = hh * 8; k < hh * 8 + 8; ++k)
-                mma_bf16_ss(tm + T_DP, desc_sw128(r2_base + (k >> 2) * (RT_BYTES / 4) + (k & 3) * 32, 16, 1024),
-                            desc_sw128(x_base + (k >> 2) * (CT_BYTES / 4) + (k & 3) * 32, 16, 1024), idesc_s, k > 0);
+              for (int k = hh * 8; k < hh * 8 + 8; ++k) {
+                const uint64_t bd = desc_sw128(x_base + (k >> 2) * (CT_BYTES / 4) + (k & 3) * 32, 16, 1024);
+                if (hh == 0)  // head-dim 0..127 of R2 from TMEM
+                  mma_bf16_ts(tm + T_DP, tm + T_R2A + k * 8, bd, idesc_s, k > 0);
+                else          // head-dim 128..255 from smem
+                  mma_bf16_ss(tm + T_DP, desc_sw128(r2b_base + ((k >> 2) - 2) * (RT_BYTES / 4) + (k & 3) * 32, 16, 1024),
+                              bd, idesc_s, 1);
+              }
               mma_commit_mc(&x_empty[hh], 0x3);
             }
             __syncwarp();
@@ -382,6 +412,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       tmem_st_wait();
       tc_fence_before();
       mbar_arrive(r1_done);
+    } else if (ntiles > 0) {
+      // R2 head-dim 0..127 (this warp's 64 columns): smem staging -> TMEM as bf16 pairs
+      mbar_wait(r2a_full, 0);
+      const uint8_t* box = smem + OFF_R2B + half * (RT_BYTES / 4);
+      uint32_t w[32];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const uint4 v = *reinterpret_cast<const uint4*>(box + sw128(row, j));
+        w[4 * j] = v.x; w[4 * j + 1] = v.y; w[4 * j + 2] = v.z; w[4 * j + 3] = v.w;
+      }
+      tmem_st32(tmem + T_R2A + half * 32 + lane_off, w);
+      tmem_st_wait();
+      tc_fence_before();
+      mbar_arrive(r2a_done);
     }
     if (warp == 4 && lane == 0) DBG(10 * 64 + 3);
 
@@ -488,7 +532,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     const bool row_ok = my < us.L;
     const float dg = (row_ok && my >= us.ns) ? a.diag[g * a.H + h] : 0.f;  // static rows: none
     uint8_t* sE = smem + OFF_E;
-    uint8_t* sU = smem + OFF_U;
 #pragma unroll 1
     for (int cc = 0; cc < 4; ++cc) {
       const int acol = half * 128 + cc * 32;  // head-dim column of this chunk
@@ -502,7 +545,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       }
       const int bx = acol >> 6, j0 = (acol & 63) >> 3;
       uint8_t* ebox = sE + bx * (RT_BYTES / 4);
-      uint8_t* ubox = sU + bx * (RT_BYTES / 4);
+      uint8_t* ubox = u_box(bx);
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const uint32_t off = sw128(row, j0 + i);
@@ -552,7 +595,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       const int64_t go = (int64_t)(row0 + rr) * a.ld_out + hcol + lane * 8;
       const uint4 w = *reinterpret_cast<const uint4*>(sE + off);
       *reinterpret_cast<uint4*>(a.out + go) = w;
-      if (MODE == FWD) *reinterpret_cast<uint4*>(a.out2 + go) = *reinterpret_cast<const uint4*>(sU + off);
+      if (MODE == FWD)
+        *reinterpret_cast<uint4*>(a.out2 + go) = *reinterpret_cast<const uint4*>(u_box(bx) + sw128(rr, jj));
       if (MODE != FWD) {
         const __nv_bfloat162* hh = reinterpret_cast<const __nv_bfloat162*>(&w);
 #pragma unroll
