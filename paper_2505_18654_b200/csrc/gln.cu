@@ -164,7 +164,7 @@ constexpr int GLNB_WARPS = 4;
 // the same (tokens of a group are contiguous within a user) and flushed to the block's smem
 // accumulator [G][2][d] on a group change; block partials go to global with red.add.
 template <class T, int MODE, int NC>
-__global__ void __launch_bounds__(32 * GLNB_WARPS, (NC <= 2 ? (MODE == GLN_GATE ? 3 : 4) : 3)) gln_bwd_kernel(GlnBwdArgs<T> a) {
+__global__ void __launch_bounds__(32 * GLNB_WARPS, (NC <= 2 ? (MODE == GLN_GATE ? 3 : 4) : 2)) gln_bwd_kernel(GlnBwdArgs<T> a) {
   extern __shared__ float sacc[];  // [G][2][d] (+ [d] column sums)
   const int d = a.d, G = a.G;
   const bool csum = MODE != GLN_PLAIN && a.dcol != nullptr;

@@ -24,16 +24,24 @@
 namespace mtgr {
 namespace tcg {
 
-constexpr int BM = 128, BN = 256, BK = 64, STAGES = 3;
+constexpr int BM = 128, BN = 256, BK = 64;  // BM = rows per CTA; a CTA pair covers 256 rows
 constexpr int A_BYTES = BM * BK * 2;
-constexpr int B_BYTES = BN * BK * 2;
-constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int NUM_EPI_WARPS = 8;                     // 2 per TMEM lane quadrant
 constexpr int STG_BYTES = 2 * 32 * 128;              // per epilogue warp: 2 x [32 rows][64 bf16]
-constexpr int OFF_STG = STAGES * STAGE_BYTES;
-constexpr int OFF_BAR = OFF_STG + NUM_EPI_WARPS * STG_BYTES;
-constexpr int SMEM_BYTES = OFF_BAR + 512 + 1024;
 constexpr int NTHREADS = 128 + 32 * NUM_EPI_WARPS;
+
+// per-cta_group geometry: CG = 1 (one CTA, M=128 MMA) or 2 (CTA pair, M=256 MMA; each CTA holds
+// its 128 rows of A and half of the 256 B rows, so per-SM operand traffic halves)
+template <int CG>
+struct Geo {
+  static constexpr int B_ROWS = BN / CG;
+  static constexpr int B_BYTES = B_ROWS * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = CG == 2 ? 4 : 3;
+  static constexpr int OFF_STG = STAGES * STAGE_BYTES;
+  static constexpr int OFF_BAR = OFF_STG + NUM_EPI_WARPS * STG_BYTES;
+  static constexpr int SMEM_BYTES = OFF_BAR + 512 + 1024;
+};
 
 struct Params {
   int M, N, K;
@@ -57,47 +65,54 @@ __device__ __forceinline__ float silu_tanh(float x) {
 }
 
 // Epilogue layout: epilogue warp ew (warps 4..11) owns TMEM lane quadrant q = warp % 4 (rows
-// q*32..q*32+31 of the tile) and column half ew / 4; it drains two 64-column chunks per tile:
-// tcgen05.ld -> fused math -> bf16 into a SWIZZLE_128B smem staging tile [32][64] ->
+// q*32..q*32+31 of the CTA's 128 rows) and column half ew / 4; it drains two 64-column chunks
+// per tile: tcgen05.ld -> fused math -> bf16 into a SWIZZLE_128B smem staging tile [32][64] ->
 // TMA store (bulk group).  The residual tile is TMA-loaded into the same staging buffer.
-template <int EPI>
+template <int EPI, int CG>
 __global__ void __launch_bounds__(NTHREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmC2,
                    const __grid_constant__ CUtensorMap tmR, Params p) {
   using namespace sm100;
+  using G = Geo<CG>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
-  uint8_t* sB = smem + STAGES * A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
-  uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;
+  uint8_t* sB = smem + G::STAGES * A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + G::OFF_BAR);
+  uint64_t* empty = full + G::STAGES;
+  uint64_t* tfull = empty + G::STAGES;
   uint64_t* tempty = tfull + 2;
   uint64_t* rbar = tempty + 2;  // [NUM_EPI_WARPS]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rbar + NUM_EPI_WARPS);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;
+  const bool leader = rank == 0;
+  const int cta_id = blockIdx.x / CG, ncta = gridDim.x / CG;  // cluster-level work distribution
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
     if (EPI != EPI_F32) tma_prefetch(&tmC);
     if (EPI == EPI_QKVU) tma_prefetch(&tmC2);
     if (EPI == EPI_RESID) tma_prefetch(&tmR);
-    for (int s = 0; s < STAGES; ++s) {
+    for (int s = 0; s < G::STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], 32 * NUM_EPI_WARPS);
+      mbar_init(&tempty[b], CG * 32 * NUM_EPI_WARPS);  // the leader collects both CTAs' epilogues
     }
     for (int w = 0; w < NUM_EPI_WARPS; ++w) mbar_init(&rbar[w], 1);
     fence_barrier_init();
   }
-  if (warp == 2) tmem_alloc<512>(tmem_slot);
+  if (warp == 2) {
+    if (CG == 2) tmem_alloc_2sm<512>(tmem_slot);
+    else tmem_alloc<512>(tmem_slot);
+  }
   tc_fence_before();
-  __syncthreads();
+  if (CG == 2) cluster_sync(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const int total = p.num_m * p.num_n * p.num_splits;
@@ -106,87 +121,101 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int item = blockIdx.x; item < total; item += gridDim.x) {
+      for (int item = cta_id; item < total; item += ncta) {
         const int nb = item % p.num_n, rest = item / p.num_n;
         const int mb = rest % p.num_m, sp = rest / p.num_m;
         const int kb0 = sp * p.kb_per_split, kb1 = min(p.num_kb, kb0 + p.kb_per_split);
+        const int m0 = mb * BM * CG + rank * BM;
+        const int n0 = nb * BN + rank * G::B_ROWS;
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          mbar_expect_tx(&full[stage], STAGE_BYTES);
+          if (leader) mbar_expect_tx(&full[stage], CG * G::STAGE_BYTES);
           const int k = kb * BK;
           uint8_t* a_dst = sA + stage * A_BYTES;
-          uint8_t* b_dst = sB + stage * B_BYTES;
+          uint8_t* b_dst = sB + stage * G::B_BYTES;
+          auto load = [&](void* dst, const CUtensorMap* m, int c0, int c1) {
+            if (CG == 2) tma_load_2d_2sm(dst, m, &full[stage], c0, c1);
+            else tma_load_2d(dst, m, &full[stage], c0, c1);
+          };
           if (!p.a_mn) {
-            tma_load_2d(a_dst, &tmA, &full[stage], k, mb * BM);
+            load(a_dst, &tmA, k, m0);
           } else {
 #pragma unroll
-            for (int c = 0; c < BM / 64; ++c) tma_load_2d(a_dst + c * 8192, &tmA, &full[stage], mb * BM + c * 64, k);
+            for (int c = 0; c < BM / 64; ++c) load(a_dst + c * 8192, &tmA, m0 + c * 64, k);
           }
           if (!p.b_mn) {
-            tma_load_2d(b_dst, &tmB, &full[stage], k, nb * BN);
+            load(b_dst, &tmB, k, n0);
           } else {
 #pragma unroll
-            for (int c = 0; c < BN / 64; ++c) tma_load_2d(b_dst + c * 8192, &tmB, &full[stage], nb * BN + c * 64, k);
+            for (int c = 0; c < G::B_ROWS / 64; ++c) load(b_dst + c * 8192, &tmB, n0 + c * 64, k);
           }
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          if (++stage == G::STAGES) { stage = 0; phase ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
-    // the whole warp walks the schedule (warp-uniform operands); one elected lane issues
-    const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
-    const int a_mn = __shfl_sync(0xffffffffu, p.a_mn, 0), b_mn = __shfl_sync(0xffffffffu, p.b_mn, 0);
-    const uint32_t idesc = idesc_bf16_f32(BM, BN, a_mn, b_mn);
-    int stage = 0;
-    uint32_t phase = 0;
-    int it = 0;
-    for (int item = blockIdx.x; item < total; item += gridDim.x, ++it) {
-      const int sp = item / (p.num_n * p.num_m);
-      const int kb0 = sp * p.kb_per_split, kb1 = min(p.num_kb, kb0 + p.kb_per_split);
-      const int buf = it & 1;
-      const uint32_t acc_phase = (it >> 1) & 1;
-      mbar_wait(&tempty[buf], acc_phase ^ 1);
-      tc_fence_after();
-      const uint32_t d_tmem = tm + buf * BN;
-      for (int kb = kb0; kb < kb1; ++kb) {
-        mbar_wait(&full[stage], phase);
+    // the whole warp walks the schedule (warp-uniform operands); one elected lane of the leader
+    // CTA issues (cta_group::2: one MMA covers both CTAs' rows)
+    if (leader) {
+      const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
+      const int a_mn = __shfl_sync(0xffffffffu, p.a_mn, 0), b_mn = __shfl_sync(0xffffffffu, p.b_mn, 0);
+      const uint32_t idesc = idesc_bf16_f32(BM * CG, BN, a_mn, b_mn);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int item = cta_id; item < total; item += ncta, ++it) {
+        const int sp = item / (p.num_n * p.num_m);
+        const int kb0 = sp * p.kb_per_split, kb1 = min(p.num_kb, kb0 + p.kb_per_split);
+        const int buf = it & 1;
+        const uint32_t acc_phase = (it >> 1) & 1;
+        mbar_wait(&tempty[buf], acc_phase ^ 1);
         tc_fence_after();
-        const uint32_t a_base = smem_u32(sA + stage * A_BYTES);
-        const uint32_t b_base = smem_u32(sB + stage * B_BYTES);
-        if (elect_one()) {
+        const uint32_t d_tmem = tm + buf * BN;
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a_base = smem_u32(sA + stage * A_BYTES);
+          const uint32_t b_base = smem_u32(sB + stage * G::B_BYTES);
+          if (elect_one()) {
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k) {
-            const uint64_t ad = a_mn ? desc_sw128(a_base + k * 2048, 8192, 1024)
-                                     : desc_sw128(a_base + k * 32, 16, 1024);
-            const uint64_t bd = b_mn ? desc_sw128(b_base + k * 2048, 8192, 1024)
-                                     : desc_sw128(b_base + k * 32, 16, 1024);
-            mma_bf16_ss(d_tmem, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+            for (int k = 0; k < BK / 16; ++k) {
+              const uint64_t ad = a_mn ? desc_sw128(a_base + k * 2048, 8192, 1024)
+                                       : desc_sw128(a_base + k * 32, 16, 1024);
+              const uint64_t bd = b_mn ? desc_sw128(b_base + k * 2048, 8192, 1024)
+                                       : desc_sw128(b_base + k * 32, 16, 1024);
+              if (CG == 2) mma_bf16_ss_2sm(d_tmem, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+              else mma_bf16_ss(d_tmem, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+            }
+            if (CG == 2) mma_commit_2sm_mc(&empty[stage], 0x3);
+            else mma_commit(&empty[stage]);
           }
-          mma_commit(&empty[stage]);
+          __syncwarp();
+          if (++stage == G::STAGES) { stage = 0; phase ^= 1; }
+        }
+        if (elect_one()) {
+          if (CG == 2) mma_commit_2sm_mc(&tfull[buf], 0x3);
+          else mma_commit(&tfull[buf]);
         }
         __syncwarp();
-        if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
-      if (elect_one()) mma_commit(&tfull[buf]);
-      __syncwarp();
     }
   } else if (warp >= 4) {
     const int ew = warp - 4;
     const int q = warp & 3;
     const int hf = ew >> 2;
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
-    uint8_t* stg = smem + OFF_STG + ew * STG_BYTES;
+    uint8_t* stg = smem + G::OFF_STG + ew * STG_BYTES;
     uint8_t* srow = stg + lane * 128;
     uint32_t rphase = 0;
     int it = 0;
-    for (int item = blockIdx.x; item < total; item += gridDim.x, ++it) {
+    for (int item = cta_id; item < total; item += ncta, ++it) {
       const int nb = item % p.num_n, rest = item / p.num_n;
       const int mb = rest % p.num_m, sp = rest / p.num_m;
       const int buf = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
       mbar_wait(&tfull[buf], acc_phase);
       tc_fence_after();
-      const int m0 = mb * BM + q * 32;
+      const int m0 = mb * BM * CG + rank * BM + q * 32;
 #pragma unroll 1
       for (int c = 0; c < 2; ++c) {
         const int col = hf * 128 + c * 64;
@@ -197,7 +226,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         tmem_ld_wait();
         if (c == 1) {
           tc_fence_before();
-          mbar_arrive(&tempty[buf]);
+          if (CG == 2 && !leader) mbar_arrive_cluster(&tempty[buf], 0);
+          else mbar_arrive(&tempty[buf]);
         }
         if (n0 >= p.N || m0 >= p.M) continue;  // warp-uniform
         float v[64];
@@ -299,10 +329,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
     if (lane == 0) tma_store_wait<0>();
   }
-  __syncthreads();
+  tc_fence_before();
+  if (CG == 2) cluster_sync(); else __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc<512>(tmem);
+    if (CG == 2) tmem_dealloc_2sm<512>(tmem);
+    else tmem_dealloc<512>(tmem);
   }
 }
 
@@ -335,12 +367,15 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 struct Split {
   int splits, kb_per_split;
 };
+constexpr int CG_USE = 2;  // the layer GEMMs run on CTA pairs (cta_group::2)
+
 static Split choose_split(int M, int N, int K, int epi) {
   const int num_kb = ceil_div(K, BK);
-  const int tiles = ceil_div(M, BM) * ceil_div(N, BN);
+  const int tiles = ceil_div(M, BM * CG_USE) * ceil_div(N, BN);  // pair tiles
+  const int units = num_sms() / CG_USE;
   Split s{1, num_kb};
-  if (epi == EPI_F32 && tiles < num_sms() && num_kb > 1) {
-    int want = ceil_div(2 * num_sms(), tiles);
+  if (epi == EPI_F32 && tiles < units && num_kb > 1) {
+    int want = ceil_div(2 * units, tiles);
     want = std::min(want, num_kb);
     s.kb_per_split = ceil_div(num_kb, want);
     s.splits = ceil_div(num_kb, s.kb_per_split);
@@ -384,10 +419,12 @@ mtgr_status_t gemm_bf16_launch(const GemmIO& g, int epi, void* ws, size_t ws_byt
   MTGR_CHECK(g.ldc % 8 == 0 && aligned16(g.C) && (!g.C2 || aligned16(g.C2)) &&
                  (!g.R || (g.ldr % 8 == 0 && aligned16(g.R))) && (!g.bias || aligned16(g.bias)),
              MTGR_E_LAYOUT, "tc gemm: outputs need 16-byte aligned rows");
+  constexpr int CG = CG_USE;
+  using Gm = Geo<CG>;
   CUtensorMap ta, tb;
   if (g.a_kmajor) MTGR_TRY(make_tmap_bf16(&ta, g.A, g.K, g.M, g.lda, 64, BM));
   else MTGR_TRY(make_tmap_bf16(&ta, g.A, g.M, g.K, g.lda, 64, 64));
-  if (g.b_kmajor) MTGR_TRY(make_tmap_bf16(&tb, g.B, g.K, g.N, g.ldb, 64, BN));
+  if (g.b_kmajor) MTGR_TRY(make_tmap_bf16(&tb, g.B, g.K, g.N, g.ldb, 64, Gm::B_ROWS));
   else MTGR_TRY(make_tmap_bf16(&tb, g.B, g.N, g.K, g.ldb, 64, 64));
   CUtensorMap tc = ta, tc2 = ta, tr = ta;
   if (epi != EPI_F32) MTGR_TRY(make_tmap_bf16(&tc, g.C, g.N, g.M, g.ldc, 64, 32));
@@ -395,7 +432,7 @@ mtgr_status_t gemm_bf16_launch(const GemmIO& g, int epi, void* ws, size_t ws_byt
   if (epi == EPI_RESID) MTGR_TRY(make_tmap_bf16(&tr, g.R, g.N, g.M, g.ldr, 64, 32));
   Params p{};
   p.M = g.M; p.N = g.N; p.K = g.K;
-  p.num_m = ceil_div(g.M, BM); p.num_n = ceil_div(g.N, BN); p.num_kb = ceil_div(g.K, BK);
+  p.num_m = ceil_div(g.M, BM * CG); p.num_n = ceil_div(g.N, BN); p.num_kb = ceil_div(g.K, BK);
   Split s = choose_split(g.M, g.N, g.K, epi);
   p.num_splits = s.splits; p.kb_per_split = s.kb_per_split;
   p.a_mn = g.a_kmajor ? 0 : 1; p.b_mn = g.b_kmajor ? 0 : 1;
@@ -407,18 +444,30 @@ mtgr_status_t gemm_bf16_launch(const GemmIO& g, int epi, void* ws, size_t ws_byt
     p.part = (float*)ws;
   }
   const int total = p.num_m * p.num_n * p.num_splits;
-  const int grid = std::min(total, num_sms());
+  const int grid = CG * std::min(total, num_sms() / CG);
   ProfScope ps(epi == EPI_QKVU ? PROF_GEMM_QKVU : epi == EPI_RESID ? PROF_GEMM_OUT
                : epi == EPI_STORE ? PROF_GEMM_DGRAD : PROF_GEMM_WGRAD, st);
   auto launch = [&](auto kern) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-    kern<<<grid, NTHREADS, SMEM_BYTES, st>>>(ta, tb, tc, tc2, tr, p);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Gm::SMEM_BYTES);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(NTHREADS);
+    cfg.dynamicSmemBytes = Gm::SMEM_BYTES;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CG;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, tc2, tr, p);
   };
   switch (epi) {
-    case EPI_STORE: launch(gemm_tc_kernel<EPI_STORE>); break;
-    case EPI_QKVU: launch(gemm_tc_kernel<EPI_QKVU>); break;
-    case EPI_RESID: launch(gemm_tc_kernel<EPI_RESID>); break;
-    default: launch(gemm_tc_kernel<EPI_F32>); break;
+    case EPI_STORE: launch(gemm_tc_kernel<EPI_STORE, CG>); break;
+    case EPI_QKVU: launch(gemm_tc_kernel<EPI_QKVU, CG>); break;
+    case EPI_RESID: launch(gemm_tc_kernel<EPI_RESID, CG>); break;
+    default: launch(gemm_tc_kernel<EPI_F32, CG>); break;
   }
   MTGR_TRY(check_launch("gemm_tc"));
   if (epi == EPI_F32 && s.splits > 1) {
