@@ -90,6 +90,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tmC1, const __grid_constant__ CUtensorMap tmX,
                    const __grid_constant__ CUtensorMap tmR1, const __grid_constant__ CUtensorMap tmR2,
                    const __grid_constant__ CUtensorMap tmE, const __grid_constant__ CUtensorMap tmU,
+                   const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmO2,
                    Args a) {
   using namespace sm100;
   constexpr bool TWO = (MODE == DQ || MODE == DK);
@@ -246,9 +247,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
         }
         mbar_wait(sc_done, 0);  // the E (and TWO: U) regions are free from here on
       }
-      mbar_expect_tx(e_full, RT_BYTES);
+      if (r0 + BR > us.ns) {  // only tiles with non-static rows have diagonal terms (E)
+        mbar_expect_tx(e_full, RT_BYTES);
 #pragma unroll
-      for (int c = 0; c < 4; ++c) tma_load_2d(smem + OFF_E + c * (RT_BYTES / 4), &tmE, e_full, hcol + c * 64, row0);
+        for (int c = 0; c < 4; ++c) tma_load_2d(smem + OFF_E + c * (RT_BYTES / 4), &tmE, e_full, hcol + c * 64, row0);
+      }
       if (TWO && a.has_u) {
         mbar_expect_tx(u_full, RT_BYTES);
 #pragma unroll
@@ -527,8 +530,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     mbar_wait(o_full, 0);
     if (warp == 4 && lane == 0) DBG(10 * 64 + 1);
     tc_fence_after();
-    mbar_wait(e_full, 0);
+    const bool need_e = r0 + BR > us.ns;
+    if (need_e) mbar_wait(e_full, 0);
+    if (warp == 4 && lane == 0) DBG(10 * 64 + 5);
     if (a.has_u) mbar_wait(u_full, 0);
+    if (warp == 4 && lane == 0) DBG(10 * 64 + 6);
     const bool row_ok = my < us.L;
     const float dg = (row_ok && my >= us.ns) ? a.diag[g * a.H + h] : 0.f;  // static rows: none
     uint8_t* sE = smem + OFF_E;
@@ -549,7 +555,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const uint32_t off = sw128(row, j0 + i);
-        uint4 w = *reinterpret_cast<const uint4*>(ebox + off);
+        uint4 w = need_e ? *reinterpret_cast<const uint4*>(ebox + off) : make_uint4(0u, 0u, 0u, 0u);
         const __nv_bfloat162* hh = reinterpret_cast<const __nv_bfloat162*>(&w);
         float v[8];
 #pragma unroll
@@ -584,20 +590,43 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
             make_uint4(pack2(v[0], v[1]), pack2(v[2], v[3]), pack2(v[4], v[5]), pack2(v[6], v[7]));
       }
     }
+    if (warp == 4 && lane == 0) DBG(10 * 64 + 7);
+    fence_proxy_async_smem();  // the TMA stores below read these smem tiles
     named_bar_sync(1, 32 * NSM);
-    // coalesced row stores: warp w writes rows w, w+8, ...; lane l covers head-dim columns l*8..+7
+    if (warp == 4 && lane == 0) DBG(10 * 64 + 8);
+    // stores: full 32-row chunks by TMA straight from the swizzled smem tiles (asynchronous, so
+    // the HBM writes drain after the CTA has moved on); a partial last chunk row by row (rows of
+    // the next user must not be touched).  Warps 0-3 store `out`, warps 4-7 `out2` (FWD).
     const int sw = warp - 4;
     const int nrows = min(BR, us.L - r0);
     const int bx = lane >> 3, jj = lane & 7;
+    {
+      const int rc = sw & 3;
+      const bool second = sw >= 4;
+      if (MODE == FWD || !second) {
+        const CUtensorMap* tmo = second ? &tmO2 : &tmO;
+        if (rc * 32 + 32 <= nrows) {
+          if (lane == 0) {
+#pragma unroll
+            for (int b = 0; b < 4; ++b)
+              tma_store_2d(tmo, (second ? u_box(b) : sE + b * (RT_BYTES / 4)) + rc * 32 * 128, hcol + b * 64,
+                           row0 + rc * 32);
+            tma_store_commit();
+          }
+        } else {
+          __nv_bfloat16* dst = second ? a.out2 : a.out;
+          for (int rr = rc * 32; rr < nrows; ++rr) {
+            const uint8_t* src = (second ? u_box(bx) : sE + bx * (RT_BYTES / 4)) + sw128(rr, jj);
+            *reinterpret_cast<uint4*>(dst + (int64_t)(row0 + rr) * a.ld_out + hcol + lane * 8) =
+                *reinterpret_cast<const uint4*>(src);
+          }
+        }
+      }
+    }
     float cs[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-    for (int rr = sw; rr < nrows; rr += NSM) {
-      const uint32_t off = bx * (RT_BYTES / 4) + sw128(rr, jj);
-      const int64_t go = (int64_t)(row0 + rr) * a.ld_out + hcol + lane * 8;
-      const uint4 w = *reinterpret_cast<const uint4*>(sE + off);
-      *reinterpret_cast<uint4*>(a.out + go) = w;
-      if (MODE == FWD)
-        *reinterpret_cast<uint4*>(a.out2 + go) = *reinterpret_cast<const uint4*>(u_box(bx) + sw128(rr, jj));
-      if (MODE != FWD) {
+    if (MODE != FWD && a.dbias != nullptr) {
+      for (int rr = sw; rr < nrows; rr += NSM) {
+        const uint4 w = *reinterpret_cast<const uint4*>(sE + bx * (RT_BYTES / 4) + sw128(rr, jj));
         const __nv_bfloat162* hh = reinterpret_cast<const __nv_bfloat162*>(&w);
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
@@ -620,6 +649,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       for (int w2 = 0; w2 < NSM; ++w2) sum += red[w2 * DH + col];
       if (sum != 0.f) atomicAdd(a.dbias + hcol + col, sum);
     }
+    if (lane == 0) tma_store_wait_read<0>();  // smem must outlive the bulk stores' reads
+    if (warp == 4 && lane == 0) DBG(10 * 64 + 9);
   }
   if (warp == 4 && lane == 0) DBG(10 * 64 + 2);
   tc_fence_before();
@@ -631,7 +662,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
 }
 
 struct Maps {
-  CUtensorMap c1, x, r1, r2, e, u;
+  CUtensorMap c1, x, r1, r2, e, u, o, o2;
 };
 
 template <int MODE>
@@ -647,6 +678,8 @@ static mtgr_status_t launch_mode(const AttnIO& io, const void* c1, int64_t ld_c1
   if (r2) MTGR_TRY(make_tmap_bf16(&m.r2, r2, d, T, ld_r2, 64, BR)); else m.r2 = m.r1;
   MTGR_TRY(make_tmap_bf16(&m.e, e, d, T, ld_e, 64, BR));
   if (uu) MTGR_TRY(make_tmap_bf16(&m.u, uu, d, T, ld_u, 64, BR)); else m.u = m.e;
+  MTGR_TRY(make_tmap_bf16(&m.o, args.out, d, T, args.ld_out, 64, 32));
+  if (args.out2) MTGR_TRY(make_tmap_bf16(&m.o2, args.out2, d, T, args.ld_out, 64, 32)); else m.o2 = m.o;
   Args a2 = args;
   a2.has_u = uu != nullptr;
   dim3 grid(2 * ceil_div(io.jag.max_len, 2 * BR), io.H, io.jag.num_users);  // cluster pairs
@@ -657,7 +690,7 @@ static mtgr_status_t launch_mode(const AttnIO& io, const void* c1, int64_t ld_c1
     cudaMalloc(&a2.dbg, 11 * 64 * sizeof(long long));
     cudaMemsetAsync(a2.dbg, 0, 11 * 64 * sizeof(long long), st);
   }
-  attn_tc_kernel<MODE><<<grid, 384, SMEM_BYTES, st>>>(m.c1, m.x, m.r1, m.r2, m.e, m.u, a2);
+  attn_tc_kernel<MODE><<<grid, 384, SMEM_BYTES, st>>>(m.c1, m.x, m.r1, m.r2, m.e, m.u, m.o, m.o2, a2);
   if (trace) {
     long long hb[11 * 64];
     cudaMemcpyAsync(hb, a2.dbg, sizeof(hb), cudaMemcpyDeviceToHost, st);
