@@ -179,6 +179,7 @@ static mtgr_status_t layer_fwd_t(const mtgr_layer_cfg_t* c, const mtgr_jagged_t*
   g.A = xt; g.lda = d; g.a_kmajor = 1;
   g.B = P->w1; g.ldb = d; g.b_kmajor = 1;
   g.C = p; g.ldc = 4 * d; g.C2 = a; g.bias = P->b1; g.silu = c->qkvu_silu;
+  g.c_dsilu = 1;  // the backward needs only silu'(p): saved in p's place
   MTGR_TRY(run_gemm<T>(g, EPI_QKVU, gws, gws_bytes, st));
   // O = silu(Q K^T)/N (.) M V;  Y = O (.) U  (Eq.5, Eq.6 gate)
   AttnIO at{};
@@ -257,14 +258,14 @@ static mtgr_status_t layer_bwd_t(const mtgr_layer_cfg_t* c, const mtgr_jagged_t*
   GlnBwdIO gi{};
   gi.dy = buf; gi.x = y; gi.mean = mu2; gi.rstd = r2; gi.gamma = P->gamma2; gi.gid = j->group_id;
   gi.dx = dO; gi.ntok = ntok; gi.d = d; gi.G = c->num_groups;
-  gi.o = o; gi.u = a + 3 * d; gi.pre_u = c->qkvu_silu ? p + 3 * d : nullptr; gi.ld_a = 4 * d;
+  gi.o = o; gi.u = a + 3 * d; gi.pre_u = c->qkvu_silu ? p + 3 * d : nullptr; gi.pre_dsilu = 1; gi.ld_a = 4 * d;
   gi.dpu = dp + 3 * d; gi.ld_dp = 4 * d; gi.dcol = G->b1 + 3 * d;  // db1 of the U block
   MTGR_TRY(gln_bwd_launch<T>(gi, GLNB_GATE, (float*)scratch, G->gamma2, G->beta2, acc, st));
   // attention backward (+ silu' of Q, K, V) into dp[:, 0:3d]
   AttnIO at{};
   at.jag = *j; at.H = H; at.dh = d / H; at.d = d; at.nb = c->rab_buckets;
   at.q = a; at.k = a + d; at.v = a + 2 * d; at.ld = 4 * d;
-  at.dO = dO; at.pre = c->qkvu_silu ? p : nullptr; at.ld_pre = 4 * d;
+  at.dO = dO; at.pre = c->qkvu_silu ? p : nullptr; at.ld_pre = 4 * d; at.pre_dsilu = 1;
   at.dq = dp; at.dk = dp + d; at.dv = dp + 2 * d; at.ld_out = 4 * d;
   at.rab_w = P->rab_w; at.drab = c->rab_buckets > 0 ? G->rab_w : nullptr;
   at.dbias = tc_attn ? G->b1 : nullptr;  // db1 of the Q|K|V blocks fused into the epilogues

@@ -148,6 +148,7 @@ struct GlnBwdArgs {
   const T* o;     // [T][d]
   const T* u;     // rows ld_a
   const T* pre_u; // rows ld_a (pre-activation of U) or NULL (linear)
+  int pre_dsilu;  // pre_u holds silu'(p_U) already
   int64_t ld_a;
   T* dpu;         // rows ld_dp
   int64_t ld_dp;
@@ -270,7 +271,7 @@ __global__ void __launch_bounds__(32 * GLNB_WARPS, (NC <= 2 ? (MODE == GLN_GATE 
           for (int e = 0; e < 8; ++e) {
             dO[e] = o[e] * uu[e];
             du[e] = o[e] * oo[e];
-            if (a.pre_u) du[e] *= dsilu_f(pp[e]);
+            if (a.pre_u) du[e] *= a.pre_dsilu ? pp[e] : dsilu_f(pp[e]);
             pc[k][e] += du[e];
           }
           store8(a.dx + (int64_t)t * d + c * 8, dO);
@@ -376,7 +377,7 @@ mtgr_status_t gln_bwd_launch(const GlnBwdIO& io, int mode, float* part, float* d
   a.dy = (const T*)io.dy; a.x = (const T*)io.x; a.mean = io.mean; a.rstd = io.rstd;
   a.gamma = io.gamma; a.gid = io.gid; a.dx = (T*)io.dx; a.part = part;
   a.ntok = io.ntok; a.d = io.d; a.G = io.G;
-  a.o = (const T*)io.o; a.u = (const T*)io.u; a.pre_u = (const T*)io.pre_u; a.ld_a = io.ld_a;
+  a.o = (const T*)io.o; a.u = (const T*)io.u; a.pre_u = (const T*)io.pre_u; a.pre_dsilu = io.pre_dsilu; a.ld_a = io.ld_a;
   a.dpu = (T*)io.dpu; a.ld_dp = io.ld_dp; a.dz = (const T*)io.dz; a.dcol = io.dcol;
   a.tok_per_warp = gln_bwd_tok_per_warp(io.ntok);
   int nb = io.ntok > 0 ? gln_bwd_blocks(io.ntok) : 0;

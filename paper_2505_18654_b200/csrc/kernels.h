@@ -16,6 +16,7 @@ struct GlnBwdIO {
   const void* o; const void* u; const void* pre_u; int64_t ld_a; void* dpu; int64_t ld_dp;
   const void* dz;
   float* dcol;  // optional fused column sum (red.add): sum_t dz (RESID) or sum_t dp_U (GATE)
+  int pre_dsilu;  // pre_u already holds silu'(p_U) (the layer's saved form)
 };
 size_t gln_bwd_ws_bytes(int ntok, int d, int G);
 template <class T>
@@ -38,6 +39,7 @@ struct GemmIO {
   const void* R; int64_t ldr;  // EPI_RESID residual
   int accumulate;              // EPI_F32
   int silu;                    // EPI_QKVU: 1 = C2 = silu(C), 0 = C2 = C
+  int c_dsilu;                 // EPI_QKVU with silu: C receives silu'(pre) instead of pre
 };
 template <class T>
 mtgr_status_t gemm_simt_launch(const GemmIO& g, int epi, cudaStream_t st);
@@ -54,6 +56,7 @@ struct AttnIO {
   void* o; void* y;            // fwd outputs [T][d]
   const void* dO;              // bwd input [T][d]
   const void* pre; int64_t ld_pre;  // silu' source (points at Q block) or NULL
+  int pre_dsilu;               // pre already holds silu'(p) (the layer's saved form)
   void* dq; void* dk; void* dv; int64_t ld_out;
   const float* diag_a;         // [T][H]  nu*silu(s_ii) for non-static tokens, 0 otherwise
   const float* diag_ds;        // [T][H]  nu*silu'(s_ii)*(dO_i . v_i)

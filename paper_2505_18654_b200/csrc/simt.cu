@@ -71,7 +71,7 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmIO g) {
         float* C = (float*)g.C + (int64_t)m * g.ldc + n;
         *C = g.accumulate ? *C + v : v;
       } else if (EPI == EPI_QKVU) {
-        ((T*)g.C)[(int64_t)m * g.ldc + n] = from_f<T>(v);
+        ((T*)g.C)[(int64_t)m * g.ldc + n] = from_f<T>(g.silu && g.c_dsilu ? dsilu_f(v) : v);
         ((T*)g.C2)[(int64_t)m * g.ldc + n] = from_f<T>(g.silu ? silu_f(v) : v);
       } else if (EPI == EPI_RESID) {
         v += to_f(((const T*)g.R)[(int64_t)m * g.ldr + n]);
@@ -342,8 +342,10 @@ __global__ void __launch_bounds__(256) attn_simt_dkv_kernel(AttnIO a) {
     float gv = us.nu * accv[c] + da * to_f(dO[t * a.d + cc]);
     float gk = us.nu * acck[c] + dd * to_f(q[t * a.ld + cc]);
     if (pre) {
-      gk *= dsilu_f(to_f(pre[t * a.ld_pre + (int64_t)a.d + col0 + cc]));
-      gv *= dsilu_f(to_f(pre[t * a.ld_pre + 2 * (int64_t)a.d + col0 + cc]));
+      const float pk = to_f(pre[t * a.ld_pre + (int64_t)a.d + col0 + cc]);
+      const float pv = to_f(pre[t * a.ld_pre + 2 * (int64_t)a.d + col0 + cc]);
+      gk *= a.pre_dsilu ? pk : dsilu_f(pk);
+      gv *= a.pre_dsilu ? pv : dsilu_f(pv);
     }
     ((T*)a.dk)[t * a.ld_out + col0 + cc] = from_f<T>(gk);
     ((T*)a.dv)[t * a.ld_out + col0 + cc] = from_f<T>(gv);
@@ -417,7 +419,10 @@ __global__ void __launch_bounds__(256) attn_simt_dq_kernel(AttnIO a) {
     if (c >= ncol) break;
     int cc = cg + 8 * c;
     float g = us.nu * acc[c] + dd * to_f(k[t * a.ld + cc]);
-    if (pre) g *= dsilu_f(to_f(pre[t * a.ld_pre + col0 + cc]));
+    if (pre) {
+      const float pq = to_f(pre[t * a.ld_pre + col0 + cc]);
+      g *= a.pre_dsilu ? pq : dsilu_f(pq);
+    }
     ((T*)a.dq)[t * a.ld_out + col0 + cc] = from_f<T>(g);
   }
 }

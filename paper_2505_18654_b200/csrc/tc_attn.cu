@@ -44,7 +44,6 @@ constexpr int DH = 256;
 constexpr int BR = 128;                 // rows per CTA
 constexpr int BC = 64;                  // columns per iterated tile
 constexpr int KB = 1024;
-constexpr int CT_BYTES = BC * DH * 2;   // 32 KB: 4 boxes {64 dh, 64 rows}
 constexpr int RT_BYTES = BR * DH * 2;   // 64 KB: 4 boxes {64 dh, 128 rows}
 constexpr int T_BYTES = BR * BC * 2;    // 16 KB
 constexpr int OFF_T = 192 * KB;
@@ -62,13 +61,16 @@ struct Args {
   __nv_bfloat16* out2;                      // FWD y (ld_out)
   const float* diag;                        // [T][H]
   int has_u;                                // U / pre tile present
+  int pre_dsilu;                            // the pre tile holds silu'(p) already
   float* dbias;                             // bwd: red.add column sums of the outputs, or NULL
   long long* dbg;                           // debug timestamps (MTGR_ATTN_TRACE) or NULL
 };
 
 // debug tracing of one CTA (MTGR_ATTN_TRACE=1): slot layout [event][tile]
-#define DBG_ON (a.dbg != nullptr && blockIdx.x == 2 && blockIdx.y == 0 && blockIdx.z == 0)
-#define DBG(slot) do { if (DBG_ON) a.dbg[(slot)] = clock64(); } while (0)
+// (the CTA pair (2,0,0) / (3,0,0); slot 10*64+10 = after the start-up cluster barrier, the
+// common time base of the two SMs' clocks)
+#define DBG_ON (a.dbg != nullptr && (blockIdx.x == 2 || blockIdx.x == 3) && blockIdx.y == 0 && blockIdx.z == 0)
+#define DBG(slot) do { if (DBG_ON) a.dbg[(blockIdx.x - 2) * 11 * 64 + (slot)] = clock64(); } while (0)
 
 __device__ __forceinline__ float silu_fast(float s) {
   const float h = 0.5f * s;
@@ -87,37 +89,40 @@ __device__ __forceinline__ uint32_t sw128(int r, int j) { return r * 128 + ((j ^
 
 template <int MODE>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
-    attn_tc_kernel(const __grid_constant__ CUtensorMap tmC1, const __grid_constant__ CUtensorMap tmX,
-                   const __grid_constant__ CUtensorMap tmR1, const __grid_constant__ CUtensorMap tmR2,
-                   const __grid_constant__ CUtensorMap tmE, const __grid_constant__ CUtensorMap tmU,
-                   const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmO2,
-                   Args a) {
+    attn_tc_kernel(const __grid_constant__ CUtensorMap tmC1, const __grid_constant__ CUtensorMap tmC2,
+                   const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmR1,
+                   const __grid_constant__ CUtensorMap tmR2, const __grid_constant__ CUtensorMap tmE,
+                   const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUtensorMap tmO,
+                   const __grid_constant__ CUtensorMap tmO2, Args a) {
   using namespace sm100;
   constexpr bool TWO = (MODE == DQ || MODE == DK);
   constexpr bool TRANS = (MODE == DV || MODE == DK);
-  // smem map (KB):      !TWO (FWD, DV)                      TWO (DQ, DK)
-  //   [0,64)     C1 slots 0,1 -> E (after last S)        R1 (S A operand) -> E
-  //   [64,96)    C1 slot 2                                R2 head-dim 128..255 (dP A, SS);
-  //                                                       prologue: staging of R2 0..127 -> U 0,1
-  //   [96,128)   X slot 0                                 C1 slot 0
-  //   [128,160)  X slot 1                                 C1 slot 1
-  //   [160,192)  R1 staging, then U (prefetched early)    C1 slot 2
-  //   [192,224)  R1 staging, then U                       C2 slot (two halves) -> U 2,3
-  // (The rings receive multicast data from the peer CTA, so nothing CTA-private may alias them
-  //  while the peer can still be filling them.)
-  // TMEM columns:  !TWO: R1 [0,128) (TS A operand), acc [128,384), S [384,448), P [448,512)
-  //                 TWO: acc [0,256), S [256,320), dP [320,384), P [384,448),
-  //                      R2 head-dim 0..127 [448,512) (TS A operand of the first dP half)
-  // (Measured, tools/microbench: an SS M=128 N=64 MMA is smem-bound at 48 cycles, a TS one
-  //  runs at its 32-cycle floor.  FWD/DV keep R1 in TMEM; DQ/DK cannot hold both row operands
-  //  in TMEM, so half of R2 lives in TMEM to free smem for a 3-slot C1 ring.)
+  // A CTA pair (cluster of 2) owns two consecutive 128-row tiles of one (user, head) and runs
+  // every MMA as tcgen05.mma.cta_group::2 with M = 256: each CTA keeps its own 128 rows of the
+  // A operands and receives only HALF of every column tile — the score MMA's B operand is split
+  // by columns (32 of the 64), the accumulate MMA's B operand by head dim (128 of the 256) — so
+  // per-SM operand traffic is halved.  The leader CTA issues the MMAs; both CTAs run the softmax
+  // and epilogue warps on their own rows.
+  // smem (KB):     !TWO (FWD, DV)                        TWO (DQ, DK)
+  //   [0,48)      C1 ring: 3 x 16 (32 cols x 256 dh)    R1 (S A operand, SS)   [0,64) -> E
+  //   [48,96)     X ring:  3 x 16 (64 cols x 128 dh)    R2 dh 128..255 [64,96) (staging of
+  //                                                     R2 dh 0..127 first) -> U 0,1
+  //   [96,160)    R1 staging -> U                       C1 ring 3 x 16 [96,144)
+  //   [160,224)   E (prefetched at start)               C2 ring 2 x 16 [144,176) -> U 2,3
+  //                                                     X ring 2 x 16 [176,208)
+  // TMEM:  !TWO: R1 [0,128) (TS A), acc [128,384), S [384,448), P [448,512)
+  //         TWO: acc [0,256), S [256,320), dP [320,384), P [384,448), R2 dh 0..127 [448,512)
+  constexpr int C1_BYTES = 32 * DH * 2;        // 16 KB: 4 boxes {64 dh, 32 cols}
+  constexpr int X_BYTES = BC * (DH / 2) * 2;   // 16 KB: 2 boxes {64 dh, 64 cols}
   constexpr int NC1 = 3;
-  constexpr int NX = TWO ? 1 : 2;
-  constexpr int OFF_R1 = 0, OFF_R2B = 64 * KB;
-  constexpr int OFF_R1STAGE = 160 * KB;
-  constexpr int OFF_E = 0;
-  constexpr int OFF_X = TWO ? 192 * KB : 96 * KB;
+  constexpr int NC2 = 2;
+  constexpr int NX = TWO ? 2 : 3;
   constexpr int OFF_C1 = TWO ? 96 * KB : 0;
+  constexpr int OFF_C2 = 144 * KB;
+  constexpr int OFF_X = TWO ? 176 * KB : 48 * KB;
+  constexpr int OFF_R1 = 0, OFF_R2B = 64 * KB;
+  constexpr int OFF_R1STAGE = 96 * KB;
+  constexpr int OFF_E = TWO ? 0 : 160 * KB;
   constexpr uint32_t T_R1 = 0;
   constexpr uint32_t T_ACC = TWO ? 0 : 128;
   constexpr uint32_t T_S = TWO ? 256 : 384;
@@ -125,13 +130,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
   constexpr uint32_t T_P = TWO ? 384 : 448;
   constexpr uint32_t T_R2A = 448;
 
-  // A cluster = two consecutive row tiles of the same (user, head): the column tiles they both
-  // stream are loaded once from L2 and multicast into both CTAs (each CTA issues half of the
-  // boxes), halving L2->SM traffic.  The column range is the union over the pair (the mask
-  // predicate makes the extra tiles exact zeros).  The second CTA of a user with an odd number
-  // of row tiles runs the pipeline on masked rows and stores nothing.
   const int u = blockIdx.z, h = blockIdx.y, r0 = blockIdx.x * BR;
-  const uint16_t crank = (uint16_t)sm100::cluster_ctarank();
+  const uint32_t crank = cluster_ctarank();
+  const bool leader = crank == 0;
   const UserSpan us = load_user(a.jag, u);
   const int pr0 = (blockIdx.x & ~1) * BR;
   if (pr0 >= us.L) return;  // uniform over the cluster
@@ -145,290 +146,311 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     c_end = us.L;
   }
   const int ntiles = c_end > c_begin ? (c_end - c_begin + BC - 1) / BC : 0;
+  const bool need_e = r0 + BR > us.ns;  // only tiles with non-static rows have diagonal terms
 
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-B aligned base, derived by indexing the shared array so the compiler keeps the shared
+  // address space (LDS/STS rather than generic LD/ST for every staged access)
+  uint8_t* smem = smem_raw + ((1024u - (sm100::smem_u32(smem_raw) & 1023u)) & 1023u);
   long long* sTs = reinterpret_cast<long long*>(smem + OFF_TS);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
-  uint64_t* c1_full = bars;           // [3]
+  uint64_t* c1_full = bars;           // [3] leader
   uint64_t* c1_empty = bars + 3;      // [3]
-  uint64_t* x_full = bars + 6;        // [3]
+  uint64_t* x_full = bars + 6;        // [3] leader
   uint64_t* x_empty = bars + 9;       // [3]
-  uint64_t* s_full = bars + 12;       // [2]
-  uint64_t* s_free = bars + 14;       // [2]
-  uint64_t* t_full = bars + 16;       // [2]  P buffer written
-  uint64_t* t_free = bars + 18;       // [2]  P buffer consumed by its acc MMAs
-  uint64_t* r1_full = bars + 20;
-  uint64_t* r1_done = bars + 21;      // R1 copied into TMEM (FWD/DV)
-  uint64_t* r2_full = bars + 22;
-  uint64_t* e_full = bars + 23;
-  uint64_t* u_full = bars + 24;
-  uint64_t* o_full = bars + 25;
-  uint64_t* sc_done = bars + 26;      // every score MMA (S, dP) has completed
-  uint64_t* r2a_full = bars + 27;     // TWO: R2 head-dim 0..127 staged in smem
-  uint64_t* r2a_done = bars + 28;     // TWO: ... and copied into TMEM
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 29);
-  auto c1_slot = [&](int t) -> uint8_t* { return smem + OFF_C1 + (t % NC1) * CT_BYTES; };
+  uint64_t* c2_full = bars + 12;      // [2] leader
+  uint64_t* c2_empty = bars + 14;     // [2]
+  uint64_t* s_full = bars + 16;
+  uint64_t* s_free = bars + 17;       // leader, both CTAs' softmax threads
+  uint64_t* t_full = bars + 18;       // [2] leader, both CTAs
+  uint64_t* t_free = bars + 20;       // [2]
+  uint64_t* r1_full = bars + 22;
+  uint64_t* r1_done = bars + 23;      // leader, both CTAs (R1 in TMEM)
+  uint64_t* r1_copied = bars + 24;    // own (staging area reusable)
+  uint64_t* r2a_full = bars + 25;
+  uint64_t* r2a_done = bars + 26;     // leader, both CTAs
+  uint64_t* r2a_copied = bars + 27;   // own
+  uint64_t* r2_full = bars + 28;      // leader: R2B of both CTAs (SS A operand)
+  uint64_t* r1s_full = bars + 29;     // leader: R1 of both CTAs (TWO: SS A operand)
+  uint64_t* e_full = bars + 30;
+  uint64_t* u_full = bars + 31;
+  uint64_t* o_full = bars + 32;
+  uint64_t* sc_done = bars + 33;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 34);
   auto u_box = [&](int b) -> uint8_t* {  // smem of U box b (16 KB each)
-    if (TWO) return b < 2 ? smem + 64 * KB + b * (RT_BYTES / 4) : smem + 192 * KB + (b - 2) * (RT_BYTES / 4);
-    return smem + 160 * KB + b * (RT_BYTES / 4);
+    if (TWO) return b < 2 ? smem + 64 * KB + b * (RT_BYTES / 4) : smem + OFF_C2 + (b - 2) * (RT_BYTES / 4);
+    return smem + OFF_R1STAGE + b * (RT_BYTES / 4);
+  };
+  auto arrive_leader = [&](uint64_t* bar) {  // one arrival per warp (whole warp calls)
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) {
+      if (leader) mbar_arrive(bar);
+      else mbar_arrive_cluster(bar, 0);
+    }
   };
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) DBG(10 * 64 + 4);
   if (warp == 0 && lane == 0) {
-    tma_prefetch(&tmC1);
-    tma_prefetch(&tmX);
-    tma_prefetch(&tmR1);
     for (int s = 0; s < 3; ++s) {
-      mbar_init(&c1_full[s], 1); mbar_init(&c1_empty[s], 2);  // empties: released by both CTAs
-      mbar_init(&x_full[s], 1); mbar_init(&x_empty[s], 2);
+      mbar_init(&c1_full[s], 1); mbar_init(&c1_empty[s], 1);
+      mbar_init(&x_full[s], 1); mbar_init(&x_empty[s], 1);
     }
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(&s_full[b], 1); mbar_init(&s_free[b], 32 * NSM);
-      mbar_init(&t_full[b], 32 * NSM); mbar_init(&t_free[b], 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&c2_full[s], 1); mbar_init(&c2_empty[s], 1);
+      mbar_init(&t_full[s], 2 * NSM); mbar_init(&t_free[s], 1);
     }
+    mbar_init(s_full, 1);
+    mbar_init(s_free, 2 * NSM);
     mbar_init(r1_full, 1);
-    mbar_init(r1_done, 32 * NSM);
+    mbar_init(r1_done, 2 * NSM);
+    mbar_init(r1_copied, 32 * NSM);
+    mbar_init(r2a_full, 1);
+    mbar_init(r2a_done, 2 * NSM);
+    mbar_init(r2a_copied, 32 * NSM);
     mbar_init(r2_full, 1);
+    mbar_init(r1s_full, 1);
     mbar_init(e_full, 1);
     mbar_init(u_full, 1);
     mbar_init(o_full, 1);
     mbar_init(sc_done, 1);
-    mbar_init(r2a_full, 1);
-    mbar_init(r2a_done, 32 * NSM);
     fence_barrier_init();
   }
-  if (warp == 2) tmem_alloc<512>(tmem_slot);
+  if (warp == 2) tmem_alloc_2sm<512>(tmem_slot);
   tc_fence_before();
-  cluster_sync();  // barriers of both CTAs initialised before any multicast traffic
+  cluster_sync();  // barriers of both CTAs initialised, TMEM allocated in both
   tc_fence_after();
+  if (threadIdx.x == 0) DBG(10 * 64 + 10);
   const uint32_t tmem = *tmem_slot;
   const int hcol = h * DH;
-  const int row0 = us.off + r0;  // global row of the tile's first row
+  const int row0 = us.off + r0;  // global row of this CTA's first row
 
   if (warp == 0) {
-    // ---------------------------------------------------------------- producer A: R1, R2, C1, E (, U)
+    // ---------------------------------------------------------------- producer A: R1 / R2, C1, E (, U)
     if (lane == 0) {
-      if (ntiles > 0 || !TWO) {
-        mbar_expect_tx(r1_full, RT_BYTES);
-        uint8_t* r1dst = smem + (TWO ? OFF_R1 : OFF_R1STAGE);
-#pragma unroll
-        for (int c = 0; c < 4; ++c) tma_load_2d(r1dst + c * (RT_BYTES / 4), &tmR1, r1_full, hcol + c * 64, row0);
-      }
       if (ntiles > 0) {
-        if (TWO) {  // R2 head-dim 0..127 -> staging (copied to TMEM by the softmax warps)
+        if (!TWO) {
+          mbar_expect_tx(r1_full, RT_BYTES);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) tma_load_2d(smem + OFF_R1STAGE + c * (RT_BYTES / 4), &tmR1, r1_full, hcol + c * 64, row0);
+        } else {
+          // R1 (SS A operand of S): both CTAs' bytes complete on the leader's r1s_full
+          if (leader) mbar_expect_tx(r1s_full, 2 * RT_BYTES);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) tma_load_2d_2sm(smem + OFF_R1 + c * (RT_BYTES / 4), &tmR1, r1s_full, hcol + c * 64, row0);
+          // R2 head-dim 0..127 -> staging (then TMEM via the softmax warps)
           mbar_expect_tx(r2a_full, RT_BYTES / 2);
 #pragma unroll
           for (int c = 0; c < 2; ++c) tma_load_2d(smem + OFF_R2B + c * (RT_BYTES / 4), &tmR2, r2a_full, hcol + c * 64, row0);
         }
         for (int t = 0; t < ntiles; ++t) {
           if (TWO && t == NC1) {
-            // R2 head-dim 128..255 replaces the staging once its first half sits in TMEM
-            mbar_wait(r2a_done, 0);
-            mbar_expect_tx(r2_full, RT_BYTES / 2);
+            mbar_wait(r2a_copied, 0);
+            if (leader) mbar_expect_tx(r2_full, RT_BYTES);
 #pragma unroll
-            for (int c = 2; c < 4; ++c) tma_load_2d(smem + OFF_R2B + (c - 2) * (RT_BYTES / 4), &tmR2, r2_full, hcol + c * 64, row0);
+            for (int c = 2; c < 4; ++c) tma_load_2d_2sm(smem + OFF_R2B + (c - 2) * (RT_BYTES / 4), &tmR2, r2_full, hcol + c * 64, row0);
           }
           const int slot = t % NC1;
           mbar_wait(&c1_empty[slot], ((t / NC1) & 1) ^ 1);
-          mbar_expect_tx(&c1_full[slot], CT_BYTES);
-          const int row = us.off + c_begin + t * BC;
-          uint8_t* dst = c1_slot(t);
+          if (leader) mbar_expect_tx(&c1_full[slot], 2 * C1_BYTES);
+          const int row = us.off + c_begin + t * BC + 32 * crank;  // this CTA's 32 columns
+          uint8_t* dst = smem + OFF_C1 + slot * C1_BYTES;
 #pragma unroll
-          for (int c = crank * 2; c < crank * 2 + 2; ++c)
-            tma_load_2d_mc(dst + c * (CT_BYTES / 4), &tmC1, &c1_full[slot], hcol + c * 64, row, 0x3);
+          for (int c = 0; c < 4; ++c) tma_load_2d_2sm(dst + c * (C1_BYTES / 4), &tmC1, &c1_full[slot], hcol + c * 64, row);
         }
         if (TWO && ntiles <= NC1) {
-          mbar_wait(r2a_done, 0);
-          mbar_expect_tx(r2_full, RT_BYTES / 2);
+          mbar_wait(r2a_copied, 0);
+          if (leader) mbar_expect_tx(r2_full, RT_BYTES);
 #pragma unroll
-          for (int c = 2; c < 4; ++c) tma_load_2d(smem + OFF_R2B + (c - 2) * (RT_BYTES / 4), &tmR2, r2_full, hcol + c * 64, row0);
+          for (int c = 2; c < 4; ++c) tma_load_2d_2sm(smem + OFF_R2B + (c - 2) * (RT_BYTES / 4), &tmR2, r2_full, hcol + c * 64, row0);
         }
-        mbar_wait(sc_done, 0);  // the E (and TWO: U) regions are free from here on
+        if (TWO) mbar_wait(sc_done, 0);  // R1 / R2B / C2 regions are free from here on
       }
-      if (r0 + BR > us.ns) {  // only tiles with non-static rows have diagonal terms (E)
+      if (!TWO && need_e) {  // private region, needed only by the epilogue: behind the C1 ring
         mbar_expect_tx(e_full, RT_BYTES);
 #pragma unroll
         for (int c = 0; c < 4; ++c) tma_load_2d(smem + OFF_E + c * (RT_BYTES / 4), &tmE, e_full, hcol + c * 64, row0);
       }
-      if (TWO && a.has_u) {
-        mbar_expect_tx(u_full, RT_BYTES);
+      if (TWO) {
+        if (need_e) {
+          mbar_expect_tx(e_full, RT_BYTES);
 #pragma unroll
-        for (int c = 0; c < 4; ++c) tma_load_2d(u_box(c), &tmU, u_full, hcol + c * 64, row0);
-      }
-    }
-  } else if (warp == 3) {
-    // ---------------------------------------------------------------- producer B: X or C2 (, U)
-    if (lane == 0) {
-      if (!TWO && a.has_u) {
-        mbar_wait(r1_done, 0);  // U replaces the (CTA-private) R1 staging area
-        mbar_expect_tx(u_full, RT_BYTES);
+          for (int c = 0; c < 4; ++c) tma_load_2d(smem + OFF_E + c * (RT_BYTES / 4), &tmE, e_full, hcol + c * 64, row0);
+        }
+        if (a.has_u) {
+          mbar_expect_tx(u_full, RT_BYTES);
 #pragma unroll
-        for (int c = 0; c < 4; ++c) tma_load_2d(u_box(c), &tmU, u_full, hcol + c * 64, row0);
-      }
-      for (int t = 0; t < ntiles; ++t) {
-        const int row = us.off + c_begin + t * BC;
-        if (TWO) {
-          // C2: one slot split in two head-dim halves with their own barriers, so the first half
-          // of the next tile is refilled while the dP MMAs still read the second half
-          for (int hh = 0; hh < 2; ++hh) {
-            mbar_wait(&x_empty[hh], (t & 1) ^ 1);
-            mbar_expect_tx(&x_full[hh], CT_BYTES / 2);
-            const int c = 2 * hh + crank;
-            tma_load_2d_mc(smem + OFF_X + c * (CT_BYTES / 4), &tmX, &x_full[hh], hcol + c * 64, row, 0x3);
-          }
-        } else {
-          const int slot = t % NX;
-          mbar_wait(&x_empty[slot], ((t / NX) & 1) ^ 1);
-          mbar_expect_tx(&x_full[slot], CT_BYTES);
-          uint8_t* dst = smem + OFF_X + slot * CT_BYTES;
-#pragma unroll
-          for (int c = crank * 2; c < crank * 2 + 2; ++c)
-            tma_load_2d_mc(dst + c * (CT_BYTES / 4), &tmX, &x_full[slot], hcol + c * 64, row, 0x3);
+          for (int c = 0; c < 4; ++c) tma_load_2d(u_box(c), &tmU, u_full, hcol + c * 64, row0);
         }
       }
     }
+  } else if (warp == 3) {
+    // ---------------------------------------------------------------- producer B: X (, U) | C2
+    if (lane == 0) {
+      auto load_u = [&]() {  // !TWO: U replaces the R1 staging area
+        if (!TWO && a.has_u) {
+          if (ntiles > 0) mbar_wait(r1_copied, 0);
+          mbar_expect_tx(u_full, RT_BYTES);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) tma_load_2d(u_box(c), &tmU, u_full, hcol + c * 64, row0);
+        }
+      };
+      for (int t = 0; t < ntiles; ++t) {
+        if (TWO) {
+          const int slot = t % NC2;
+          mbar_wait(&c2_empty[slot], ((t / NC2) & 1) ^ 1);
+          if (leader) mbar_expect_tx(&c2_full[slot], 2 * C1_BYTES);
+          const int row = us.off + c_begin + t * BC + 32 * crank;
+          uint8_t* dst = smem + OFF_C2 + slot * C1_BYTES;
+#pragma unroll
+          for (int c = 0; c < 4; ++c) tma_load_2d_2sm(dst + c * (C1_BYTES / 4), &tmC2, &c2_full[slot], hcol + c * 64, row);
+        } else {
+          const int slot = t % NX;
+          mbar_wait(&x_empty[slot], ((t / NX) & 1) ^ 1);
+          if (leader) mbar_expect_tx(&x_full[slot], 2 * X_BYTES);
+          const int row = us.off + c_begin + t * BC;
+          uint8_t* dst = smem + OFF_X + slot * X_BYTES;
+#pragma unroll
+          for (int c = 0; c < 2; ++c)  // this CTA's half of the head dim
+            tma_load_2d_2sm(dst + c * (X_BYTES / 2), &tmX, &x_full[slot], hcol + (2 * crank + c) * 64, row);
+        }
+      }
+      load_u();
+    }
+  } else if (warp == 2) {
+    // ---------------------------------------------------------------- producer C (TWO): X
+    if (TWO && lane == 0) {
+      for (int t = 0; t < ntiles; ++t) {
+        const int slot = t % NX;
+        mbar_wait(&x_empty[slot], ((t / NX) & 1) ^ 1);
+        if (leader) mbar_expect_tx(&x_full[slot], 2 * X_BYTES);
+        const int row = us.off + c_begin + t * BC;
+        uint8_t* dst = smem + OFF_X + slot * X_BYTES;
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+          tma_load_2d_2sm(dst + c * (X_BYTES / 2), &tmX, &x_full[slot], hcol + (2 * crank + c) * 64, row);
+      }
+    }
   } else if (warp == 1) {
-    // ---------------------------------------------------------------- MMA issuer
-    // The whole warp walks the schedule so every operand is warp-uniform (uniform registers, no
-    // per-instruction waterfall); one elected lane issues the tcgen05 instructions.
+    // ---------------------------------------------------------------- MMA issuer (leader CTA)
+    // The whole warp walks the schedule so every operand is warp-uniform; one lane issues.
     const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
     const int nt = __shfl_sync(0xffffffffu, ntiles, 0);
-    if (nt == 0) {
+    if (leader && nt == 0) {
+      if (elect_one()) mbar_arrive(o_full);
+      __syncwarp();
+    }
+    if (!leader && nt == 0) {
       if (lane == 0) mbar_arrive(o_full);
-    } else {
-      constexpr uint32_t idesc_s = idesc_bf16_f32(BR, BC, 0, 0);
-      constexpr uint32_t idesc_acc = idesc_bf16_f32(BR, DH, 0, 1);
+    }
+    if (leader && nt > 0) {
+      constexpr uint32_t idesc_s = idesc_bf16_f32(2 * BR, BC, 0, 0);
+      constexpr uint32_t idesc_acc = idesc_bf16_f32(2 * BR, DH, 0, 1);
       const uint32_t r1_base = smem_u32(smem + OFF_R1);
       const uint32_t r2b_base = smem_u32(smem + OFF_R2B);
+      const uint32_t c1_base = smem_u32(smem + OFF_C1);
+      const uint32_t c2_base = smem_u32(smem + OFF_C2);
       const uint32_t x_base = smem_u32(smem + OFF_X);
       if (TWO) {
-        mbar_wait(r1_full, 0);
+        mbar_wait(r1s_full, 0);
         mbar_wait(r2a_done, 0);
         mbar_wait(r2_full, 0);
       } else {
-        mbar_wait(r1_done, 0);  // R1 copied into TMEM by the softmax warps
+        mbar_wait(r1_done, 0);  // R1 of both CTAs copied into TMEM
       }
-      // acc += P_j X_j  (A = P from TMEM, B = X MN-major)
+      // acc += P_j X_j  (A = P from each CTA's TMEM, B = X: each CTA's half of the head dim)
       auto acc = [&](int j) {
         const int tb = j & 1;
         if (j < 64 && lane == 0) DBG(3 * 64 + j);
         mbar_wait(&t_full[tb], (j >> 1) & 1);
         if (j < 64 && lane == 0) DBG(4 * 64 + j);
-        uint32_t x;
-        if (TWO) {
-          x = smem_u32(c1_slot(j));  // X = C1 (held in the C1 ring until here)
-        } else {
-          mbar_wait(&x_full[j % NX], (j / NX) & 1);
-          x = x_base + (j % NX) * CT_BYTES;
-        }
+        mbar_wait(&x_full[j % NX], (j / NX) & 1);
+        const uint32_t x = x_base + (j % NX) * X_BYTES;
         tc_fence_after();
         if (elect_one()) {
 #pragma unroll
           for (int k = 0; k < BC / 16; ++k)
-            mma_bf16_ts(tm + T_ACC, tm + T_P + tb * 32 + k * 8,
-                        desc_sw128(x + k * 2048, CT_BYTES / 4, 1024), idesc_acc, (j > 0 || k > 0));
-          mma_commit(&t_free[tb]);
-          if (TWO) mma_commit_mc(&c1_empty[j % NC1], 0x3);
-          else mma_commit_mc(&x_empty[j % NX], 0x3);
+            mma_bf16_ts_2sm(tm + T_ACC, tm + T_P + tb * 32 + k * 8,
+                            desc_sw128(x + k * 2048, X_BYTES / 2, 1024), idesc_acc, (j > 0 || k > 0));
+          mma_commit_2sm_mc(&t_free[tb], 0x3);
+          mma_commit_2sm_mc(&x_empty[j % NX], 0x3);
         }
         __syncwarp();
       };
       for (int t = 0; t < nt; ++t) {
         if (t < 64 && lane == 0) DBG(0 * 64 + t);
         mbar_wait(&c1_full[t % NC1], (t / NC1) & 1);
+        if (TWO) mbar_wait(&c2_full[t % NC2], (t / NC2) & 1);
         if (t < 64 && lane == 0) DBG(1 * 64 + t);
-        mbar_wait(&s_free[0], (t & 1) ^ 1);  // single S (and dP) buffer, released on tcgen05.ld
+        mbar_wait(s_free, (t & 1) ^ 1);  // single S (and dP) buffer, released on tcgen05.ld
         if (t < 64 && lane == 0) DBG(2 * 64 + t);
         tc_fence_after();
-        const uint32_t c1 = smem_u32(c1_slot(t));
-        if (TWO) {
-          // dP first, per head-dim half, so each half of the C2 slot is released (and refilled)
-          // as early as possible
-          for (int hh = 0; hh < 2; ++hh) {
-            mbar_wait(&x_full[hh], t & 1);
-            tc_fence_after();
-            if (elect_one()) {
-#pragma unroll
-              for (int k = hh * 8; k < hh * 8 + 8; ++k) {
-                const uint64_t bd = desc_sw128(x_base + (k >> 2) * (CT_BYTES / 4) + (k & 3) * 32, 16, 1024);
-                if (hh == 0)  // head-dim 0..127 of R2 from TMEM
-                  mma_bf16_ts(tm + T_DP, tm + T_R2A + k * 8, bd, idesc_s, k > 0);
-                else          // head-dim 128..255 from smem
-                  mma_bf16_ss(tm + T_DP, desc_sw128(r2b_base + ((k >> 2) - 2) * (RT_BYTES / 4) + (k & 3) * 32, 16, 1024),
-                              bd, idesc_s, 1);
-              }
-              mma_commit_mc(&x_empty[hh], 0x3);
-            }
-            __syncwarp();
-          }
-        }
+        const uint32_t c1 = c1_base + (t % NC1) * C1_BYTES;
+        const uint32_t c2 = c2_base + (t % NC2) * C1_BYTES;
         if (elect_one()) {
           if (TWO) {
+            // dP = R2 C2^T (head dim 0..127 of R2 from TMEM, 128..255 from smem), then S = R1 C1^T
+#pragma unroll
+            for (int k = 0; k < DH / 16; ++k) {
+              const uint64_t bd = desc_sw128(c2 + (k >> 2) * (C1_BYTES / 4) + (k & 3) * 32, 16, 1024);
+              if (k < 8)
+                mma_bf16_ts_2sm(tm + T_DP, tm + T_R2A + k * 8, bd, idesc_s, k > 0);
+              else
+                mma_bf16_ss_2sm(tm + T_DP, desc_sw128(r2b_base + ((k >> 2) - 2) * (RT_BYTES / 4) + (k & 3) * 32, 16, 1024),
+                                bd, idesc_s, 1);
+            }
+            mma_commit_2sm_mc(&c2_empty[t % NC2], 0x3);
 #pragma unroll
             for (int k = 0; k < DH / 16; ++k)
-              mma_bf16_ss(tm + T_S, desc_sw128(r1_base + (k >> 2) * (RT_BYTES / 4) + (k & 3) * 32, 16, 1024),
-                          desc_sw128(c1 + (k >> 2) * (CT_BYTES / 4) + (k & 3) * 32, 16, 1024), idesc_s, k > 0);
-            mma_commit(&s_full[0]);
+              mma_bf16_ss_2sm(tm + T_S, desc_sw128(r1_base + (k >> 2) * (RT_BYTES / 4) + (k & 3) * 32, 16, 1024),
+                              desc_sw128(c1 + (k >> 2) * (C1_BYTES / 4) + (k & 3) * 32, 16, 1024), idesc_s, k > 0);
           } else {
 #pragma unroll
             for (int k = 0; k < DH / 16; ++k)
-              mma_bf16_ts(tm + T_S, tm + T_R1 + k * 8,
-                          desc_sw128(c1 + (k >> 2) * (CT_BYTES / 4) + (k & 3) * 32, 16, 1024), idesc_s, k > 0);
-            mma_commit(&s_full[0]);
-            mma_commit_mc(&c1_empty[t % NC1], 0x3);
+              mma_bf16_ts_2sm(tm + T_S, tm + T_R1 + k * 8,
+                              desc_sw128(c1 + (k >> 2) * (C1_BYTES / 4) + (k & 3) * 32, 16, 1024), idesc_s, k > 0);
           }
-          if (t + 1 == nt) mma_commit(sc_done);
+          mma_commit_2sm_mc(s_full, 0x3);
+          mma_commit_2sm_mc(&c1_empty[t % NC1], 0x3);
+          if (t + 1 == nt) mma_commit_2sm_mc(sc_done, 0x3);
         }
         __syncwarp();
         if (t >= 1) acc(t - 1);
       }
       acc(nt - 1);
-      if (elect_one()) mma_commit(o_full);
+      if (elect_one()) mma_commit_2sm_mc(o_full, 0x3);
       __syncwarp();
     }
   } else if (warp >= 4) {
     // ---------------------------------------------------------------- softmax + epilogue
-    // quadrant q = warp % 4 owns TMEM lanes (rows) q*32..q*32+31; half = which 32 of the 64 tile
-    // columns (and which 128 of the 256 head-dim columns) the warp handles.
+    // quadrant q = warp % 4 owns TMEM lanes (this CTA's rows) q*32..q*32+31; half = which 32 of
+    // the 64 tile columns (and which 128 of the 256 head-dim columns) the warp handles.
     const int q = warp & 3;
     const int half = (warp - 4) >> 2;
     const int row = q * 32 + lane;
     const int my = r0 + row;                 // user-local index of this thread's row
     const int64_t g = (int64_t)row0 + row;   // global token index
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
-    if (!TWO) {
-      // R1 row (this warp's 128 head-dim columns): smem staging -> TMEM as bf16 pairs
-      mbar_wait(r1_full, 0);
+    if (ntiles > 0) {
+      // row operand -> TMEM (bf16 pairs): !TWO: R1 (this warp's 128 head-dim columns),
+      // TWO: R2 head-dim 0..127 (this warp's 64)
+      mbar_wait(TWO ? r2a_full : r1_full, 0);
 #pragma unroll 1
-      for (int cc = 0; cc < 2; ++cc) {
-        const uint8_t* box = smem + OFF_R1STAGE + (half * 2 + cc) * (RT_BYTES / 4);
+      for (int cc = 0; cc < (TWO ? 1 : 2); ++cc) {
+        const uint8_t* box = TWO ? smem + OFF_R2B + half * (RT_BYTES / 4)
+                                 : smem + OFF_R1STAGE + (half * 2 + cc) * (RT_BYTES / 4);
         uint32_t w[32];
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           const uint4 v = *reinterpret_cast<const uint4*>(box + sw128(row, j));
           w[4 * j] = v.x; w[4 * j + 1] = v.y; w[4 * j + 2] = v.z; w[4 * j + 3] = v.w;
         }
-        tmem_st32(tmem + T_R1 + half * 64 + cc * 32 + lane_off, w);
+        tmem_st32(tmem + (TWO ? T_R2A + half * 32 : T_R1 + half * 64 + cc * 32) + lane_off, w);
       }
       tmem_st_wait();
       tc_fence_before();
-      mbar_arrive(r1_done);
-    } else if (ntiles > 0) {
-      // R2 head-dim 0..127 (this warp's 64 columns): smem staging -> TMEM as bf16 pairs
-      mbar_wait(r2a_full, 0);
-      const uint8_t* box = smem + OFF_R2B + half * (RT_BYTES / 4);
-      uint32_t w[32];
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const uint4 v = *reinterpret_cast<const uint4*>(box + sw128(row, j));
-        w[4 * j] = v.x; w[4 * j + 1] = v.y; w[4 * j + 2] = v.z; w[4 * j + 3] = v.w;
-      }
-      tmem_st32(tmem + T_R2A + half * 32 + lane_off, w);
-      tmem_st_wait();
-      tc_fence_before();
-      mbar_arrive(r2a_done);
+      mbar_arrive(TWO ? r2a_copied : r1_copied);
+      arrive_leader(TWO ? r2a_done : r1_done);
     }
     if (warp == 4 && lane == 0) DBG(10 * 64 + 3);
 
@@ -446,10 +468,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
         if (i < BC) tsb[i] = (c0 + i < us.L && a.jag.ts) ? a.jag.ts[us.off + c0 + i] : 0;
         named_bar_sync(1, 32 * NSM);
       }
-      const int sb = 0, use = t;  // single S (and dP) buffer
       const bool dbgt = warp == 4 && lane == 0 && t < 64;
       if (dbgt) DBG(5 * 64 + t);
-      mbar_wait(&s_full[sb], use & 1);
+      mbar_wait(s_full, t & 1);
       if (dbgt) DBG(6 * 64 + t);
       tc_fence_after();
       uint32_t s[32];
@@ -461,7 +482,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       }
       tmem_ld_wait();
       tc_fence_before();
-      mbar_arrive(&s_free[sb]);
+      arrive_leader(s_free);
       // visibility of this warp's 32 columns for this row (dynamic mask, R#8-R#12)
       const int cb = c0 + j_half;
       uint32_t vis;
@@ -494,7 +515,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
           vis = 0;
         }
       }
-      // P (T) values -> bf16 pairs -> TMEM P buffer (A operand of the acc MMA)
+      // P (T) values -> bf16 pairs -> TMEM P buffer (A operand of the accumulate MMA)
       uint32_t pk[16];
 #pragma unroll
       for (int e = 0; e < 32; e += 2) {
@@ -521,16 +542,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       tmem_st16(tmem + T_P + tb * 32 + half * 16 + lane_off, pk);
       tmem_st_wait();
       tc_fence_before();
-      mbar_arrive(&t_full[tb]);
+      arrive_leader(&t_full[tb]);
       if (dbgt) DBG(9 * 64 + t);
     }
 
     // ---------------------------------------------------------------- epilogue
+    // Warp (q, half) owns rows q*32..q*32+31 and head-dim columns half*128..half*128+127: four
+    // 32-column chunks, the TMEM load of chunk cc+1 in flight while chunk cc is processed; each
+    // finished 64-column box (cc = 1, 3) is stored by the warp right away (TMA for a full 32-row
+    // chunk, row stores for the ragged last one), so the HBM writes overlap the rest.
     if (warp == 4 && lane == 0) DBG(10 * 64 + 0);
     mbar_wait(o_full, 0);
     if (warp == 4 && lane == 0) DBG(10 * 64 + 1);
     tc_fence_after();
-    const bool need_e = r0 + BR > us.ns;
     if (need_e) mbar_wait(e_full, 0);
     if (warp == 4 && lane == 0) DBG(10 * 64 + 5);
     if (a.has_u) mbar_wait(u_full, 0);
@@ -538,16 +562,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     const bool row_ok = my < us.L;
     const float dg = (row_ok && my >= us.ns) ? a.diag[g * a.H + h] : 0.f;  // static rows: none
     uint8_t* sE = smem + OFF_E;
-#pragma unroll 1
+    if (warp == 4 && lane == 0) DBG(10 * 64 + 11);
+    const int nrows = min(BR, us.L - r0);
+    const bool full_chunk = q * 32 + 32 <= nrows;
+    uint32_t r[2][32];
+    if (ntiles > 0) tmem_ld32(tmem + T_ACC + half * 128 + lane_off, r[0]);
+#pragma unroll
     for (int cc = 0; cc < 4; ++cc) {
       const int acol = half * 128 + cc * 32;  // head-dim column of this chunk
-      uint32_t r[32];
+      uint32_t (&rc)[32] = r[cc & 1];
       if (ntiles > 0) {
-        tmem_ld32(tmem + T_ACC + acol + lane_off, r);
         tmem_ld_wait();
+        if (cc < 3) tmem_ld32(tmem + T_ACC + acol + 32 + lane_off, r[(cc + 1) & 1]);
       } else {
 #pragma unroll
-        for (int i = 0; i < 32; ++i) r[i] = 0u;
+        for (int i = 0; i < 32; ++i) rc[i] = 0u;
       }
       const int bx = acol >> 6, j0 = (acol & 63) >> 3;
       uint8_t* ebox = sE + bx * (RT_BYTES / 4);
@@ -561,8 +590,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           const float2 f = __bfloat1622float2(hh[k]);
-          v[2 * k] = fmaf(us.nu, __uint_as_float(r[8 * i + 2 * k]), dg * f.x);
-          v[2 * k + 1] = fmaf(us.nu, __uint_as_float(r[8 * i + 2 * k + 1]), dg * f.y);
+          v[2 * k] = fmaf(us.nu, __uint_as_float(rc[8 * i + 2 * k]), dg * f.x);
+          v[2 * k + 1] = fmaf(us.nu, __uint_as_float(rc[8 * i + 2 * k + 1]), dg * f.y);
         }
         if (MODE == FWD) {
           const uint4 uw = *reinterpret_cast<const uint4*>(ubox + off);
@@ -582,49 +611,44 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
             const float2 f = __bfloat1622float2(ph[k]);
-            v[2 * k] *= dsilu_fast(f.x);
-            v[2 * k + 1] *= dsilu_fast(f.y);
+            v[2 * k] *= a.pre_dsilu ? f.x : dsilu_fast(f.x);
+            v[2 * k + 1] *= a.pre_dsilu ? f.y : dsilu_fast(f.y);
           }
         }
         *reinterpret_cast<uint4*>(ebox + off) =
             make_uint4(pack2(v[0], v[1]), pack2(v[2], v[3]), pack2(v[4], v[5]), pack2(v[6], v[7]));
       }
-    }
-    if (warp == 4 && lane == 0) DBG(10 * 64 + 7);
-    fence_proxy_async_smem();  // the TMA stores below read these smem tiles
-    named_bar_sync(1, 32 * NSM);
-    if (warp == 4 && lane == 0) DBG(10 * 64 + 8);
-    // stores: full 32-row chunks by TMA straight from the swizzled smem tiles (asynchronous, so
-    // the HBM writes drain after the CTA has moved on); a partial last chunk row by row (rows of
-    // the next user must not be touched).  Warps 0-3 store `out`, warps 4-7 `out2` (FWD).
-    const int sw = warp - 4;
-    const int nrows = min(BR, us.L - r0);
-    const int bx = lane >> 3, jj = lane & 7;
-    {
-      const int rc = sw & 3;
-      const bool second = sw >= 4;
-      if (MODE == FWD || !second) {
-        const CUtensorMap* tmo = second ? &tmO2 : &tmO;
-        if (rc * 32 + 32 <= nrows) {
+      if (warp == 4 && lane == 0) DBG(10 * 64 + 12 + cc);
+      if (cc & 1) {  // box bx of this warp's 32 rows is complete: store it
+        if (full_chunk) {
+          fence_proxy_async_smem();  // the bulk store reads what the generic proxy wrote
+          __syncwarp();
           if (lane == 0) {
-#pragma unroll
-            for (int b = 0; b < 4; ++b)
-              tma_store_2d(tmo, (second ? u_box(b) : sE + b * (RT_BYTES / 4)) + rc * 32 * 128, hcol + b * 64,
-                           row0 + rc * 32);
+            tma_store_2d(&tmO, ebox + q * 32 * 128, hcol + bx * 64, row0 + q * 32);
+            if (MODE == FWD) tma_store_2d(&tmO2, ubox + q * 32 * 128, hcol + bx * 64, row0 + q * 32);
             tma_store_commit();
           }
         } else {
-          __nv_bfloat16* dst = second ? a.out2 : a.out;
-          for (int rr = rc * 32; rr < nrows; ++rr) {
-            const uint8_t* src = (second ? u_box(bx) : sE + bx * (RT_BYTES / 4)) + sw128(rr, jj);
-            *reinterpret_cast<uint4*>(dst + (int64_t)(row0 + rr) * a.ld_out + hcol + lane * 8) =
-                *reinterpret_cast<const uint4*>(src);
+          __syncwarp();
+          // rows of the next user must not be touched: 4 rows x 8 16-byte pieces per pass
+          for (int rr = q * 32 + (lane >> 3); rr < nrows; rr += 4) {
+            const uint32_t off = sw128(rr, lane & 7);
+            const int64_t go = (int64_t)(row0 + rr) * a.ld_out + hcol + bx * 64 + (lane & 7) * 8;
+            *reinterpret_cast<uint4*>(a.out + go) = *reinterpret_cast<const uint4*>(ebox + off);
+            if (MODE == FWD) *reinterpret_cast<uint4*>(a.out2 + go) = *reinterpret_cast<const uint4*>(ubox + off);
           }
         }
       }
     }
-    float cs[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    if (warp == 4 && lane == 0) DBG(10 * 64 + 7);
     if (MODE != FWD && a.dbias != nullptr) {
+      // bias gradient of this projection block: column sums over the tile's rows (fused, so
+      // the layer never re-reads dp for it); [8 warps][256 columns] partials in free smem
+      named_bar_sync(1, 32 * NSM);  // every warp's output rows are in smem
+      if (warp == 4 && lane == 0) DBG(10 * 64 + 8);
+      const int sw = warp - 4;
+      const int bx = lane >> 3, jj = lane & 7;
+      float cs[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
       for (int rr = sw; rr < nrows; rr += NSM) {
         const uint4 w = *reinterpret_cast<const uint4*>(sE + bx * (RT_BYTES / 4) + sw128(rr, jj));
         const __nv_bfloat162* hh = reinterpret_cast<const __nv_bfloat162*>(&w);
@@ -635,11 +659,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
           cs[2 * k + 1] += f.y;
         }
       }
-    }
-    if (MODE != FWD && a.dbias != nullptr) {
-      // bias gradient of this projection block: column sums over the tile's rows (fused, so
-      // the layer never re-reads dp for it); [8 warps][256 columns] partials in free smem
-      float* red = reinterpret_cast<float*>(smem + 192 * KB);
+      float* red = reinterpret_cast<float*>(smem + OFF_C1);  // C1 ring is free by now
 #pragma unroll
       for (int e = 0; e < 8; ++e) red[sw * DH + lane * 8 + e] = cs[e];
       named_bar_sync(1, 32 * NSM);
@@ -657,12 +677,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
   cluster_sync();  // no CTA leaves while its peer may still signal its barriers
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc<512>(tmem);
+    tmem_dealloc_2sm<512>(tmem);
   }
 }
 
 struct Maps {
-  CUtensorMap c1, x, r1, r2, e, u, o, o2;
+  CUtensorMap c1, c2, x, r1, r2, e, u, o, o2;
 };
 
 template <int MODE>
@@ -672,8 +692,17 @@ static mtgr_status_t launch_mode(const AttnIO& io, const void* c1, int64_t ld_c1
                                  int64_t ld_u, const Args& args, cudaStream_t st) {
   const int T = io.jag.total_tokens, d = io.d;
   Maps m;
-  MTGR_TRY(make_tmap_bf16(&m.c1, c1, d, T, ld_c1, 64, BC));
-  MTGR_TRY(make_tmap_bf16(&m.x, x, d, T, ld_x, 64, BC));
+  constexpr bool TWO = (MODE == DQ || MODE == DK);
+  // column operands: each CTA of a pair loads half of every tile (32 columns of C1 / C2,
+  // 128 head-dim columns of X); for DQ / DK, X is the C1 tensor and `x` is C2
+  MTGR_TRY(make_tmap_bf16(&m.c1, c1, d, T, ld_c1, 64, BC / 2));
+  if (TWO) {
+    MTGR_TRY(make_tmap_bf16(&m.c2, x, d, T, ld_x, 64, BC / 2));
+    MTGR_TRY(make_tmap_bf16(&m.x, c1, d, T, ld_c1, 64, BC));
+  } else {
+    MTGR_TRY(make_tmap_bf16(&m.x, x, d, T, ld_x, 64, BC));
+    m.c2 = m.c1;
+  }
   MTGR_TRY(make_tmap_bf16(&m.r1, r1, d, T, ld_r1, 64, BR));
   if (r2) MTGR_TRY(make_tmap_bf16(&m.r2, r2, d, T, ld_r2, 64, BR)); else m.r2 = m.r1;
   MTGR_TRY(make_tmap_bf16(&m.e, e, d, T, ld_e, 64, BR));
@@ -682,22 +711,23 @@ static mtgr_status_t launch_mode(const AttnIO& io, const void* c1, int64_t ld_c1
   if (args.out2) MTGR_TRY(make_tmap_bf16(&m.o2, args.out2, d, T, args.ld_out, 64, 32)); else m.o2 = m.o;
   Args a2 = args;
   a2.has_u = uu != nullptr;
+  a2.pre_dsilu = io.pre_dsilu;
   dim3 grid(2 * ceil_div(io.jag.max_len, 2 * BR), io.H, io.jag.num_users);  // cluster pairs
   ProfScope ps(MODE == FWD ? PROF_ATTN_FWD : MODE == DV ? PROF_ATTN_DV : MODE == DK ? PROF_ATTN_DK : PROF_ATTN_DQ, st);
   cudaFuncSetAttribute(attn_tc_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
   static const bool trace = getenv("MTGR_ATTN_TRACE") != nullptr;
   if (trace) {  // debug only: time-stamp one CTA's pipeline events
-    cudaMalloc(&a2.dbg, 11 * 64 * sizeof(long long));
-    cudaMemsetAsync(a2.dbg, 0, 11 * 64 * sizeof(long long), st);
+    cudaMalloc(&a2.dbg, 2 * 11 * 64 * sizeof(long long));
+    cudaMemsetAsync(a2.dbg, 0, 2 * 11 * 64 * sizeof(long long), st);
   }
-  attn_tc_kernel<MODE><<<grid, 384, SMEM_BYTES, st>>>(m.c1, m.x, m.r1, m.r2, m.e, m.u, m.o, m.o2, a2);
+  attn_tc_kernel<MODE><<<grid, 384, SMEM_BYTES, st>>>(m.c1, m.c2, m.x, m.r1, m.r2, m.e, m.u, m.o, m.o2, a2);
   if (trace) {
-    long long hb[11 * 64];
+    long long hb[2 * 11 * 64];
     cudaMemcpyAsync(hb, a2.dbg, sizeof(hb), cudaMemcpyDeviceToHost, st);
     cudaStreamSynchronize(st);
     cudaFree(a2.dbg);
     fprintf(stderr, "ATTN_TRACE mode=%d", MODE);
-    for (int i = 0; i < 11 * 64; ++i) fprintf(stderr, " %lld", hb[i]);
+    for (int i = 0; i < 2 * 11 * 64; ++i) fprintf(stderr, " %lld", hb[i]);
     fprintf(stderr, "\n");
   }
   return check_launch("attn_tc");

@@ -53,6 +53,7 @@ struct Params {
   float* part;  // split-K partials [splits][M][N]
   int accumulate;
   int silu;
+  int c_dsilu;  // QKVU with silu: C = silu'(pre) instead of pre
 };
 
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
@@ -76,7 +77,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   using namespace sm100;
   using G = Geo<CG>;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-B aligned base, derived by indexing the shared array so the compiler keeps the shared
+  // address space (LDS/STS rather than generic LD/ST for every staged access)
+  uint8_t* smem = smem_raw + ((1024u - (sm100::smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem;
   uint8_t* sB = smem + G::STAGES * A_BYTES;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + G::OFF_BAR);
@@ -300,6 +303,25 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             }
           }
         }
+        if (EPI == EPI_QKVU && p.silu && p.c_dsilu) {
+          // C2 = silu(p), C = silu'(p) = sg + silu(p) (1 - sg): one tanh per element for both
+          uint8_t* srow2 = srow + 32 * 128;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            float a[8], ds[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              const float x = v[8 * j + k];
+              const float sg = fmaf(0.5f, sm100::tanh_approx(0.5f * x), 0.5f);
+              a[k] = x * sg;
+              ds[k] = fmaf(a[k], 1.0f - sg, sg);
+            }
+            *reinterpret_cast<uint4*>(srow + ((j ^ (lane & 7)) << 4)) =
+                make_uint4(pack_bf16(ds[0], ds[1]), pack_bf16(ds[2], ds[3]), pack_bf16(ds[4], ds[5]), pack_bf16(ds[6], ds[7]));
+            *reinterpret_cast<uint4*>(srow2 + ((j ^ (lane & 7)) << 4)) =
+                make_uint4(pack_bf16(a[0], a[1]), pack_bf16(a[2], a[3]), pack_bf16(a[4], a[5]), pack_bf16(a[6], a[7]));
+          }
+        } else {
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           const uint4 w = make_uint4(pack_bf16(v[8 * j], v[8 * j + 1]), pack_bf16(v[8 * j + 2], v[8 * j + 3]),
@@ -317,6 +339,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                                        pack_bf16(a[4], a[5]), pack_bf16(a[6], a[7]));
             *reinterpret_cast<uint4*>(srow2 + ((j ^ (lane & 7)) << 4)) = w;
           }
+        }
         }
         fence_proxy_async_smem();
         __syncwarp();
@@ -437,7 +460,7 @@ mtgr_status_t gemm_bf16_launch(const GemmIO& g, int epi, void* ws, size_t ws_byt
   p.num_splits = s.splits; p.kb_per_split = s.kb_per_split;
   p.a_mn = g.a_kmajor ? 0 : 1; p.b_mn = g.b_kmajor ? 0 : 1;
   p.C = g.C; p.ldc = g.ldc; p.bias = g.bias;
-  p.accumulate = g.accumulate; p.silu = g.silu;
+  p.accumulate = g.accumulate; p.silu = g.silu; p.c_dsilu = g.c_dsilu;
   if (epi == EPI_F32 && s.splits > 1) {
     MTGR_CHECK(ws && ws_bytes >= gemm_ws_bytes(g.M, g.N, g.K, epi, true), MTGR_E_WORKSPACE,
                "tc gemm: split-K workspace too small");
