@@ -1,9 +1,10 @@
-"""Parse MTGR_ATTN_TRACE=1 output: clock64 pipeline events of the CTA pair (2,0,0)/(3,0,0) of
-each attention launch.  usage: attn_trace.py <stderr log> [mode=N]"""
+"""Parse MTGR_ATTN_TRACE=1 output of the persistent attention kernel: per-item clock64 events of
+the CTA pair of cluster 1.  usage: attn_trace.py <stderr log> [mode=N]"""
 import sys
 
 import numpy as np
 
+EV = ["start", "tiles_done", "next_R1", "o_full", "epi_done", "S0_issued", "last_acc", "R1_load", "lastC1"]
 for line in open(sys.argv[1]):
     if not line.startswith("ATTN_TRACE"):
         continue
@@ -11,22 +12,16 @@ for line in open(sys.argv[1]):
     mode = parts[1]
     if len(sys.argv) > 2 and mode != sys.argv[2]:
         continue
-    v = np.array([int(x) for x in parts[2:]], dtype=np.int64).reshape(-1, 11, 64)
+    v = np.array([int(x) for x in parts[2:]], dtype=np.int64).reshape(-1, 16, 64)
     for c in range(v.shape[0]):
         w = v[c]
-        base = w[10, 10] if w[10, 10] else w[10, 4]
-
-        def rel(x):
-            return (x - base) if x else -1
-        print(mode, "cta", c, "start", rel(w[10, 4]), "r1_ready", rel(w[10, 3]), "mainloop_end", rel(w[10, 0]),
-              "o_full", rel(w[10, 1]), "e_ok", rel(w[10, 5]), "u_ok", rel(w[10, 6]), "computed", rel(w[10, 7]),
-              "barrier", rel(w[10, 8]), "stored", rel(w[10, 9]), "end", rel(w[10, 2]))
-        print("   epilogue: dg", rel(w[10, 11]), "chunks", [rel(w[10, 12 + i]) for i in range(4)])
-        n = int((w[6] > 0).sum())
-        print(" t | mma: kvwait_s kv_ok sfree_ok | acc: twait t_ok | smx: swait s_ok tfreewait tfree_ok tfull")
-        for t in range(min(n, 20)):
-            print("%2d | %7d %7d %7d | %7d %7d | %7d %7d %7d %7d %7d" % (
-                t, rel(w[0, t]), rel(w[1, t]), rel(w[2, t]), rel(w[3, t]), rel(w[4, t]),
-                rel(w[5, t]), rel(w[6, t]), rel(w[7, t]), rel(w[8, t]), rel(w[9, t])))
+        base = w[10, 0]
+        n = int((w[0] > 0).sum())
+        print(mode, "cta", c, "items", n, "end", int(w[4, n - 1] - base) if n else -1)
+        print(" i  nt | " + " ".join("%9s" % e for e in EV) + " | epilogue chunks (from o_full)")
+        for i in range(min(n, 32)):
+            row = [(int(w[e, i] - base) if w[e, i] else -1) for e in range(9)]
+            ch = [(int(w[11 + c, i] - w[3, i]) if w[11 + c, i] else -1) for c in range(4)]
+            print("%2d %3d | " % (i, w[9, i]) + " ".join("%9d" % x for x in row) + " | " + str(ch))
     if len(sys.argv) > 2:
         break
