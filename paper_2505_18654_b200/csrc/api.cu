@@ -78,7 +78,7 @@ static size_t esize(mtgr_dtype_t d) { return d == MTGR_BF16 ? 2 : 4; }
 
 // ------------------------------------------------------------------ saved-buffer layout
 struct SavedLayout {
-  size_t xt, p, a, o, y, yt, mu1, r1, mu2, r2, total;
+  size_t xt, p, a, o, yt, mu1, r1, mu2, r2, total;
 };
 static SavedLayout saved_layout(int d, int ntok, size_t es) {
   SavedLayout s;
@@ -89,7 +89,6 @@ static SavedLayout saved_layout(int d, int ntok, size_t es) {
   s.p = take(T * 4 * d * es);
   s.a = take(T * 4 * d * es);
   s.o = take(T * d * es);
-  s.y = take(T * d * es);
   s.yt = take(T * d * es);
   s.mu1 = take(T * 4);
   s.r1 = take(T * 4);
@@ -137,7 +136,7 @@ static mtgr_status_t run_attn_fwd(const AttnIO& a, float* diag, cudaStream_t st)
   MTGR_TRY(attn_diag_launch<T>(a, false, diag, nullptr, st));
   AttnIO b = a;
   b.diag_a = diag;
-  if (std::is_same<T, __nv_bfloat16>::value && a.nb == 0 && a.u && attn_tc_supported(a.dh))
+  if (std::is_same<T, __nv_bfloat16>::value && a.nb == 0 && attn_tc_supported(a.dh))
     return attn_tc_fwd_launch(b, st);
   return attn_simt_fwd_launch<T>(b, st);
 }
@@ -167,7 +166,7 @@ static mtgr_status_t layer_fwd_t(const mtgr_layer_cfg_t* c, const mtgr_jagged_t*
   size_t gws_bytes = cw.cap > cw.used ? cw.cap - align_up(cw.used, 256) : 0;
   void* gws = cw.take<char>(0);
   T* xt = (T*)(sv + L.xt); T* p = (T*)(sv + L.p); T* a = (T*)(sv + L.a);
-  T* o = (T*)(sv + L.o); T* y = (T*)(sv + L.y); T* yt = (T*)(sv + L.yt);
+  T* o = (T*)(sv + L.o); T* yt = (T*)(sv + L.yt);
   float* mu1 = (float*)(sv + L.mu1); float* r1 = (float*)(sv + L.r1);
   float* mu2 = (float*)(sv + L.mu2); float* r2 = (float*)(sv + L.r2);
   if (ntok == 0) return MTGR_OK;
@@ -181,14 +180,15 @@ static mtgr_status_t layer_fwd_t(const mtgr_layer_cfg_t* c, const mtgr_jagged_t*
   g.C = p; g.ldc = 4 * d; g.C2 = a; g.bias = P->b1; g.silu = c->qkvu_silu;
   g.c_dsilu = 1;  // the backward needs only silu'(p): saved in p's place
   MTGR_TRY(run_gemm<T>(g, EPI_QKVU, gws, gws_bytes, st));
-  // O = silu(Q K^T)/N (.) M V;  Y = O (.) U  (Eq.5, Eq.6 gate)
+  // O = silu(Q K^T)/N (.) M V  (Eq.5); the gate Y = O (.) U (Eq.6) is formed inside GLN2
   AttnIO at{};
   at.jag = *j; at.H = c->n_heads; at.dh = d / c->n_heads; at.d = d; at.nb = c->rab_buckets;
-  at.q = a; at.k = a + d; at.v = a + 2 * d; at.u = a + 3 * d; at.ld = 4 * d;
-  at.o = o; at.y = y; at.rab_w = P->rab_w;
+  at.q = a; at.k = a + d; at.v = a + 2 * d; at.ld = 4 * d;
+  at.o = o; at.u = nullptr; at.y = nullptr; at.rab_w = P->rab_w;  // gate folded into GLN2
   MTGR_TRY(run_attn_fwd<T>(at, diag, st));
-  // Y~ = GroupLN2(Y)  (Eq.6)
-  MTGR_TRY(gln_fwd_launch<T>(y, j->group_id, P->gamma2, P->beta2, yt, mu2, r2, ntok, d, c->eps, st));
+  // Y~ = GroupLN2(O (.) U)  (Eq.6)
+  MTGR_TRY(gln_fwd_launch<T>(o, j->group_id, P->gamma2, P->beta2, yt, mu2, r2, ntok, d, c->eps, st,
+                             a + 3 * d, 4 * d));
   // Z = Y~ W2^T + b2 + X  (Eq.6)
   GemmIO h{};
   h.M = ntok; h.N = d; h.K = d;
@@ -208,7 +208,7 @@ static mtgr_status_t layer_bwd_t(const mtgr_layer_cfg_t* c, const mtgr_jagged_t*
   SavedLayout L = saved_layout(d, ntok, sizeof(T));
   const T* xt = (const T*)(sv + L.xt); const T* p = (const T*)(sv + L.p);
   const T* a = (const T*)(sv + L.a); const T* o = (const T*)(sv + L.o);
-  const T* y = (const T*)(sv + L.y); const T* yt = (const T*)(sv + L.yt);
+  const T* yt = (const T*)(sv + L.yt);
   const float* mu1 = (const float*)(sv + L.mu1); const float* r1 = (const float*)(sv + L.r1);
   const float* mu2 = (const float*)(sv + L.mu2); const float* r2 = (const float*)(sv + L.r2);
   Carve cw(ws, wsb);
@@ -256,7 +256,8 @@ static mtgr_status_t layer_bwd_t(const mtgr_layer_cfg_t* c, const mtgr_jagged_t*
   MTGR_TRY(run_gemm<T>(h, EPI_STORE, scratch, scratch_bytes, st));
   // GLN2 backward fused with the gate: dO = dY (.) U, dp_U = dY (.) O (.) silu'(p_U)
   GlnBwdIO gi{};
-  gi.dy = buf; gi.x = y; gi.mean = mu2; gi.rstd = r2; gi.gamma = P->gamma2; gi.gid = j->group_id;
+  gi.dy = buf; gi.x = nullptr;  // norm input x = O (.) U, recomputed from o and u
+  gi.mean = mu2; gi.rstd = r2; gi.gamma = P->gamma2; gi.gid = j->group_id;
   gi.dx = dO; gi.ntok = ntok; gi.d = d; gi.G = c->num_groups;
   gi.o = o; gi.u = a + 3 * d; gi.pre_u = c->qkvu_silu ? p + 3 * d : nullptr; gi.pre_dsilu = 1; gi.ld_a = 4 * d;
   gi.dpu = dp + 3 * d; gi.ld_dp = 4 * d; gi.dcol = G->b1 + 3 * d;  // db1 of the U block

@@ -77,7 +77,8 @@ __global__ void __launch_bounds__(256) gln_fwd_kernel(const T* __restrict__ x,
                                                       const float* __restrict__ beta,
                                                       T* __restrict__ y, float* __restrict__ mean,
                                                       float* __restrict__ rstd, int ntok, int d,
-                                                      float eps) {
+                                                      float eps, const T* __restrict__ gate,
+                                                      int64_t ld_gate) {
   const int lane = threadIdx.x & 31;
   const int nwarps = gridDim.x * (blockDim.x >> 5);
   const int nch = d >> 3;
@@ -91,6 +92,12 @@ __global__ void __launch_bounds__(256) gln_fwd_kernel(const T* __restrict__ x,
       int c = lane + 32 * k;
       if (c < nch) {
         load8(xr + c * 8, v[k]);
+        if (gate != nullptr) {  // input = x (.) gate (Eq.6 gate folded into the norm's load)
+          float gv[8];
+          load8(gate + (int64_t)t * ld_gate + c * 8, gv);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) v[k][e] *= gv[e];
+        }
 #pragma unroll
         for (int e = 0; e < 8; ++e) s += v[k][e];
       }
@@ -205,7 +212,7 @@ __global__ void __launch_bounds__(32 * GLNB_WARPS, (NC <= 2 ? (MODE == GLN_GATE 
     for (int k = 0; k < NC; ++k) {
       const int c = lane + 32 * k;
       if (c < nch) {
-        rload(a.x + (int64_t)t * d + c * 8, xr[k]);
+        if (MODE != GLN_GATE || a.x != nullptr) rload(a.x + (int64_t)t * d + c * 8, xr[k]);
         rload(a.dy + (int64_t)t * d + c * 8, dyr[k]);
         if (MODE == GLN_RESID) rload(a.dz + (int64_t)t * d + c * 8, e1r[k]);
         if (MODE == GLN_GATE) {
@@ -220,13 +227,25 @@ __global__ void __launch_bounds__(32 * GLNB_WARPS, (NC <= 2 ? (MODE == GLN_GATE 
       cur_g = g;
     }
     const float* gr = a.gamma + (int64_t)g * d;
+    // gated norm input (x == NULL): x = o (.) u, recomputed exactly as the forward formed it
+    auto x_of = [&](int k, float* xv) {
+      if (MODE == GLN_GATE && a.x == nullptr) {
+        float uu[8], oo[8];
+        unpack(e1r[k], uu);
+        unpack(e2r[k], oo);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) xv[e] = oo[e] * uu[e];
+      } else {
+        unpack(xr[k], xv);
+      }
+    };
     float s1 = 0.f, s2 = 0.f;
 #pragma unroll
     for (int k = 0; k < NC; ++k) {
       const int c = lane + 32 * k;
       if (c < nch) {
         float xv[8], dyv[8], gg[8];
-        unpack(xr[k], xv);
+        x_of(k, xv);
         unpack(dyr[k], dyv);
         load8(gr + c * 8, gg);
 #pragma unroll
@@ -246,7 +265,7 @@ __global__ void __launch_bounds__(32 * GLNB_WARPS, (NC <= 2 ? (MODE == GLN_GATE 
       const int c = lane + 32 * k;
       if (c < nch) {
         float xv[8], dyv[8], gg[8], o[8];
-        unpack(xr[k], xv);
+        x_of(k, xv);
         unpack(dyr[k], dyv);
         load8(gr + c * 8, gg);
 #pragma unroll
@@ -333,22 +352,24 @@ size_t gln_bwd_ws_bytes(int ntok, int d, int G) {
 
 template <class T, int NC>
 static void gln_fwd_go(const T* x, const uint8_t* gid, const float* gamma, const float* beta, T* y,
-                       float* mean, float* rstd, int ntok, int d, float eps, cudaStream_t st) {
+                       float* mean, float* rstd, int ntok, int d, float eps, const T* gate,
+                       int64_t ld_gate, cudaStream_t st) {
   int blocks = min(ceil_div(ntok, 8), 16 * num_sms());
-  gln_fwd_kernel<T, NC><<<blocks, 256, 0, st>>>(x, gid, gamma, beta, y, mean, rstd, ntok, d, eps);
+  gln_fwd_kernel<T, NC><<<blocks, 256, 0, st>>>(x, gid, gamma, beta, y, mean, rstd, ntok, d, eps,
+                                                gate, ld_gate);
 }
 
 template <class T>
 mtgr_status_t gln_fwd_launch(const T* x, const uint8_t* gid, const float* gamma,
                              const float* beta, T* y, float* mean, float* rstd, int ntok, int d,
-                             float eps, cudaStream_t st) {
+                             float eps, cudaStream_t st, const T* gate, int64_t ld_gate) {
   if (ntok == 0) return MTGR_OK;
   ProfScope ps(PROF_GLN_FWD, st);
   switch (gln_nc(d)) {
-    case 1: gln_fwd_go<T, 1>(x, gid, gamma, beta, y, mean, rstd, ntok, d, eps, st); break;
-    case 2: gln_fwd_go<T, 2>(x, gid, gamma, beta, y, mean, rstd, ntok, d, eps, st); break;
-    case 3: gln_fwd_go<T, 3>(x, gid, gamma, beta, y, mean, rstd, ntok, d, eps, st); break;
-    default: gln_fwd_go<T, 4>(x, gid, gamma, beta, y, mean, rstd, ntok, d, eps, st); break;
+    case 1: gln_fwd_go<T, 1>(x, gid, gamma, beta, y, mean, rstd, ntok, d, eps, gate, ld_gate, st); break;
+    case 2: gln_fwd_go<T, 2>(x, gid, gamma, beta, y, mean, rstd, ntok, d, eps, gate, ld_gate, st); break;
+    case 3: gln_fwd_go<T, 3>(x, gid, gamma, beta, y, mean, rstd, ntok, d, eps, gate, ld_gate, st); break;
+    default: gln_fwd_go<T, 4>(x, gid, gamma, beta, y, mean, rstd, ntok, d, eps, gate, ld_gate, st); break;
   }
   return check_launch("gln_fwd");
 }
@@ -397,11 +418,11 @@ mtgr_status_t gln_bwd_launch(const GlnBwdIO& io, int mode, float* part, float* d
 
 template mtgr_status_t gln_fwd_launch<float>(const float*, const uint8_t*, const float*,
                                              const float*, float*, float*, float*, int, int,
-                                             float, cudaStream_t);
+                                             float, cudaStream_t, const float*, int64_t);
 template mtgr_status_t gln_fwd_launch<__nv_bfloat16>(const __nv_bfloat16*, const uint8_t*,
                                                      const float*, const float*, __nv_bfloat16*,
                                                      float*, float*, int, int, float,
-                                                     cudaStream_t);
+                                                     cudaStream_t, const __nv_bfloat16*, int64_t);
 template mtgr_status_t gln_bwd_launch<float>(const GlnBwdIO&, int, float*, float*, float*, int,
                                              cudaStream_t);
 template mtgr_status_t gln_bwd_launch<__nv_bfloat16>(const GlnBwdIO&, int, float*, float*,

@@ -22,7 +22,8 @@ size_t gln_bwd_ws_bytes(int ntok, int d, int G);
 template <class T>
 mtgr_status_t gln_fwd_launch(const T* x, const uint8_t* gid, const float* gamma,
                              const float* beta, T* y, float* mean, float* rstd, int ntok, int d,
-                             float eps, cudaStream_t st);
+                             float eps, cudaStream_t st, const T* gate = nullptr,
+                             int64_t ld_gate = 0);
 template <class T>
 mtgr_status_t gln_bwd_launch(const GlnBwdIO& io, int mode, float* part, float* dgamma,
                              float* dbeta, int accumulate, cudaStream_t st);
@@ -82,6 +83,8 @@ mtgr_status_t colsum_launch(const T* X, int64_t ld, int ntok, int n, float* out,
                             int accumulate, cudaStream_t st);
 size_t colsum_ws_bytes(int ntok, int n);
 mtgr_status_t scale_launch(float* g, int64_t n, float s, cudaStream_t st);
+mtgr_status_t gate_mul_launch(const void* o, int64_t ldo, const void* u, int64_t ldu, void* y,
+                              int64_t ldy, int ntok, int d, cudaStream_t st);
 mtgr_status_t mask_dense_launch(const mtgr_jagged_t& j, int user, uint8_t* out, cudaStream_t st);
 mtgr_status_t validate_launch(const mtgr_jagged_t& j, int G, cudaStream_t st);
 

@@ -98,6 +98,40 @@ mtgr_status_t scale_launch(float* g, int64_t n, float s, cudaStream_t st) {
   return check_launch("scale");
 }
 
+// ------------------------------------------------------------------ gate: y = o (.) u (bf16)
+// (Eq.6 gate for the public attention call; the layer folds it into the GLN2 load instead)
+__global__ void gate_mul_kernel(const __nv_bfloat16* o, int64_t ldo, const __nv_bfloat16* u,
+                                int64_t ldu, __nv_bfloat16* y, int64_t ldy, int ntok, int d) {
+  const int nv = d >> 3;
+  const int64_t n = (int64_t)ntok * nv;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = e / nv;
+    const int c = (int)(e % nv) * 8;
+    const uint4 ow = *reinterpret_cast<const uint4*>(o + t * ldo + c);
+    const uint4 uw = *reinterpret_cast<const uint4*>(u + t * ldu + c);
+    const __nv_bfloat162* oh = reinterpret_cast<const __nv_bfloat162*>(&ow);
+    const __nv_bfloat162* uh = reinterpret_cast<const __nv_bfloat162*>(&uw);
+    uint4 yw;
+    __nv_bfloat162* yh = reinterpret_cast<__nv_bfloat162*>(&yw);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float2 a = __bfloat1622float2(oh[k]), b = __bfloat1622float2(uh[k]);
+      yh[k] = __floats2bfloat162_rn(a.x * b.x, a.y * b.y);
+    }
+    *reinterpret_cast<uint4*>(y + t * ldy + c) = yw;
+  }
+}
+mtgr_status_t gate_mul_launch(const void* o, int64_t ldo, const void* u, int64_t ldu, void* y,
+                              int64_t ldy, int ntok, int d, cudaStream_t st) {
+  const int64_t n = (int64_t)ntok * (d >> 3);
+  if (n == 0) return MTGR_OK;
+  int64_t nb64 = ceil_div64(n, 256); int blocks = (int)(nb64 < 8 * num_sms() ? nb64 : 8 * num_sms());
+  gate_mul_kernel<<<blocks, 256, 0, st>>>((const __nv_bfloat16*)o, ldo, (const __nv_bfloat16*)u, ldu,
+                                          (__nv_bfloat16*)y, ldy, ntok, d);
+  return check_launch("gate_mul");
+}
+
 // ------------------------------------------------------------------ dense mask export
 // The exact composition the attention kernels use: the off-diagonal predicate on the key range
 // [0, n_static + n_rt) plus the diagonal of non-static rows (R#8-R#12).

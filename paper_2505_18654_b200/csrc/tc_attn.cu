@@ -59,7 +59,6 @@ struct Args {
   int pmax, nitems;                         // row pairs per user (max), work items B*pmax*H
   int* ctr;                                 // work-queue counter (zeroed before the launch)
   __nv_bfloat16* out; int64_t ld_out;
-  __nv_bfloat16* out2;                      // FWD y (ld_out)
   const __nv_bfloat16* e; int64_t ld_e;     // diagonal-term rows (E) of the epilogue
   const __nv_bfloat16* uu; int64_t ld_u;    // gate (FWD) / SiLU' source (bwd) rows, or NULL
   const float* diag;                        // [T][H]
@@ -128,7 +127,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tmC1, const __grid_constant__ CUtensorMap tmC2,
                    const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmR1,
                    const __grid_constant__ CUtensorMap tmR2, const __grid_constant__ CUtensorMap tmE,
-                   const __grid_constant__ CUtensorMap tmU, Args a) {
+                   const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUtensorMap tmO,
+                   Args a) {
   using namespace sm100;
   constexpr bool TWO = (MODE == DQ || MODE == DK);
   constexpr bool TRANS = (MODE == DV || MODE == DK);
@@ -143,10 +143,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
   // the next item while the epilogue (which reads E/U rows straight from L2 and writes the
   // outputs from registers) drains the accumulator.
   // smem (KB):     !TWO (FWD, DV)                        TWO (DQ, DK)
-  //   [0,48)      C1 ring: 3 x 16 (32 cols x 256 dh)    R1 (S A operand, SS)   [0,64)
-  //   [48,96)     X ring:  3 x 16 (64 cols x 128 dh)    R2 dh 128..255 [64,96) (staging of
-  //                                                     R2 dh 0..127 first)
-  //   [96,160)    R1 staging                            C1 ring 3 x 16 [96,144)
+  //   [0,32)      C1 ring: 2 x 16 (32 cols x 256 dh)    R1 (S A operand, SS) / epilogue tile
+  //   [32,80)     X ring:  3 x 16 (64 cols x 128 dh)      [0,64)
+  //   [80,144)    R1 staging                            R2 dh 128..255 [64,96) (staging of
+  //   [144,208)   epilogue tile                           R2 dh 0..127 first)
+  //                                                     C1 ring 3 x 16 [96,144)
   //                                                     C2 ring 2 x 16 [144,176)
   //                                                     X ring 2 x 16 [176,208)
   //   [208,212)   dbias scratch
@@ -154,14 +155,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
   //         TWO: acc [0,256), S [256,320), dP [320,384), P [384,448), R2 dh 0..127 [448,512)
   constexpr int C1_BYTES = 32 * DH * 2;        // 16 KB: 4 boxes {64 dh, 32 cols}
   constexpr int X_BYTES = BC * (DH / 2) * 2;   // 16 KB: 2 boxes {64 dh, 64 cols}
-  constexpr int NC1 = 3;
+  constexpr int NC1 = TWO ? 3 : 2;
   constexpr int NC2 = 2;
   constexpr int NX = TWO ? 2 : 3;
   constexpr int OFF_C1 = TWO ? 96 * KB : 0;
   constexpr int OFF_C2 = 144 * KB;
-  constexpr int OFF_X = TWO ? 176 * KB : 48 * KB;
+  constexpr int OFF_X = TWO ? 176 * KB : 32 * KB;
   constexpr int OFF_R1 = 0, OFF_R2B = 64 * KB;
-  constexpr int OFF_R1STAGE = 96 * KB;
+  constexpr int OFF_R1STAGE = 80 * KB;
+  // epilogue tile (4 SW128 boxes of 128 rows x 64 head-dim columns): the SiLU' source (bwd)
+  // arrives here by TMA and the outputs are formed in place and leave by TMA stores.  !TWO: a
+  // dedicated region; TWO: the R1 region, free once the item's score MMAs are done (the next
+  // item's R1 is loaded after the epilogue released it)
+  constexpr int OFF_EPI = TWO ? 0 : 144 * KB;
   constexpr uint32_t T_R1 = 0;
   constexpr uint32_t T_ACC = TWO ? 0 : 128;
   constexpr uint32_t T_S = TWO ? 256 : 384;
@@ -201,8 +207,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
   uint64_t* sc_done = bars + 31;
   uint64_t* q_full = bars + 32;       // [4] work queue: item index published (own)
   uint64_t* q_empty = bars + 36;      // [4] leader: every consumer of both CTAs has read it
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 40);
-  int* q_item = reinterpret_cast<int*>(bars + 41);  // [4]
+  uint64_t* eu_full = bars + 40;      // epilogue SiLU' source tile landed (own)
+  uint64_t* epi_free = bars + 41;     // epilogue tile free again (own; 8 softmax warps)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 42);
+  int* q_item = reinterpret_cast<int*>(bars + 43);  // [4]
   auto arrive_leader = [&](uint64_t* bar) {  // one arrival per warp (whole warp calls)
     __syncwarp();
     if ((threadIdx.x & 31) == 0) {
@@ -233,9 +241,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     mbar_init(r1s_full, 1);
     mbar_init(o_full, 1);
     mbar_init(sc_done, 1);
+    mbar_init(eu_full, 1);
+    mbar_init(epi_free, NSM);
     for (int s = 0; s < 4; ++s) {
       mbar_init(&q_full[s], 1);
-      mbar_init(&q_empty[s], 2 * (NSM + 2 + (TWO ? 1 : 0)));
+      mbar_init(&q_empty[s], 2 * (NSM + 3));  // per CTA: B, C / epilogue loader, 8 softmax, MMA | A
     }
     fence_barrier_init();
   }
@@ -291,30 +301,41 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
         Item it;
         decode_item<TRANS>(a, k, crank, it);
         const int row0 = it.us.off + it.r0;
+        auto load_u = [&]() {  // SiLU' source tile of the epilogue (bwd modes)
+          if (a.uu != nullptr) {
+            mbar_expect_tx(eu_full, RT_BYTES);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) tma_load_2d(smem + OFF_EPI + c * (RT_BYTES / 4), &tmU, eu_full, it.hcol + c * 64, row0);
+          }
+        };
+        auto wait_epi = [&]() { if (idx > 0) mbar_wait(epi_free, (idx - 1) & 1); };
         if (it.ntiles > 0) {
           if (!TWO) {
             if (mi > 0) mbar_wait(r1_copied, (mi - 1) & 1);  // staging free again
             mbar_expect_tx(r1_full, RT_BYTES);
 #pragma unroll
             for (int c = 0; c < 4; ++c) tma_load_2d(smem + OFF_R1STAGE + c * (RT_BYTES / 4), &tmR1, r1_full, it.hcol + c * 64, row0);
-          } else {
-            if (mi > 0) mbar_wait(sc_done, (mi - 1) & 1);  // previous item's S / dP MMAs done
+            DBG(7, idx);
+          }
+          // TWO: the row operands go into the region the previous epilogue used; the first
+          // column tiles are prefetched before waiting for it
+          auto head = [&]() {
+            wait_epi();
             if (leader) mbar_expect_tx(r1s_full, 2 * RT_BYTES);
 #pragma unroll
             for (int c = 0; c < 4; ++c) tma_load_2d_2sm(smem + OFF_R1 + c * (RT_BYTES / 4), &tmR1, r1s_full, it.hcol + c * 64, row0);
             mbar_expect_tx(r2a_full, RT_BYTES / 2);  // R2 head-dim 0..127 -> staging (then TMEM)
 #pragma unroll
             for (int c = 0; c < 2; ++c) tma_load_2d(smem + OFF_R2B + c * (RT_BYTES / 4), &tmR2, r2a_full, it.hcol + c * 64, row0);
-          }
-          DBG(7, idx);
-          auto load_r2b = [&]() {
+            DBG(7, idx);
             mbar_wait(r2a_copied, mi & 1);
             if (leader) mbar_expect_tx(r2_full, RT_BYTES);
 #pragma unroll
             for (int c = 2; c < 4; ++c) tma_load_2d_2sm(smem + OFF_R2B + (c - 2) * (RT_BYTES / 4), &tmR2, r2_full, it.hcol + c * 64, row0);
           };
+          const int npre = min(NC1, it.ntiles);
           for (int t = 0; t < it.ntiles; ++t, ++gt) {
-            if (TWO && t == NC1) load_r2b();
+            if (TWO && t == npre) head();
             const int slot = gt % NC1;
             mbar_wait(&c1_empty[slot], ((gt / NC1) & 1) ^ 1);
             if (leader) mbar_expect_tx(&c1_full[slot], 2 * C1_BYTES);
@@ -323,18 +344,35 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
 #pragma unroll
             for (int c = 0; c < 4; ++c) tma_load_2d_2sm(dst + c * (C1_BYTES / 4), &tmC1, &c1_full[slot], it.hcol + c * 64, row);
           }
-          if (TWO && it.ntiles <= NC1) load_r2b();
+          if (TWO && npre == it.ntiles) head();
           DBG(8, idx);
+          if (TWO) {  // the R1 region becomes the epilogue tile once the score MMAs are done
+            mbar_wait(sc_done, mi & 1);
+            load_u();
+          }
           ++mi;
+        } else if (TWO) {
+          wait_epi();
+          load_u();
         }
-        // the epilogue reads its E / U rows through L2: warm them while the item's last tiles run
-        if (it.need_e) {
+        ++idx;
+      }
+    }
+  } else if (!TWO && warp == 2) {
+    // ---------------------------------------------------------------- !TWO: epilogue tile loader
+    if (lane == 0) {
+      int idx = 0;
+      for (int n = 0;; ++n) {
+        const int k = q_read(n);
+        q_release(n);
+        if (k < 0) break;
+        Item it;
+        decode_item<TRANS>(a, k, crank, it);
+        if (a.uu != nullptr) {
+          if (idx > 0) mbar_wait(epi_free, (idx - 1) & 1);
+          mbar_expect_tx(eu_full, RT_BYTES);
 #pragma unroll
-          for (int c = 0; c < 4; ++c) tma_prefetch_l2_2d(&tmE, it.hcol + c * 64, row0);
-        }
-        if (a.uu != nullptr && it.r0 < it.us.L) {
-#pragma unroll
-          for (int c = 0; c < 4; ++c) tma_prefetch_l2_2d(&tmU, it.hcol + c * 64, row0);
+          for (int c = 0; c < 4; ++c) tma_load_2d(smem + OFF_EPI + c * (RT_BYTES / 4), &tmU, eu_full, it.hcol + c * 64, it.us.off + it.r0);
         }
         ++idx;
       }
@@ -597,9 +635,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
           arrive_leader(&t_full[tb]);
         }
         if (dbgw) DBG(1, idx);
-        // every S / dP MMA of this item has completed: hand the next item's row operand to the
-        // tensor pipe before draining this item's accumulator
-        {
+        // !TWO: every S MMA of this item has completed: hand the next item's row operand (already
+        // in the staging area) to the tensor pipe before draining this item's accumulator.
+        // (TWO: the next item's rows are loaded only after this epilogue frees the region.)
+        if (!TWO) {
           const int k2 = q_read(n + 1);  // peek (released when it is processed)
           Item nx;
           if (k2 >= 0 && decode_item<TRANS>(a, k2, crank, nx) && nx.ntiles > 0) copy_rows();
@@ -612,85 +651,88 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       if (dbgw) DBG(3, idx);
 
       // ---------------------------------------------------------------- epilogue
-      // Warp (q, half): rows q*32.., head-dim columns half*128.. in four 32-column chunks.
-      // E / U rows come straight from L2 (prefetched by the producer), one chunk ahead.
+      // Warp (q, half): rows q*32.., head-dim columns half*128.. in four 32-column chunks, the
+      // TMEM load of chunk cc+1 in flight while chunk cc is processed.  The SiLU' source (bwd)
+      // is in the epilogue tile (TMA); the outputs are formed in place and each finished
+      // 64-column box of the warp's 32 rows leaves by a TMA store (row stores for a ragged last
+      // chunk).  Candidate rows add their diagonal term from E (global; R#9).
       const bool row_ok = my < us.L;
       // the diagonal of real-time rows is inside the iterated key range (added in the loop);
       // candidate rows' own column lies outside it: their diagonal term is added here
       const bool has_e = row_ok && my >= it.kv_end;
-      const bool has_u = row_ok && a.uu != nullptr;
-      if (dbgw) DBGV(15, 32 + idx, has_e ? 1 : 0);
       const float dg = has_e ? a.diag[g * a.H + it.h] : 0.f;
-      const int col0 = it.hcol + half * 128;
-      const __nv_bfloat16* erow = a.e + g * a.ld_e + col0;
-      const __nv_bfloat16* urow = a.uu + g * a.ld_u + col0;
-      uint4 eb[2][4], ub[2][4];  // [buffer][16-byte piece of the 32-column chunk]
-      auto load_chunk = [&](int cc, int b) {
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          eb[b][i] = has_e ? __ldg(reinterpret_cast<const uint4*>(erow + cc * 32 + 8 * i)) : make_uint4(0u, 0u, 0u, 0u);
-          ub[b][i] = has_u ? __ldg(reinterpret_cast<const uint4*>(urow + cc * 32 + 8 * i)) : make_uint4(0u, 0u, 0u, 0u);
-        }
-      };
-      // (the accumulator reads below are ordered before the next item's first accumulate MMA by
-      // the tcgen05 fence + t_full arrival of that item's first softmax tile)
-      load_chunk(0, 0);
+      const __nv_bfloat16* erow = a.e + g * a.ld_e + it.hcol + half * 128;
+      const int nrows = min(BR, us.L - it.r0);
+      const bool full_chunk = q * 32 + 32 <= nrows;
+      const int row0 = us.off + it.r0;
+      uint8_t* epi = smem + OFF_EPI;
+      if (a.uu != nullptr) mbar_wait(eu_full, idx & 1);
       const bool do_bias = MODE != FWD && a.dbias != nullptr;
+      uint32_t r[2][32];
+      if (it.ntiles > 0) tmem_ld32(tmem + T_ACC + half * 128 + lane_off, r[0]);
 #pragma unroll
       for (int cc = 0; cc < 4; ++cc) {
-        uint32_t r[32];
-        if (it.ntiles > 0) {
-          tmem_ld32(tmem + T_ACC + half * 128 + cc * 32 + lane_off, r);
-        }
-        if (cc < 3) load_chunk(cc + 1, (cc + 1) & 1);
+        const int acol = half * 128 + cc * 32;  // head-dim column of this chunk
+        uint32_t (&rc)[32] = r[cc & 1];
         if (it.ntiles > 0) {
           tmem_ld_wait();
+          if (cc < 3) tmem_ld32(tmem + T_ACC + acol + 32 + lane_off, r[(cc + 1) & 1]);
         } else {
 #pragma unroll
-          for (int i = 0; i < 32; ++i) r[i] = 0u;
+          for (int i = 0; i < 32; ++i) rc[i] = 0u;
         }
-        uint4 ov[4];
+        const int bx = acol >> 6, j0 = (acol & 63) >> 3;
+        uint8_t* box = epi + bx * (RT_BYTES / 4);
+        float v[32];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-          const __nv_bfloat162* eh = reinterpret_cast<const __nv_bfloat162*>(&eb[cc & 1][i]);
-          const __nv_bfloat162* uh = reinterpret_cast<const __nv_bfloat162*>(&ub[cc & 1][i]);
-          uint32_t* o32 = reinterpret_cast<uint32_t*>(&ov[i]);
-          uint32_t* u32 = reinterpret_cast<uint32_t*>(&ub[cc & 1][i]);
+          const uint32_t off = sw128(row, j0 + i);
+          uint4 ew = make_uint4(0u, 0u, 0u, 0u);
+          if (has_e) ew = __ldg(reinterpret_cast<const uint4*>(erow + cc * 32 + 8 * i));
+          uint4 uw = make_uint4(0u, 0u, 0u, 0u);
+          if (a.uu != nullptr) uw = *reinterpret_cast<const uint4*>(box + off);
+          const __nv_bfloat162* eh = reinterpret_cast<const __nv_bfloat162*>(&ew);
+          const __nv_bfloat162* uh = reinterpret_cast<const __nv_bfloat162*>(&uw);
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk) {
             const float2 fe = __bfloat1622float2(eh[kk]);
-            const float2 fu = __bfloat1622float2(uh[kk]);
-            float x0 = fmaf(us.nu, __uint_as_float(r[8 * i + 2 * kk]), dg * fe.x);
-            float x1 = fmaf(us.nu, __uint_as_float(r[8 * i + 2 * kk + 1]), dg * fe.y);
-            if (MODE != FWD && a.uu != nullptr) {
+            float x0 = fmaf(us.nu, __uint_as_float(rc[8 * i + 2 * kk]), dg * fe.x);
+            float x1 = fmaf(us.nu, __uint_as_float(rc[8 * i + 2 * kk + 1]), dg * fe.y);
+            if (a.uu != nullptr) {
+              const float2 fu = __bfloat1622float2(uh[kk]);
               x0 *= a.pre_dsilu ? fu.x : dsilu_fast(fu.x);
               x1 *= a.pre_dsilu ? fu.y : dsilu_fast(fu.y);
             }
-            o32[kk] = pack2(x0, x1);
-            if (MODE == FWD) u32[kk] = pack2(x0 * fu.x, x1 * fu.y);  // y = o * u
+            v[8 * i + 2 * kk] = x0;
+            v[8 * i + 2 * kk + 1] = x1;
           }
+          *reinterpret_cast<uint4*>(box + off) =
+              make_uint4(pack2(v[8 * i], v[8 * i + 1]), pack2(v[8 * i + 2], v[8 * i + 3]),
+                         pack2(v[8 * i + 4], v[8 * i + 5]), pack2(v[8 * i + 6], v[8 * i + 7]));
         }
-        if (row_ok) {  // 256-bit (full-sector) row stores
-          __nv_bfloat16* dst = a.out + g * a.ld_out + col0 + cc * 32;
-          stg256(dst, *reinterpret_cast<const U8*>(&ov[0]));
-          stg256(dst + 16, *reinterpret_cast<const U8*>(&ov[2]));
-          if (MODE == FWD) {
-            __nv_bfloat16* dst2 = a.out2 + g * a.ld_out + col0 + cc * 32;
-            stg256(dst2, *reinterpret_cast<const U8*>(&ub[cc & 1][0]));
-            stg256(dst2 + 16, *reinterpret_cast<const U8*>(&ub[cc & 1][2]));
+        if (cc & 1) {  // box bx of this warp's 32 rows is complete: store it
+          if (full_chunk) {
+            fence_proxy_async_smem();  // the bulk store reads what the generic proxy wrote
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_2d(&tmO, box + q * 32 * 128, it.hcol + bx * 64, row0 + q * 32);
+              tma_store_commit();
+            }
+          } else {
+            __syncwarp();
+            // rows of the next user must not be touched: 4 rows x 8 16-byte pieces per pass
+            for (int rr = q * 32 + (lane >> 3); rr < nrows; rr += 4) {
+              const int64_t go = (int64_t)(row0 + rr) * a.ld_out + it.hcol + bx * 64 + (lane & 7) * 8;
+              *reinterpret_cast<uint4*>(a.out + go) = *reinterpret_cast<const uint4*>(box + sw128(rr, lane & 7));
+            }
           }
         }
         if (dbgw) DBG(11 + cc, idx);
         if (do_bias) {
-          // column sums (of the stored bf16 values) over this warp's 32 rows: transpose-reduce
-          // through shuffles; lane c ends with column c of the chunk (rows outside the user: 0)
-          float v[32];
+          // column sums over this warp's 32 rows: transpose-reduce through shuffles; lane c ends
+          // with column c of the chunk (rows outside the user contribute 0)
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const float2 f = __bfloat1622float2(reinterpret_cast<const __nv_bfloat162*>(ov)[i]);
-            v[2 * i] = row_ok ? f.x : 0.f;
-            v[2 * i + 1] = row_ok ? f.y : 0.f;
-          }
+          for (int i = 0; i < 32; ++i) v[i] = row_ok ? v[i] : 0.f;
 #pragma unroll
           for (int off = 16; off >= 1; off >>= 1) {
             const bool upper = (lane & off) != 0;
@@ -701,7 +743,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
               v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
             }
           }
-          red[q * DH + half * 128 + cc * 32 + lane] = v[0];
+          red[q * DH + acol + lane] = v[0];
         }
       }
       if (do_bias) {
@@ -711,6 +753,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
         if (sum != 0.f) atomicAdd(a.dbias + it.hcol + col, sum);
         named_bar_sync(1, 32 * NSM);  // scratch reusable
       }
+      // the epilogue tile may be refilled once this warp's bulk stores have read it
+      if (lane == 0) tma_store_wait_read<0>();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(epi_free);
       if (dbgw) DBG(4, idx);
       if (dbgw) DBG(15, idx);
       ++idx;
@@ -736,7 +782,7 @@ static int num_sms_cached() {
 }
 
 struct Maps {
-  CUtensorMap c1, c2, x, r1, r2, e, u;
+  CUtensorMap c1, c2, x, r1, r2, e, u, o;
 };
 
 template <int MODE>
@@ -761,6 +807,7 @@ static mtgr_status_t launch_mode(const AttnIO& io, const void* c1, int64_t ld_c1
   if (r2) MTGR_TRY(make_tmap_bf16(&m.r2, r2, d, T, ld_r2, 64, BR)); else m.r2 = m.r1;
   MTGR_TRY(make_tmap_bf16(&m.e, e, d, T, ld_e, 64, BR));
   if (uu) MTGR_TRY(make_tmap_bf16(&m.u, uu, d, T, ld_u, 64, BR)); else m.u = m.e;
+  MTGR_TRY(make_tmap_bf16(&m.o, args.out, d, T, args.ld_out, 64, 32));
   Args a2 = args;
   a2.e = (const __nv_bfloat16*)e; a2.ld_e = ld_e;
   a2.uu = (const __nv_bfloat16*)uu; a2.ld_u = ld_u;
@@ -782,7 +829,7 @@ static mtgr_status_t launch_mode(const AttnIO& io, const void* c1, int64_t ld_c1
     cudaMalloc(&a2.dbg, 2 * 16 * 64 * sizeof(long long));
     cudaMemsetAsync(a2.dbg, 0, 2 * 16 * 64 * sizeof(long long), st);
   }
-  attn_tc_kernel<MODE><<<grid, 384, SMEM_BYTES, st>>>(m.c1, m.c2, m.x, m.r1, m.r2, m.e, m.u, a2);
+  attn_tc_kernel<MODE><<<grid, 384, SMEM_BYTES, st>>>(m.c1, m.c2, m.x, m.r1, m.r2, m.e, m.u, m.o, a2);
   if (trace) {
     long long hb[2 * 16 * 64];
     cudaMemcpyAsync(hb, a2.dbg, sizeof(hb), cudaMemcpyDeviceToHost, st);
@@ -802,15 +849,17 @@ bool attn_tc_supported(int dh) { return dh == tca::DH; }
 mtgr_status_t attn_tc_fwd_launch(const AttnIO& io, cudaStream_t st) {
   using namespace tca;
   if (io.jag.num_users == 0 || io.jag.max_len == 0 || io.jag.total_tokens == 0) return MTGR_OK;
-  MTGR_CHECK(io.u && io.y, MTGR_E_UNSUPPORTED, "tc attention forward needs the gate (u, y)");
+  MTGR_CHECK(!io.u || io.y, MTGR_E_ARG, "attention forward: gate without y output");
   MTGR_CHECK(io.d % 8 == 0, MTGR_E_LAYOUT, "d_model must be a multiple of 8");
   Args a{};
   a.jag = io.jag; a.H = io.H; a.d = io.d;
-  a.out = (__nv_bfloat16*)io.o; a.out2 = (__nv_bfloat16*)io.y; a.ld_out = io.d;
+  a.out = (__nv_bfloat16*)io.o; a.ld_out = io.d;
   a.diag = io.diag_a;
-  // C1 = K, X = V, R1 = Q, E = V, U = U
-  return launch_mode<FWD>(io, io.k, io.ld, io.v, io.ld, io.q, io.ld, nullptr, 0, io.v, io.ld, io.u,
-                          io.ld, a, st);
+  // C1 = K, X = V, R1 = Q, E = V; the gate (if any) is a separate elementwise pass
+  MTGR_TRY(launch_mode<FWD>(io, io.k, io.ld, io.v, io.ld, io.q, io.ld, nullptr, 0, io.v, io.ld,
+                            nullptr, 0, a, st));
+  if (io.u) MTGR_TRY(gate_mul_launch(io.o, io.d, io.u, io.ld, io.y, io.d, io.jag.total_tokens, io.d, st));
+  return MTGR_OK;
 }
 
 mtgr_status_t attn_tc_bwd_launch(const AttnIO& io, cudaStream_t st) {
