@@ -133,22 +133,24 @@ static mtgr_status_t run_gemm(const GemmIO& g, int epi, void* ws, size_t wsb, cu
 
 template <class T>
 static mtgr_status_t run_attn_fwd(const AttnIO& a, float* diag, cudaStream_t st) {
-  MTGR_TRY(attn_diag_launch<T>(a, false, diag, nullptr, st));
+  const bool tc = std::is_same<T, __nv_bfloat16>::value && a.nb == 0 && attn_tc_supported(a.dh);
   AttnIO b = a;
+  b.diag_cand_only = tc;  // the tensor-core path adds real-time diagonals inside its tile loop
+  MTGR_TRY(attn_diag_launch<T>(b, false, diag, nullptr, st));
   b.diag_a = diag;
-  if (std::is_same<T, __nv_bfloat16>::value && a.nb == 0 && attn_tc_supported(a.dh))
-    return attn_tc_fwd_launch(b, st);
+  if (tc) return attn_tc_fwd_launch(b, st);
   return attn_simt_fwd_launch<T>(b, st);
 }
 
 template <class T>
 static mtgr_status_t run_attn_bwd(const AttnIO& a, float* diag_a, float* diag_ds, cudaStream_t st) {
-  MTGR_TRY(attn_diag_launch<T>(a, true, diag_a, diag_ds, st));
+  const bool tc = std::is_same<T, __nv_bfloat16>::value && a.nb == 0 && attn_tc_supported(a.dh);
   AttnIO b = a;
+  b.diag_cand_only = tc;
+  MTGR_TRY(attn_diag_launch<T>(b, true, diag_a, diag_ds, st));
   b.diag_a = diag_a;
   b.diag_ds = diag_ds;
-  if (std::is_same<T, __nv_bfloat16>::value && a.nb == 0 && attn_tc_supported(a.dh))
-    return attn_tc_bwd_launch(b, st);
+  if (tc) return attn_tc_bwd_launch(b, st);
   return attn_simt_bwd_launch<T>(b, st);
 }
 

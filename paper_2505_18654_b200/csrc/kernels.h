@@ -62,6 +62,7 @@ struct AttnIO {
   const float* diag_a;         // [T][H]  nu*silu(s_ii) for non-static tokens, 0 otherwise
   const float* diag_ds;        // [T][H]  nu*silu'(s_ii)*(dO_i . v_i)
   const float* rab_w; float* drab;
+  int diag_cand_only;          // diagonal scalars only for candidate rows (>= ns + nr)
   float* dbias;                // optional: column sums of the (bwd) outputs, red.add into
                                // dbias[col] for the Q|K|V blocks (tensor-core path only)
 };

@@ -132,7 +132,8 @@ __global__ void __launch_bounds__(256) attn_diag_kernel(AttnIO a, int bwd, float
   const T* q = (const T*)a.q; const T* k = (const T*)a.k; const T* v = (const T*)a.v;
   const T* dO = (const T*)a.dO;
   const int nch = a.dh >> 3;
-  for (int li = us.ns + (threadIdx.x >> 5); li < us.L; li += blockDim.x >> 5) {
+  const int first = a.diag_cand_only ? us.ns + us.nr : us.ns;
+  for (int li = first + (threadIdx.x >> 5); li < us.L; li += blockDim.x >> 5) {
     const int64_t t = us.off + li;
     for (int h = 0; h < a.H; ++h) {
       float s = 0.f, pv = 0.f;

@@ -45,8 +45,8 @@ constexpr int BR = 128;                 // rows per CTA
 constexpr int BC = 64;                  // columns per iterated tile
 constexpr int KB = 1024;
 constexpr int RT_BYTES = BR * DH * 2;   // 64 KB: 4 boxes {64 dh, 128 rows}
-constexpr int OFF_RED = 208 * KB;        // dbias scratch: [4 quadrants][256 columns] fp32
-constexpr int OFF_TS = OFF_RED + 4 * DH * 4;
+constexpr int OFF_RED = 208 * KB;        // dbias scratch: [8 warps][256 columns] fp32
+constexpr int OFF_TS = OFF_RED + 8 * DH * 4;
 constexpr int OFF_BAR = OFF_TS + BC * 8;
 constexpr int SMEM_BYTES = OFF_BAR + 512 + 1024;
 constexpr int NSM = 8;  // softmax/epilogue warps
@@ -728,28 +728,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
           }
         }
         if (dbgw) DBG(11 + cc, idx);
-        if (do_bias) {
-          // column sums over this warp's 32 rows: transpose-reduce through shuffles; lane c ends
-          // with column c of the chunk (rows outside the user contribute 0)
-#pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] = row_ok ? v[i] : 0.f;
-#pragma unroll
-          for (int off = 16; off >= 1; off >>= 1) {
-            const bool upper = (lane & off) != 0;
-#pragma unroll
-            for (int i = 0; i < off; ++i) {
-              const float send = upper ? v[i] : v[i + off];
-              const float keep = upper ? v[i + off] : v[i];
-              v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
-            }
-          }
-          red[q * DH + acol + lane] = v[0];
-        }
       }
       if (do_bias) {
+        // bias gradient of this projection block: column sums of the tile's (stored) outputs,
+        // read back from the epilogue tile: warp sw sums rows sw, sw+8, ..., lane = 8 columns
+        named_bar_sync(1, 32 * NSM);  // every warp's outputs are in the tile
+        const int sw = warp - 4, bx = lane >> 3, jj = lane & 7;
+        float cs[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        const uint8_t* cbox = epi + bx * (RT_BYTES / 4);
+        for (int rr = sw; rr < nrows; rr += NSM) {
+          const uint4 w = *reinterpret_cast<const uint4*>(cbox + sw128(rr, jj));
+          const __nv_bfloat162* hh = reinterpret_cast<const __nv_bfloat162*>(&w);
+#pragma unroll
+          for (int k2 = 0; k2 < 4; ++k2) {
+            const float2 f = __bfloat1622float2(hh[k2]);
+            cs[2 * k2] += f.x;
+            cs[2 * k2 + 1] += f.y;
+          }
+        }
+        float* redw = red;  // [8 warps][256 columns]: the scratch plus the TS area after it
+#pragma unroll
+        for (int e = 0; e < 8; ++e) redw[sw * DH + lane * 8 + e] = cs[e];
         named_bar_sync(1, 32 * NSM);
         const int col = threadIdx.x - 128;
-        const float sum = red[col] + red[DH + col] + red[2 * DH + col] + red[3 * DH + col];
+        float sum = 0.f;
+#pragma unroll
+        for (int w2 = 0; w2 < NSM; ++w2) sum += redw[w2 * DH + col];
         if (sum != 0.f) atomicAdd(a.dbias + it.hcol + col, sum);
         named_bar_sync(1, 32 * NSM);  // scratch reusable
       }
