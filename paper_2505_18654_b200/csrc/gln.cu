@@ -12,6 +12,7 @@
 #include "common.cuh"
 #include "kernels.h"
 #include "prof.h"
+#include "sm100.cuh"
 
 namespace mtgr {
 
@@ -321,6 +322,194 @@ __global__ void __launch_bounds__(32 * GLNB_WARPS, (NC <= 2 ? (MODE == GLN_GATE 
   }
 }
 
+// ---- bf16 backward, bulk-copy pipelined.  The same arithmetic as gln_bwd_kernel, but a
+// token's input rows (dy, x | o, u, pre | dz: 1-D contiguous rows) are streamed into a per-warp
+// shared-memory ring by cp.async.bulk, S tokens ahead, so the bytes in flight per SM no longer
+// depend on registers (the register version keeps ~12 warps x 4 KB in flight, ~45% of HBM
+// bandwidth).  One warp per token, a contiguous token range per warp, 16-byte lanes.
+struct GlnRing {
+  int S;          // stages per warp
+  int nrows;      // input rows per token
+  int r_x, r_dz, r_o, r_u, r_pre;  // row slot of each input (-1 absent); dy is slot 0
+  uint32_t stage_bytes;
+  uint32_t ring_off;  // byte offset of the first warp's ring in dynamic smem
+};
+
+template <int MODE, int NC>
+__global__ void __launch_bounds__(512, 1) gln_bwd_bulk_kernel(GlnBwdArgs<__nv_bfloat16> a, GlnRing R) {
+  using namespace sm100;
+  typedef __nv_bfloat16 bf;
+  extern __shared__ __align__(128) uint8_t gsm[];
+  float* sacc = reinterpret_cast<float*>(gsm);  // [G][2][d] (+ [d] column sums)
+  const int d = a.d, G = a.G;
+  const int nwarps = blockDim.x >> 5;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint8_t* ring = gsm + R.ring_off + (size_t)warp * R.S * R.stage_bytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(gsm + R.ring_off + (size_t)nwarps * R.S * R.stage_bytes) + warp * R.S;
+  const bool csum = MODE != GLN_PLAIN && a.dcol != nullptr;
+  for (int i = threadIdx.x; i < G * 2 * d + d; i += blockDim.x) sacc[i] = 0.f;
+  float* sgam = sacc + G * 2 * d + d;  // gamma [G][d], staged once per block
+  for (int i = threadIdx.x; i < G * d; i += blockDim.x) sgam[i] = a.gamma[i];
+  if (lane == 0) {
+    for (int s = 0; s < R.S; ++s) mbar_init(&bars[s], 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  const int nch = d >> 3;
+  const float inv_d = 1.0f / (float)d;
+  const int w_begin = (blockIdx.x * nwarps + warp) * a.tok_per_warp;
+  const int w_end = min(a.ntok, w_begin + a.tok_per_warp);
+  const uint32_t row_bytes = (uint32_t)d * 2;
+  auto issue = [&](int t, int s) {  // lane 0: all input rows of token t -> stage s
+    uint8_t* st = ring + (size_t)s * R.stage_bytes;
+    mbar_expect_tx(&bars[s], R.nrows * row_bytes);
+    bulk_load(st, a.dy + (int64_t)t * d, row_bytes, &bars[s]);
+    if (R.r_x >= 0) bulk_load(st + R.r_x * row_bytes, a.x + (int64_t)t * d, row_bytes, &bars[s]);
+    if (R.r_dz >= 0) bulk_load(st + R.r_dz * row_bytes, a.dz + (int64_t)t * d, row_bytes, &bars[s]);
+    if (R.r_o >= 0) bulk_load(st + R.r_o * row_bytes, a.o + (int64_t)t * d, row_bytes, &bars[s]);
+    if (R.r_u >= 0) bulk_load(st + R.r_u * row_bytes, a.u + (int64_t)t * a.ld_a, row_bytes, &bars[s]);
+    if (R.r_pre >= 0) bulk_load(st + R.r_pre * row_bytes, a.pre_u + (int64_t)t * a.ld_a, row_bytes, &bars[s]);
+  };
+  if (lane == 0)
+    for (int s = 0; s < R.S && w_begin + s < w_end; ++s) issue(w_begin + s, s);
+  float pg[NC][8], pb[NC][8], pc[NC][8];
+#pragma unroll
+  for (int k = 0; k < NC; ++k)
+#pragma unroll
+    for (int e = 0; e < 8; ++e) pg[k][e] = pb[k][e] = pc[k][e] = 0.f;
+  int cur_g = w_begin < w_end ? a.gid[w_begin] : 0;
+  auto flush = [&]() {
+#pragma unroll
+    for (int k = 0; k < NC; ++k) {
+      const int c = lane + 32 * k;
+      if (c < nch) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          atomicAdd(&sacc[(cur_g * 2 + 0) * d + c * 8 + e], pg[k][e]);
+          atomicAdd(&sacc[(cur_g * 2 + 1) * d + c * 8 + e], pb[k][e]);
+          pg[k][e] = pb[k][e] = 0.f;
+        }
+      }
+    }
+  };
+  // per-token scalars one token ahead (their latency hides behind the current token)
+  int g_n = 0; float mu_n = 0.f, r_n = 0.f;
+  if (w_begin < w_end) { g_n = a.gid[w_begin]; mu_n = a.mean[w_begin]; r_n = a.rstd[w_begin]; }
+#pragma unroll 1
+  for (int t = w_begin, i = 0; t < w_end; ++t, ++i) {
+    const int s = i % R.S;
+    const int g = g_n;
+    const float mu = mu_n, r = r_n;
+    if (t + 1 < w_end) { g_n = a.gid[t + 1]; mu_n = a.mean[t + 1]; r_n = a.rstd[t + 1]; }
+    mbar_wait(&bars[s], (i / R.S) & 1);
+    const uint8_t* st = ring + (size_t)s * R.stage_bytes;
+    auto row8 = [&](int slot, int c, float* v) {  // 8 elements of an input row (16-byte lane)
+      Raw8<bf> rw;
+      asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                   : "=r"(rw.v.x), "=r"(rw.v.y), "=r"(rw.v.z), "=r"(rw.v.w)
+                   : "r"(smem_u32(st + slot * row_bytes + c * 16)));
+      unpack(rw, v);
+    };
+    auto x_of = [&](int k, float* xv) {
+      const int c = lane + 32 * k;
+      if (MODE == GLN_GATE && R.r_x < 0) {  // gated norm input x = o (.) u
+        float uu[8], oo[8];
+        row8(R.r_u, c, uu);
+        row8(R.r_o, c, oo);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) xv[e] = oo[e] * uu[e];
+      } else {
+        row8(R.r_x, c, xv);
+      }
+    };
+    if (g != cur_g) {
+      flush();
+      cur_g = g;
+    }
+    const float* gr = sgam + g * d;
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int k = 0; k < NC; ++k) {
+      const int c = lane + 32 * k;
+      if (c < nch) {
+        float xv[8], dyv[8], gg[8];
+        x_of(k, xv);
+        row8(0, c, dyv);
+        load8(gr + c * 8, gg);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const float xh = (xv[e] - mu) * r;
+          const float dxh = dyv[e] * gg[e];
+          pg[k][e] = fmaf(dyv[e], xh, pg[k][e]);
+          pb[k][e] += dyv[e];
+          s1 += dxh;
+          s2 = fmaf(dxh, xh, s2);
+        }
+      }
+    }
+    const float m1 = warp_sum(s1) * inv_d, m2 = warp_sum(s2) * inv_d;
+#pragma unroll
+    for (int k = 0; k < NC; ++k) {
+      const int c = lane + 32 * k;
+      if (c < nch) {
+        float xv[8], dyv[8], gg[8], o[8];
+        x_of(k, xv);
+        row8(0, c, dyv);
+        load8(gr + c * 8, gg);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) o[e] = r * (dyv[e] * gg[e] - m1 - (xv[e] - mu) * r * m2);
+        if (MODE == GLN_RESID) {
+          float z[8];
+          row8(R.r_dz, c, z);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            o[e] += z[e];
+            pc[k][e] += z[e];
+          }
+          store8(a.dx + (int64_t)t * d + c * 8, o);
+        } else if (MODE == GLN_GATE) {
+          // o[] = dY; dO = dY * U;  dp_U = dY * O * silu'(p_U)
+          float uu[8], oo[8], dO[8], du[8];
+          row8(R.r_u, c, uu);
+          row8(R.r_o, c, oo);
+          float pp[8];
+          if (R.r_pre >= 0) row8(R.r_pre, c, pp);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            dO[e] = o[e] * uu[e];
+            du[e] = o[e] * oo[e];
+            if (R.r_pre >= 0) du[e] *= a.pre_dsilu ? pp[e] : dsilu_f(pp[e]);
+            pc[k][e] += du[e];
+          }
+          store8(a.dx + (int64_t)t * d + c * 8, dO);
+          store8(a.dpu + (int64_t)t * a.ld_dp + c * 8, du);
+        } else {
+          store8(a.dx + (int64_t)t * d + c * 8, o);
+        }
+      }
+    }
+    __syncwarp();  // every lane has consumed stage s
+    if (lane == 0 && t + R.S < w_end) issue(t + R.S, s);
+  }
+  if (w_begin < w_end) flush();
+  if (csum) {
+#pragma unroll
+    for (int k = 0; k < NC; ++k) {
+      const int c = lane + 32 * k;
+      if (c < nch)
+#pragma unroll
+        for (int e = 0; e < 8; ++e) atomicAdd(&sacc[G * 2 * d + c * 8 + e], pc[k][e]);
+    }
+  }
+  __syncthreads();
+  if (csum)
+    for (int i = threadIdx.x; i < d; i += blockDim.x) atomicAdd(a.dcol + i, sacc[G * 2 * d + i]);
+  for (int i = threadIdx.x; i < G * 2 * d; i += blockDim.x) {
+    const float v = sacc[i];
+    if (v != 0.f) atomicAdd(a.part + i, v);
+  }
+}
+
 // dgamma/dbeta (+)= accumulators
 __global__ void gln_param_finish_kernel(const float* __restrict__ acc, int G, int d,
                                         float* __restrict__ dgamma, float* __restrict__ dbeta,
@@ -390,6 +579,49 @@ static void gln_bwd_mode(const GlnBwdArgs<T>& a, int nb, size_t smem, cudaStream
   }
 }
 
+template <int MODE, int NC>
+static void gln_bwd_bulk_go(const GlnBwdArgs<__nv_bfloat16>& a, const GlnRing& R, int blocks,
+                            int threads, size_t smem, cudaStream_t st) {
+  cudaFuncSetAttribute(gln_bwd_bulk_kernel<MODE, NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  gln_bwd_bulk_kernel<MODE, NC><<<blocks, threads, smem, st>>>(a, R);
+}
+template <int MODE>
+static void gln_bwd_bulk_mode(const GlnBwdArgs<__nv_bfloat16>& a, const GlnRing& R, int blocks,
+                              int threads, size_t smem, cudaStream_t st) {
+  switch (gln_nc(a.d)) {
+    case 1: gln_bwd_bulk_go<MODE, 1>(a, R, blocks, threads, smem, st); break;
+    case 2: gln_bwd_bulk_go<MODE, 2>(a, R, blocks, threads, smem, st); break;
+    case 3: gln_bwd_bulk_go<MODE, 3>(a, R, blocks, threads, smem, st); break;
+    default: gln_bwd_bulk_go<MODE, 4>(a, R, blocks, threads, smem, st); break;
+  }
+}
+static mtgr_status_t gln_bwd_bulk_launch(GlnBwdArgs<__nv_bfloat16> a, int mode, cudaStream_t st) {
+  GlnRing R{};
+  int n = 1;
+  auto slot = [&](bool present) { return present ? n++ : -1; };
+  R.r_x = slot(mode != GLN_GATE || a.x != nullptr);
+  R.r_dz = slot(mode == GLN_RESID);
+  R.r_o = slot(mode == GLN_GATE);
+  R.r_u = slot(mode == GLN_GATE);
+  R.r_pre = slot(mode == GLN_GATE && a.pre_u != nullptr);
+  R.nrows = n;
+  R.stage_bytes = (uint32_t)(n * a.d * 2);
+  R.S = 3;
+  const size_t acc_bytes = align_up(((size_t)a.G * 3 * a.d + a.d) * sizeof(float), 128);  // + gamma
+  R.ring_off = (uint32_t)acc_bytes;
+  const size_t budget = 200 * 1024;
+  int warps = (int)((budget - acc_bytes) / ((size_t)R.S * R.stage_bytes + R.S * 8));
+  warps = std::max(1, std::min(16, warps));
+  const int threads = 32 * warps;
+  const size_t smem = acc_bytes + (size_t)warps * R.S * R.stage_bytes + (size_t)warps * R.S * 8;
+  const int blocks = num_sms();
+  a.tok_per_warp = ceil_div(a.ntok, blocks * warps);
+  if (mode == GLN_GATE) gln_bwd_bulk_mode<GLN_GATE>(a, R, blocks, threads, smem, st);
+  else if (mode == GLN_RESID) gln_bwd_bulk_mode<GLN_RESID>(a, R, blocks, threads, smem, st);
+  else gln_bwd_bulk_mode<GLN_PLAIN>(a, R, blocks, threads, smem, st);
+  return check_launch("gln_bwd_bulk");
+}
+
 template <class T>
 mtgr_status_t gln_bwd_launch(const GlnBwdIO& io, int mode, float* part, float* dgamma,
                              float* dbeta, int accumulate, cudaStream_t st) {
@@ -404,6 +636,12 @@ mtgr_status_t gln_bwd_launch(const GlnBwdIO& io, int mode, float* part, float* d
   int nb = io.ntok > 0 ? gln_bwd_blocks(io.ntok) : 0;
   size_t smem = ((size_t)io.G * 2 * io.d + io.d) * sizeof(float);
   cudaMemsetAsync(part, 0, (size_t)io.G * 2 * io.d * sizeof(float), st);
+  if constexpr (std::is_same<T, __nv_bfloat16>::value) {
+    if (io.ntok > 0 && gln_nc(io.d) <= 4) {
+      MTGR_TRY(gln_bwd_bulk_launch(a, mode, st));
+      nb = 0;
+    }
+  }
   if (nb > 0) {
     if (mode == GLN_GATE) gln_bwd_mode<T, GLN_GATE>(a, nb, smem, st);
     else if (mode == GLN_RESID) gln_bwd_mode<T, GLN_RESID>(a, nb, smem, st);
