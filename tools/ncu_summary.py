@@ -3,7 +3,13 @@
 
   python tools/ncu_summary.py launches <launches.csv>          per-kernel share of a launch list
   python tools/ncu_summary.py full <report.ncu-rep> [...]      key metrics + top stall reasons
+  python tools/ncu_summary.py traffic <config> <report.ncu-rep> [...]
+        merge per-launch DRAM bytes (read + write) by bench kernel kind into
+        profiles/traffic_per_launch.json (read by bench.py for roofline.traffic)
 """
+import json
+import os
+import re
 import collections
 import csv
 import io
@@ -65,9 +71,46 @@ def full(path):
         print("   stalls           " + ", ".join(f"{k} {v / tot:.0%}" for k, v in top))
 
 
+# bench.py kernel kinds of the captured kernels (attention MODE enum: FWD 0, DV 1, DQ 2, DK 3;
+# GEMM EPI enum: STORE 0, QKVU 1, RESID 2, F32 3)
+KIND = [(r"attn_tc_kernel<0>", "attn_fwd"), (r"attn_tc_kernel<1>", "attn_bwd_dv"),
+        (r"attn_tc_kernel<2>", "attn_bwd_dq"), (r"attn_tc_kernel<3>", "attn_bwd_dk"),
+        (r"gemm_tc_kernel<1,", "gemm_qkvu"), (r"gemm_tc_kernel<2,", "gemm_out"),
+        (r"gemm_tc_kernel<0,", "gemm_dgrad"), (r"gemm_tc_kernel<3,", "gemm_wgrad"),
+        (r"gln_fwd_kernel", "gln_fwd"), (r"gln_bwd", "gln_bwd")]
+
+
+def traffic(config, paths):
+    out_p = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "profiles", "traffic_per_launch.json")
+    db = json.load(open(out_p)) if os.path.exists(out_p) else {}
+    per = collections.defaultdict(list)
+    for path in paths:
+        raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+        rows = list(csv.reader(io.StringIO(raw)))
+        h, units = rows[0], rows[1]
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+        for r in rows[2:]:
+            d = dict(zip(h, r))
+            u = dict(zip(h, units))
+            name = d["Kernel Name"].replace(" ", "")
+            kind = next((k for pat, k in KIND if re.search(re.escape(pat.replace(" ", "")), name)), None)
+            if kind is None:
+                continue
+            b = sum(float(d[m].replace(",", "")) * scale.get(u[m], 1)
+                    for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+            per[kind].append(b)
+    cfg = db.setdefault(config, {})
+    for k, v in per.items():
+        cfg[k] = sum(v) / len(v)
+        print(f"{k:14s} {cfg[k] / 1e9:8.3f} GB per launch ({len(v)} launches)")
+    json.dump(db, open(out_p, "w"), indent=1, sort_keys=True)
+
+
 if __name__ == "__main__":
     if sys.argv[1] == "launches":
         launches(sys.argv[2])
+    elif sys.argv[1] == "traffic":
+        traffic(sys.argv[2], sys.argv[3:])
     else:
         for p in sys.argv[2:]:
             full(p)
