@@ -464,6 +464,9 @@ def main():
     import torch.distributed as dist
     if world > 1:
         torch.cuda.set_device(local_rank)
+        # NCCL's version banner goes to stdout, which must carry exactly one JSON line
+        if os.environ.get("NCCL_DEBUG", "").upper() not in ("INFO", "TRACE"):
+            os.environ["NCCL_DEBUG"] = "WARN"
         dist.init_process_group(args.backend, device_id=torch.device("cuda", local_rank))
     try:
         run_mtgr(args, cfg, rank, world, local_rank)
