@@ -27,16 +27,23 @@ namespace tcg {
 constexpr int BM = 128, BN = 256, BK = 64;  // BM = rows per CTA; a CTA pair covers 256 rows
 constexpr int A_BYTES = BM * BK * 2;
 constexpr int NUM_EPI_WARPS = 8;                     // 2 per TMEM lane quadrant
-constexpr int STG_BYTES = 2 * 32 * 128;              // per epilogue warp: 2 x [32 rows][64 bf16]
+constexpr int CHUNK_BYTES = 32 * 128;                // one [32 rows][64 bf16] SW128 staging tile
 constexpr int NTHREADS = 128 + 32 * NUM_EPI_WARPS;
 
 // per-cta_group geometry: CG = 1 (one CTA, M=128 MMA) or 2 (CTA pair, M=256 MMA; each CTA holds
 // its 128 rows of A and half of the 256 B rows, so per-SM operand traffic halves)
-template <int CG>
+// Each epilogue warp double-buffers its staging tile, so the bulk store of one 64-column chunk
+// drains while the next chunk is formed (QKVU, two outputs per chunk, keeps one buffer pair: its
+// shared memory goes to a fourth pipeline stage instead, which measured faster).
+template <int CG, int EPI>
 struct Geo {
   static constexpr int B_ROWS = BN / CG;
   static constexpr int B_BYTES = B_ROWS * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int NOUT = EPI == 1 ? 2 : 1;  // EPI_QKVU writes C and C2
+  static constexpr int BUF_BYTES = NOUT * CHUNK_BYTES;
+  static constexpr int NBUF = NOUT == 2 ? 1 : 2;
+  static constexpr int STG_BYTES = NBUF * BUF_BYTES;
   static constexpr int STAGES = CG == 2 ? 4 : 3;
   static constexpr int OFF_STG = STAGES * STAGE_BYTES;
   static constexpr int OFF_BAR = OFF_STG + NUM_EPI_WARPS * STG_BYTES;
@@ -75,7 +82,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                    const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmC2,
                    const __grid_constant__ CUtensorMap tmR, Params p) {
   using namespace sm100;
-  using G = Geo<CG>;
+  using G = Geo<CG, EPI>;
   extern __shared__ uint8_t smem_raw[];
   // 1024-B aligned base, derived by indexing the shared array so the compiler keeps the shared
   // address space (LDS/STS rather than generic LD/ST for every staged access)
@@ -207,9 +214,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const int q = warp & 3;
     const int hf = ew >> 2;
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
-    uint8_t* stg = smem + G::OFF_STG + ew * STG_BYTES;
-    uint8_t* srow = stg + lane * 128;
+    uint8_t* stg_base = smem + G::OFF_STG + ew * G::STG_BYTES;
     uint32_t rphase = 0;
+    int nchunk = 0;  // chunks staged by this warp (buffer = nchunk & 1)
     int it = 0;
     for (int item = cta_id; item < total; item += ncta, ++it) {
       const int nb = item % p.num_n, rest = item / p.num_n;
@@ -281,8 +288,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             for (int e = 0; e < 64; ++e) v[e] += (n0 + e < p.N) ? __ldg(p.bias + n0 + e) : 0.f;
           }
         }
-        // the previous TMA store of this warp must have finished reading the staging tile
-        if (lane == 0) tma_store_wait_read<0>();
+        // the bulk store issued from this buffer two chunks ago must have finished reading it
+        uint8_t* stg = stg_base + (G::NBUF == 2 ? (nchunk & 1) : 0) * G::BUF_BYTES;
+        uint8_t* srow = stg + lane * 128;
+        ++nchunk;
+        if (lane == 0) {
+          if (G::NBUF == 2) tma_store_wait_read<1>();
+          else tma_store_wait_read<0>();
+        }
         __syncwarp();
         if (EPI == EPI_RESID) {
           if (lane == 0) {
@@ -398,10 +411,23 @@ static Split choose_split(int M, int N, int K, int epi) {
   const int units = num_sms() / CG_USE;
   Split s{1, num_kb};
   if (epi == EPI_F32 && tiles < units && num_kb > 1) {
-    int want = ceil_div(2 * units, tiles);
-    want = std::min(want, num_kb);
-    s.kb_per_split = ceil_div(num_kb, want);
-    s.splits = ceil_div(num_kb, s.kb_per_split);
+    // the persistent grid walks tiles x splits work items in rounds of `units` CTA pairs: pick
+    // the split count whose item count fills the last round best (fewest splits on ties), from
+    // one to four rounds' worth -- e.g. dW1 of `small` (16 tiles): 9 splits = 144 items over 74
+    // pairs (97%), where 10 splits left a third round mostly idle
+    const int lo = ceil_div(units, tiles);
+    double best = -1.0;
+    for (int want = lo; want <= 4 * lo && want <= num_kb; ++want) {
+      const int kbs = ceil_div(num_kb, want);
+      const int sp = ceil_div(num_kb, kbs);
+      const int items = tiles * sp;
+      const double eff = (double)items / ((double)units * ceil_div(items, units));
+      if (eff > best + 1e-9) {
+        best = eff;
+        s.kb_per_split = kbs;
+        s.splits = sp;
+      }
+    }
   }
   return s;
 }
@@ -443,7 +469,7 @@ mtgr_status_t gemm_bf16_launch(const GemmIO& g, int epi, void* ws, size_t ws_byt
                  (!g.R || (g.ldr % 8 == 0 && aligned16(g.R))) && (!g.bias || aligned16(g.bias)),
              MTGR_E_LAYOUT, "tc gemm: outputs need 16-byte aligned rows");
   constexpr int CG = CG_USE;
-  using Gm = Geo<CG>;
+  using Gm = Geo<CG, EPI_QKVU>;  // the largest footprint
   CUtensorMap ta, tb;
   if (g.a_kmajor) MTGR_TRY(make_tmap_bf16(&ta, g.A, g.K, g.M, g.lda, 64, BM));
   else MTGR_TRY(make_tmap_bf16(&ta, g.A, g.M, g.K, g.lda, 64, 64));
