@@ -10,6 +10,9 @@ import os
 from ctypes import POINTER, c_float, c_int32, c_int64, c_size_t, c_void_p, c_char_p, c_uint8
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libmtgr.so")
+# A/B measurements only: another in-tree build of the same ABI (e.g. libmtgr_ab.so)
+if os.environ.get("MTGR_LIBRARY"):
+    LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), os.path.basename(os.environ["MTGR_LIBRARY"]))
 
 MTGR_F32, MTGR_BF16 = 0, 1
 STATUS = {0: "MTGR_OK", 1: "MTGR_E_ARG", 2: "MTGR_E_SHAPE", 3: "MTGR_E_LAYOUT", 4: "MTGR_E_DTYPE",

@@ -45,10 +45,11 @@ constexpr int BR = 128;                 // rows per CTA
 constexpr int BC = 64;                  // columns per iterated tile
 constexpr int KB = 1024;
 constexpr int RT_BYTES = BR * DH * 2;   // 64 KB: 4 boxes {64 dh, 128 rows}
-constexpr int OFF_RED = 208 * KB;        // dbias scratch: [8 warps][256 columns] fp32
-constexpr int OFF_TS = OFF_RED + 8 * DH * 4;
-constexpr int OFF_BAR = OFF_TS + BC * 8;
-constexpr int SMEM_BYTES = OFF_BAR + 512 + 1024;
+// key timestamps of the current tile (int64 x 64) and the barriers: after the epilogue tile
+// (!TWO) / after the dbias scratch [208,216) KB (TWO)
+constexpr int off_ts(bool two) { return (two ? 216 : 224) * KB; }
+constexpr int off_bar(bool two) { return off_ts(two) + BC * 8; }
+constexpr int SMEM_BYTES = off_bar(false) + 512 + 1024;
 constexpr int NSM = 8;  // softmax/epilogue warps
 
 enum { FWD = 0, DV = 1, DQ = 2, DK = 3 };
@@ -72,7 +73,7 @@ struct Args {
 // (softmax warp 4); 5 first S issued, 6 last acc issued (MMA warp); 7 R1 load issued, 8 last C1
 // load issued (producer); 9 ntiles (value); 10*64 = time base after the start-up cluster barrier
 #define DBG_ON (a.dbg != nullptr && (blockIdx.x >> 1) == 1)
-#define DBGV(ev, i, val) do { if (DBG_ON && (i) < 64) a.dbg[(blockIdx.x & 1) * 16 * 64 + (ev) * 64 + (i)] = (val); } while (0)
+#define DBGV(ev, i, val) do { if (DBG_ON && (i) < 64) a.dbg[(blockIdx.x & 1) * 20 * 64 + (ev) * 64 + (i)] = (val); } while (0)
 #define DBG(ev, i) DBGV(ev, i, clock64())
 
 __device__ __forceinline__ float silu_fast(float s) {
@@ -143,31 +144,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
   // the next item while the epilogue (which reads E/U rows straight from L2 and writes the
   // outputs from registers) drains the accumulator.
   // smem (KB):     !TWO (FWD, DV)                        TWO (DQ, DK)
-  //   [0,32)      C1 ring: 2 x 16 (32 cols x 256 dh)    R1 (S A operand, SS) / epilogue tile
-  //   [32,80)     X ring:  3 x 16 (64 cols x 128 dh)      [0,64)
-  //   [80,144)    R1 staging                            R2 dh 128..255 [64,96) (staging of
-  //   [144,208)   epilogue tile                           R2 dh 0..127 first)
+  //   [0,48)      C1 ring: 3 x 16 (32 cols x 256 dh)    R1 (S A operand, SS) / epilogue tile
+  //   [48,96)     X ring:  3 x 16 (64 cols x 128 dh)      [0,64)
+  //   [96,160)    R1 staging                            R2 dh 128..255 [64,96) (staging of
+  //   [160,224)   epilogue tile                           R2 dh 0..127 first)
   //                                                     C1 ring 3 x 16 [96,144)
   //                                                     C2 ring 2 x 16 [144,176)
   //                                                     X ring 2 x 16 [176,208)
-  //   [208,212)   dbias scratch
+  //   [224,224.5) key timestamps; barriers
   // TMEM:  !TWO: R1 [0,128) (TS A), acc [128,384), S [384,448), P [448,512)
   //         TWO: acc [0,256), S [256,320), dP [320,384), P [384,448), R2 dh 0..127 [448,512)
   constexpr int C1_BYTES = 32 * DH * 2;        // 16 KB: 4 boxes {64 dh, 32 cols}
   constexpr int X_BYTES = BC * (DH / 2) * 2;   // 16 KB: 2 boxes {64 dh, 64 cols}
-  constexpr int NC1 = TWO ? 3 : 2;
+  constexpr int NC1 = 3;
   constexpr int NC2 = 2;
   constexpr int NX = TWO ? 2 : 3;
   constexpr int OFF_C1 = TWO ? 96 * KB : 0;
   constexpr int OFF_C2 = 144 * KB;
-  constexpr int OFF_X = TWO ? 176 * KB : 32 * KB;
+  constexpr int OFF_X = TWO ? 176 * KB : 48 * KB;
   constexpr int OFF_R1 = 0, OFF_R2B = 64 * KB;
-  constexpr int OFF_R1STAGE = 80 * KB;
+  constexpr int OFF_R1STAGE = 96 * KB;
   // epilogue tile (4 SW128 boxes of 128 rows x 64 head-dim columns): the SiLU' source (bwd)
   // arrives here by TMA and the outputs are formed in place and leave by TMA stores.  !TWO: a
   // dedicated region; TWO: the R1 region, free once the item's score MMAs are done (the next
   // item's R1 is loaded after the epilogue released it)
-  constexpr int OFF_EPI = TWO ? 0 : 144 * KB;
+  constexpr int OFF_EPI = TWO ? 0 : 160 * KB;
   constexpr uint32_t T_R1 = 0;
   constexpr uint32_t T_ACC = TWO ? 0 : 128;
   constexpr uint32_t T_S = TWO ? 256 : 384;
@@ -182,9 +183,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
   // 1024-B aligned base, derived by indexing the shared array so the compiler keeps the shared
   // address space (LDS/STS rather than generic LD/ST)
   uint8_t* smem = smem_raw + ((1024u - (sm100::smem_u32(smem_raw) & 1023u)) & 1023u);
-  long long* sTs = reinterpret_cast<long long*>(smem + OFF_TS);
-  float* red = reinterpret_cast<float*>(smem + OFF_RED);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
+  long long* sTs = reinterpret_cast<long long*>(smem + off_ts(TWO));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + off_bar(TWO));
   uint64_t* c1_full = bars;           // [3] leader
   uint64_t* c1_empty = bars + 3;      // [3]
   uint64_t* x_full = bars + 6;        // [3] leader
@@ -729,9 +729,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
         }
         if (dbgw) DBG(11 + cc, idx);
       }
-      if (do_bias) {
+      if constexpr (TWO) {
+       if (do_bias) {
         // bias gradient of this projection block: column sums of the tile's (stored) outputs,
-        // read back from the epilogue tile: warp sw sums rows sw, sw+8, ..., lane = 8 columns
+        // read back from the epilogue tile: warp sw sums rows sw, sw+8, ..., lane = 8 columns;
+        // the [8 warps][256 columns] partials go through the scratch after the rings
         named_bar_sync(1, 32 * NSM);  // every warp's outputs are in the tile
         const int sw = warp - 4, bx = lane >> 3, jj = lane & 7;
         float cs[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
@@ -746,16 +748,34 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
             cs[2 * k2 + 1] += f.y;
           }
         }
-        float* redw = red;  // [8 warps][256 columns]: the scratch plus the TS area after it
+        float* red = reinterpret_cast<float*>(smem + 208 * KB);
 #pragma unroll
-        for (int e = 0; e < 8; ++e) redw[sw * DH + lane * 8 + e] = cs[e];
+        for (int e = 0; e < 8; ++e) red[sw * DH + lane * 8 + e] = cs[e];
         named_bar_sync(1, 32 * NSM);
         const int col = threadIdx.x - 128;
         float sum = 0.f;
 #pragma unroll
-        for (int w2 = 0; w2 < NSM; ++w2) sum += redw[w2 * DH + col];
+        for (int w2 = 0; w2 < NSM; ++w2) sum += red[w2 * DH + col];
         if (sum != 0.f) atomicAdd(a.dbias + it.hcol + col, sum);
         named_bar_sync(1, 32 * NSM);  // scratch reusable
+       }
+      } else if (do_bias) {
+        // (!TWO has no room for the scratch) warp sw owns columns sw*32.., lane = one column
+        named_bar_sync(1, 32 * NSM);  // every warp's outputs are in the tile
+        const int col = (warp - 4) * 32 + lane;
+        const uint8_t* cbox = epi + (col >> 6) * (RT_BYTES / 4);
+        const int cj = (col & 63) >> 3, ce = (col & 7) * 2;
+        float ps[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // 8 independent chains
+        int rr = 0;
+        for (; rr + 8 <= nrows; rr += 8) {
+#pragma unroll
+          for (int k2 = 0; k2 < 8; ++k2)
+            ps[k2] += __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(cbox + sw128(rr + k2, cj) + ce));
+        }
+        for (; rr < nrows; ++rr)
+          ps[0] += __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(cbox + sw128(rr, cj) + ce));
+        const float sum = ((ps[0] + ps[1]) + (ps[2] + ps[3])) + ((ps[4] + ps[5]) + (ps[6] + ps[7]));
+        if (sum != 0.f) atomicAdd(a.dbias + it.hcol + col, sum);
       }
       // the epilogue tile may be refilled once this warp's bulk stores have read it
       if (lane == 0) tma_store_wait_read<0>();
@@ -830,17 +850,17 @@ static mtgr_status_t launch_mode(const AttnIO& io, const void* c1, int64_t ld_c1
   cudaFuncSetAttribute(attn_tc_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
   static const bool trace = getenv("MTGR_ATTN_TRACE") != nullptr;
   if (trace) {  // debug only: time-stamp one CTA pair's pipeline events
-    cudaMalloc(&a2.dbg, 2 * 16 * 64 * sizeof(long long));
-    cudaMemsetAsync(a2.dbg, 0, 2 * 16 * 64 * sizeof(long long), st);
+    cudaMalloc(&a2.dbg, 2 * 20 * 64 * sizeof(long long));
+    cudaMemsetAsync(a2.dbg, 0, 2 * 20 * 64 * sizeof(long long), st);
   }
   attn_tc_kernel<MODE><<<grid, 384, SMEM_BYTES, st>>>(m.c1, m.c2, m.x, m.r1, m.r2, m.e, m.u, m.o, a2);
   if (trace) {
-    long long hb[2 * 16 * 64];
+    long long hb[2 * 20 * 64];
     cudaMemcpyAsync(hb, a2.dbg, sizeof(hb), cudaMemcpyDeviceToHost, st);
     cudaStreamSynchronize(st);
     cudaFree(a2.dbg);
     fprintf(stderr, "ATTN_TRACE mode=%d", MODE);
-    for (int i = 0; i < 2 * 16 * 64; ++i) fprintf(stderr, " %lld", hb[i]);
+    for (int i = 0; i < 2 * 20 * 64; ++i) fprintf(stderr, " %lld", hb[i]);
     fprintf(stderr, "\n");
   }
   return check_launch("attn_tc");
