@@ -84,18 +84,36 @@ __global__ void __launch_bounds__(256) gln_fwd_kernel(const T* __restrict__ x,
   const int nwarps = gridDim.x * (blockDim.x >> 5);
   const int nch = d >> 3;
   const float inv_d = 1.0f / (float)d;
-  for (int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); t < ntok; t += nwarps) {
+  // software pipelined: the next token's rows (and group id) are in flight while this one is
+  // reduced, normalised and stored (two tokens' bytes in flight per warp)
+  Raw8<T> cx[NC], cg[NC], nx[NC], ng[NC];
+  auto issue = [&](int tt, Raw8<T>* xa, Raw8<T>* ga) {
+#pragma unroll
+    for (int k = 0; k < NC; ++k) {
+      const int c = lane + 32 * k;
+      if (c < nch) {
+        rload(x + (int64_t)tt * d + c * 8, xa[k]);
+        if (gate != nullptr) rload(gate + (int64_t)tt * ld_gate + c * 8, ga[k]);
+      }
+    }
+  };
+  int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  int g_cur = 0;
+  if (t < ntok) { issue(t, cx, cg); g_cur = gid[t]; }
+  for (; t < ntok; t += nwarps) {
+    const int tn = t + nwarps;
+    int g_next = 0;
+    if (tn < ntok) { issue(tn, nx, ng); g_next = gid[tn]; }
     float v[NC][8];
     float s = 0.f;
-    const T* xr = x + (int64_t)t * d;
 #pragma unroll
     for (int k = 0; k < NC; ++k) {
       int c = lane + 32 * k;
       if (c < nch) {
-        load8(xr + c * 8, v[k]);
+        unpack(cx[k], v[k]);
         if (gate != nullptr) {  // input = x (.) gate (Eq.6 gate folded into the norm's load)
           float gv[8];
-          load8(gate + (int64_t)t * ld_gate + c * 8, gv);
+          unpack(cg[k], gv);
 #pragma unroll
           for (int e = 0; e < 8; ++e) v[k][e] *= gv[e];
         }
@@ -116,7 +134,7 @@ __global__ void __launch_bounds__(256) gln_fwd_kernel(const T* __restrict__ x,
       }
     const float var = warp_sum(q) * inv_d;
     const float r = 1.0f / sqrtf(var + eps);
-    const int g = gid[t];
+    const int g = g_cur;
     const float* gr = gamma + (int64_t)g * d;
     const float* br = beta + (int64_t)g * d;
     T* yr = y + (int64_t)t * d;
@@ -136,6 +154,9 @@ __global__ void __launch_bounds__(256) gln_fwd_kernel(const T* __restrict__ x,
       if (mean) mean[t] = mu;
       if (rstd) rstd[t] = r;
     }
+#pragma unroll
+    for (int k = 0; k < NC; ++k) { cx[k] = nx[k]; cg[k] = ng[k]; }
+    g_cur = g_next;
   }
 }
 
