@@ -144,12 +144,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
   // the next item while the epilogue (which reads E/U rows straight from L2 and writes the
   // outputs from registers) drains the accumulator.
   // smem (KB):     !TWO (FWD, DV)                        TWO (DQ, DK)
-  //   [0,48)      C1 ring: 3 x 16 (32 cols x 256 dh)    R1 (S A operand, SS) / epilogue tile
-  //   [48,96)     X ring:  3 x 16 (64 cols x 128 dh)      [0,64)
+  //   [0,48)      C1 ring: 3 x 16 (32 cols x 256 dh)    R1 (S A operand, SS) [0,64)
+  //   [48,96)     X ring:  3 x 16 (64 cols x 128 dh)
   //   [96,160)    R1 staging                            R2 dh 128..255 [64,96) (staging of
   //   [160,224)   epilogue tile                           R2 dh 0..127 first)
-  //                                                     C1 ring 3 x 16 [96,144)
-  //                                                     C2 ring 2 x 16 [144,176)
+  //                                                     C1 ring 3 x 16 [96,144) \ epilogue
+  //                                                     C2 ring 2 x 16 [144,176) / tile [96,160)
   //                                                     X ring 2 x 16 [176,208)
   //   [224,224.5) key timestamps; barriers
   // TMEM:  !TWO: R1 [0,128) (TS A), acc [128,384), S [384,448), P [448,512)
@@ -166,9 +166,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
   constexpr int OFF_R1STAGE = 96 * KB;
   // epilogue tile (4 SW128 boxes of 128 rows x 64 head-dim columns): the SiLU' source (bwd)
   // arrives here by TMA and the outputs are formed in place and leave by TMA stores.  !TWO: a
-  // dedicated region; TWO: the R1 region, free once the item's score MMAs are done (the next
-  // item's R1 is loaded after the epilogue released it)
-  constexpr int OFF_EPI = TWO ? 0 : 160 * KB;
+  // dedicated region; TWO: the C1 ring plus the first C2 slot, free once the item's score MMAs
+  // are done (the next item's column tiles are loaded after the epilogue released it, its row
+  // operands before)
+  constexpr int OFF_EPI = TWO ? 96 * KB : 160 * KB;
   constexpr uint32_t T_R1 = 0;
   constexpr uint32_t T_ACC = TWO ? 0 : 128;
   constexpr uint32_t T_S = TWO ? 256 : 384;
@@ -317,10 +318,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
             for (int c = 0; c < 4; ++c) tma_load_2d(smem + OFF_R1STAGE + c * (RT_BYTES / 4), &tmR1, r1_full, it.hcol + c * 64, row0);
             DBG(7, idx);
           }
-          // TWO: the row operands go into the region the previous epilogue used; the first
-          // column tiles are prefetched before waiting for it
-          auto head = [&]() {
-            wait_epi();
+          // TWO: the row operands are loaded as soon as the previous item's score MMAs are done
+          // (they overlap its epilogue); the column ring doubles as that epilogue's tile, so the
+          // column tiles wait for the epilogue to release it
+          if (TWO) {
+            if (mi > 0) mbar_wait(sc_done, (mi - 1) & 1);
             if (leader) mbar_expect_tx(r1s_full, 2 * RT_BYTES);
 #pragma unroll
             for (int c = 0; c < 4; ++c) tma_load_2d_2sm(smem + OFF_R1 + c * (RT_BYTES / 4), &tmR1, r1s_full, it.hcol + c * 64, row0);
@@ -328,6 +330,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
 #pragma unroll
             for (int c = 0; c < 2; ++c) tma_load_2d(smem + OFF_R2B + c * (RT_BYTES / 4), &tmR2, r2a_full, it.hcol + c * 64, row0);
             DBG(7, idx);
+            wait_epi();
+          }
+          auto head = [&]() {  // TWO: R2 head-dim 128..255 once the staging was copied out
             mbar_wait(r2a_copied, mi & 1);
             if (leader) mbar_expect_tx(r2_full, RT_BYTES);
 #pragma unroll
@@ -346,7 +351,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
           }
           if (TWO && npre == it.ntiles) head();
           DBG(8, idx);
-          if (TWO) {  // the R1 region becomes the epilogue tile once the score MMAs are done
+          if (TWO) {  // the column ring becomes the epilogue tile once the score MMAs are done
             mbar_wait(sc_done, mi & 1);
             load_u();
           }
@@ -381,13 +386,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     // ---------------------------------------------------------------- producers B (X | C2), C (TWO: X)
     if (lane == 0) {
       const bool load_x = !TWO || warp == 2;
-      int gt = 0;
+      int gt = 0, idx = 0;
       for (int n = 0;; ++n) {
         const int k = q_read(n);
         q_release(n);
         if (k < 0) break;
         Item it;
         decode_item<TRANS>(a, k, crank, it);
+        // TWO: the C2 ring's first slot is part of the previous item's epilogue tile
+        if (TWO && !load_x && idx > 0 && it.ntiles > 0) mbar_wait(epi_free, (idx - 1) & 1);
+        ++idx;
         for (int t = 0; t < it.ntiles; ++t, ++gt) {
           if (!load_x) {
             const int slot = gt % NC2;
