@@ -459,7 +459,7 @@ __global__ void __launch_bounds__(512, 1) gln_bwd_bulk_kernel(GlnBwdArgs<__nv_bf
         load8(gr + c * 8, gg);
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
-          const float xh = (xv[e] - mu) * r;
+          const float xh = fmaf(xv[e], r, -mu * r);
           const float dxh = dyv[e] * gg[e];
           pg[k][e] = fmaf(dyv[e], xh, pg[k][e]);
           pb[k][e] += dyv[e];
@@ -469,16 +469,28 @@ __global__ void __launch_bounds__(512, 1) gln_bwd_bulk_kernel(GlnBwdArgs<__nv_bf
       }
     }
     const float m1 = warp_sum(s1) * inv_d, m2 = warp_sum(s2) * inv_d;
+    const float mur = mu * r;
 #pragma unroll
     for (int k = 0; k < NC; ++k) {
       const int c = lane + 32 * k;
       if (c < nch) {
-        float xv[8], dyv[8], gg[8], o[8];
-        x_of(k, xv);
+        float xv[8], dyv[8], gg[8], o[8], uu[8], oo[8];
+        if (MODE == GLN_GATE && R.r_x < 0) {  // x = o (.) u, keeping o and u for the gate
+          row8(R.r_u, c, uu);
+          row8(R.r_o, c, oo);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) xv[e] = oo[e] * uu[e];
+        } else {
+          x_of(k, xv);
+          if (MODE == GLN_GATE) {
+            row8(R.r_u, c, uu);
+            row8(R.r_o, c, oo);
+          }
+        }
         row8(0, c, dyv);
         load8(gr + c * 8, gg);
 #pragma unroll
-        for (int e = 0; e < 8; ++e) o[e] = r * (dyv[e] * gg[e] - m1 - (xv[e] - mu) * r * m2);
+        for (int e = 0; e < 8; ++e) o[e] = r * (dyv[e] * gg[e] - m1 - fmaf(xv[e], r, -mur) * m2);
         if (MODE == GLN_RESID) {
           float z[8];
           row8(R.r_dz, c, z);
@@ -490,18 +502,25 @@ __global__ void __launch_bounds__(512, 1) gln_bwd_bulk_kernel(GlnBwdArgs<__nv_bf
           store8(a.dx + (int64_t)t * d + c * 8, o);
         } else if (MODE == GLN_GATE) {
           // o[] = dY; dO = dY * U;  dp_U = dY * O * silu'(p_U)
-          float uu[8], oo[8], dO[8], du[8];
-          row8(R.r_u, c, uu);
-          row8(R.r_o, c, oo);
-          float pp[8];
-          if (R.r_pre >= 0) row8(R.r_pre, c, pp);
+          float dO[8], du[8];
 #pragma unroll
           for (int e = 0; e < 8; ++e) {
             dO[e] = o[e] * uu[e];
             du[e] = o[e] * oo[e];
-            if (R.r_pre >= 0) du[e] *= a.pre_dsilu ? pp[e] : dsilu_f(pp[e]);
-            pc[k][e] += du[e];
           }
+          if (R.r_pre >= 0) {
+            float pp[8];
+            row8(R.r_pre, c, pp);
+            if (a.pre_dsilu) {
+#pragma unroll
+              for (int e = 0; e < 8; ++e) du[e] *= pp[e];
+            } else {
+#pragma unroll
+              for (int e = 0; e < 8; ++e) du[e] *= dsilu_f(pp[e]);
+            }
+          }
+#pragma unroll
+          for (int e = 0; e < 8; ++e) pc[k][e] += du[e];
           store8(a.dx + (int64_t)t * d + c * 8, dO);
           store8(a.dpu + (int64_t)t * a.ld_dp + c * 8, du);
         } else {
