@@ -393,8 +393,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
         if (k < 0) break;
         Item it;
         decode_item<TRANS>(a, k, crank, it);
-        // TWO: the C2 ring's first slot is part of the previous item's epilogue tile
-        if (TWO && !load_x && idx > 0 && it.ntiles > 0) mbar_wait(epi_free, (idx - 1) & 1);
+        // TWO: the C2 ring's first slot is part of the previous item's epilogue tile.  Wait for
+        // every item, tiles or not: parity waits must not skip a phase (a skipped one lets the
+        // wait for phase i pass while phase i-1 is still pending)
+        if (TWO && !load_x && idx > 0) mbar_wait(epi_free, (idx - 1) & 1);
         ++idx;
         for (int t = 0; t < it.ntiles; ++t, ++gt) {
           if (!load_x) {

@@ -85,3 +85,34 @@ def test_large_shape_one_layer(dev):
     zo, dxo = _oracle_user(cfg, seg, u, ts[a:b], X[a:b], dZ[a:b], Ps)
     assert rel_err(z[a:b], zo) <= 2e-2
     assert rel_err(dx[a:b], dxo) <= 2e-2
+
+
+def test_attention_bitwise_deterministic(dev):
+    """The attention kernels own their outputs (no atomics on the public path), so repeated runs
+    on identical inputs must agree bit for bit.  The bench batch mixes long items with short and
+    tile-less (candidate-only) pairs, the pattern under which a skipped barrier phase once let a
+    producer refill the shared epilogue tile early (dk rows of the following item differed
+    between runs)."""
+    cfg = synth.config("small")
+    seg = synth.gen_segments(cfg)
+    L = seg.astype(np.int64).sum(1)
+    ts = np.concatenate([synth.gen_user_ts(cfg, u, seg[u]) for u in range(len(seg))])
+    jb = m.JaggedBatch.build(seg, ts, dev)
+    lc = m.layer_cfg(cfg["d"], cfg["H"], cfg["groups"])
+    T, d = jb.total_tokens, cfg["d"]
+    g = torch.Generator(device="cpu").manual_seed(11)
+    qkvu = (torch.randn(T, 4 * d, generator=g) * 0.5).to(dev, torch.bfloat16)
+    dO = torch.randn(T, d, generator=g).to(dev, torch.bfloat16)
+    pre = torch.randn(T, 4 * d, generator=g).to(dev, torch.bfloat16)
+    q, k, v = qkvu[:, :d], qkvu[:, d:2 * d], qkvu[:, 2 * d:3 * d]
+    ref = None
+    for _ in range(6):
+        o, _ = m.attn_fwd(lc, jb, q, k, v, 4 * d)
+        dq, dk, dv, _ = m.attn_bwd(lc, jb, dO, q, k, v, 4 * d, silu_pre=pre)
+        torch.cuda.synchronize()
+        cur = [t.clone() for t in (o, dq, dk, dv)]
+        if ref is None:
+            ref = cur
+            continue
+        for name, a_, b_ in zip(("o", "dq", "dk", "dv"), ref, cur):
+            assert torch.equal(a_, b_), name
