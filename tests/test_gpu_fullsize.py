@@ -62,7 +62,9 @@ def test_small_config_sampled_users_and_additivity(dev):
         zo, dxo = _oracle_user(cfg, seg, u, ts[a:b], X[a:b], dZ[a:b], Ps)
         assert rel_err(z[a:b], zo) <= 2e-2, ("Z", u)
         assert rel_err(dx[a:b], dxo) <= 2e-2, ("dX", u)
-    # parameter gradients are sums over users: full batch == first half + second half
+    # parameter gradients are sums over users: full batch == first half + second half (the
+    # per-user arithmetic is identical; only fp32 summation order differs: split-K bounds,
+    # atomics), so 1e-4 leaves room for that and nothing else
     h = len(seg) // 2
     parts = []
     for us_ in (np.arange(h), np.arange(h, len(seg))):
@@ -71,7 +73,7 @@ def test_small_config_sampled_users_and_additivity(dev):
     for li in range(cfg["n_layers"]):
         full = grads[li].cpu().numpy()
         summed = (parts[0][li] + parts[1][li]).cpu().numpy()
-        assert rel_err(full, summed) <= 1e-3, li
+        assert rel_err(full, summed) <= 1e-4, li
 
 
 def test_large_shape_one_layer(dev):
