@@ -128,12 +128,14 @@ template <class T>
 __global__ void __launch_bounds__(256) attn_diag_kernel(AttnIO a, int bwd, float* __restrict__ diag_a,
                                                         float* __restrict__ diag_ds) {
   const int lane = threadIdx.x & 31;
-  const UserSpan us = load_user(a.jag, blockIdx.x);
+  const UserSpan us = load_user(a.jag, blockIdx.y);
   const T* q = (const T*)a.q; const T* k = (const T*)a.k; const T* v = (const T*)a.v;
   const T* dO = (const T*)a.dO;
   const int nch = a.dh >> 3;
   const int first = a.diag_cand_only ? us.ns + us.nr : us.ns;
-  for (int li = first + (threadIdx.x >> 5); li < us.L; li += blockDim.x >> 5) {
+  // grid (row blocks, users): a single long request still spreads over many SMs
+  const int wpb = blockDim.x >> 5;
+  for (int li = first + blockIdx.x * wpb + (threadIdx.x >> 5); li < us.L; li += gridDim.x * wpb) {
     const int64_t t = us.off + li;
     for (int h = 0; h < a.H; ++h) {
       float s = 0.f, pv = 0.f;
@@ -175,7 +177,10 @@ mtgr_status_t attn_diag_launch(const AttnIO& a, bool bwd, float* diag_a, float* 
                                cudaStream_t st) {
   if (a.jag.total_tokens == 0 || a.jag.num_users == 0) return MTGR_OK;
   ProfScope ps(PROF_ATTN_DIAG, st);
-  attn_diag_kernel<T><<<a.jag.num_users, 256, 0, st>>>(a, bwd ? 1 : 0, diag_a, diag_ds);
+  // one warp per token; enough row blocks per user that ~4 waves cover the batch
+  const int users = a.jag.num_users;
+  int rb = std::max(1, std::min(ceil_div(a.jag.max_len, 8), ceil_div(4 * num_sms(), users)));
+  attn_diag_kernel<T><<<dim3(rb, users), 256, 0, st>>>(a, bwd ? 1 : 0, diag_a, diag_ds);
   return check_launch("attn_diag");
 }
 template mtgr_status_t attn_diag_launch<float>(const AttnIO&, bool, float*, float*, cudaStream_t);
