@@ -43,6 +43,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-users", type=int, default=24, help="users in the CPU oracle sample (~10 s)")
     ap.add_argument("--backend", default="nccl")
+    ap.add_argument("--balance", default="tokens", choices=["tokens", "flops"],
+                    help="LPT cost: token count (R#19, default) or per-user FLOPs (SURVEY f3)")
     return ap.parse_args()
 
 
@@ -67,17 +69,22 @@ def visible_pairs(seg_u, ts_u):
     return L * ns + int(np.searchsorted(rt, rows, side="left").sum()) + (L - ns)
 
 
-def workload(cfg, rank, world, balance):
+def workload(cfg, rank, world, balance, cost_kind="tokens"):
     B_rank = cfg["users"]
     B_g = B_rank * world
     seg = synth.gen_segments(cfg, B_g)
     L = seg.astype(np.int64).sum(1)
-    rank_of, load = balance(L, world)
+    if cost_kind == "flops":
+        from paper_2505_18654_b200.dp import flop_cost
+        cost = flop_cost(seg, [synth.gen_user_ts(cfg, u, seg[u]) for u in range(B_g)], cfg["d"])
+    else:
+        cost = L
+    rank_of, load = balance(cost, world)
     users = np.nonzero(rank_of == rank)[0].astype(np.int32)
     ts = [synth.gen_user_ts(cfg, int(u), seg[u]) for u in users]
     P = sum(visible_pairs(seg[u], t) for u, t in zip(users, ts))
     return dict(seg=seg, users=users, ts=ts, L=L, load=load, B_g=B_g, pairs=P,
-                tokens=int(L[users].sum()), tokens_global=int(L.sum()))
+                tokens=int(L[users].sum()), tokens_global=int(L.sum()), balance=cost_kind)
 
 
 def step_flops(cfg, tokens, pairs):
@@ -101,7 +108,8 @@ def kernel_algorithmic(cfg, tokens, pairs):
         "gemm_dgrad": ("tensor", nl * 10.0 * T * d * d),
         "gemm_wgrad": ("tensor", nl * 10.0 * T * d * d),
         # GLN fwd: read x, write y (bf16) + 2 fp32 stats; GLN bwd: read dy, x, (o, u, p_U) ...
-        "gln_fwd": ("hbm", nl * 2 * T * (4.0 * d + 8)),
+        # GLN1 reads x, writes x~; GLN2 reads O and U (the gate), writes y~
+        "gln_fwd": ("hbm", nl * T * ((4.0 * d + 8) + (6.0 * d + 8))),
         "gln_bwd": ("hbm", nl * T * ((12.0 * d + 8) + (8.0 * d + 8))),
     }
 
@@ -220,7 +228,8 @@ def workload_desc(cfg, wl, world):
                         f"n_r={_seg_desc(cfg['nR'])}, K={_seg_desc(cfg['K'])})",
             "users_per_rank": cfg["users"], "global_batch_users": wl["B_g"],
             "tokens_global": wl["tokens_global"], "mean_len": round(wl["tokens_global"] / wl["B_g"], 1),
-            "parallelism": f"dp{world}", "balancer": "token-count LPT",
+            "parallelism": f"dp{world}",
+            "balancer": "FLOP-cost LPT" if wl.get("balance") == "flops" else "token-count LPT",
             "l2": "no flush: per-step activations are several GB (>> 126 MB L2)"}
 
 
@@ -261,7 +270,7 @@ def run_mtgr(args, cfg, rank, world, local_rank):
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
     dt = torch.bfloat16
-    wl = workload(cfg, rank, world, m.balance_lpt)
+    wl = workload(cfg, rank, world, m.balance_lpt, args.balance)
     users = wl["users"]
     ts = np.concatenate(wl["ts"]) if len(users) else np.zeros(0, np.int64)
     Ls = wl["L"][users]

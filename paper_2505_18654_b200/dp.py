@@ -16,6 +16,26 @@ from __future__ import annotations
 import numpy as np
 
 
+def visible_pairs(seg_u, ts_u) -> int:
+    """Attention work of one user: P_u = L*n_s + sum_{i>=n_s} |{j in rt: ts_j < ts_i}| + (L-n_s)
+    (static rows read the n_s static keys; real-time and candidate rows additionally read the
+    earlier real-time tokens and themselves)."""
+    nU, nS, nR, K = (int(v) for v in seg_u)
+    ns, L = nU + nS, nU + nS + nR + K
+    rt = np.sort(np.asarray(ts_u[ns:ns + nR]))
+    return L * ns + int(np.searchsorted(rt, np.asarray(ts_u[ns:]), side="left").sum()) + (L - ns)
+
+
+def flop_cost(seg4, ts_list, d: int) -> np.ndarray:
+    """FLOP-aware balancer cost: per-user fwd+bwd FLOPs of one layer divided
+    by d, `30 L_u d + 12 P_u` (projections 30 L d^2, attention 12 d P_u), as int64.  The
+    token count L_u (the default cost) ignores that attention work grows like L_u n_s."""
+    seg4 = np.asarray(seg4)
+    L = seg4.astype(np.int64).sum(1)
+    P = np.array([visible_pairs(seg4[u], ts_list[u]) for u in range(len(seg4))], dtype=np.int64)
+    return 30 * L * int(d) + 12 * P
+
+
 def shard_users(seg4: np.ndarray, world: int, rank: int, cost=None, balance=None):
     """Users (ascending global index) assigned to `rank` by LPT over `cost` (default L_u)."""
     seg4 = np.asarray(seg4)

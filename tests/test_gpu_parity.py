@@ -273,3 +273,35 @@ def test_scale(dev):
     g = torch.arange(1000, dtype=torch.float32, device=dev)
     m.scale_(g, 0.25)
     np.testing.assert_array_equal(g.cpu().numpy(), np.arange(1000, dtype=np.float32) * 0.25)
+
+
+@pytest.mark.parametrize("name", ["toy", "parity"])
+def test_layer_single_shared_ln(dev, name):
+    """Table 4 "w/o GLN": one LayerNorm for every token is the layer with
+    num_groups = 1 and every group id 0 (the group-affine parameters collapse to one row)."""
+    cfg, seg, ts, X, dZ, P = make_batch(name)
+    P1 = dict(P)
+    for k in ("gamma1", "beta1", "gamma2", "beta2"):
+        P1[k] = np.ascontiguousarray(P[k][:1])
+    dt = _dt(cfg)
+    jb = m.JaggedBatch.build(seg, ts, dev)
+    jb.group_id.zero_()
+    lc = m.layer_cfg(cfg["d"], cfg["H"], 1)
+    stack = m.HstuStack(lc, [m.params_to_device(P1, dt, dev)], dt, dev)
+    stack.bind(jb)
+    z = stack.forward(_t(X, dev, dt)).float().cpu().numpy()
+    dx = stack.backward(_t(dZ, dev, dt)).float().cpu().numpy()
+    grads = [{k: v.cpu().numpy() for k, v in g.items()} for g in stack.grads]
+    h = oracle.build_jagged(seg)
+    ocfg = dict(d=cfg["d"], H=cfg["H"])
+    Z, dX = np.zeros(X.shape), np.zeros(X.shape)
+    G = None
+    for u in range(len(seg)):
+        s, e = h["offsets"][u], h["offsets"][u + 1]
+        gid0 = np.zeros(e - s, dtype=np.uint8)
+        args = (gid0, int(h["n_static"][u]), int(h["n_rt"][u]), int(h["n_cand"][u]), ts[s:e])
+        zz, caches = oracle.stack_fwd_user(X[s:e], *args, [P1], ocfg)
+        dd, gs = oracle.stack_bwd_user(dZ[s:e], caches, [P1], ocfg)
+        Z[s:e], dX[s:e] = zz, dd
+        G = [{k: v.copy() for k, v in gs[0].items()}] if G is None else [{k: G[0][k] + gs[0][k] for k in G[0]}]
+    _compare(z, dx, grads, Z, dX, G, TOL[dt])
