@@ -100,7 +100,12 @@ static SavedLayout saved_layout(int d, int ntok, size_t es) {
 
 size_t attn_ws_bytes(int ntok, int H) { return 2 * align_up((size_t)ntok * H * sizeof(float), 256); }
 
-static size_t bwd_ws_bytes(const mtgr_layer_cfg_t* c, int ntok, mtgr_dtype_t dt) {
+static bool tc_attn_path(const mtgr_layer_cfg_t* c, mtgr_dtype_t dt) {
+  return dt == MTGR_BF16 && c->rab_buckets == 0 && c->n_heads > 0 && attn_tc_supported(c->d_model / c->n_heads);
+}
+
+static size_t bwd_ws_bytes(const mtgr_layer_cfg_t* c, const mtgr_jagged_t* j, mtgr_dtype_t dt) {
+  const int ntok = j->total_tokens;
   const size_t es = esize(dt), T = ntok;
   const int d = c->d_model;
   size_t b = 0;
@@ -112,7 +117,8 @@ static size_t bwd_ws_bytes(const mtgr_layer_cfg_t* c, int ntok, mtgr_dtype_t dt)
   size_t cs = colsum_ws_bytes(ntok, 4 * d);
   size_t gm = std::max(gemm_ws_bytes(4 * d, d, ntok, EPI_F32, dt == MTGR_BF16),
                        gemm_ws_bytes(ntok, d, 4 * d, EPI_STORE, dt == MTGR_BF16));
-  b += std::max(std::max(g, cs), gm);
+  const size_t mm = tc_attn_path(c, dt) ? attn_store_ws_bytes(*j, c->n_heads) : 0;
+  b += std::max(std::max(std::max(g, cs), gm), mm);
   return b;
 }
 
@@ -272,6 +278,7 @@ static mtgr_status_t layer_bwd_t(const mtgr_layer_cfg_t* c, const mtgr_jagged_t*
   at.dq = dp; at.dk = dp + d; at.dv = dp + 2 * d; at.ld_out = 4 * d;
   at.rab_w = P->rab_w; at.drab = c->rab_buckets > 0 ? G->rab_w : nullptr;
   at.dbias = tc_attn ? G->b1 : nullptr;  // db1 of the Q|K|V blocks fused into the epilogues
+  at.mm_ws = scratch; at.mm_ws_bytes = scratch_bytes;  // stored scores (free until the wgrad GEMM)
   MTGR_TRY(run_attn_bwd<T>(at, diag_a, diag_ds, st));
   if (!tc_attn) MTGR_TRY(colsum_launch<T>(dp, 4 * d, ntok, 3 * d, G->b1, (float*)scratch, 1, st));
   // dW1 = dp^T X~, db1 = sum dp, dX~ = dp W1
@@ -386,9 +393,9 @@ MTGR_API mtgr_status_t mtgr_gln_bwd(const mtgr_layer_cfg_t* cfg, const mtgr_jagg
 
 MTGR_API size_t mtgr_attn_workspace_bytes(const mtgr_layer_cfg_t* cfg, const mtgr_jagged_t* jag,
                                           mtgr_dtype_t dtype) {
-  (void)dtype;
   if (!cfg || !jag) return 0;
-  return attn_ws_bytes(jag->total_tokens, cfg->n_heads);
+  const size_t mm = (cfg->n_heads > 0 && tc_attn_path(cfg, dtype)) ? attn_store_ws_bytes(*jag, cfg->n_heads) : 0;
+  return attn_ws_bytes(jag->total_tokens, cfg->n_heads) + mm;
 }
 
 static mtgr_status_t attn_common_checks(const mtgr_layer_cfg_t* cfg, const mtgr_jagged_t* jag,
@@ -447,6 +454,8 @@ MTGR_API mtgr_status_t mtgr_hstu_attn_bwd(const mtgr_layer_cfg_t* cfg, const mtg
   at.rab_w = rab_w; at.drab = drab_w;
   float* da = (float*)ws;
   float* dd = (float*)((char*)ws + half);
+  at.mm_ws = (char*)ws + 2 * half;
+  at.mm_ws_bytes = ws_bytes > 2 * half ? ws_bytes - 2 * half : 0;
   if (dtype == MTGR_BF16) return run_attn_bwd<__nv_bfloat16>(at, da, dd, st);
   return run_attn_bwd<float>(at, da, dd, st);
 }
@@ -461,7 +470,7 @@ MTGR_API size_t mtgr_layer_workspace_bytes(const mtgr_layer_cfg_t* cfg, const mt
                                            mtgr_dtype_t dtype) {
   if (!cfg || !jag) return 0;
   return std::max(fwd_ws_bytes(cfg, jag->total_tokens, dtype, true),
-                  bwd_ws_bytes(cfg, jag->total_tokens, dtype)) + 4096;
+                  bwd_ws_bytes(cfg, jag, dtype)) + 4096;
 }
 
 static mtgr_status_t check_params(const mtgr_layer_cfg_t* cfg, const mtgr_layer_params_t* P) {

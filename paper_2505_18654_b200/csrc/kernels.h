@@ -65,7 +65,10 @@ struct AttnIO {
   int diag_cand_only;          // diagonal scalars only for candidate rows (>= ns + nr)
   float* dbias;                // optional: column sums of the (bwd) outputs, red.add into
                                // dbias[col] for the Q|K|V blocks (tensor-core path only)
+  void* mm_ws; size_t mm_ws_bytes;  // stored-score backward scratch (attn_store_ws_bytes), or NULL
 };
+// scratch of the stored-score tensor-core backward for this batch (0: recompute path)
+size_t attn_store_ws_bytes(const mtgr_jagged_t& j, int H);
 size_t attn_ws_bytes(int ntok, int H);
 template <class T>
 mtgr_status_t attn_diag_launch(const AttnIO& a, bool bwd, float* diag_a, float* diag_ds,

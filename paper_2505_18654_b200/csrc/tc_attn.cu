@@ -66,6 +66,14 @@ struct Args {
   int pre_dsilu;                            // the pre rows hold silu'(p) already
   float* dbias;                             // bwd: red.add column sums of the outputs, or NULL
   long long* dbg;                           // debug timestamps (MTGR_ATTN_TRACE) or NULL
+  // stored-score backward (DK writes P^T and dS^T, the DV / DQ products read them back):
+  // matrices [H][st_rows][st_pitch] bf16, row = koff[u] + key (user-local), column = query
+  __nv_bfloat16* st_p;                      // P^T  = silu(S^T) * m      (DK writes, or NULL)
+  __nv_bfloat16* st_ds;                     // dS^T = dP^T silu'(S^T) m  (DK writes, or NULL)
+  int64_t st_pitch, st_rows;
+  const int* koff;                          // [B+1] padded key-row offsets (multiples of 256)
+  int c_align;                              // TRANS items of real-time keys start their query
+                                            // range at the 256-aligned pair holding n_static
 };
 
 // debug tracing (MTGR_ATTN_TRACE=1) of the CTA pair of cluster 1: slot layout [event][item]
@@ -94,7 +102,7 @@ __device__ __forceinline__ uint32_t sw128(int r, int j) { return r * 128 + ((j ^
 // One work item = (user u, row pair p, head h): rows [p*256, p*256+256) of user u, 128 per CTA.
 struct Item {
   UserSpan us;
-  int h, hcol, pr0, r0, kv_end, c_begin, ntiles;
+  int u, h, hcol, pr0, r0, kv_end, c_begin, ntiles;
   bool need_e;  // some rows of this CTA are candidates (diagonal terms outside the key range)
 };
 
@@ -103,7 +111,8 @@ __device__ __forceinline__ bool decode_item(const Args& a, int k, uint32_t crank
   it.h = k % a.H;
   const int rest = k / a.H;
   const int p = rest % a.pmax;
-  it.us = load_user(a.jag, rest / a.pmax);
+  it.u = rest / a.pmax;
+  it.us = load_user(a.jag, it.u);
   it.pr0 = p * 2 * BR;
   if (it.pr0 >= it.us.L) return false;
   it.r0 = it.pr0 + (int)crank * BR;
@@ -115,7 +124,10 @@ __device__ __forceinline__ bool decode_item(const Args& a, int k, uint32_t crank
   if (!TRANS) {
     c_end = (pair_end > it.us.ns) ? it.kv_end : it.us.ns;
   } else if (it.pr0 < it.kv_end) {
-    it.c_begin = (it.pr0 < it.us.ns) ? 0 : it.us.ns;
+    // keys that only non-static queries read.  With c_align the range starts at the query pair
+    // holding n_static, so that every query pair that reads these keys finds them stored (its
+    // static rows read masked zeros)
+    it.c_begin = (it.pr0 < it.us.ns) ? 0 : (a.c_align ? (it.us.ns / (2 * BR)) * (2 * BR) : it.us.ns);
     c_end = it.us.L;
   }
   it.ntiles = c_end > it.c_begin ? (c_end - it.c_begin + BC - 1) / BC : 0;
@@ -524,6 +536,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
     const int j_half = half * 32;
     const bool dbgw = warp == 4 && lane == 0;
+    const bool store_scores = MODE == DK && a.st_ds != nullptr;  // uniform
+    constexpr int PPN = 16;  // P^T words (stored-score DK; dead in the other modes)
     int gt = 0;      // global tile counter
     int mi = 0;      // items with tiles, in order
     int copied = 0;  // R1 (R2A) copies issued so far (the row operand of mma-item `copied - 1`)
@@ -565,6 +579,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       if (it.ntiles > 0) {
         if (copied == mi) copy_rows();  // not prefetched by the previous item
         const long long my_ts = (my < us.L && a.jag.ts) ? a.jag.ts[g] : 0;
+        // stored-score row of this key (DK): [h][koff[u] + my][query]
+        const int64_t st_row = store_scores ? ((int64_t)it.h * a.st_rows + a.koff[it.u] + my) * a.st_pitch : 0;
         const bool need_ts_rows = TRANS && (it.r0 + BR > us.ns) && (it.r0 < it.kv_end);
 #pragma unroll 1
         for (int t = 0; t < it.ntiles; ++t, ++gt) {
@@ -619,6 +635,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
           }
           // P (T) values -> bf16 pairs -> TMEM P buffer (A operand of the accumulate MMA)
           uint32_t pk[16];
+          uint32_t pp[PPN];
+          if (store_scores) {
+            // DK with stored scores: dS^T for the MMA and the store, P^T for the store only
+            // (silu and silu' share sigma(s) = 0.5 + 0.5 tanh(s/2))
+#pragma unroll
+            for (int e = 0; e < 32; e += 2) {
+              const float s0 = __uint_as_float(s[e]), s1 = __uint_as_float(s[e + 1]);
+              const float g0 = fmaf(0.5f, sm100::tanh_approx(0.5f * s0), 0.5f);
+              const float g1 = fmaf(0.5f, sm100::tanh_approx(0.5f * s1), 0.5f);
+              float p0 = s0 * g0, p1 = s1 * g1;
+              float v0 = __uint_as_float(dp[e]) * fmaf(p0, 1.0f - g0, g0);
+              float v1 = __uint_as_float(dp[e + 1]) * fmaf(p1, 1.0f - g1, g1);
+              if (vis != 0xffffffffu) {
+                const bool m0 = (vis >> e) & 1u, m1 = (vis >> (e + 1)) & 1u;
+                v0 = m0 ? v0 : 0.f; p0 = m0 ? p0 : 0.f;
+                v1 = m1 ? v1 : 0.f; p1 = m1 ? p1 : 0.f;
+              }
+              pk[e >> 1] = pack2(v0, v1);
+              pp[(e >> 1) % PPN] = pack2(p0, p1);
+            }
+          } else {
 #pragma unroll
           for (int e = 0; e < 32; e += 2) {
             const float s0 = __uint_as_float(s[e]), s1 = __uint_as_float(s[e + 1]);
@@ -636,6 +673,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
             }
             pk[e >> 1] = pack2(v0, v1);
           }
+          }
           const int tb = gt & 1;
           mbar_wait(&t_free[tb], ((gt >> 1) & 1) ^ 1);
           tc_fence_after();
@@ -643,6 +681,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
           tmem_st_wait();
           tc_fence_before();
           arrive_leader(&t_full[tb]);
+          if (store_scores) {
+            // this row's 32 query columns are 64 contiguous bytes per matrix.  Lane pairs swap
+            // halves so that each 256-bit store instruction writes 16 whole 64-byte row pieces
+            // (lanes 2k, 2k+1: row 2k, then row 2k+1) instead of 32 scattered 16-byte pieces
+            const int b = lane & 1;
+            auto put = [&](__nv_bfloat16* base, const uint32_t* w) {
+              U8 own, oth;
+#pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                own.v[i] = b ? w[8 + i] : w[i];  // selects, not dynamic register indexing
+                oth.v[i] = __shfl_xor_sync(0xffffffffu, b ? w[i] : w[8 + i], 1);
+              }
+              __nv_bfloat16* p0 = base + st_row + cb + 16 * b;
+              stg256(p0 - (int64_t)b * a.st_pitch, b ? oth : own);        // row (lane & ~1)
+              stg256(p0 + (int64_t)(1 - b) * a.st_pitch, b ? own : oth);  // row (lane | 1)
+            };
+            put(a.st_ds, pk);
+            put(a.st_p, pp);
+          }
         }
         if (dbgw) DBG(1, idx);
         // !TWO: every S MMA of this item has completed: hand the next item's row operand (already
@@ -804,6 +861,375 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// Stored-score backward products (the DK kernel wrote P^T and dS^T of every visible key row):
+//
+//   MM_DV: dV_j = nu sum_i P^T_ji dO_i   rows = keys    A = P^T  (K-major: queries contiguous)
+//   MM_DQ: dQ_i = nu sum_j dS^T_ji K_j   rows = queries A = dS^T (MN-major: queries contiguous)
+//
+// plus the candidate diagonal term, silu'(p) and the bias-gradient column sums in the same
+// epilogue as the attention kernel.  These are plain jagged GEMMs (M = 256 rows per CTA pair,
+// N = 256 head dims, K = 64 per tile): both operands come from smem by TMA (B = dO / K rows,
+// each CTA loads half of the head dim), and the accumulator is double-buffered in TMEM
+// (2 x 256 columns) so an item's epilogue overlaps the next item's MMAs.  The work items, key /
+// query ranges and the dynamic work queue are those of the attention kernel, so every tile read
+// here was written by the DK kernel (rows of a user's padded key block, see attn_koff_kernel).
+// Warp roles (384 threads): w0 TMA producer (A, B), w1 MMA issuer (leader CTA), w2 TMEM
+// allocator + SiLU' tile loader, w3 idle, w4-w11 epilogue.
+enum { MM_DV = 0, MM_DQ = 1 };
+constexpr int MM_STAGES = 4;
+constexpr int MM_A_BYTES = BR * BC * 2;             // 16 KB
+constexpr int MM_B_BYTES = BC * (DH / 2) * 2;       // 16 KB (this CTA's half of the head dim)
+constexpr int MM_STAGE_BYTES = MM_A_BYTES + MM_B_BYTES;
+constexpr int MM_OFF_EPI = MM_STAGES * MM_STAGE_BYTES;  // 128 KB
+constexpr int MM_OFF_RED = MM_OFF_EPI + RT_BYTES;       // 192 KB: dbias partials [8][256] fp32
+constexpr int MM_OFF_BAR = MM_OFF_RED + NSM * DH * 4;   // 200 KB
+constexpr int MM_SMEM_BYTES = MM_OFF_BAR + 512 + 1024;
+
+template <int M2>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
+    attn_mm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUtensorMap tmO,
+                   Args a) {
+  using namespace sm100;
+  constexpr bool TRANS = (M2 == MM_DV);
+  const uint32_t crank = cluster_ctarank();
+  const bool leader = crank == 0;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (sm100::smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + MM_OFF_BAR);
+  uint64_t* full = bars;              // [4] leader
+  uint64_t* empty = bars + 4;         // [4]
+  uint64_t* tfull = bars + 8;         // [2] (multicast commit)
+  uint64_t* tempty = bars + 10;       // [2] leader, both CTAs' epilogue warps
+  uint64_t* eu_full = bars + 12;      // own
+  uint64_t* epi_free = bars + 13;     // own
+  uint64_t* q_full = bars + 14;       // [4]
+  uint64_t* q_empty = bars + 18;      // [4] leader
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 22);
+  int* q_item = reinterpret_cast<int*>(bars + 23);  // [4]
+  auto arrive_leader = [&](uint64_t* bar) {
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) {
+      if (leader) mbar_arrive(bar);
+      else mbar_arrive_cluster(bar, 0);
+    }
+  };
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < MM_STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], 2 * NSM); }
+    mbar_init(eu_full, 1);
+    mbar_init(epi_free, NSM);
+    for (int s = 0; s < 4; ++s) {
+      mbar_init(&q_full[s], 1);
+      mbar_init(&q_empty[s], 2 * (NSM + 2));  // per CTA: 8 epilogue warps, U loader, MMA | producer
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc_2sm<512>(tmem_slot);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  auto q_read = [&](int n) -> int {
+    mbar_wait_cluster(&q_full[n & 3], (n >> 2) & 1);
+    return *reinterpret_cast<volatile int*>(&q_item[n & 3]);
+  };
+  auto q_release = [&](int n) {
+    if (leader) mbar_arrive(&q_empty[n & 3]);
+    else mbar_arrive_cluster(&q_empty[n & 3], 0);
+  };
+  auto q_push = [&](int n) -> int {
+    if (n >= 4) mbar_wait(&q_empty[n & 3], ((n >> 2) & 1) ^ 1);
+    int k;
+    for (;;) {
+      k = atomicAdd(a.ctr, 1);
+      if (k >= a.nitems) { k = -1; break; }
+      const int rest = k / a.H;
+      const int u = rest / a.pmax, p = rest % a.pmax;
+      if (p * 2 * BR < a.jag.offsets[u + 1] - a.jag.offsets[u]) break;
+    }
+    q_item[n & 3] = k;
+    st_cluster_u32(reinterpret_cast<uint32_t*>(&q_item[n & 3]), 1, (uint32_t)k);
+    mbar_arrive(&q_full[n & 3]);
+    mbar_arrive_cluster_release(&q_full[n & 3], 1);
+    return k;
+  };
+
+  if (warp == 0) {
+    // ---------------------------------------------------------------- producer: A and B tiles
+    if (lane == 0) {
+      int gt = 0;
+      for (int n = 0;; ++n) {
+        int k;
+        if (leader) {
+          k = q_push(n);
+        } else {
+          k = q_read(n);
+          q_release(n);
+        }
+        if (k < 0) break;
+        Item it;
+        decode_item<TRANS>(a, k, crank, it);
+        const int64_t krow = (int64_t)it.h * a.st_rows + a.koff[it.u];  // user's key block
+        for (int t = 0; t < it.ntiles; ++t, ++gt) {
+          const int slot = gt % MM_STAGES;
+          mbar_wait(&empty[slot], ((gt / MM_STAGES) & 1) ^ 1);
+          if (leader) mbar_expect_tx(&full[slot], 2 * MM_STAGE_BYTES);
+          uint8_t* sa = smem + slot * MM_STAGE_BYTES;
+          uint8_t* sb = sa + MM_A_BYTES;
+          const int c0 = it.c_begin + t * BC;
+          if (M2 == MM_DV) {  // P^T rows = this CTA's 128 keys, 64 query columns (K-major)
+            tma_load_2d_2sm(sa, &tmA, &full[slot], c0, (int)(krow + it.r0));
+          } else {            // dS^T rows = 64 keys, this CTA's 128 query columns (MN-major)
+#pragma unroll
+            for (int c = 0; c < 2; ++c)
+              tma_load_2d_2sm(sa + c * (MM_A_BYTES / 2), &tmA, &full[slot], it.r0 + c * 64, (int)(krow + c0));
+          }
+#pragma unroll
+          for (int c = 0; c < 2; ++c)  // B: 64 rows (dO for DV, K for DQ), this CTA's 128 head dims
+            tma_load_2d_2sm(sb + c * (MM_B_BYTES / 2), &tmB, &full[slot], it.hcol + (2 * crank + c) * 64,
+                            it.us.off + c0);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------------------------------------------------------- MMA issuer (leader CTA)
+    if (leader) {
+      const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
+      constexpr uint32_t idesc = idesc_bf16_f32(2 * BR, DH, M2 == MM_DQ ? 1 : 0, 1);
+      const uint32_t base = smem_u32(smem);
+      int gt = 0, mi = 0;
+      for (int n = 0;; ++n) {
+        const int k = q_read(n);
+        if (lane == 0) q_release(n);
+        if (k < 0) break;
+        Item it;
+        decode_item<TRANS>(a, k, crank, it);
+        if (it.ntiles == 0) continue;
+        const int buf = mi & 1;
+        mbar_wait(&tempty[buf], ((mi >> 1) & 1) ^ 1);
+        tc_fence_after();
+        for (int t = 0; t < it.ntiles; ++t, ++gt) {
+          const int slot = gt % MM_STAGES;
+          mbar_wait(&full[slot], (gt / MM_STAGES) & 1);
+          tc_fence_after();
+          const uint32_t sa = base + slot * MM_STAGE_BYTES, sb = sa + MM_A_BYTES;
+          if (elect_one()) {
+#pragma unroll
+            for (int kk = 0; kk < BC / 16; ++kk) {
+              const uint64_t ad = M2 == MM_DQ ? desc_sw128(sa + kk * 2048, MM_A_BYTES / 2, 1024)
+                                              : desc_sw128(sa + kk * 32, 16, 1024);
+              mma_bf16_ss_2sm(tm + buf * DH, ad, desc_sw128(sb + kk * 2048, MM_B_BYTES / 2, 1024), idesc,
+                              (t > 0 || kk > 0) ? 1u : 0u);
+            }
+            mma_commit_2sm_mc(&empty[slot], 0x3);
+            if (t + 1 == it.ntiles) mma_commit_2sm_mc(&tfull[buf], 0x3);
+          }
+          __syncwarp();
+        }
+        ++mi;
+      }
+    }
+  } else if (warp == 2) {
+    // ---------------------------------------------------------------- SiLU' source tile loader
+    if (lane == 0) {
+      int idx = 0;
+      for (int n = 0;; ++n) {
+        const int k = q_read(n);
+        q_release(n);
+        if (k < 0) break;
+        Item it;
+        decode_item<TRANS>(a, k, crank, it);
+        if (a.uu != nullptr) {
+          if (idx > 0) mbar_wait(epi_free, (idx - 1) & 1);
+          mbar_expect_tx(eu_full, RT_BYTES);
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            tma_load_2d(smem + MM_OFF_EPI + c * (RT_BYTES / 4), &tmU, eu_full, it.hcol + c * 64, it.us.off + it.r0);
+        }
+        ++idx;
+      }
+    }
+  } else if (warp >= 4) {
+    // ---------------------------------------------------------------- epilogue
+    const int q = warp & 3;
+    const int half = (warp - 4) >> 2;
+    const int row = q * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+    int mi = 0, idx = 0;
+    for (int n = 0;; ++n) {
+      const int k = q_read(n);
+      __syncwarp();
+      if (lane == 0) q_release(n);
+      if (k < 0) break;
+      Item it;
+      decode_item<TRANS>(a, k, crank, it);
+      const UserSpan& us = it.us;
+      const int my = it.r0 + row;
+      const int64_t g = (int64_t)us.off + my;
+      const bool has_acc = it.ntiles > 0;
+      const int buf = mi & 1;
+      if (has_acc) {
+        mbar_wait(&tfull[buf], (mi >> 1) & 1);
+        tc_fence_after();
+      }
+      const uint32_t tacc = tmem + buf * DH + half * 128 + lane_off;
+      const bool row_ok = my < us.L;
+      const bool has_e = row_ok && my >= it.kv_end;  // candidate rows: diagonal term (R#9)
+      const float dg = has_e ? a.diag[g * a.H + it.h] : 0.f;
+      const __nv_bfloat16* erow = a.e + g * a.ld_e + it.hcol + half * 128;
+      const int nrows = min(BR, us.L - it.r0);
+      const bool full_chunk = q * 32 + 32 <= nrows;
+      const int row0 = us.off + it.r0;
+      uint8_t* epi = smem + MM_OFF_EPI;
+      if (a.uu != nullptr) mbar_wait(eu_full, idx & 1);
+      uint32_t r[2][32];
+      if (has_acc) tmem_ld32(tacc, r[0]);
+#pragma unroll
+      for (int cc = 0; cc < 4; ++cc) {
+        const int acol = half * 128 + cc * 32;
+        uint32_t (&rc)[32] = r[cc & 1];
+        if (has_acc) {
+          tmem_ld_wait();
+          if (cc < 3) {
+            tmem_ld32(tacc + (cc + 1) * 32, r[(cc + 1) & 1]);
+          } else {  // the whole accumulator is in registers: the next item may overwrite it
+            tc_fence_before();
+            arrive_leader(&tempty[buf]);
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) rc[i] = 0u;
+        }
+        const int bx = acol >> 6, j0 = (acol & 63) >> 3;
+        uint8_t* box = epi + bx * (RT_BYTES / 4);
+        float v[32];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const uint32_t off = sw128(row, j0 + i);
+          uint4 ew = make_uint4(0u, 0u, 0u, 0u);
+          if (has_e) ew = __ldg(reinterpret_cast<const uint4*>(erow + cc * 32 + 8 * i));
+          uint4 uw = make_uint4(0u, 0u, 0u, 0u);
+          if (a.uu != nullptr) uw = *reinterpret_cast<const uint4*>(box + off);
+          const __nv_bfloat162* eh = reinterpret_cast<const __nv_bfloat162*>(&ew);
+          const __nv_bfloat162* uh = reinterpret_cast<const __nv_bfloat162*>(&uw);
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            const float2 fe = __bfloat1622float2(eh[kk]);
+            float x0 = fmaf(us.nu, __uint_as_float(rc[8 * i + 2 * kk]), dg * fe.x);
+            float x1 = fmaf(us.nu, __uint_as_float(rc[8 * i + 2 * kk + 1]), dg * fe.y);
+            if (a.uu != nullptr) {
+              const float2 fu = __bfloat1622float2(uh[kk]);
+              x0 *= a.pre_dsilu ? fu.x : dsilu_fast(fu.x);
+              x1 *= a.pre_dsilu ? fu.y : dsilu_fast(fu.y);
+            }
+            v[8 * i + 2 * kk] = x0;
+            v[8 * i + 2 * kk + 1] = x1;
+          }
+          *reinterpret_cast<uint4*>(box + off) =
+              make_uint4(pack2(v[8 * i], v[8 * i + 1]), pack2(v[8 * i + 2], v[8 * i + 3]),
+                         pack2(v[8 * i + 4], v[8 * i + 5]), pack2(v[8 * i + 6], v[8 * i + 7]));
+        }
+        if (cc & 1) {
+          if (full_chunk) {
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_2d(&tmO, box + q * 32 * 128, it.hcol + bx * 64, row0 + q * 32);
+              tma_store_commit();
+            }
+          } else {
+            __syncwarp();
+            for (int rr = q * 32 + (lane >> 3); rr < nrows; rr += 4) {
+              const int64_t go = (int64_t)(row0 + rr) * a.ld_out + it.hcol + bx * 64 + (lane & 7) * 8;
+              *reinterpret_cast<uint4*>(a.out + go) = *reinterpret_cast<const uint4*>(box + sw128(rr, lane & 7));
+            }
+          }
+        }
+      }
+      if (has_acc) ++mi;
+      if (a.dbias != nullptr) {
+        // bias gradient: column sums of the stored outputs, read back from the epilogue tile
+        named_bar_sync(1, 32 * NSM);
+        const int sw = warp - 4, bx = lane >> 3, jj = lane & 7;
+        float cs[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        const uint8_t* cbox = epi + bx * (RT_BYTES / 4);
+        for (int rr = sw; rr < nrows; rr += NSM) {
+          const uint4 w = *reinterpret_cast<const uint4*>(cbox + sw128(rr, jj));
+          const __nv_bfloat162* hh = reinterpret_cast<const __nv_bfloat162*>(&w);
+#pragma unroll
+          for (int k2 = 0; k2 < 4; ++k2) {
+            const float2 f = __bfloat1622float2(hh[k2]);
+            cs[2 * k2] += f.x;
+            cs[2 * k2 + 1] += f.y;
+          }
+        }
+        float* red = reinterpret_cast<float*>(smem + MM_OFF_RED);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) red[sw * DH + lane * 8 + e] = cs[e];
+        named_bar_sync(1, 32 * NSM);
+        const int col = threadIdx.x - 128;
+        float sum = 0.f;
+#pragma unroll
+        for (int w2 = 0; w2 < NSM; ++w2) sum += red[w2 * DH + col];
+        if (sum != 0.f) atomicAdd(a.dbias + it.hcol + col, sum);
+        named_bar_sync(1, 32 * NSM);
+      }
+      if (lane == 0) tma_store_wait_read<0>();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(epi_free);
+      ++idx;
+    }
+  }
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc_2sm<512>(tmem);
+  }
+}
+
+// Padded key-row offsets of the stored scores: user u owns rows [koff[u], koff[u+1]) of every
+// head's slab, koff[u+1] - koff[u] = 256 * ceil((n_static + n_rt) / 256) (the key pairs the DK
+// kernel visits).  One block, sequential over chunks of 1024 users.
+__global__ void attn_koff_kernel(mtgr_jagged_t j, int* koff) {
+  __shared__ int wsum[32];
+  __shared__ int carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int base = 0; base < j.num_users; base += 1024) {
+    const int u = base + threadIdx.x;
+    const int v = u < j.num_users ? ((j.n_static[u] + j.n_rt[u] + 2 * BR - 1) / (2 * BR)) * (2 * BR) : 0;
+    int x = v;  // inclusive warp scan
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if ((threadIdx.x & 31) >= o) x += y;
+    }
+    if ((threadIdx.x & 31) == 31) wsum[threadIdx.x >> 5] = x;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      int w = wsum[threadIdx.x];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, w, o);
+        if (threadIdx.x >= o) w += y;
+      }
+      wsum[threadIdx.x] = w;
+    }
+    __syncthreads();
+    const int incl = carry + x + ((threadIdx.x >> 5) > 0 ? wsum[(threadIdx.x >> 5) - 1] : 0);
+    if (u < j.num_users) koff[u + 1] = incl;
+    if (base == 0 && threadIdx.x == 0) koff[0] = 0;
+    __syncthreads();
+    if (threadIdx.x == 1023) carry = incl;
+    __syncthreads();
+  }
+}
+
 static int num_sms_cached() {
   static int n = 0;
   if (n == 0) {
@@ -876,9 +1302,68 @@ static mtgr_status_t launch_mode(const AttnIO& io, const void* c1, int64_t ld_c1
   return check_launch("attn_tc");
 }
 
+// Stored-score scratch: koff [B+1] int32, then P^T and dS^T, each [H][rows][pitch] bf16 with
+// rows = T + 256 B (>= sum_u 256 ceil(kv_u / 256)) and pitch = 256 ceil(max_len / 256).
+struct MmLayout {
+  int64_t pitch = 0, rows = 0;
+  size_t koff = 0, p = 0, ds = 0, total = 0;
+};
+static MmLayout mm_layout(const mtgr_jagged_t& j, int H) {
+  MmLayout l;
+  l.pitch = (int64_t)ceil_div(std::max(j.max_len, 1), 2 * BR) * 2 * BR;
+  l.rows = (int64_t)j.total_tokens + (int64_t)2 * BR * j.num_users;
+  const size_t mat = (size_t)H * l.rows * l.pitch * 2;
+  l.koff = 0;
+  l.p = ((size_t)(j.num_users + 1) * 4 + 1023) / 1024 * 1024;
+  l.ds = l.p + (mat + 1023) / 1024 * 1024;
+  l.total = l.ds + (mat + 1023) / 1024 * 1024;
+  return l;
+}
+
+template <int M2>
+static mtgr_status_t launch_mm(const AttnIO& io, const void* amat, const void* b, int64_t ld_b,
+                               const void* e, int64_t ld_e, const void* uu, int64_t ld_u,
+                               const MmLayout& l, const Args& args, cudaStream_t st) {
+  const int T = io.jag.total_tokens, d = io.d;
+  CUtensorMap ta, tb, tu, to;
+  MTGR_TRY(make_tmap_bf16(&ta, amat, (uint64_t)l.pitch, (uint64_t)io.H * l.rows, (uint64_t)l.pitch, 64,
+                          M2 == MM_DV ? BR : BC));
+  MTGR_TRY(make_tmap_bf16(&tb, b, d, T, ld_b, 64, BC));
+  if (uu) MTGR_TRY(make_tmap_bf16(&tu, uu, d, T, ld_u, 64, BR)); else tu = tb;
+  MTGR_TRY(make_tmap_bf16(&to, args.out, d, T, args.ld_out, 64, 32));
+  Args a2 = args;
+  a2.e = (const __nv_bfloat16*)e; a2.ld_e = ld_e;
+  a2.uu = (const __nv_bfloat16*)uu; a2.ld_u = ld_u;
+  a2.pre_dsilu = io.pre_dsilu;
+  a2.pmax = ceil_div(io.jag.max_len, 2 * BR);
+  a2.nitems = io.jag.num_users * a2.pmax * io.H;
+  a2.st_pitch = l.pitch; a2.st_rows = l.rows;
+  a2.c_align = 1;
+  static int* ctr = nullptr;
+  if (ctr == nullptr) {
+    if (cudaMalloc(&ctr, 2 * sizeof(int)) != cudaSuccess) return set_error(MTGR_E_CUDA, "attention work counter");
+  }
+  a2.ctr = ctr + M2;
+  cudaMemsetAsync(a2.ctr, 0, sizeof(int), st);
+  const int pairs = std::max(1, std::min(num_sms_cached() / 2, a2.nitems));
+  ProfScope ps(M2 == MM_DV ? PROF_ATTN_DV : PROF_ATTN_DQ, st);
+  cudaFuncSetAttribute(attn_mm_kernel<M2>, cudaFuncAttributeMaxDynamicSharedMemorySize, MM_SMEM_BYTES);
+  attn_mm_kernel<M2><<<2 * pairs, 384, MM_SMEM_BYTES, st>>>(ta, tb, tu, to, a2);
+  return check_launch("attn_mm");
+}
+
 }  // namespace tca
 
 bool attn_tc_supported(int dh) { return dh == tca::DH; }
+
+size_t attn_store_ws_bytes(const mtgr_jagged_t& j, int H) {
+  if (j.num_users == 0 || j.total_tokens == 0) return 0;
+  const char* env = getenv("MTGR_ATTN_RECOMPUTE");  // tests / A-B: force the recompute kernels
+  if (env != nullptr && env[0] == '1') return 0;
+  const size_t b = tca::mm_layout(j, H).total;
+  // beyond this the backward recomputes the scores in the DV / DQ kernels instead
+  return b <= ((size_t)48 << 30) ? b : 0;
+}
 
 mtgr_status_t attn_tc_fwd_launch(const AttnIO& io, cudaStream_t st) {
   using namespace tca;
@@ -902,6 +1387,45 @@ mtgr_status_t attn_tc_bwd_launch(const AttnIO& io, cudaStream_t st) {
   typedef __nv_bfloat16 bf;
   const bf* pre = (const bf*)io.pre;
   const int64_t D = io.d;
+  const size_t need = attn_store_ws_bytes(io.jag, io.H);
+  if (need > 0 && io.mm_ws != nullptr && io.mm_ws_bytes >= need) {
+    // stored-score backward: DK computes S^T, dP^T once and writes P^T and dS^T; dV and dQ are
+    // then plain jagged GEMMs over them (no recomputation of S and dP)
+    const MmLayout l = mm_layout(io.jag, io.H);
+    char* ws = (char*)io.mm_ws;
+    int* koff = (int*)(ws + l.koff);
+    bf* sp = (bf*)(ws + l.p);
+    bf* sds = (bf*)(ws + l.ds);
+    attn_koff_kernel<<<1, 1024, 0, st>>>(io.jag, koff);
+    MTGR_TRY(check_launch("attn_koff"));
+    {  // dK = nu dS^T Q (+ diag), * silu'(p_K); also stores P^T, dS^T
+      Args a{};
+      a.jag = io.jag; a.H = io.H; a.d = io.d;
+      a.out = (bf*)io.dk; a.ld_out = io.ld_out; a.diag = io.diag_ds;
+      a.dbias = io.dbias ? io.dbias + D : nullptr;
+      a.st_p = sp; a.st_ds = sds; a.st_pitch = l.pitch; a.st_rows = l.rows; a.koff = koff;
+      a.c_align = 1;
+      MTGR_TRY(launch_mode<DK>(io, io.q, io.ld, io.dO, D, io.k, io.ld, io.v, io.ld, io.q, io.ld,
+                               pre ? pre + D : nullptr, io.ld_pre, a, st));
+    }
+    {  // dV = nu P^T dO (+ diag a_jj dO_j), * silu'(p_V)
+      Args a{};
+      a.jag = io.jag; a.H = io.H; a.d = io.d;
+      a.out = (bf*)io.dv; a.ld_out = io.ld_out; a.diag = io.diag_a;
+      a.dbias = io.dbias ? io.dbias + 2 * D : nullptr;
+      a.koff = koff;
+      MTGR_TRY(launch_mm<MM_DV>(io, sp, io.dO, D, io.dO, D, pre ? pre + 2 * D : nullptr, io.ld_pre, l, a, st));
+    }
+    {  // dQ = nu dS K (+ diag ds_ii k_i), * silu'(p_Q)
+      Args a{};
+      a.jag = io.jag; a.H = io.H; a.d = io.d;
+      a.out = (bf*)io.dq; a.ld_out = io.ld_out; a.diag = io.diag_ds;
+      a.dbias = io.dbias;
+      a.koff = koff;
+      MTGR_TRY(launch_mm<MM_DQ>(io, sds, io.k, io.ld, io.k, io.ld, pre, io.ld_pre, l, a, st));
+    }
+    return MTGR_OK;
+  }
   {  // dV = nu P^T dO (+ diag a_jj dO_j), * silu'(p_V): C1 = Q, X = dO, R1 = K, E = dO, U = p_V
     Args a{};
     a.jag = io.jag; a.H = io.H; a.d = io.d;

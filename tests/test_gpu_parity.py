@@ -105,8 +105,19 @@ def _attn_case(name, seed=0):
     return cfg, seg, ts, qkvu, dO
 
 
+@pytest.fixture(params=["stored", "recompute"])
+def bwd_path(request, monkeypatch):
+    """The tensor-core backward stores P^T / dS^T by default; MTGR_ATTN_RECOMPUTE=1 selects the
+    kernels that recompute the scores (the path used when the scratch would not fit)."""
+    if request.param == "recompute":
+        monkeypatch.setenv("MTGR_ATTN_RECOMPUTE", "1")
+    else:
+        monkeypatch.delenv("MTGR_ATTN_RECOMPUTE", raising=False)
+    return request.param
+
+
 @pytest.mark.parametrize("name", ["toy", "parity", "parity768"])
-def test_attention_fwd_bwd(dev, name):
+def test_attention_fwd_bwd(dev, name, bwd_path):
     cfg, seg, ts, qkvu, dO = _attn_case(name)
     dt = _dt(cfg)
     d, H = cfg["d"], cfg["H"]
@@ -186,7 +197,7 @@ def _compare(z, dx, grads, Z, dX, G, tol, rows=None):
 
 
 @pytest.mark.parametrize("name", ["toy", "parity", "parity768"])
-def test_layer_fwd_bwd(dev, name):
+def test_layer_fwd_bwd(dev, name, bwd_path):
     cfg, seg, ts, X, dZ, P = make_batch(name)
     z, dx, grads = _run_layer(dev, cfg, seg, ts, X, dZ, P)
     Z, dX, G = _oracle_stack(cfg, seg, ts, X, dZ, [P])
@@ -194,7 +205,7 @@ def test_layer_fwd_bwd(dev, name):
 
 
 @pytest.mark.parametrize("name", ["toy", "parity"])
-def test_layer_edge_cases(dev, name):
+def test_layer_edge_cases(dev, name, bwd_path):
     """Empty users, users without static / real-time / candidate segments, single tokens."""
     seg = np.array([[0, 0, 0, 0], [0, 0, 3, 2], [4, 3, 0, 0], [1, 0, 0, 1], [0, 0, 0, 1],
                     [2, 130, 0, 5], [0, 0, 0, 0], [3, 1, 140, 0], [1, 1, 1, 1]], np.int32)
