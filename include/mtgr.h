@@ -81,7 +81,12 @@ typedef struct {
                           s_ij += rab_w[h][min(NB-1, floor(log2(max(|ts_i-ts_j|,1))))]        */
   float eps;           /* LayerNorm epsilon (1e-6, R#14)                                     */
   int32_t qkvu_silu;   /* 1: Q,K,V,U = SiLU(X~ W1^T + b1) (R#5); 0: linear                   */
+  int32_t mask_mode;   /* MTGR_MASK_DYNAMIC (0): MTGR's dynamic mask (R#8-R#12).
+                          MTGR_MASK_CAUSAL (1): the plain causal mask over the packed order,
+                          m_ij = [j <= i] (HSTU's) -- the "w/o dynamic mask"
+                          ablation of Table 4.  Other values: MTGR_E_ARG.          */
 } mtgr_layer_cfg_t;
+enum { MTGR_MASK_DYNAMIC = 0, MTGR_MASK_CAUSAL = 1 };
 
 /* Parameters of one layer.  W1/W2 have the activation dtype; everything else fp32. */
 typedef struct {

@@ -21,7 +21,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from .gln import gln_fwd, gln_bwd
-from .mask import mask_dense, rab_bucket
+from .mask import mask_dense, mask_for, rab_bucket
 
 
 def silu(s):
@@ -42,13 +42,14 @@ def _heads(d, H):
     return [slice(h * dh, (h + 1) * dh) for h in range(H)]
 
 
-def attn_fwd_user(q, k, v, n_s, n_r, n_c, ts, H, nu, rab_w=None):
+def attn_fwd_user(q, k, v, n_s, n_r, n_c, ts, H, nu, rab_w=None, mask_mode="dynamic"):
     """Eq.5 per head h:  s_ij = q_i . k_j (+ rab),  A_ij = silu(s_ij) * m_ij * nu,  o_i = sum_j A_ij v_j.
 
     Masked entries are exact zeros (select, not multiply: R#2).  Returns (o, S list, M).
+    mask_mode: "dynamic" (MTGR) or "causal" (the Table 4 ablation).
     """
     L, d = q.shape
-    M = mask_dense(n_s, n_r, n_c, ts)
+    M = mask_for(mask_mode, n_s, n_r, n_c, ts)
     vis = M.astype(bool)
     o = np.zeros((L, d))
     S = []
@@ -116,7 +117,8 @@ def _f64(P):
 def layer_fwd_user(x, gid, n_s, n_r, n_c, ts, P, cfg, nu=None):
     """One HSTU layer for one user.  x [L][d]; P params (synth.gen_layer_params layout).
 
-    cfg: dict(d, H, eps=1e-6, qkvu_silu=True).  nu: 1/N override (default 1/L_u, R#3).
+    cfg: dict(d, H, eps=1e-6, qkvu_silu=True, mask_mode="dynamic").  nu: 1/N override (default
+    1/L_u, R#3).
     Returns (z [L][d], LayerCache).
     """
     P = _f64(P)
@@ -132,7 +134,8 @@ def layer_fwd_user(x, gid, n_s, n_r, n_c, ts, P, cfg, nu=None):
     p = xt @ P["W1"].T + P["b1"]
     a = silu(p) if cfg.get("qkvu_silu", True) else p.copy()
     q, k, v, u = a[:, :d], a[:, d:2 * d], a[:, 2 * d:3 * d], a[:, 3 * d:]
-    o, S, M = attn_fwd_user(q, k, v, n_s, n_r, n_c, ts, H, nu, P.get("rab_w"))  # Eq.5
+    o, S, M = attn_fwd_user(q, k, v, n_s, n_r, n_c, ts, H, nu, P.get("rab_w"),    # Eq.5
+                            cfg.get("mask_mode", "dynamic"))
     y = o * u                                                            # Eq.6 gate
     yt, mu2, r2 = gln_fwd(y, gid, P["gamma2"], P["beta2"], eps)          # Eq.6 GroupLN
     z = yt @ P["W2"].T + P["b2"] + x                                     # Eq.6 MLP + X

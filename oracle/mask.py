@@ -41,6 +41,30 @@ def mask_dense(n_s: int, n_r: int, n_c: int, ts: np.ndarray) -> np.ndarray:
     return m
 
 
+def mask_causal(L: int) -> np.ndarray:
+    """The plain causal mask over the packed order, m[i, j] = [j <= i]  (uint8 [L][L]).
+
+    HSTU's mask, which MTGR replaces ("utilizes the causal mask for sequence
+    modeling ... Using a simple causal mask in MTGR could result in information leakage");
+    Table 4's "w/o dynamic mask" ablation.  Candidates read every earlier candidate.
+    """
+    i = np.arange(L)[:, None]
+    j = np.arange(L)[None, :]
+    return (j <= i).astype(np.uint8)
+
+
+MASK_MODES = ("dynamic", "causal")
+
+
+def mask_for(mode: str, n_s: int, n_r: int, n_c: int, ts) -> np.ndarray:
+    """Mask of a user under `mode` (layer config mask_mode; include/mtgr.h MTGR_MASK_*)."""
+    if mode == "dynamic":
+        return mask_dense(n_s, n_r, n_c, ts)
+    if mode == "causal":
+        return mask_causal(n_s + n_r + n_c)
+    raise ValueError(mode)
+
+
 def mask_rules_pairwise(kinds, ts) -> np.ndarray:
     """Rule interpreter: evaluates the three textual rules pairwise from token kinds.
 

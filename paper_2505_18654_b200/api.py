@@ -109,8 +109,13 @@ class JaggedBatch:
                       None if self.inv_norm is None else self.inv_norm.data_ptr())
 
 
-def layer_cfg(d_model, n_heads, num_groups=4, rab_buckets=0, eps=1e-6, qkvu_silu=True) -> LayerCfg:
-    return LayerCfg(d_model, n_heads, num_groups, rab_buckets, eps, 1 if qkvu_silu else 0)
+MASK_MODES = {"dynamic": 0, "causal": 1}  # include/mtgr.h MTGR_MASK_*
+
+
+def layer_cfg(d_model, n_heads, num_groups=4, rab_buckets=0, eps=1e-6, qkvu_silu=True,
+              mask_mode="dynamic") -> LayerCfg:
+    return LayerCfg(d_model, n_heads, num_groups, rab_buckets, eps, 1 if qkvu_silu else 0,
+                    MASK_MODES[mask_mode])
 
 
 def validate_jagged(jb: JaggedBatch, num_groups: int):

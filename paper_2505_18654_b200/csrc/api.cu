@@ -55,6 +55,8 @@ static mtgr_status_t check_cfg(const mtgr_layer_cfg_t* c) {
   MTGR_CHECK(dh % 8 == 0 && dh <= 256, MTGR_E_UNSUPPORTED, "head dim %d must be a multiple of 8, <= 256", dh);
   MTGR_CHECK(c->rab_buckets >= 0 && c->rab_buckets <= 64, MTGR_E_ARG, "rab_buckets must be in [0, 64]");
   MTGR_CHECK(c->eps > 0.f, MTGR_E_ARG, "eps must be positive");
+  MTGR_CHECK(c->mask_mode == MTGR_MASK_DYNAMIC || c->mask_mode == MTGR_MASK_CAUSAL, MTGR_E_ARG,
+             "mask_mode must be MTGR_MASK_DYNAMIC or MTGR_MASK_CAUSAL");
   return MTGR_OK;
 }
 
@@ -142,7 +144,8 @@ static mtgr_status_t run_attn_fwd(const AttnIO& a, float* diag, cudaStream_t st)
   const bool tc = std::is_same<T, __nv_bfloat16>::value && a.nb == 0 && attn_tc_supported(a.dh);
   AttnIO b = a;
   b.diag_cand_only = tc;  // the tensor-core path adds real-time diagonals inside its tile loop
-  MTGR_TRY(attn_diag_launch<T>(b, false, diag, nullptr, st));
+  // causal: every diagonal entry is inside the key range of the tile loops (no diagonal terms)
+  if (!a.causal) MTGR_TRY(attn_diag_launch<T>(b, false, diag, nullptr, st));
   b.diag_a = diag;
   if (tc) return attn_tc_fwd_launch(b, st);
   return attn_simt_fwd_launch<T>(b, st);
@@ -153,7 +156,7 @@ static mtgr_status_t run_attn_bwd(const AttnIO& a, float* diag_a, float* diag_ds
   const bool tc = std::is_same<T, __nv_bfloat16>::value && a.nb == 0 && attn_tc_supported(a.dh);
   AttnIO b = a;
   b.diag_cand_only = tc;
-  MTGR_TRY(attn_diag_launch<T>(b, true, diag_a, diag_ds, st));
+  if (!a.causal) MTGR_TRY(attn_diag_launch<T>(b, true, diag_a, diag_ds, st));
   b.diag_a = diag_a;
   b.diag_ds = diag_ds;
   if (tc) return attn_tc_bwd_launch(b, st);
@@ -190,7 +193,7 @@ static mtgr_status_t layer_fwd_t(const mtgr_layer_cfg_t* c, const mtgr_jagged_t*
   MTGR_TRY(run_gemm<T>(g, EPI_QKVU, gws, gws_bytes, st));
   // O = silu(Q K^T)/N (.) M V  (Eq.5); the gate Y = O (.) U (Eq.6) is formed inside GLN2
   AttnIO at{};
-  at.jag = *j; at.H = c->n_heads; at.dh = d / c->n_heads; at.d = d; at.nb = c->rab_buckets;
+  at.jag = *j; at.causal = c->mask_mode == MTGR_MASK_CAUSAL; at.H = c->n_heads; at.dh = d / c->n_heads; at.d = d; at.nb = c->rab_buckets;
   at.q = a; at.k = a + d; at.v = a + 2 * d; at.ld = 4 * d;
   at.o = o; at.u = nullptr; at.y = nullptr; at.rab_w = P->rab_w;  // gate folded into GLN2
   MTGR_TRY(run_attn_fwd<T>(at, diag, st));
@@ -272,7 +275,7 @@ static mtgr_status_t layer_bwd_t(const mtgr_layer_cfg_t* c, const mtgr_jagged_t*
   MTGR_TRY(gln_bwd_launch<T>(gi, GLNB_GATE, (float*)scratch, G->gamma2, G->beta2, acc, st));
   // attention backward (+ silu' of Q, K, V) into dp[:, 0:3d]
   AttnIO at{};
-  at.jag = *j; at.H = H; at.dh = d / H; at.d = d; at.nb = c->rab_buckets;
+  at.jag = *j; at.causal = c->mask_mode == MTGR_MASK_CAUSAL; at.H = H; at.dh = d / H; at.d = d; at.nb = c->rab_buckets;
   at.q = a; at.k = a + d; at.v = a + 2 * d; at.ld = 4 * d;
   at.dO = dO; at.pre = c->qkvu_silu ? p : nullptr; at.ld_pre = 4 * d; at.pre_dsilu = 1;
   at.dq = dp; at.dk = dp + d; at.dv = dp + 2 * d; at.ld_out = 4 * d;
@@ -422,7 +425,7 @@ MTGR_API mtgr_status_t mtgr_hstu_attn_fwd(const mtgr_layer_cfg_t* cfg, const mtg
   MTGR_CHECK(aligned16(q) && aligned16(k) && aligned16(v) && aligned16(o) && (!u || aligned16(u)),
              MTGR_E_LAYOUT, "attn_fwd: pointers must be 16-byte aligned");
   AttnIO at{};
-  at.jag = *jag; at.H = cfg->n_heads; at.dh = cfg->d_model / cfg->n_heads; at.d = cfg->d_model;
+  at.jag = *jag; at.causal = cfg->mask_mode == MTGR_MASK_CAUSAL; at.H = cfg->n_heads; at.dh = cfg->d_model / cfg->n_heads; at.d = cfg->d_model;
   at.nb = cfg->rab_buckets; at.q = q; at.k = k; at.v = v; at.ld = ld; at.u = u; at.o = o; at.y = y;
   at.rab_w = rab_w;
   cudaStream_t st = (cudaStream_t)stream;
@@ -448,7 +451,7 @@ MTGR_API mtgr_status_t mtgr_hstu_attn_bwd(const mtgr_layer_cfg_t* cfg, const mtg
              MTGR_E_LAYOUT, "attn_bwd: pointers must be 16-byte aligned");
   const size_t half = attn_ws_bytes(jag->total_tokens, cfg->n_heads) / 2;
   AttnIO at{};
-  at.jag = *jag; at.H = cfg->n_heads; at.dh = cfg->d_model / cfg->n_heads; at.d = cfg->d_model;
+  at.jag = *jag; at.causal = cfg->mask_mode == MTGR_MASK_CAUSAL; at.H = cfg->n_heads; at.dh = cfg->d_model / cfg->n_heads; at.d = cfg->d_model;
   at.nb = cfg->rab_buckets; at.q = q; at.k = k; at.v = v; at.ld = ld; at.dO = dO;
   at.pre = silu_pre; at.ld_pre = ld; at.dq = dq; at.dk = dk; at.dv = dv; at.ld_out = ld_out;
   at.rab_w = rab_w; at.drab = drab_w;

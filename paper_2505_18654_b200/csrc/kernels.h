@@ -51,6 +51,7 @@ mtgr_status_t gemm_bf16_launch(const GemmIO& g, int epi, void* ws, size_t ws_byt
 // ------------------------------------------------------------------ attention
 struct AttnIO {
   mtgr_jagged_t jag;
+  int causal;                  // mask mode MTGR_MASK_CAUSAL: m_ij = [j <= i] (else dynamic)
   int H, dh, d, nb;            // heads, head dim, d_model, rab buckets (0 = off)
   const void* q; const void* k; const void* v; int64_t ld;
   const void* u;               // gate or NULL

@@ -211,7 +211,7 @@ __global__ void __launch_bounds__(256) attn_simt_fwd_kernel(AttnIO a) {
   const int i0 = blockIdx.x * SA_B;
   if (i0 >= us.L) return;
   const int nq = min(SA_B, us.L - i0);
-  const int kv_end = (i0 + nq > us.ns) ? us.ns + us.nr : us.ns;
+  const int kv_end = a.causal ? min(us.L, i0 + nq) : ((i0 + nq > us.ns) ? us.ns + us.nr : us.ns);
   const int r = threadIdx.x / 8, cg = threadIdx.x % 8;
   const int i = i0 + r;
   const int64_t col0 = (int64_t)h * dh;
@@ -237,7 +237,7 @@ __global__ void __launch_bounds__(256) attn_simt_fwd_kernel(AttnIO a) {
       int j = j0 + jj;
       float s = 0.f;
       for (int c = 0; c < dh; ++c) s = fmaf(Qs[r * dh + c], Ks[jj * dh + c], s);
-      bool vis = i < us.L && jj < nk && visible_offdiag(i, j, us.ns, ts_i, tsk[jj]);
+      bool vis = i < us.L && jj < nk && (a.causal ? j <= i : visible_offdiag(i, j, us.ns, ts_i, tsk[jj]));
       if (a.nb > 0) s += a.rab_w[h * a.nb + rab_bucket(ts_i - tsk[jj], a.nb)];
       Ps[r * (SA_B + 1) + jj] = vis ? silu_f(s) : 0.f;
     }
@@ -251,7 +251,7 @@ __global__ void __launch_bounds__(256) attn_simt_fwd_kernel(AttnIO a) {
   }
   if (i >= us.L) return;
   const int64_t t = us.off + i;
-  const float da = i >= us.ns ? a.diag_a[t * a.H + h] : 0.f;
+  const float da = (!a.causal && i >= us.ns) ? a.diag_a[t * a.H + h] : 0.f;
 #pragma unroll
   for (int c = 0; c < 32; ++c) {
     if (c >= ncol) break;
@@ -280,7 +280,8 @@ __global__ void __launch_bounds__(256) attn_simt_dkv_kernel(AttnIO a) {
   const int j0 = blockIdx.x * SA_B;
   if (j0 >= us.L) return;
   const int nk = min(SA_B, us.L - j0);
-  const int key_end = us.ns + us.nr;  // candidate keys only ever meet the diagonal
+  // dynamic: candidate keys only ever meet the diagonal; causal: every key up to the end
+  const int key_end = a.causal ? us.L : us.ns + us.nr;
   const int r = threadIdx.x / 8, cg = threadIdx.x % 8;
   const int j = j0 + r;
   const int64_t col0 = (int64_t)h * dh;
@@ -294,7 +295,7 @@ __global__ void __launch_bounds__(256) attn_simt_dkv_kernel(AttnIO a) {
 #pragma unroll
   for (int c = 0; c < 32; ++c) accv[c] = acck[c] = 0.f;
   const int ncol = dh / 8;
-  const int q_begin = (j0 < us.ns) ? 0 : us.ns;
+  const int q_begin = a.causal ? j0 : ((j0 < us.ns) ? 0 : us.ns);
   const int q_end = (j0 < key_end) ? us.L : 0;
   for (int i0 = q_begin; i0 < q_end; i0 += SA_B) {
     const int nq = min(SA_B, us.L - i0);
@@ -313,7 +314,7 @@ __global__ void __launch_bounds__(256) attn_simt_dkv_kernel(AttnIO a) {
         s = fmaf(Qs[ii * dh + c], Ks[r * dh + c], s);
         dp = fmaf(Ds[ii * dh + c], Vs[r * dh + c], dp);
       }
-      bool vis = ii < nq && j < key_end && visible_offdiag(i, j, us.ns, tsq[ii], ts_j);
+      bool vis = ii < nq && j < key_end && (a.causal ? i >= j : visible_offdiag(i, j, us.ns, tsq[ii], ts_j));
       int bk = 0;
       if (a.nb > 0) { bk = rab_bucket(tsq[ii] - ts_j, a.nb); s += a.rab_w[h * a.nb + bk]; }
       float ds = vis ? dp * dsilu_f(s) : 0.f;
@@ -338,8 +339,8 @@ __global__ void __launch_bounds__(256) attn_simt_dkv_kernel(AttnIO a) {
       if (rab_acc[e] != 0.f) atomicAdd(&a.drab[h * a.nb + e], us.nu * rab_acc[e]);
   if (j >= us.L) return;
   const int64_t t = us.off + j;
-  const float da = j >= us.ns ? a.diag_a[t * a.H + h] : 0.f;
-  const float dd = j >= us.ns ? a.diag_ds[t * a.H + h] : 0.f;
+  const float da = (!a.causal && j >= us.ns) ? a.diag_a[t * a.H + h] : 0.f;
+  const float dd = (!a.causal && j >= us.ns) ? a.diag_ds[t * a.H + h] : 0.f;
   const T* pre = (const T*)a.pre;
 #pragma unroll
   for (int c = 0; c < 32; ++c) {
@@ -374,7 +375,7 @@ __global__ void __launch_bounds__(256) attn_simt_dq_kernel(AttnIO a) {
   const int i0 = blockIdx.x * SA_B;
   if (i0 >= us.L) return;
   const int nq = min(SA_B, us.L - i0);
-  const int kv_end = (i0 + nq > us.ns) ? us.ns + us.nr : us.ns;
+  const int kv_end = a.causal ? min(us.L, i0 + nq) : ((i0 + nq > us.ns) ? us.ns + us.nr : us.ns);
   const int r = threadIdx.x / 8, cg = threadIdx.x % 8;
   const int i = i0 + r;
   const int64_t col0 = (int64_t)h * dh;
@@ -404,7 +405,7 @@ __global__ void __launch_bounds__(256) attn_simt_dq_kernel(AttnIO a) {
         s = fmaf(Qs[r * dh + c], Ks[jj * dh + c], s);
         dp = fmaf(Ds[r * dh + c], Vs[jj * dh + c], dp);
       }
-      bool vis = i < us.L && jj < nk && visible_offdiag(i, j, us.ns, ts_i, tsk[jj]);
+      bool vis = i < us.L && jj < nk && (a.causal ? j <= i : visible_offdiag(i, j, us.ns, ts_i, tsk[jj]));
       if (a.nb > 0) s += a.rab_w[h * a.nb + rab_bucket(ts_i - tsk[jj], a.nb)];
       Ss[r * (SA_B + 1) + jj] = vis ? dp * dsilu_f(s) : 0.f;
     }
@@ -418,7 +419,7 @@ __global__ void __launch_bounds__(256) attn_simt_dq_kernel(AttnIO a) {
   }
   if (i >= us.L) return;
   const int64_t t = us.off + i;
-  const float dd = i >= us.ns ? a.diag_ds[t * a.H + h] : 0.f;
+  const float dd = (!a.causal && i >= us.ns) ? a.diag_ds[t * a.H + h] : 0.f;
   const T* pre = (const T*)a.pre;
 #pragma unroll
   for (int c = 0; c < 32; ++c) {

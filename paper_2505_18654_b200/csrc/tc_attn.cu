@@ -72,6 +72,7 @@ struct Args {
   __nv_bfloat16* st_ds;                     // dS^T = dP^T silu'(S^T) m  (DK writes, or NULL)
   int64_t st_pitch, st_rows;
   const int* koff;                          // [B+1] padded key-row offsets (multiples of 256)
+  int causal;                               // MTGR_MASK_CAUSAL: m_ij = [j <= i]
   int c_align;                              // TRANS items of real-time keys start their query
                                             // range at the 256-aligned pair holding n_static
 };
@@ -117,11 +118,16 @@ __device__ __forceinline__ bool decode_item(const Args& a, int k, uint32_t crank
   if (it.pr0 >= it.us.L) return false;
   it.r0 = it.pr0 + (int)crank * BR;
   it.hcol = it.h * DH;
-  it.kv_end = it.us.ns + it.us.nr;
+  // keys that can be visible to some row (beyond them only the candidates' own diagonal):
+  // dynamic mask [0, ns + nr); causal mask every key
+  it.kv_end = a.causal ? it.us.L : it.us.ns + it.us.nr;
   const int pair_end = min(it.us.L, it.pr0 + 2 * BR);
   int c_end = 0;
   it.c_begin = 0;
-  if (!TRANS) {
+  if (a.causal) {  // keys [0, pair_end) of a query pair; queries [pr0, L) of a key pair
+    if (!TRANS) c_end = pair_end;
+    else { it.c_begin = it.pr0; c_end = it.us.L; }
+  } else if (!TRANS) {
     c_end = (pair_end > it.us.ns) ? it.kv_end : it.us.ns;
   } else if (it.pr0 < it.kv_end) {
     // keys that only non-static queries read.  With c_align the range starts at the query pair
@@ -581,11 +587,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
         const long long my_ts = (my < us.L && a.jag.ts) ? a.jag.ts[g] : 0;
         // stored-score row of this key (DK): [h][koff[u] + my][query]
         const int64_t st_row = store_scores ? ((int64_t)it.h * a.st_rows + a.koff[it.u] + my) * a.st_pitch : 0;
-        const bool need_ts_rows = TRANS && (it.r0 + BR > us.ns) && (it.r0 < it.kv_end);
+        const bool need_ts_rows = TRANS && !a.causal && (it.r0 + BR > us.ns) && (it.r0 < it.kv_end);
 #pragma unroll 1
         for (int t = 0; t < it.ntiles; ++t, ++gt) {
           const int c0 = it.c_begin + t * BC;
-          const bool need_ts = TRANS ? need_ts_rows : (c0 + BC > us.ns && c0 < it.kv_end);
+          const bool need_ts = TRANS ? need_ts_rows : (!a.causal && c0 + BC > us.ns && c0 < it.kv_end);
           long long* tsb = sTs;
           if (need_ts) {  // uniform over the 8 softmax warps
             const int i = threadIdx.x - 128;
@@ -608,7 +614,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
           // visibility of this warp's 32 columns for this row (dynamic mask, R#8-R#12)
           const int cb = c0 + j_half;
           uint32_t vis;
-          if (!TRANS) {
+          if (a.causal) {
+            // causal (uniform branch): row i reads keys j <= i (rows are readers for !TRANS,
+            // keys for TRANS, whose columns are the queries i >= j, i < L)
+            const int lo = TRANS ? min(max(my - cb, 0), 32) : 0;
+            const int hi = TRANS ? min(max(us.L - cb, 0), 32) : min(max(my - cb + 1, 0), 32);
+            const uint32_t below_hi = hi >= 32 ? 0xffffffffu : ((1u << hi) - 1u);
+            const uint32_t below_lo = lo >= 32 ? 0xffffffffu : ((1u << lo) - 1u);
+            vis = (my < us.L) ? (below_hi & ~below_lo) : 0u;
+          } else if (!TRANS) {
             // static columns [0, ns) are visible to every row; real-time columns [ns, kv_end)
             // only to non-static rows with an earlier timestamp (diagonal: epilogue)
             const int n_stat = min(max(us.ns - cb, 0), 32);
@@ -1194,15 +1208,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
 
 // Padded key-row offsets of the stored scores: user u owns rows [koff[u], koff[u+1]) of every
 // head's slab, koff[u+1] - koff[u] = 256 * ceil((n_static + n_rt) / 256) (the key pairs the DK
-// kernel visits).  One block, sequential over chunks of 1024 users.
-__global__ void attn_koff_kernel(mtgr_jagged_t j, int* koff) {
+// kernel visits; causal: 256 * ceil(L / 256)).  One block, sequential over chunks of 1024 users.
+__global__ void attn_koff_kernel(mtgr_jagged_t j, int causal, int* koff) {
   __shared__ int wsum[32];
   __shared__ int carry;
   if (threadIdx.x == 0) carry = 0;
   __syncthreads();
   for (int base = 0; base < j.num_users; base += 1024) {
     const int u = base + threadIdx.x;
-    const int v = u < j.num_users ? ((j.n_static[u] + j.n_rt[u] + 2 * BR - 1) / (2 * BR)) * (2 * BR) : 0;
+    const int kv = u < j.num_users ? (causal ? j.offsets[u + 1] - j.offsets[u] : j.n_static[u] + j.n_rt[u]) : 0;
+    const int v = ((kv + 2 * BR - 1) / (2 * BR)) * (2 * BR);
     int x = v;  // inclusive warp scan
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -1269,6 +1284,7 @@ static mtgr_status_t launch_mode(const AttnIO& io, const void* c1, int64_t ld_c1
   if (uu) MTGR_TRY(make_tmap_bf16(&m.u, uu, d, T, ld_u, 64, BR)); else m.u = m.e;
   MTGR_TRY(make_tmap_bf16(&m.o, args.out, d, T, args.ld_out, 64, 32));
   Args a2 = args;
+  a2.causal = io.causal;
   a2.e = (const __nv_bfloat16*)e; a2.ld_e = ld_e;
   a2.uu = (const __nv_bfloat16*)uu; a2.ld_u = ld_u;
   a2.pre_dsilu = io.pre_dsilu;
@@ -1332,6 +1348,7 @@ static mtgr_status_t launch_mm(const AttnIO& io, const void* amat, const void* b
   if (uu) MTGR_TRY(make_tmap_bf16(&tu, uu, d, T, ld_u, 64, BR)); else tu = tb;
   MTGR_TRY(make_tmap_bf16(&to, args.out, d, T, args.ld_out, 64, 32));
   Args a2 = args;
+  a2.causal = io.causal;
   a2.e = (const __nv_bfloat16*)e; a2.ld_e = ld_e;
   a2.uu = (const __nv_bfloat16*)uu; a2.ld_u = ld_u;
   a2.pre_dsilu = io.pre_dsilu;
@@ -1396,7 +1413,7 @@ mtgr_status_t attn_tc_bwd_launch(const AttnIO& io, cudaStream_t st) {
     int* koff = (int*)(ws + l.koff);
     bf* sp = (bf*)(ws + l.p);
     bf* sds = (bf*)(ws + l.ds);
-    attn_koff_kernel<<<1, 1024, 0, st>>>(io.jag, koff);
+    attn_koff_kernel<<<1, 1024, 0, st>>>(io.jag, io.causal, koff);
     MTGR_TRY(check_launch("attn_koff"));
     {  // dK = nu dS^T Q (+ diag), * silu'(p_K); also stores P^T, dS^T
       Args a{};

@@ -52,6 +52,9 @@ def test_host_side_argument_errors():
     ok = LayerCfg(64, 2, 4, 0, 1e-6, 1)
     assert L.mtgr_gln_fwd(ctypes.byref(ok), ctypes.byref(j), 7, None, None, None, None, None, None, None) == 4
     assert b"dtype" in L.mtgr_last_error()
+    badmask = LayerCfg(64, 2, 4, 0, 1e-6, 1, 7)  # mask_mode must be MTGR_MASK_DYNAMIC / _CAUSAL
+    assert L.mtgr_gln_fwd(ctypes.byref(badmask), ctypes.byref(j), 0, None, None, None, None, None, None, None) == 1
+    assert b"mask_mode" in L.mtgr_last_error()
 
 
 @pytest.mark.parametrize("seed", range(10))

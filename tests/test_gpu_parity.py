@@ -116,13 +116,14 @@ def bwd_path(request, monkeypatch):
     return request.param
 
 
+@pytest.mark.parametrize("mask", ["dynamic", "causal"])
 @pytest.mark.parametrize("name", ["toy", "parity", "parity768"])
-def test_attention_fwd_bwd(dev, name, bwd_path):
+def test_attention_fwd_bwd(dev, name, bwd_path, mask):
     cfg, seg, ts, qkvu, dO = _attn_case(name)
     dt = _dt(cfg)
     d, H = cfg["d"], cfg["H"]
     jb = m.JaggedBatch.build(seg, ts, dev)
-    lc = m.layer_cfg(d, H)
+    lc = m.layer_cfg(d, H, mask_mode=mask)
     a = _t(qkvu, dev, dt)
     o, y = m.attn_fwd(lc, jb, a[:, 0:], a[:, d:], a[:, 2 * d:], 4 * d, u=a[:, 3 * d:])
     dq, dk, dv, _ = m.attn_bwd(lc, jb, _t(dO, dev, dt), a[:, 0:], a[:, d:], a[:, 2 * d:], 4 * d)
@@ -135,7 +136,7 @@ def test_attention_fwd_bwd(dev, name, bwd_path):
         ns, nr, nc = int(h["n_static"][u]), int(h["n_rt"][u]), int(h["n_cand"][u])
         q, k, v, uu = (qkvu[s:e, i * d:(i + 1) * d].astype(np.float64) for i in range(4))
         nu = 1.0 / (e - s)
-        oo, S, M = oracle.attn_fwd_user(q, k, v, ns, nr, nc, ts[s:e], H, nu)
+        oo, S, M = oracle.attn_fwd_user(q, k, v, ns, nr, nc, ts[s:e], H, nu, mask_mode=mask)
         ref["o"][s:e] = oo
         ref["y"][s:e] = oo * uu
         dq_, dk_, dv_, _ = oracle.attn_bwd_user(dO[s:e].astype(np.float64), q, k, v, S, M, H, nu)
@@ -150,7 +151,8 @@ def test_attention_fwd_bwd(dev, name, bwd_path):
 def _run_layer(dev, cfg, seg, ts, X, dZ, P, n_layers=1, Ps=None, inv_norm=None):
     dt = _dt(cfg)
     jb = m.JaggedBatch.build(seg, ts, dev, inv_norm=inv_norm)
-    lc = m.layer_cfg(cfg["d"], cfg["H"], cfg["groups"], cfg.get("rab_buckets", 0))
+    lc = m.layer_cfg(cfg["d"], cfg["H"], cfg["groups"], cfg.get("rab_buckets", 0),
+                     mask_mode=cfg.get("mask_mode", "dynamic"))
     Ps = Ps or [P]
     stack = m.HstuStack(lc, [m.params_to_device(p, dt, dev) for p in Ps], dt, dev)
     stack.bind(jb)
@@ -162,7 +164,7 @@ def _run_layer(dev, cfg, seg, ts, X, dZ, P, n_layers=1, Ps=None, inv_norm=None):
 
 def _oracle_stack(cfg, seg, ts, X, dZ, Ps, inv_norm=None, users=None):
     h = oracle.build_jagged(seg)
-    ocfg = dict(d=cfg["d"], H=cfg["H"])
+    ocfg = dict(d=cfg["d"], H=cfg["H"], mask_mode=cfg.get("mask_mode", "dynamic"))
     Z = np.full(X.shape, np.nan)
     dX = np.full(X.shape, np.nan)
     tot = [None] * len(Ps)
@@ -199,6 +201,15 @@ def _compare(z, dx, grads, Z, dX, G, tol, rows=None):
 @pytest.mark.parametrize("name", ["toy", "parity", "parity768"])
 def test_layer_fwd_bwd(dev, name, bwd_path):
     cfg, seg, ts, X, dZ, P = make_batch(name)
+    z, dx, grads = _run_layer(dev, cfg, seg, ts, X, dZ, P)
+    Z, dX, G = _oracle_stack(cfg, seg, ts, X, dZ, [P])
+    print(_compare(z, dx, grads, Z, dX, G, TOL[_dt(cfg)]))
+
+
+@pytest.mark.parametrize("name", ["toy", "parity", "parity768"])
+def test_layer_causal_mask(dev, name, bwd_path):
+    """Table 4's "w/o dynamic mask" ablation: the plain causal mask."""
+    cfg, seg, ts, X, dZ, P = make_batch(name, mask_mode="causal")
     z, dx, grads = _run_layer(dev, cfg, seg, ts, X, dZ, P)
     Z, dX, G = _oracle_stack(cfg, seg, ts, X, dZ, [P])
     print(_compare(z, dx, grads, Z, dX, G, TOL[_dt(cfg)]))
