@@ -43,6 +43,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-users", type=int, default=24, help="users in the CPU oracle sample (~10 s)")
     ap.add_argument("--backend", default="nccl")
+    ap.add_argument("--mask", default="dynamic", choices=["dynamic", "causal"],
+                    help="mask mode: MTGR's dynamic mask, or the causal mask of the Table 4 ablation")
     ap.add_argument("--balance", default="tokens", choices=["tokens", "flops"],
                     help="LPT cost: token count (R#19, default) or per-user FLOPs (SURVEY f3)")
     return ap.parse_args()
@@ -59,11 +61,14 @@ def peaks():
 
 # ------------------------------------------------------------------ workload (both arms)
 
-def visible_pairs(seg_u, ts_u):
-    """P_u = L*n_s + sum_{i >= n_s} |{j in rt : ts_j < ts_i}| + (L - n_s).
+def visible_pairs(seg_u, ts_u, mask="dynamic"):
+    """P_u = L*n_s + sum_{i >= n_s} |{j in rt : ts_j < ts_i}| + (L - n_s)  (SURVEY §8(d));
+    causal mask: L (L + 1) / 2.
     Measurement bookkeeping for the algorithmic FLOP count (not part of the hot path)."""
     nU, nS, nR, K = (int(v) for v in seg_u)
     ns, L = nU + nS, nU + nS + nR + K
+    if mask == "causal":
+        return L * (L + 1) // 2
     rt = np.sort(ts_u[ns:ns + nR])
     rows = ts_u[ns:]
     return L * ns + int(np.searchsorted(rt, rows, side="left").sum()) + (L - ns)
@@ -82,7 +87,7 @@ def workload(cfg, rank, world, balance, cost_kind="tokens"):
     rank_of, load = balance(cost, world)
     users = np.nonzero(rank_of == rank)[0].astype(np.int32)
     ts = [synth.gen_user_ts(cfg, int(u), seg[u]) for u in users]
-    P = sum(visible_pairs(seg[u], t) for u, t in zip(users, ts))
+    P = sum(visible_pairs(seg[u], t, cfg.get("mask_mode", "dynamic")) for u, t in zip(users, ts))
     return dict(seg=seg, users=users, ts=ts, L=L, load=load, B_g=B_g, pairs=P,
                 tokens=int(L[users].sum()), tokens_global=int(L.sum()), balance=cost_kind)
 
@@ -194,7 +199,7 @@ def blas_threads():
 
 def time_oracle(cfg, wl, n_users, start=0):
     import oracle
-    ocfg = dict(d=cfg["d"], H=cfg["H"])
+    ocfg = dict(d=cfg["d"], H=cfg["H"], mask_mode=cfg.get("mask_mode", "dynamic"))
     Ps = [synth.gen_layer_params(cfg, li) for li in range(cfg["n_layers"])]
     tok, secs = 0, 0.0
     for k in range(n_users):
@@ -230,6 +235,7 @@ def workload_desc(cfg, wl, world):
             "tokens_global": wl["tokens_global"], "mean_len": round(wl["tokens_global"] / wl["B_g"], 1),
             "parallelism": f"dp{world}",
             "balancer": "FLOP-cost LPT" if wl.get("balance") == "flops" else "token-count LPT",
+            "mask": cfg.get("mask_mode", "dynamic"),
             "l2": "no flush: per-step activations are several GB (>> 126 MB L2)"}
 
 
@@ -277,7 +283,7 @@ def run_mtgr(args, cfg, rank, world, local_rank):
     X = np.concatenate([synth.gen_user_x(cfg, int(u), int(l)) for u, l in zip(users, Ls)])
     dZ = np.concatenate([synth.gen_user_dz(cfg, int(u), int(l)) for u, l in zip(users, Ls)])
     jb = m.JaggedBatch.build(wl["seg"], ts, dev, users=users)
-    lc = m.layer_cfg(cfg["d"], cfg["H"], cfg["groups"])
+    lc = m.layer_cfg(cfg["d"], cfg["H"], cfg["groups"], mask_mode=cfg.get("mask_mode", "dynamic"))
     Ps = [m.params_to_device(synth.gen_layer_params(cfg, li), dt, dev) for li in range(cfg["n_layers"])]
     stack = m.HstuStack(lc, Ps, dt, dev)
     stack.bind(jb)
@@ -465,7 +471,7 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    cfg = synth.config(args.config)
+    cfg = synth.config(args.config, mask_mode=args.mask)
     if args.impl == "reference":
         run_reference(args, cfg, rank, world)
         return
