@@ -238,6 +238,46 @@ mtgr_status_t mtgr_gemm(mtgr_dtype_t dtype, int32_t M, int32_t N, int32_t K, con
 size_t mtgr_gemm_workspace_bytes(mtgr_dtype_t dtype, int32_t M, int32_t N, int32_t K,
                                  int32_t c_f32);
 
+/* ---------------------------------------------------------------- candidate head */
+
+/* Candidate logit head + two-task loss: "the representation of the tokens of candidates are
+ * used for logit via another MLP module" (Fig.2(a) caption), tasks CTR and CTCVR.
+ * Reading R#21: per candidate row c of the encoder output Z,
+ *   h = SiLU(W_a z_c + b_a) (d_hidden),  [l_ctr, l_ctcvr] = W_b h + b_b,
+ *   loss[0] = sum_c BCE(l_ctr, click_c),  loss[1] = sum_c BCE(l_ctcvr, click_c AND purchase_c),
+ * with BCE(l, y) = softplus(l) - y l.  Losses and gradients are SUMS over the batch's candidates
+ * (the 1/B_global scaling is the aggregation step, R#20). */
+typedef struct {
+  int32_t d_model;   /* d                                                                     */
+  int32_t d_hidden;  /* hidden width (d/2); multiple of 8, <= 1024                      */
+} mtgr_head_cfg_t;
+typedef struct {
+  const void* w_a;   /* [d_hidden][d] activation dtype                                        */
+  const float* b_a;  /* [d_hidden]                                                             */
+  const float* w_b;  /* [2][d_hidden] fp32 (row 0: CTR, row 1: CTCVR)                          */
+  const float* b_b;  /* [2]                                                                    */
+} mtgr_head_params_t;
+typedef struct { float* w_a; float* b_a; float* w_b; float* b_b; } mtgr_head_grads_t; /* fp32 */
+
+size_t mtgr_head_workspace_bytes(const mtgr_head_cfg_t* cfg, const mtgr_jagged_t* jag,
+                                 int32_t total_candidates, mtgr_dtype_t dtype);
+/* One forward (+ backward) of the head over the jagged batch (DEVICE pointers, stream-ordered).
+ *   total_candidates: host-known sum of n_cand (the compact candidate count K).
+ *   z:      [T][d] encoder output (dtype); only candidate rows [n_s+n_r, L_u) are read.
+ *   labels: [T] uint8, bit 0 = click, bit 1 = purchase; only candidate rows are read.
+ *   logits: [K][2] fp32 in candidate order (user-major), or NULL.
+ *   loss:   [2] fp32 sums (CTR, CTCVR), or NULL.
+ *   dz:     [T][d] (dtype) d(loss[0] + loss[1]) / dz, zero on non-candidate rows; NULL = forward
+ *           only (grads ignored).  grads: overwritten fp32 sums.
+ * Errors: MTGR_E_ARG (null pointers, K > T), MTGR_E_UNSUPPORTED (dims), MTGR_E_LAYOUT (z / dz not
+ * 16-byte aligned), MTGR_E_WORKSPACE.  Deterministic (fixed-order reductions). */
+mtgr_status_t mtgr_head_fwd_bwd(const mtgr_head_cfg_t* cfg, const mtgr_jagged_t* jag,
+                                int32_t total_candidates, mtgr_dtype_t dtype,
+                                const mtgr_head_params_t* params, const void* z,
+                                const uint8_t* labels, float* logits, float* loss, void* dz,
+                                const mtgr_head_grads_t* grads, void* ws, size_t ws_bytes,
+                                mtgr_stream_t stream);
+
 /* ---------------------------------------------------------------- tracing */
 
 /* Number of CUDA kernels libmtgr has launched in this process (all streams). */

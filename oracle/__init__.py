@@ -37,3 +37,4 @@ __all__ = [
     "attn_fwd_user", "attn_bwd_user", "build_jagged", "lpt", "BudgetError",
     "aggregate_sum", "aggregate_weighted", "layer_fwd_jagged", "layer_bwd_jagged",
 ]
+from .head import candidate_rows, bce_with_logits, head_fwd_bwd

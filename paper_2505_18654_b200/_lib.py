@@ -50,6 +50,21 @@ class LayerGrads(ctypes.Structure):
     _fields_ = [(n, c_void_p) for n in _PNAMES]
 
 
+class HeadCfg(ctypes.Structure):
+    _fields_ = [("d_model", c_int32), ("d_hidden", c_int32)]
+
+
+_HNAMES = ("w_a", "b_a", "w_b", "b_b")
+
+
+class HeadParams(ctypes.Structure):
+    _fields_ = [(n, c_void_p) for n in _HNAMES]
+
+
+class HeadGrads(ctypes.Structure):
+    _fields_ = [(n, c_void_p) for n in _HNAMES]
+
+
 # name -> (restype, argtypes); mirrors include/mtgr.h
 _S = c_int32  # mtgr_status_t
 _P = c_void_p
@@ -80,6 +95,9 @@ SIGNATURES = {
     "mtgr_gemm": (_S, [c_int32, c_int32, c_int32, c_int32, _P, c_int64, c_int32, _P, c_int64,
                        c_int32, _P, c_int64, c_int32, _P, c_int32, _P, c_size_t, _P]),
     "mtgr_gemm_workspace_bytes": (c_size_t, [c_int32, c_int32, c_int32, c_int32, c_int32]),
+    "mtgr_head_workspace_bytes": (c_size_t, [POINTER(HeadCfg), POINTER(Jagged), c_int32, c_int32]),
+    "mtgr_head_fwd_bwd": (_S, [POINTER(HeadCfg), POINTER(Jagged), c_int32, c_int32, POINTER(HeadParams),
+                               _P, _P, _P, _P, _P, POINTER(HeadGrads), _P, c_size_t, _P]),
     "mtgr_launch_count": (c_int64, []),
     "mtgr_prof_enable": (None, [c_int32]),
     "mtgr_prof_reset": (None, []),

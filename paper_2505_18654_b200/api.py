@@ -12,7 +12,8 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._lib import Jagged, LayerCfg, LayerParams, LayerGrads, check, lib, MTGR_F32, MTGR_BF16
+from ._lib import (Jagged, LayerCfg, LayerParams, LayerGrads, HeadCfg, HeadParams, HeadGrads, check, lib,
+                   MTGR_F32, MTGR_BF16)
 
 
 def _dt(t: torch.dtype) -> int:
@@ -342,6 +343,47 @@ class HstuStack:
 
 
 # ------------------------------------------------------------------ tracing
+
+# ------------------------------------------------------------------ candidate head
+
+def head_params_to_device(p: dict, dtype: torch.dtype, device) -> dict:
+    """w_a in the activation dtype; b_a, w_b, b_b fp32 (include/mtgr.h mtgr_head_params_t)."""
+    out = {}
+    for k, v in p.items():
+        t = torch.as_tensor(np.ascontiguousarray(v, dtype=np.float32))
+        out[k] = t.to(device, dtype if k == "w_a" else torch.float32).contiguous()
+    return out
+
+
+def head_fwd_bwd(jb: JaggedBatch, params: dict, z: torch.Tensor, labels: torch.Tensor,
+                 d_hidden: int | None = None, want_grad: bool = True, ws=None):
+    """Candidate logit head + CTR/CTCVR BCE sums (mtgr_head_fwd_bwd).  labels: uint8 [T]
+    (bit 0 click, bit 1 purchase).  Returns (logits [K][2], loss [2], dz or None, grads or None)."""
+    d = z.shape[1]
+    dh = d_hidden or params["w_a"].shape[0]
+    cfg = HeadCfg(d, dh)
+    K = int(jb.host["n_cand"].sum()) if jb.num_users else 0
+    j = jb.c()
+    dt = _dt(z.dtype)
+    nbytes = lib().mtgr_head_workspace_bytes(ctypes.byref(cfg), ctypes.byref(j), K, dt)
+    ws = _ws(nbytes, z.device) if ws is None else ws
+    logits = torch.empty((max(K, 1), 2), dtype=torch.float32, device=z.device)
+    loss = torch.empty(2, dtype=torch.float32, device=z.device)
+    dz = torch.empty_like(z) if want_grad else None
+    grads = None
+    if want_grad:
+        grads = {"w_a": torch.empty((dh, d), dtype=torch.float32, device=z.device),
+                 "b_a": torch.empty(dh, dtype=torch.float32, device=z.device),
+                 "w_b": torch.empty((2, dh), dtype=torch.float32, device=z.device),
+                 "b_b": torch.empty(2, dtype=torch.float32, device=z.device)}
+    P = HeadParams(*(params[k].data_ptr() for k in ("w_a", "b_a", "w_b", "b_b")))
+    G = HeadGrads(*(grads[k].data_ptr() for k in ("w_a", "b_a", "w_b", "b_b"))) if want_grad else None
+    check(lib().mtgr_head_fwd_bwd(ctypes.byref(cfg), ctypes.byref(j), K, dt, ctypes.byref(P),
+                                  _p(z), _p(labels), _p(logits), _p(loss), _p(dz),
+                                  ctypes.byref(G) if G is not None else None, _p(ws), ws.numel(),
+                                  _stream()))
+    return logits[:K], loss, dz, grads
+
 
 def launch_count() -> int:
     """Kernels libmtgr has launched in this process."""

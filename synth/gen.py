@@ -24,7 +24,7 @@ import numpy as np
 T0 = 1_700_000_000
 
 # stream ids
-_S_SEG, _S_TS, _S_X, _S_DZ, _S_PARAM = 11, 12, 13, 14, 15
+_S_SEG, _S_TS, _S_X, _S_DZ, _S_PARAM, _S_LABEL, _S_HEAD = 11, 12, 13, 14, 15, 16, 17
 
 CONFIGS = {
     # name: layers, d_model, heads, users (per rank), segment recipe, dtype, seed
@@ -150,3 +150,27 @@ def gen_layer_params(cfg: dict, layer: int, rab_buckets: int = 0) -> dict:
     if rab_buckets:
         p["rab_w"] = (0.1 * rng.standard_normal((H, rab_buckets))).astype(np.float32)
     return p
+
+
+def gen_user_labels(cfg: dict, user: int, n_tokens: int, p_click: float = 0.3,
+                    p_buy: float = 0.3) -> np.ndarray:
+    """Per-token uint8 labels (only candidate rows are used): bit 0 click ~ Bernoulli(p_click),
+    bit 1 purchase ~ Bernoulli(p_buy) given a click (purchase implies click)."""
+    rng = _rng(cfg["seed"], _S_LABEL, user)
+    click = rng.random(n_tokens) < p_click
+    buy = click & (rng.random(n_tokens) < p_buy)
+    return (click.astype(np.uint8) | (buy.astype(np.uint8) << 1)).astype(np.uint8)
+
+
+def gen_head_params(cfg: dict, d_hidden: int | None = None) -> dict:
+    """Random-init candidate head (float32; w_a bf16-exact for bf16 configs):
+    w_a [dh][d], b_a [dh], w_b [2][dh], b_b [2]; dh = d/2 by default."""
+    d = cfg["d"]
+    dh = d_hidden or d // 2
+    rng = _rng(cfg["seed"], _S_HEAD)
+    return {
+        "w_a": _vals(cfg, rng.standard_normal((dh, d)) / np.sqrt(d)),
+        "b_a": (rng.standard_normal(dh) * 0.02).astype(np.float32),
+        "w_b": (rng.standard_normal((2, dh)) / np.sqrt(dh)).astype(np.float32),
+        "b_b": (rng.standard_normal(2) * 0.02).astype(np.float32),
+    }
