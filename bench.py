@@ -45,6 +45,8 @@ def parse():
     ap.add_argument("--backend", default="nccl")
     ap.add_argument("--mask", default="dynamic", choices=["dynamic", "causal"],
                     help="mask mode: MTGR's dynamic mask, or the causal mask of the Table 4 ablation")
+    ap.add_argument("--head", action="store_true",
+                    help="step = stack fwd + candidate head/BCE (SURVEY f2) + stack bwd from the head's dZ")
     ap.add_argument("--balance", default="tokens", choices=["tokens", "flops"],
                     help="LPT cost: token count (R#19, default) or per-user FLOPs (SURVEY f3)")
     return ap.parse_args()
@@ -292,8 +294,19 @@ def run_mtgr(args, cfg, rank, world, local_rank):
     from paper_2505_18654_b200.dp import GradAggregator
     agg = GradAggregator(wl["B_g"])  # per-layer bucket all-reduce (NCCL) + 1/B_global
 
+    head_state = {}
+    if args.head:  # candidate head + two-task BCE on the encoder output
+        lab = np.concatenate([synth.gen_user_labels(cfg, int(u), int(l)) for u, l in zip(users, Ls)])
+        head_state = dict(params=m.head_params_to_device(synth.gen_head_params(cfg), dt, dev),
+                          labels=torch.from_numpy(lab).to(dev),
+                          ws=None, K=int(jb.host["n_cand"].sum()))
+
     def step(xin=x_dev, dzin=dz_dev):
-        stack.forward(xin)
+        z = stack.forward(xin)
+        if args.head:
+            _, loss, dzin, hg = m.head_fwd_bwd(jb, head_state["params"], z, head_state["labels"])
+            if world > 1:
+                dist.all_reduce(torch.cat([t.reshape(-1) for t in hg.values()]))
         stack.backward(dzin, on_layer_done=agg.on_layer_done)
         agg.finish(stack.grad_flat)
 
@@ -393,6 +406,9 @@ def run_mtgr(args, cfg, rank, world, local_rank):
                 "algorithmic_tflops_per_gpu": flops_rank * args.steps / (ms_max / 1000.0) / 1e12,
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
                 "gpu_launches": int(launches), "kernels": kernels, "impl": "mtgr"}
+        if args.head:
+            line["config"]["step"] = "stack fwd + candidate head/BCE + stack bwd (dZ from the head)"
+            line["config"]["candidates_per_rank"] = head_state["K"]
         print(json.dumps(line), flush=True)
 
 
