@@ -278,6 +278,50 @@ mtgr_status_t mtgr_head_fwd_bwd(const mtgr_head_cfg_t* cfg, const mtgr_jagged_t*
                                 const mtgr_head_grads_t* grads, void* ws, size_t ws_bytes,
                                 mtgr_stream_t stream);
 
+/* ---------------------------------------------------------------- token construction */
+
+/* Eq.4: U tokens are the given d-wide feature embeddings ("each feature is
+ * naturally converted to individual token"); every S / R / candidate item token is
+ * MLP(Concat(Emb)) of its concatenated feature embeddings.  Reading R#23: one MLP
+ * per item type, Linear(k_t -> d) -> SiLU -> Linear(d -> d).  Features are packed per type in
+ * user-major order; X rows follow the jagged layout [U | S | R | candidates] of each user. */
+typedef struct {
+  int32_t d_model;             /* d                                                          */
+  int32_t k_s, k_r, k_c;       /* concatenated feature widths of S, R and candidate items   */
+} mtgr_token_cfg_t;            /* (all multiples of 8)                                       */
+typedef struct {
+  const void* w1;  /* [d][k] activation dtype */  const float* b1;  /* [d] */
+  const void* w2;  /* [d][d] activation dtype */  const float* b2;  /* [d] */
+} mtgr_mlp_params_t;
+typedef struct { float* w1; float* b1; float* w2; float* b2; } mtgr_mlp_grads_t; /* fp32 sums */
+typedef struct { mtgr_mlp_params_t s, r, c; } mtgr_token_params_t;
+typedef struct { mtgr_mlp_grads_t s, r, c; } mtgr_token_grads_t;
+
+/* n_tot: HOST int32[4] = total U, S, R, candidate tokens of the batch (sum == total_tokens). */
+size_t mtgr_token_saved_bytes(const mtgr_token_cfg_t* cfg, const int32_t* n_tot, mtgr_dtype_t dtype);
+size_t mtgr_token_workspace_bytes(const mtgr_token_cfg_t* cfg, const mtgr_jagged_t* jag,
+                                  const int32_t* n_tot, mtgr_dtype_t dtype);
+/* X [T][d] <- tokens.  n_user: DEVICE int32 [B] profile tokens per user (the U part of
+ * n_static; n_static - n_user are the S tokens).  feat_u [n_U][d], feat_s [n_S][k_s],
+ * feat_r [n_R][k_r], feat_c [n_C][k_c] (dtype, device; NULL allowed for an empty type).
+ * saved: mtgr_token_saved_bytes, written here and read by the backward.
+ * Errors: MTGR_E_ARG (null pointers, n_tot inconsistent with total_tokens), MTGR_E_UNSUPPORTED
+ * (widths), MTGR_E_LAYOUT (alignment), MTGR_E_WORKSPACE. */
+mtgr_status_t mtgr_token_fwd(const mtgr_token_cfg_t* cfg, const mtgr_jagged_t* jag,
+                             const int32_t* n_user, const int32_t* n_tot, mtgr_dtype_t dtype,
+                             const mtgr_token_params_t* params, const void* feat_u,
+                             const void* feat_s, const void* feat_r, const void* feat_c, void* x,
+                             void* saved, void* ws, size_t ws_bytes, mtgr_stream_t stream);
+/* Given dX [T][d]: parameter gradients (overwritten fp32 sums) and, when non-NULL, the feature
+ * gradients dfeat_* (same shapes as the features; for the embedding tables). */
+mtgr_status_t mtgr_token_bwd(const mtgr_token_cfg_t* cfg, const mtgr_jagged_t* jag,
+                             const int32_t* n_user, const int32_t* n_tot, mtgr_dtype_t dtype,
+                             const mtgr_token_params_t* params, const void* feat_s,
+                             const void* feat_r, const void* feat_c, const void* saved,
+                             const void* dx, void* dfeat_u, void* dfeat_s, void* dfeat_r,
+                             void* dfeat_c, const mtgr_token_grads_t* grads, void* ws,
+                             size_t ws_bytes, mtgr_stream_t stream);
+
 /* ---------------------------------------------------------------- tracing */
 
 /* Number of CUDA kernels libmtgr has launched in this process (all streams). */

@@ -38,3 +38,4 @@ __all__ = [
     "aggregate_sum", "aggregate_weighted", "layer_fwd_jagged", "layer_bwd_jagged",
 ]
 from .head import candidate_rows, bce_with_logits, head_fwd_bwd
+from .token import mlp_fwd, mlp_bwd, tokens_user, tokens_user_bwd

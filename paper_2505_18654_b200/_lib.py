@@ -65,6 +65,25 @@ class HeadGrads(ctypes.Structure):
     _fields_ = [(n, c_void_p) for n in _HNAMES]
 
 
+class TokenCfg(ctypes.Structure):
+    _fields_ = [("d_model", c_int32), ("k_s", c_int32), ("k_r", c_int32), ("k_c", c_int32)]
+
+
+_MNAMES = ("w1", "b1", "w2", "b2")
+
+
+class MlpParams(ctypes.Structure):
+    _fields_ = [(n, c_void_p) for n in _MNAMES]
+
+
+class TokenParams(ctypes.Structure):
+    _fields_ = [("s", MlpParams), ("r", MlpParams), ("c", MlpParams)]
+
+
+class TokenGrads(ctypes.Structure):  # mtgr_mlp_grads_t has the same layout as MlpParams
+    _fields_ = [("s", MlpParams), ("r", MlpParams), ("c", MlpParams)]
+
+
 # name -> (restype, argtypes); mirrors include/mtgr.h
 _S = c_int32  # mtgr_status_t
 _P = c_void_p
@@ -98,6 +117,12 @@ SIGNATURES = {
     "mtgr_head_workspace_bytes": (c_size_t, [POINTER(HeadCfg), POINTER(Jagged), c_int32, c_int32]),
     "mtgr_head_fwd_bwd": (_S, [POINTER(HeadCfg), POINTER(Jagged), c_int32, c_int32, POINTER(HeadParams),
                                _P, _P, _P, _P, _P, POINTER(HeadGrads), _P, c_size_t, _P]),
+    "mtgr_token_saved_bytes": (c_size_t, [POINTER(TokenCfg), _P, c_int32]),
+    "mtgr_token_workspace_bytes": (c_size_t, [POINTER(TokenCfg), POINTER(Jagged), _P, c_int32]),
+    "mtgr_token_fwd": (_S, [POINTER(TokenCfg), POINTER(Jagged), _P, _P, c_int32, POINTER(TokenParams),
+                            _P, _P, _P, _P, _P, _P, _P, c_size_t, _P]),
+    "mtgr_token_bwd": (_S, [POINTER(TokenCfg), POINTER(Jagged), _P, _P, c_int32, POINTER(TokenParams),
+                            _P, _P, _P, _P, _P, _P, _P, _P, _P, POINTER(TokenGrads), _P, c_size_t, _P]),
     "mtgr_launch_count": (c_int64, []),
     "mtgr_prof_enable": (None, [c_int32]),
     "mtgr_prof_reset": (None, []),

@@ -12,8 +12,8 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._lib import (Jagged, LayerCfg, LayerParams, LayerGrads, HeadCfg, HeadParams, HeadGrads, check, lib,
-                   MTGR_F32, MTGR_BF16)
+from ._lib import (Jagged, LayerCfg, LayerParams, LayerGrads, HeadCfg, HeadParams, HeadGrads, TokenCfg,
+                   MlpParams, TokenParams, TokenGrads, check, lib, MTGR_F32, MTGR_BF16)
 
 
 def _dt(t: torch.dtype) -> int:
@@ -383,6 +383,66 @@ def head_fwd_bwd(jb: JaggedBatch, params: dict, z: torch.Tensor, labels: torch.T
                                   ctypes.byref(G) if G is not None else None, _p(ws), ws.numel(),
                                   _stream()))
     return logits[:K], loss, dz, grads
+
+
+# ------------------------------------------------------------------ token construction
+
+class TokenEmbed:
+    """Eq.4 token construction (mtgr_token_fwd / _bwd): U rows from the given embeddings, one
+    Linear-SiLU-Linear MLP per item type (S, R, candidates).  `params`: {"s","r","c"} ->
+    {"w1","b1","w2","b2"} on the device (w1, w2 in the activation dtype)."""
+
+    def __init__(self, d_model: int, widths: dict, params: dict, dtype: torch.dtype, device):
+        self.cfg = TokenCfg(d_model, widths["s"], widths["r"], widths["c"])
+        self.d, self.dtype, self.device = d_model, dtype, device
+        self.params = params
+        self._cp = TokenParams(*(MlpParams(*(params[t][k].data_ptr() for k in ("w1", "b1", "w2", "b2")))
+                                 for t in ("s", "r", "c")))
+
+    @staticmethod
+    def params_to_device(p: dict, dtype: torch.dtype, device) -> dict:
+        out = {}
+        for t, q in p.items():
+            out[t] = {k: torch.as_tensor(np.ascontiguousarray(v, dtype=np.float32)).to(
+                device, dtype if k in ("w1", "w2") else torch.float32).contiguous() for k, v in q.items()}
+        return out
+
+    def bind(self, jb: JaggedBatch, seg4: np.ndarray):
+        """seg4 [B][4] host (n_U, n_S, n_r, K) of the batch's users, in batch order."""
+        seg4 = np.asarray(seg4, dtype=np.int64)
+        self.jb = jb
+        self.n_user = torch.from_numpy(np.ascontiguousarray(seg4[:, 0], dtype=np.int32)).to(self.device)
+        self.n_tot = (ctypes.c_int32 * 4)(*(int(seg4[:, i].sum()) for i in range(4)))
+        dt = _dt(self.dtype)
+        j = jb.c()
+        self.saved = _ws(lib().mtgr_token_saved_bytes(ctypes.byref(self.cfg), self.n_tot, dt), self.device)
+        self.ws = _ws(lib().mtgr_token_workspace_bytes(ctypes.byref(self.cfg), ctypes.byref(j), self.n_tot, dt),
+                      self.device)
+
+    def forward(self, feats: dict) -> torch.Tensor:
+        self.feats = feats
+        x = torch.empty((max(self.jb.total_tokens, 1), self.d), dtype=self.dtype, device=self.device)
+        j = self.jb.c()
+        check(lib().mtgr_token_fwd(ctypes.byref(self.cfg), ctypes.byref(j), _p(self.n_user), self.n_tot,
+                                   _dt(self.dtype), ctypes.byref(self._cp), *(_p(feats.get(t)) for t in "usrc"),
+                                   _p(x), _p(self.saved), _p(self.ws), self.ws.numel(), _stream()))
+        return x[:self.jb.total_tokens]
+
+    def backward(self, dx: torch.Tensor, want_dfeats: bool = True):
+        """Returns (dfeats dict or None, grads {"s","r","c"} -> {"w1","b1","w2","b2"} fp32 sums)."""
+        f = lambda *s: torch.empty(s, dtype=torch.float32, device=self.device)
+        grads = {t: {"w1": f(*self.params[t]["w1"].shape), "b1": f(self.d), "w2": f(self.d, self.d), "b2": f(self.d)}
+                 for t in ("s", "r", "c")}
+        cg = TokenGrads(*(MlpParams(*(grads[t][k].data_ptr() for k in ("w1", "b1", "w2", "b2")))
+                          for t in ("s", "r", "c")))
+        dfe = {t: torch.empty_like(v) for t, v in self.feats.items() if v is not None} if want_dfeats else {}
+        j = self.jb.c()
+        check(lib().mtgr_token_bwd(ctypes.byref(self.cfg), ctypes.byref(j), _p(self.n_user), self.n_tot,
+                                   _dt(self.dtype), ctypes.byref(self._cp),
+                                   *(_p(self.feats.get(t)) for t in "src"), _p(self.saved), _p(dx),
+                                   *(_p(dfe.get(t)) for t in "usrc"), ctypes.byref(cg), _p(self.ws),
+                                   self.ws.numel(), _stream()))
+        return (dfe if want_dfeats else None), grads
 
 
 def launch_count() -> int:

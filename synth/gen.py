@@ -24,7 +24,7 @@ import numpy as np
 T0 = 1_700_000_000
 
 # stream ids
-_S_SEG, _S_TS, _S_X, _S_DZ, _S_PARAM, _S_LABEL, _S_HEAD = 11, 12, 13, 14, 15, 16, 17
+_S_SEG, _S_TS, _S_X, _S_DZ, _S_PARAM, _S_LABEL, _S_HEAD, _S_FEAT, _S_TOK = 11, 12, 13, 14, 15, 16, 17, 18, 19
 
 CONFIGS = {
     # name: layers, d_model, heads, users (per rank), segment recipe, dtype, seed
@@ -174,3 +174,37 @@ def gen_head_params(cfg: dict, d_hidden: int | None = None) -> dict:
         "w_b": (rng.standard_normal((2, dh)) / np.sqrt(dh)).astype(np.float32),
         "b_b": (rng.standard_normal(2) * 0.02).astype(np.float32),
     }
+
+
+TOKEN_TYPES = ("u", "s", "r", "c")
+
+
+def token_widths(cfg: dict) -> dict:
+    """Concatenated feature-embedding widths per item type: a token of k features uses
+    embeddings of ~d/k each, so the concatenation is ~d wide; varied per type here so the
+    tests exercise distinct shapes."""
+    d = cfg["d"]
+    return {"u": d, "s": d, "r": max(8, (d // 2) // 8 * 8), "c": max(8, (3 * d // 4) // 8 * 8)}
+
+
+def gen_user_features(cfg: dict, user: int, seg) -> dict:
+    """Per-type feature rows of one user (N(0,1); bf16-exact for bf16 configs):
+    u [n_U][d] (the profile tokens' embeddings), s [n_S][k_s], r [n_r][k_r], c [K][k_c]."""
+    rng = _rng(cfg["seed"], _S_FEAT, user)
+    k = token_widths(cfg)
+    n = dict(zip(TOKEN_TYPES, (int(v) for v in seg)))
+    return {t: _vals(cfg, rng.standard_normal((n[t], k[t]))) for t in TOKEN_TYPES}
+
+
+def gen_token_params(cfg: dict) -> dict:
+    """Per item type (s, r, c): w1 [d][k_t] ~ N(0, 1/k_t), b1 [d], w2 [d][d] ~ N(0, 1/d), b2 [d]."""
+    d = cfg["d"]
+    k = token_widths(cfg)
+    rng = _rng(cfg["seed"], _S_TOK)
+    out = {}
+    for t in ("s", "r", "c"):
+        out[t] = {"w1": _vals(cfg, rng.standard_normal((d, k[t])) / np.sqrt(k[t])),
+                  "b1": (rng.standard_normal(d) * 0.02).astype(np.float32),
+                  "w2": _vals(cfg, rng.standard_normal((d, d)) / np.sqrt(d)),
+                  "b2": (rng.standard_normal(d) * 0.02).astype(np.float32)}
+    return out
