@@ -45,6 +45,8 @@ def parse():
     ap.add_argument("--backend", default="nccl")
     ap.add_argument("--mask", default="dynamic", choices=["dynamic", "causal"],
                     help="mask mode: MTGR's dynamic mask, or the causal mask of the Table 4 ablation")
+    ap.add_argument("--tokens", action="store_true",
+                    help="step also runs the Eq.4 token construction (SURVEY f2) before the stack and its backward after")
     ap.add_argument("--head", action="store_true",
                     help="step = stack fwd + candidate head/BCE (SURVEY f2) + stack bwd from the head's dZ")
     ap.add_argument("--balance", default="tokens", choices=["tokens", "flops"],
@@ -301,13 +303,29 @@ def run_mtgr(args, cfg, rank, world, local_rank):
                           labels=torch.from_numpy(lab).to(dev),
                           ws=None, K=int(jb.host["n_cand"].sum()))
 
+    tok = {}
+    if args.tokens:  # Eq.4 token construction from synthetic per-type feature embeddings
+        k = synth.token_widths(cfg)
+        per_user = [synth.gen_user_features(cfg, int(u), wl["seg"][u]) for u in users]
+        feats = {t: torch.from_numpy(np.concatenate([f[t] for f in per_user] + [np.zeros((0, k[t]), np.float32)]))
+                 .to(dev, dt) for t in synth.TOKEN_TYPES}
+        emb = m.TokenEmbed(cfg["d"], k, m.TokenEmbed.params_to_device(synth.gen_token_params(cfg), dt, dev), dt, dev)
+        emb.bind(jb, wl["seg"][users])
+        tok = dict(emb=emb, feats=feats)
+
     def step(xin=x_dev, dzin=dz_dev):
+        if args.tokens:
+            xin = tok["emb"].forward(tok["feats"]).contiguous()
         z = stack.forward(xin)
         if args.head:
             _, loss, dzin, hg = m.head_fwd_bwd(jb, head_state["params"], z, head_state["labels"])
             if world > 1:
                 dist.all_reduce(torch.cat([t.reshape(-1) for t in hg.values()]))
-        stack.backward(dzin, on_layer_done=agg.on_layer_done)
+        dx = stack.backward(dzin, on_layer_done=agg.on_layer_done)
+        if args.tokens:
+            _, tg = tok["emb"].backward(dx)
+            if world > 1:
+                dist.all_reduce(torch.cat([t.reshape(-1) for q in tg.values() for t in q.values()]))
         agg.finish(stack.grad_flat)
 
     def barrier():
@@ -406,6 +424,8 @@ def run_mtgr(args, cfg, rank, world, local_rank):
                 "algorithmic_tflops_per_gpu": flops_rank * args.steps / (ms_max / 1000.0) / 1e12,
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
                 "gpu_launches": int(launches), "kernels": kernels, "impl": "mtgr"}
+        if args.tokens:
+            line["config"]["tokens"] = "Eq.4 token construction (U embeddings + per-type MLPs) fwd/bwd in the step"
         if args.head:
             line["config"]["step"] = "stack fwd + candidate head/BCE + stack bwd (dZ from the head)"
             line["config"]["candidates_per_rank"] = head_state["K"]

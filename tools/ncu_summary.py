@@ -77,7 +77,9 @@ KIND = [(r"attn_tc_kernel<0>", "attn_fwd"), (r"attn_tc_kernel<1>", "attn_bwd_dv"
         (r"attn_tc_kernel<2>", "attn_bwd_dq"), (r"attn_tc_kernel<3>", "attn_bwd_dk"),
         (r"gemm_tc_kernel<1,", "gemm_qkvu"), (r"gemm_tc_kernel<2,", "gemm_out"),
         (r"gemm_tc_kernel<0,", "gemm_dgrad"), (r"gemm_tc_kernel<3,", "gemm_wgrad"),
-        (r"gln_fwd_kernel", "gln_fwd"), (r"gln_bwd", "gln_bwd")]
+        (r"gln_fwd_kernel", "gln_fwd"), (r"gln_bwd", "gln_bwd"),
+        # stored-score backward GEMMs (MM_DV 0, MM_DQ 1)
+        (r"attn_mm_kernel<0>", "attn_bwd_dv"), (r"attn_mm_kernel<1>", "attn_bwd_dq")]
 
 
 def traffic(config, paths):
