@@ -322,6 +322,72 @@ mtgr_status_t mtgr_token_bwd(const mtgr_token_cfg_t* cfg, const mtgr_jagged_t* j
                              void* dfeat_c, const mtgr_token_grads_t* grads, void* ws,
                              size_t ws_bytes, mtgr_stream_t stream);
 
+/* ---------------------------------------------------------------- hash embedding */
+
+/* Dynamic hash embedding table: a decoupled KEY structure (open addressing, linear
+ * probing over cap_k = 2^m buckets of (int64 key, int32 value slot)) and VALUE structure (rows
+ * [cap_v][dim] fp32 plus per-slot access counter, last-access timestamp and owning key for
+ * eviction).  A missing key gets a value slot (recycled by eviction first, else fresh) whose row
+ * is initialised to init_scale * U(-1, 1) from a counter-based hash of (seed, key, column).
+ * Expansion replicates only the key structure (mtgr_hash_expand).  Keys INT64_MIN and
+ * INT64_MIN+1 are reserved.  All buffers are caller-owned DEVICE memory; every call is
+ * stream-ordered (no two calls on one table may run concurrently). */
+typedef struct {
+  int64_t* keys;       /* [cap_k] key structure                                               */
+  int32_t* slots;      /* [cap_k] value slot of each bucket (-1 empty / being published)     */
+  int64_t cap_k;       /* power of two; keep the load factor below ~0.7                      */
+  float* values;       /* [cap_v][dim] value structure                                        */
+  uint32_t* counter;   /* [cap_v] accesses since insertion                                    */
+  int64_t* ts;         /* [cap_v] last access time (caller's clock)                           */
+  int64_t* slot_key;   /* [cap_v] key owning the slot                                         */
+  int64_t cap_v;
+  int32_t dim;
+  int32_t* alloc;      /* [3]: fresh-slot bump pointer, free-stack size, failed inserts (full) */
+  int32_t* free_stack; /* [cap_v] slots returned by eviction                                  */
+  uint64_t seed;
+  float init_scale;
+} mtgr_hash_table_t;
+
+mtgr_status_t mtgr_hash_init(const mtgr_hash_table_t* t, mtgr_stream_t stream);
+/* slots[i] = value slot of ids[i]; missing keys are inserted when `insert` (else -1).  -2: the
+ * value structure was full (counted in alloc[2]).  Touches counter / ts (= now). */
+mtgr_status_t mtgr_hash_find_or_insert(const mtgr_hash_table_t* t, const int64_t* ids, int32_t n,
+                                       int64_t now, int32_t insert, int32_t* slots,
+                                       mtgr_stream_t stream);
+/* out[i][:] = values[slots[i]] (zeros for a negative slot), in dtype. */
+mtgr_status_t mtgr_hash_gather(const mtgr_hash_table_t* t, const int32_t* slots, int32_t n,
+                               mtgr_dtype_t dtype, void* out, mtgr_stream_t stream);
+/* values[slots[i]] -= lr * grads[i] (duplicate slots accumulate). */
+mtgr_status_t mtgr_hash_sgd(const mtgr_hash_table_t* t, const int32_t* slots, int32_t n,
+                            mtgr_dtype_t dtype, const void* grads, float lr, mtgr_stream_t stream);
+/* Evict every key whose last access is < ts_before: bucket -> tombstone, slot -> free stack. */
+mtgr_status_t mtgr_hash_evict(const mtgr_hash_table_t* t, int64_t ts_before, mtgr_stream_t stream);
+/* Re-insert the live (key, slot) pairs into a new key structure of new_cap_k buckets (the value
+ * structure is shared, untouched); the caller then points the table at new_keys / new_slots. */
+mtgr_status_t mtgr_hash_expand(const mtgr_hash_table_t* t, int64_t* new_keys, int32_t* new_slots,
+                               int64_t new_cap_k, mtgr_stream_t stream);
+
+/* ID unique ("two-stage ID unique"): uniq[0..count) = the distinct ids (order
+ * unspecified), inverse[i] = position of ids[i] in uniq; count is a DEVICE int32. */
+size_t mtgr_unique_workspace_bytes(int32_t n);
+mtgr_status_t mtgr_unique(const int64_t* ids, int32_t n, int64_t* uniq, int32_t* inverse,
+                          int32_t* count, void* ws, size_t ws_bytes, mtgr_stream_t stream);
+/* out[inverse[i]][:] += g[i][:] over i < n; out [n_out][dim] fp32 is zeroed first. */
+mtgr_status_t mtgr_segment_sum(mtgr_dtype_t dtype, const void* g, const int32_t* inverse, int32_t n,
+                               int32_t dim, float* out, int32_t n_out, mtgr_stream_t stream);
+/* out[i][:] = src[idx[i]][:]. */
+mtgr_status_t mtgr_take_rows(mtgr_dtype_t dtype, const void* src, const int32_t* idx, int32_t n,
+                             int32_t dim, void* out, mtgr_stream_t stream);
+/* out[idx[i]][:] = src[i][:] (idx injective). */
+mtgr_status_t mtgr_put_rows(mtgr_dtype_t dtype, const void* src, const int32_t* idx, int32_t n,
+                            int32_t dim, void* out, mtgr_stream_t stream);
+/* All-to-all packing: dest[i] = owner rank of ids[i] (hash(ids[i] ^ salt) % world), counts[r] =
+ * ids owned by r, send = ids grouped by owner (rank-major; order within a rank unspecified),
+ * pos[i] = position of ids[i] in send.  starts_ws: DEVICE int32 [2*world] scratch. */
+mtgr_status_t mtgr_partition_ids(const int64_t* ids, int32_t n, int32_t world, uint64_t salt,
+                                 int32_t* counts, int32_t* dest, int32_t* starts_ws, int64_t* send,
+                                 int32_t* pos, mtgr_stream_t stream);
+
 /* ---------------------------------------------------------------- tracing */
 
 /* Number of CUDA kernels libmtgr has launched in this process (all streams). */

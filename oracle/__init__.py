@@ -39,3 +39,4 @@ __all__ = [
 ]
 from .head import candidate_rows, bce_with_logits, head_fwd_bwd
 from .token import mlp_fwd, mlp_bwd, tokens_user, tokens_user_bwd
+from .embed import mix64, init_row, TableModel, unique_with_inverse

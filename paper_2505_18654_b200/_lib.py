@@ -84,6 +84,13 @@ class TokenGrads(ctypes.Structure):  # mtgr_mlp_grads_t has the same layout as M
     _fields_ = [("s", MlpParams), ("r", MlpParams), ("c", MlpParams)]
 
 
+class HashTable(ctypes.Structure):
+    _fields_ = [("keys", c_void_p), ("slots", c_void_p), ("cap_k", c_int64), ("values", c_void_p),
+                ("counter", c_void_p), ("ts", c_void_p), ("slot_key", c_void_p), ("cap_v", c_int64),
+                ("dim", c_int32), ("alloc", c_void_p), ("free_stack", c_void_p), ("seed", ctypes.c_uint64),
+                ("init_scale", c_float)]
+
+
 # name -> (restype, argtypes); mirrors include/mtgr.h
 _S = c_int32  # mtgr_status_t
 _P = c_void_p
@@ -123,6 +130,18 @@ SIGNATURES = {
                             _P, _P, _P, _P, _P, _P, _P, c_size_t, _P]),
     "mtgr_token_bwd": (_S, [POINTER(TokenCfg), POINTER(Jagged), _P, _P, c_int32, POINTER(TokenParams),
                             _P, _P, _P, _P, _P, _P, _P, _P, _P, POINTER(TokenGrads), _P, c_size_t, _P]),
+    "mtgr_hash_init": (_S, [POINTER(HashTable), _P]),
+    "mtgr_hash_find_or_insert": (_S, [POINTER(HashTable), _P, c_int32, c_int64, c_int32, _P, _P]),
+    "mtgr_hash_gather": (_S, [POINTER(HashTable), _P, c_int32, c_int32, _P, _P]),
+    "mtgr_hash_sgd": (_S, [POINTER(HashTable), _P, c_int32, c_int32, _P, c_float, _P]),
+    "mtgr_hash_evict": (_S, [POINTER(HashTable), c_int64, _P]),
+    "mtgr_hash_expand": (_S, [POINTER(HashTable), _P, _P, c_int64, _P]),
+    "mtgr_unique_workspace_bytes": (c_size_t, [c_int32]),
+    "mtgr_unique": (_S, [_P, c_int32, _P, _P, _P, _P, c_size_t, _P]),
+    "mtgr_segment_sum": (_S, [c_int32, _P, _P, c_int32, c_int32, _P, c_int32, _P]),
+    "mtgr_take_rows": (_S, [c_int32, _P, _P, c_int32, c_int32, _P, _P]),
+    "mtgr_put_rows": (_S, [c_int32, _P, _P, c_int32, c_int32, _P, _P]),
+    "mtgr_partition_ids": (_S, [_P, c_int32, c_int32, ctypes.c_uint64, _P, _P, _P, _P, _P, _P]),
     "mtgr_launch_count": (c_int64, []),
     "mtgr_prof_enable": (None, [c_int32]),
     "mtgr_prof_reset": (None, []),
