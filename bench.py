@@ -109,9 +109,14 @@ def kernel_algorithmic(cfg, tokens, pairs):
     T = tokens
     return {
         "attn_fwd": ("tensor", nl * 4.0 * d * pairs),
+        # stored-score backward: the score kernel does the dP product (S^T is the recompute the
+        # algorithmic count excludes), then one jagged GEMM each for dV, dK, dQ
+        "attn_bwd_scores": ("tensor", nl * 2.0 * d * pairs),
         "attn_bwd_dv": ("tensor", nl * 2.0 * d * pairs),
-        "attn_bwd_dk": ("tensor", nl * 4.0 * d * pairs),
+        "attn_bwd_dk": ("tensor", nl * 2.0 * d * pairs),
         "attn_bwd_dq": ("tensor", nl * 2.0 * d * pairs),
+        # DK kernel that also forms dP (recompute path, MTGR_ATTN_RECOMPUTE / MTGR_ATTN_FUSED_DK)
+        "attn_bwd_dk_fused": ("tensor", nl * 4.0 * d * pairs),
         "gemm_qkvu": ("tensor", nl * 8.0 * T * d * d),
         "gemm_out": ("tensor", nl * 2.0 * T * d * d),
         "gemm_dgrad": ("tensor", nl * 10.0 * T * d * d),

@@ -876,6 +876,331 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
 }
 
 // ---------------------------------------------------------------------------------------------
+// Score kernel of the stored-score backward.  Per (key pair, head) item: S^T = K Q^T and
+// dP^T = V dO^T tile by tile, both row operands in TMEM (TS MMAs, M=256 on CTA pairs, N=64 query
+// columns, K=256), and the softmax warps write P^T = silu(S^T) m and dS^T = dP^T silu'(S^T) m
+// into the stored-score matrices.  No accumulator and no epilogue: dK, dV and dQ are the three
+// stored-score GEMMs (attn_mm_kernel).  Warp roles: w0 producer (Q tiles), w3 producer (dO
+// tiles), w2 TMEM allocator + row loader (K, V of the next item into the staging as soon as the
+// previous rows are in TMEM), w1 MMA issuer (leader), w4-w11 softmax.
+// smem: R1 (K) staging [0,64) KB, R2 (V) staging [64,128), Q ring 3 x 16 [128,176), dO ring
+// 3 x 16 [176,224), query timestamps, barriers.  TMEM: R1 [0,128), R2 [128,256), S/dP double
+// buffered [256,512).
+constexpr int SC_OFF_R1 = 0, SC_OFF_R2 = 64 * KB, SC_OFF_C1 = 128 * KB, SC_OFF_C2 = 176 * KB;
+constexpr int SC_OFF_TS = 224 * KB;
+constexpr int SC_OFF_BAR = SC_OFF_TS + BC * 8;
+constexpr int SC_SMEM_BYTES = 227 * KB;
+constexpr int SC_NC = 3;
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
+    attn_sc_kernel(const __grid_constant__ CUtensorMap tmC1, const __grid_constant__ CUtensorMap tmC2,
+                   const __grid_constant__ CUtensorMap tmR1, const __grid_constant__ CUtensorMap tmR2, Args a) {
+  using namespace sm100;
+  constexpr bool TRANS = true;
+  constexpr int C1_BYTES = 32 * DH * 2;  // 16 KB: 4 boxes {64 dh, 32 cols}
+  constexpr uint32_t T_R1 = 0, T_R2 = 128, T_S0 = 256;  // S[b] = T_S0 + 128 b, dP[b] = S[b] + 64
+  const uint32_t crank = cluster_ctarank();
+  const bool leader = crank == 0;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (sm100::smem_u32(smem_raw) & 1023u)) & 1023u);
+  long long* sTs = reinterpret_cast<long long*>(smem + SC_OFF_TS);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SC_OFF_BAR);
+  uint64_t* c1_full = bars;        // [3] leader
+  uint64_t* c1_empty = bars + 3;   // [3]
+  uint64_t* c2_full = bars + 6;    // [3] leader
+  uint64_t* c2_empty = bars + 9;   // [3]
+  uint64_t* s_full = bars + 12;    // [2]
+  uint64_t* s_free = bars + 14;    // [2] leader, both CTAs' softmax warps
+  uint64_t* r_full = bars + 16;    // own: R1 + R2 staging landed
+  uint64_t* r_copied = bars + 17;  // own: staging copied into TMEM (8 softmax warps)
+  uint64_t* r_done = bars + 18;    // leader: both CTAs' rows in TMEM
+  uint64_t* r_free = bars + 19;    // every MMA of the item done (TMEM rows reusable)
+  uint64_t* q_full = bars + 20;    // [4]
+  uint64_t* q_empty = bars + 24;   // [4] leader
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 28);
+  int* q_item = reinterpret_cast<int*>(bars + 29);  // [4]
+  auto arrive_leader = [&](uint64_t* bar) {
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) {
+      if (leader) mbar_arrive(bar);
+      else mbar_arrive_cluster(bar, 0);
+    }
+  };
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < SC_NC; ++s) {
+      mbar_init(&c1_full[s], 1); mbar_init(&c1_empty[s], 1);
+      mbar_init(&c2_full[s], 1); mbar_init(&c2_empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) { mbar_init(&s_full[s], 1); mbar_init(&s_free[s], 2 * NSM); }
+    mbar_init(r_full, 1);
+    mbar_init(r_copied, NSM);
+    mbar_init(r_done, 2 * NSM);
+    mbar_init(r_free, 1);
+    for (int s = 0; s < 4; ++s) {
+      mbar_init(&q_full[s], 1);
+      // per CTA: 8 softmax warps, producer B, row loader, MMA | producer A
+      mbar_init(&q_empty[s], 2 * (NSM + 3));
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc_2sm<512>(tmem_slot);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  auto q_read = [&](int n) -> int {
+    mbar_wait_cluster(&q_full[n & 3], (n >> 2) & 1);
+    return *reinterpret_cast<volatile int*>(&q_item[n & 3]);
+  };
+  auto q_release = [&](int n) {
+    if (leader) mbar_arrive(&q_empty[n & 3]);
+    else mbar_arrive_cluster(&q_empty[n & 3], 0);
+  };
+  auto q_push = [&](int n) -> int {
+    if (n >= 4) mbar_wait(&q_empty[n & 3], ((n >> 2) & 1) ^ 1);
+    int k;
+    for (;;) {
+      k = atomicAdd(a.ctr, 1);
+      if (k >= a.nitems) { k = -1; break; }
+      const int rest = k / a.H;
+      const int u = rest / a.pmax, p = rest % a.pmax;
+      const int L = a.jag.offsets[u + 1] - a.jag.offsets[u];
+      // items with query tiles only: key pairs below kv_end (dynamic) / below L (causal)
+      const int kv = a.causal ? L : a.jag.n_static[u] + a.jag.n_rt[u];
+      if (p * 2 * BR < kv) break;
+    }
+    q_item[n & 3] = k;
+    st_cluster_u32(reinterpret_cast<uint32_t*>(&q_item[n & 3]), 1, (uint32_t)k);
+    mbar_arrive(&q_full[n & 3]);
+    mbar_arrive_cluster_release(&q_full[n & 3], 1);
+    return k;
+  };
+
+  if (warp == 2) {
+    // ---------------------------------------------------------------- row loader: K, V rows of the
+    // next item into the staging as soon as the softmax warps copied the previous ones to TMEM
+    if (lane == 0) {
+      int mi = 0;
+      for (int n = 0;; ++n) {
+        const int k = q_read(n);
+        q_release(n);
+        if (k < 0) break;
+        Item it;
+        decode_item<true>(a, k, crank, it);
+        if (it.ntiles == 0) continue;
+        const int row0 = it.us.off + it.r0;
+        if (mi > 0) mbar_wait(r_copied, (mi - 1) & 1);
+        mbar_expect_tx(r_full, 2 * RT_BYTES);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          tma_load_2d(smem + SC_OFF_R1 + c * (RT_BYTES / 4), &tmR1, r_full, it.hcol + c * 64, row0);
+          tma_load_2d(smem + SC_OFF_R2 + c * (RT_BYTES / 4), &tmR2, r_full, it.hcol + c * 64, row0);
+        }
+        ++mi;
+      }
+    }
+  } else if (warp == 0 || warp == 3) {
+    // ---------------------------------------------------------------- producers
+    if (lane == 0) {
+      const bool pa = warp == 0;
+      int gt = 0;
+      for (int n = 0;; ++n) {
+        int k;
+        if (pa && leader) {
+          k = q_push(n);
+        } else {
+          k = q_read(n);
+          q_release(n);
+        }
+        if (k < 0) break;
+        Item it;
+        decode_item<TRANS>(a, k, crank, it);
+        if (it.ntiles == 0) continue;
+        const CUtensorMap* tm = pa ? &tmC1 : &tmC2;
+        uint64_t* full = pa ? c1_full : c2_full;
+        uint64_t* empty = pa ? c1_empty : c2_empty;
+        uint8_t* ring = smem + (pa ? SC_OFF_C1 : SC_OFF_C2);
+        for (int t = 0; t < it.ntiles; ++t, ++gt) {
+          const int slot = gt % SC_NC;
+          mbar_wait(&empty[slot], ((gt / SC_NC) & 1) ^ 1);
+          if (leader) mbar_expect_tx(&full[slot], 2 * C1_BYTES);
+          const int row = it.us.off + it.c_begin + t * BC + 32 * crank;  // this CTA's 32 columns
+          uint8_t* dst = ring + slot * C1_BYTES;
+#pragma unroll
+          for (int c = 0; c < 4; ++c) tma_load_2d_2sm(dst + c * (C1_BYTES / 4), tm, &full[slot], it.hcol + c * 64, row);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------------------------------------------------------- MMA issuer (leader CTA)
+    if (leader) {
+      const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
+      constexpr uint32_t idesc_s = idesc_bf16_f32(2 * BR, BC, 0, 0);
+      const uint32_t c1_base = smem_u32(smem + SC_OFF_C1), c2_base = smem_u32(smem + SC_OFF_C2);
+      int gt = 0, mi = 0;
+      for (int n = 0;; ++n) {
+        const int k = q_read(n);
+        if (lane == 0) q_release(n);
+        if (k < 0) break;
+        Item it;
+        decode_item<TRANS>(a, k, crank, it);
+        if (it.ntiles == 0) continue;
+        mbar_wait(r_done, mi & 1);  // both CTAs' K and V rows in TMEM
+        for (int t = 0; t < it.ntiles; ++t, ++gt) {
+          const int slot = gt % SC_NC, b = gt & 1;
+          mbar_wait(&c1_full[slot], (gt / SC_NC) & 1);
+          mbar_wait(&c2_full[slot], (gt / SC_NC) & 1);
+          mbar_wait(&s_free[b], ((gt >> 1) & 1) ^ 1);
+          tc_fence_after();
+          const uint32_t c1 = c1_base + slot * C1_BYTES, c2 = c2_base + slot * C1_BYTES;
+          const uint32_t ts = tm + T_S0 + 128 * b;
+          if (elect_one()) {
+#pragma unroll
+            for (int kk = 0; kk < DH / 16; ++kk)  // dP^T = V dO^T
+              mma_bf16_ts_2sm(ts + 64, tm + T_R2 + kk * 8,
+                              desc_sw128(c2 + (kk >> 2) * (C1_BYTES / 4) + (kk & 3) * 32, 16, 1024), idesc_s, kk > 0);
+            mma_commit_2sm_mc(&c2_empty[slot], 0x3);
+#pragma unroll
+            for (int kk = 0; kk < DH / 16; ++kk)  // S^T = K Q^T
+              mma_bf16_ts_2sm(ts, tm + T_R1 + kk * 8,
+                              desc_sw128(c1 + (kk >> 2) * (C1_BYTES / 4) + (kk & 3) * 32, 16, 1024), idesc_s, kk > 0);
+            mma_commit_2sm_mc(&c1_empty[slot], 0x3);
+            mma_commit_2sm_mc(&s_full[b], 0x3);
+            if (t + 1 == it.ntiles) mma_commit_2sm_mc(r_free, 0x3);
+          }
+          __syncwarp();
+        }
+        ++mi;
+      }
+    }
+  } else if (warp >= 4) {
+    // ---------------------------------------------------------------- softmax + stores
+    const int q = warp & 3;
+    const int half = (warp - 4) >> 2;
+    const int row = q * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+    const int j_half = half * 32;
+    int gt = 0, mi = 0;
+    for (int n = 0;; ++n) {
+      const int k = q_read(n);
+      __syncwarp();
+      if (lane == 0) q_release(n);
+      if (k < 0) break;
+      Item it;
+      decode_item<TRANS>(a, k, crank, it);
+      if (it.ntiles == 0) continue;
+      const UserSpan& us = it.us;
+      const int my = it.r0 + row;  // this thread's key (user-local)
+      // K and V rows of this item into TMEM (this warp: rows q*32.., head dims half*128..)
+      if (mi > 0) mbar_wait(r_free, (mi - 1) & 1);
+      mbar_wait(r_full, mi & 1);
+      tc_fence_after();
+#pragma unroll 1
+      for (int op = 0; op < 2; ++op)
+#pragma unroll 1
+        for (int cc = 0; cc < 2; ++cc) {
+          const uint8_t* box = smem + (op ? SC_OFF_R2 : SC_OFF_R1) + (half * 2 + cc) * (RT_BYTES / 4);
+          uint32_t w[32];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const uint4 v = *reinterpret_cast<const uint4*>(box + sw128(row, j));
+            w[4 * j] = v.x; w[4 * j + 1] = v.y; w[4 * j + 2] = v.z; w[4 * j + 3] = v.w;
+          }
+          tmem_st32(tmem + (op ? T_R2 : T_R1) + half * 64 + cc * 32 + lane_off, w);
+        }
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(r_copied);
+      arrive_leader(r_done);
+      const long long my_ts = (my < us.L && a.jag.ts) ? a.jag.ts[(int64_t)us.off + my] : 0;
+      const bool need_ts = !a.causal && (it.r0 + BR > us.ns) && (it.r0 < it.kv_end);  // uniform
+      const int64_t st_row = ((int64_t)it.h * a.st_rows + a.koff[it.u] + my) * a.st_pitch;
+#pragma unroll 1
+      for (int t = 0; t < it.ntiles; ++t, ++gt) {
+        const int c0 = it.c_begin + t * BC;
+        const int b = gt & 1;
+        if (need_ts) {
+          const int i = threadIdx.x - 128;
+          named_bar_sync(1, 32 * NSM);
+          if (i < BC) sTs[i] = (c0 + i < us.L && a.jag.ts) ? a.jag.ts[us.off + c0 + i] : 0;
+          named_bar_sync(1, 32 * NSM);
+        }
+        mbar_wait(&s_full[b], (gt >> 1) & 1);
+        tc_fence_after();
+        uint32_t s[32], dp[32];
+        tmem_ld32(tmem + T_S0 + 128 * b + j_half + lane_off, s);
+        tmem_ld32(tmem + T_S0 + 128 * b + 64 + j_half + lane_off, dp);
+        tmem_ld_wait();
+        tc_fence_before();
+        arrive_leader(&s_free[b]);
+        const int cb = c0 + j_half;  // this warp's 32 query columns
+        uint32_t vis;
+        if (a.causal) {  // queries i >= key j, i < L
+          const int lo = min(max(my - cb, 0), 32), hi = min(max(us.L - cb, 0), 32);
+          const uint32_t below_hi = hi >= 32 ? 0xffffffffu : ((1u << hi) - 1u);
+          const uint32_t below_lo = lo >= 32 ? 0xffffffffu : ((1u << lo) - 1u);
+          vis = (my < us.L) ? (below_hi & ~below_lo) : 0u;
+        } else if (my < us.ns) {  // static keys: every query of the user
+          const int nvalid = us.L - cb;
+          vis = nvalid >= 32 ? 0xffffffffu : (nvalid <= 0 ? 0u : ((1u << nvalid) - 1u));
+        } else if (my < it.kv_end) {  // real-time keys: later non-static queries, and itself
+          vis = 0;
+          const int lo = min(max(us.ns - cb, 0), 32), hi = min(max(us.L - cb, 0), 32);
+          for (int jj = lo; jj < hi; ++jj) vis |= (uint32_t)(my_ts < sTs[j_half + jj]) << jj;
+          const int jd = my - cb;
+          if (jd >= 0 && jd < 32) vis |= 1u << jd;
+        } else {
+          vis = 0;
+        }
+        uint32_t pk[16], pp[16];
+#pragma unroll
+        for (int e = 0; e < 32; e += 2) {
+          const float s0 = __uint_as_float(s[e]), s1 = __uint_as_float(s[e + 1]);
+          const float g0 = fmaf(0.5f, sm100::tanh_approx(0.5f * s0), 0.5f);
+          const float g1 = fmaf(0.5f, sm100::tanh_approx(0.5f * s1), 0.5f);
+          float p0 = s0 * g0, p1 = s1 * g1;
+          float v0 = __uint_as_float(dp[e]) * fmaf(p0, 1.0f - g0, g0);
+          float v1 = __uint_as_float(dp[e + 1]) * fmaf(p1, 1.0f - g1, g1);
+          if (vis != 0xffffffffu) {
+            const bool m0 = (vis >> e) & 1u, m1 = (vis >> (e + 1)) & 1u;
+            v0 = m0 ? v0 : 0.f; p0 = m0 ? p0 : 0.f;
+            v1 = m1 ? v1 : 0.f; p1 = m1 ? p1 : 0.f;
+          }
+          pk[e >> 1] = pack2(v0, v1);
+          pp[e >> 1] = pack2(p0, p1);
+        }
+        // 64 contiguous bytes per row and matrix; lane pairs swap halves so one 256-bit store
+        // writes 16 whole row pieces
+        const int bb = lane & 1;
+        auto put = [&](__nv_bfloat16* base, const uint32_t* w) {
+          U8 own, oth;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            own.v[i] = bb ? w[8 + i] : w[i];
+            oth.v[i] = __shfl_xor_sync(0xffffffffu, bb ? w[i] : w[8 + i], 1);
+          }
+          __nv_bfloat16* p0 = base + st_row + cb + 16 * bb;
+          stg256(p0 - (int64_t)bb * a.st_pitch, bb ? oth : own);
+          stg256(p0 + (int64_t)(1 - bb) * a.st_pitch, bb ? own : oth);
+        };
+        put(a.st_ds, pk);
+        put(a.st_p, pp);
+      }
+      ++mi;
+    }
+  }
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc_2sm<512>(tmem);
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
 // Stored-score backward products (the DK kernel wrote P^T and dS^T of every visible key row):
 //
 //   MM_DV: dV_j = nu sum_i P^T_ji dO_i   rows = keys    A = P^T  (K-major: queries contiguous)
@@ -1298,7 +1623,7 @@ static mtgr_status_t launch_mode(const AttnIO& io, const void* c1, int64_t ld_c1
   cudaMemsetAsync(a2.ctr, 0, sizeof(int), st);
   const int pairs = std::max(1, std::min(num_sms_cached() / 2, a2.nitems));
   dim3 grid(2 * pairs, 1, 1);  // persistent CTA pairs
-  ProfScope ps(MODE == FWD ? PROF_ATTN_FWD : MODE == DV ? PROF_ATTN_DV : MODE == DK ? PROF_ATTN_DK : PROF_ATTN_DQ, st);
+  ProfScope ps(MODE == FWD ? PROF_ATTN_FWD : MODE == DV ? PROF_ATTN_DV : MODE == DK ? PROF_ATTN_DK_FUSED : PROF_ATTN_DQ, st);
   cudaFuncSetAttribute(attn_tc_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
   static const bool trace = getenv("MTGR_ATTN_TRACE") != nullptr;
   if (trace) {  // debug only: time-stamp one CTA pair's pipeline events
@@ -1339,7 +1664,7 @@ static MmLayout mm_layout(const mtgr_jagged_t& j, int H) {
 template <int M2>
 static mtgr_status_t launch_mm(const AttnIO& io, const void* amat, const void* b, int64_t ld_b,
                                const void* e, int64_t ld_e, const void* uu, int64_t ld_u,
-                               const MmLayout& l, const Args& args, cudaStream_t st) {
+                               const MmLayout& l, const Args& args, int prof, cudaStream_t st) {
   const int T = io.jag.total_tokens, d = io.d;
   CUtensorMap ta, tb, tu, to;
   MTGR_TRY(make_tmap_bf16(&ta, amat, (uint64_t)l.pitch, (uint64_t)io.H * l.rows, (uint64_t)l.pitch, 64,
@@ -1363,10 +1688,36 @@ static mtgr_status_t launch_mm(const AttnIO& io, const void* amat, const void* b
   a2.ctr = ctr + M2;
   cudaMemsetAsync(a2.ctr, 0, sizeof(int), st);
   const int pairs = std::max(1, std::min(num_sms_cached() / 2, a2.nitems));
-  ProfScope ps(M2 == MM_DV ? PROF_ATTN_DV : PROF_ATTN_DQ, st);
+  ProfScope ps(prof, st);
   cudaFuncSetAttribute(attn_mm_kernel<M2>, cudaFuncAttributeMaxDynamicSharedMemorySize, MM_SMEM_BYTES);
   attn_mm_kernel<M2><<<2 * pairs, 384, MM_SMEM_BYTES, st>>>(ta, tb, tu, to, a2);
   return check_launch("attn_mm");
+}
+
+static mtgr_status_t launch_sc(const AttnIO& io, const MmLayout& l, const Args& args, cudaStream_t st) {
+  const int T = io.jag.total_tokens, d = io.d;
+  CUtensorMap tc1, tc2, tr1, tr2;
+  MTGR_TRY(make_tmap_bf16(&tc1, io.q, d, T, io.ld, 64, BC / 2));   // Q columns (32 per CTA)
+  MTGR_TRY(make_tmap_bf16(&tc2, io.dO, d, T, io.d, 64, BC / 2));  // dO columns
+  MTGR_TRY(make_tmap_bf16(&tr1, io.k, d, T, io.ld, 64, BR));      // K rows
+  MTGR_TRY(make_tmap_bf16(&tr2, io.v, d, T, io.ld, 64, BR));      // V rows
+  Args a2 = args;
+  a2.causal = io.causal;
+  a2.pmax = ceil_div(io.jag.max_len, 2 * BR);
+  a2.nitems = io.jag.num_users * a2.pmax * io.H;
+  a2.st_pitch = l.pitch; a2.st_rows = l.rows;
+  a2.c_align = 1;
+  static int* ctr = nullptr;
+  if (ctr == nullptr) {
+    if (cudaMalloc(&ctr, sizeof(int)) != cudaSuccess) return set_error(MTGR_E_CUDA, "attention work counter");
+  }
+  a2.ctr = ctr;
+  cudaMemsetAsync(a2.ctr, 0, sizeof(int), st);
+  const int pairs = std::max(1, std::min(num_sms_cached() / 2, a2.nitems));
+  ProfScope ps(PROF_ATTN_SC, st);
+  cudaFuncSetAttribute(attn_sc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SC_SMEM_BYTES);
+  attn_sc_kernel<<<2 * pairs, 384, SC_SMEM_BYTES, st>>>(tc1, tc2, tr1, tr2, a2);
+  return check_launch("attn_sc");
 }
 
 }  // namespace tca
@@ -1415,7 +1766,9 @@ mtgr_status_t attn_tc_bwd_launch(const AttnIO& io, cudaStream_t st) {
     bf* sds = (bf*)(ws + l.ds);
     attn_koff_kernel<<<1, 1024, 0, st>>>(io.jag, io.causal, koff);
     MTGR_TRY(check_launch("attn_koff"));
-    {  // dK = nu dS^T Q (+ diag), * silu'(p_K); also stores P^T, dS^T
+    const char* fenv = getenv("MTGR_ATTN_FUSED_DK");  // A/B and tests: the fused DK kernel + stores
+    const bool fused_dk = fenv != nullptr && fenv[0] == '1';
+    if (fused_dk) {  // dK = nu dS^T Q (+ diag), * silu'(p_K); also stores P^T, dS^T
       Args a{};
       a.jag = io.jag; a.H = io.H; a.d = io.d;
       a.out = (bf*)io.dk; a.ld_out = io.ld_out; a.diag = io.diag_ds;
@@ -1424,6 +1777,22 @@ mtgr_status_t attn_tc_bwd_launch(const AttnIO& io, cudaStream_t st) {
       a.c_align = 1;
       MTGR_TRY(launch_mode<DK>(io, io.q, io.ld, io.dO, D, io.k, io.ld, io.v, io.ld, io.q, io.ld,
                                pre ? pre + D : nullptr, io.ld_pre, a, st));
+    } else {
+      {  // scores: S^T, dP^T -> P^T, dS^T
+        Args a{};
+        a.jag = io.jag; a.H = io.H; a.d = io.d;
+        a.st_p = sp; a.st_ds = sds; a.koff = koff;
+        MTGR_TRY(launch_sc(io, l, a, st));
+      }
+      {  // dK = nu dS^T Q (+ diag ds_jj q_j), * silu'(p_K)
+        Args a{};
+        a.jag = io.jag; a.H = io.H; a.d = io.d;
+        a.out = (bf*)io.dk; a.ld_out = io.ld_out; a.diag = io.diag_ds;
+        a.dbias = io.dbias ? io.dbias + D : nullptr;
+        a.koff = koff;
+        MTGR_TRY(launch_mm<MM_DV>(io, sds, io.q, io.ld, io.q, io.ld, pre ? pre + D : nullptr, io.ld_pre, l, a,
+                                  PROF_ATTN_DK, st));
+      }
     }
     {  // dV = nu P^T dO (+ diag a_jj dO_j), * silu'(p_V)
       Args a{};
@@ -1431,7 +1800,8 @@ mtgr_status_t attn_tc_bwd_launch(const AttnIO& io, cudaStream_t st) {
       a.out = (bf*)io.dv; a.ld_out = io.ld_out; a.diag = io.diag_a;
       a.dbias = io.dbias ? io.dbias + 2 * D : nullptr;
       a.koff = koff;
-      MTGR_TRY(launch_mm<MM_DV>(io, sp, io.dO, D, io.dO, D, pre ? pre + 2 * D : nullptr, io.ld_pre, l, a, st));
+      MTGR_TRY(launch_mm<MM_DV>(io, sp, io.dO, D, io.dO, D, pre ? pre + 2 * D : nullptr, io.ld_pre, l, a,
+                                PROF_ATTN_DV, st));
     }
     {  // dQ = nu dS K (+ diag ds_ii k_i), * silu'(p_Q)
       Args a{};
@@ -1439,7 +1809,7 @@ mtgr_status_t attn_tc_bwd_launch(const AttnIO& io, cudaStream_t st) {
       a.out = (bf*)io.dq; a.ld_out = io.ld_out; a.diag = io.diag_ds;
       a.dbias = io.dbias;
       a.koff = koff;
-      MTGR_TRY(launch_mm<MM_DQ>(io, sds, io.k, io.ld, io.k, io.ld, pre, io.ld_pre, l, a, st));
+      MTGR_TRY(launch_mm<MM_DQ>(io, sds, io.k, io.ld, io.k, io.ld, pre, io.ld_pre, l, a, PROF_ATTN_DQ, st));
     }
     return MTGR_OK;
   }

@@ -105,14 +105,17 @@ def _attn_case(name, seed=0):
     return cfg, seg, ts, qkvu, dO
 
 
-@pytest.fixture(params=["stored", "recompute"])
+@pytest.fixture(params=["stored", "stored_fused_dk", "recompute"])
 def bwd_path(request, monkeypatch):
-    """The tensor-core backward stores P^T / dS^T by default; MTGR_ATTN_RECOMPUTE=1 selects the
-    kernels that recompute the scores (the path used when the scratch would not fit)."""
+    """The tensor-core backward stores P^T / dS^T (score kernel + three GEMMs) by default;
+    MTGR_ATTN_FUSED_DK=1 makes the fused DK kernel write the scores instead; MTGR_ATTN_RECOMPUTE=1
+    selects the kernels that recompute the scores (the path used when the scratch would not fit)."""
+    monkeypatch.delenv("MTGR_ATTN_RECOMPUTE", raising=False)
+    monkeypatch.delenv("MTGR_ATTN_FUSED_DK", raising=False)
     if request.param == "recompute":
         monkeypatch.setenv("MTGR_ATTN_RECOMPUTE", "1")
-    else:
-        monkeypatch.delenv("MTGR_ATTN_RECOMPUTE", raising=False)
+    elif request.param == "stored_fused_dk":
+        monkeypatch.setenv("MTGR_ATTN_FUSED_DK", "1")
     return request.param
 
 
