@@ -43,6 +43,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-users", type=int, default=24, help="users in the CPU oracle sample (~10 s)")
     ap.add_argument("--backend", default="nccl")
+    ap.add_argument("--post-mlp", type=int, default=1, choices=[1, 2],
+                    help="post-gate MLP: one Linear (R#6) or Linear-SiLU-Linear (S:354 variant)")
     ap.add_argument("--mask", default="dynamic", choices=["dynamic", "causal"],
                     help="mask mode: MTGR's dynamic mask, or the causal mask of the Table 4 ablation")
     ap.add_argument("--tokens", action="store_true",
@@ -100,13 +102,15 @@ def step_flops(cfg, tokens, pairs):
     """Algorithmic FLOPs of one fwd+bwd step: fwd 10Ld^2 + 4dP, bwd 20Ld^2 + 8dP
     per layer (S recompute and redundant backward products are not counted)."""
     d, nl = cfg["d"], cfg["n_layers"]
-    return nl * (30.0 * tokens * d * d + 12.0 * d * pairs)
+    extra = 6.0 * tokens * d * d if cfg.get("post_mlp_layers", 1) == 2 else 0.0  # second Linear
+    return nl * (30.0 * tokens * d * d + 12.0 * d * pairs + extra)
 
 
 def kernel_algorithmic(cfg, tokens, pairs):
     """Per-step algorithmic FLOPs (tensor) or bytes (hbm) of each kernel kind."""
     d, nl = cfg["d"], cfg["n_layers"]
     T = tokens
+    p2 = 1.0 if cfg.get("post_mlp_layers", 1) == 2 else 0.0
     return {
         "attn_fwd": ("tensor", nl * 4.0 * d * pairs),
         # stored-score backward: the score kernel does the dP product (S^T is the recompute the
@@ -117,10 +121,12 @@ def kernel_algorithmic(cfg, tokens, pairs):
         "attn_bwd_dq": ("tensor", nl * 2.0 * d * pairs),
         # DK kernel that also forms dP (recompute path, MTGR_ATTN_RECOMPUTE / MTGR_ATTN_FUSED_DK)
         "attn_bwd_dk_fused": ("tensor", nl * 4.0 * d * pairs),
-        "gemm_qkvu": ("tensor", nl * 8.0 * T * d * d),
+        # post_mlp_layers == 2: the first post-gate Linear runs on the SiLU epilogue (qkvu kind),
+        # the second on the residual epilogue; each adds 2Td^2 to dgrad and wgrad
+        "gemm_qkvu": ("tensor", nl * (8.0 + 2.0 * p2) * T * d * d),
         "gemm_out": ("tensor", nl * 2.0 * T * d * d),
-        "gemm_dgrad": ("tensor", nl * 10.0 * T * d * d),
-        "gemm_wgrad": ("tensor", nl * 10.0 * T * d * d),
+        "gemm_dgrad": ("tensor", nl * (10.0 + 2.0 * p2) * T * d * d),
+        "gemm_wgrad": ("tensor", nl * (10.0 + 2.0 * p2) * T * d * d),
         # GLN fwd: read x, write y (bf16) + 2 fp32 stats; GLN bwd: read dy, x, (o, u, p_U) ...
         # GLN1 reads x, writes x~; GLN2 reads O and U (the gate), writes y~
         "gln_fwd": ("hbm", nl * T * ((4.0 * d + 8) + (6.0 * d + 8))),
@@ -208,7 +214,8 @@ def blas_threads():
 
 def time_oracle(cfg, wl, n_users, start=0):
     import oracle
-    ocfg = dict(d=cfg["d"], H=cfg["H"], mask_mode=cfg.get("mask_mode", "dynamic"))
+    ocfg = dict(d=cfg["d"], H=cfg["H"], mask_mode=cfg.get("mask_mode", "dynamic"),
+                post_mlp_layers=cfg.get("post_mlp_layers", 1))
     Ps = [synth.gen_layer_params(cfg, li) for li in range(cfg["n_layers"])]
     tok, secs = 0, 0.0
     for k in range(n_users):
@@ -245,6 +252,7 @@ def workload_desc(cfg, wl, world):
             "parallelism": f"dp{world}",
             "balancer": "FLOP-cost LPT" if wl.get("balance") == "flops" else "token-count LPT",
             "mask": cfg.get("mask_mode", "dynamic"),
+            "post_mlp_layers": cfg.get("post_mlp_layers", 1),
             "l2": "no flush: per-step activations are several GB (>> 126 MB L2)"}
 
 
@@ -292,7 +300,8 @@ def run_mtgr(args, cfg, rank, world, local_rank):
     X = np.concatenate([synth.gen_user_x(cfg, int(u), int(l)) for u, l in zip(users, Ls)])
     dZ = np.concatenate([synth.gen_user_dz(cfg, int(u), int(l)) for u, l in zip(users, Ls)])
     jb = m.JaggedBatch.build(wl["seg"], ts, dev, users=users)
-    lc = m.layer_cfg(cfg["d"], cfg["H"], cfg["groups"], mask_mode=cfg.get("mask_mode", "dynamic"))
+    lc = m.layer_cfg(cfg["d"], cfg["H"], cfg["groups"], mask_mode=cfg.get("mask_mode", "dynamic"),
+                     post_mlp_layers=cfg.get("post_mlp_layers", 1))
     Ps = [m.params_to_device(synth.gen_layer_params(cfg, li), dt, dev) for li in range(cfg["n_layers"])]
     stack = m.HstuStack(lc, Ps, dt, dev)
     stack.bind(jb)
@@ -512,7 +521,7 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    cfg = synth.config(args.config, mask_mode=args.mask)
+    cfg = synth.config(args.config, mask_mode=args.mask, post_mlp_layers=args.post_mlp)
     if args.impl == "reference":
         run_reference(args, cfg, rank, world)
         return

@@ -85,6 +85,9 @@ typedef struct {
                           MTGR_MASK_CAUSAL (1): the plain causal mask over the packed order,
                           m_ij = [j <= i] (HSTU's) -- the "w/o dynamic mask"
                           ablation of Table 4.  Other values: MTGR_E_ARG.          */
+  int32_t post_mlp_layers; /* "another MLP" above the gate: 0 or 1 = one Linear
+                              d->d + b2 (R#6); 2 = Linear(W2,b2) -> SiLU -> Linear(W3,b3)
+                              (S:354 reading; the f3 variant).  Other values: MTGR_E_ARG.   */
 } mtgr_layer_cfg_t;
 enum { MTGR_MASK_DYNAMIC = 0, MTGR_MASK_CAUSAL = 1 };
 
@@ -99,6 +102,8 @@ typedef struct {
   const float* gamma2; /* [G][d]   GLN2 (Eq.6, R#7)                                    */
   const float* beta2;  /* [G][d]                                                             */
   const float* rab_w;  /* [H][NB] or NULL when rab_buckets == 0                               */
+  const void* w3;      /* [d][d] second post-gate Linear (post_mlp_layers == 2), else unused  */
+  const float* b3;     /* [d]                                                                */
 } mtgr_layer_params_t;
 
 /* Parameter gradients, all fp32, same shapes as mtgr_layer_params_t.  They are SUMS over the
@@ -107,6 +112,7 @@ typedef struct {
   float* w1; float* b1; float* w2; float* b2;
   float* gamma1; float* beta1; float* gamma2; float* beta2;
   float* rab_w; /* may be NULL when rab is off */
+  float* w3; float* b3; /* post_mlp_layers == 2 only */
 } mtgr_layer_grads_t;
 
 /* ---------------------------------------------------------------- library info */

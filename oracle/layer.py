@@ -138,8 +138,16 @@ def layer_fwd_user(x, gid, n_s, n_r, n_c, ts, P, cfg, nu=None):
                             cfg.get("mask_mode", "dynamic"))
     y = o * u                                                            # Eq.6 gate
     yt, mu2, r2 = gln_fwd(y, gid, P["gamma2"], P["beta2"], eps)          # Eq.6 GroupLN
-    z = yt @ P["W2"].T + P["b2"] + x                                     # Eq.6 MLP + X
-    return z, LayerCache(x, gid, n_s, n_r, n_c, ts, nu, xt, mu1, r1, p, a, o, S, M, y, yt, mu2, r2)
+    if cfg.get("post_mlp_layers", 1) == 2:
+        # "another MLP" read as Linear -> SiLU -> Linear (R#6 variant)
+        hpre = yt @ P["W2"].T + P["b2"]
+        z = silu(hpre) @ P["W3"].T + P["b3"] + x
+    else:
+        hpre = None
+        z = yt @ P["W2"].T + P["b2"] + x                                 # Eq.6 MLP + X (R#6)
+    c = LayerCache(x, gid, n_s, n_r, n_c, ts, nu, xt, mu1, r1, p, a, o, S, M, y, yt, mu2, r2)
+    c.hpre = hpre
+    return z, c
 
 
 def layer_bwd_user(dz, c: LayerCache, P, cfg):
@@ -149,10 +157,20 @@ def layer_bwd_user(dz, c: LayerCache, P, cfg):
     d = c.x.shape[1]
     H = cfg["H"]
     g = {}
-    # z = yt W2^T + b2 + x
-    g["W2"] = dz.T @ c.yt
-    g["b2"] = dz.sum(axis=0)
-    dyt = dz @ P["W2"]
+    if getattr(c, "hpre", None) is not None:
+        # z = silu(hpre) W3^T + b3 + x,  hpre = yt W2^T + b2
+        h = silu(c.hpre)
+        g["W3"] = dz.T @ h
+        g["b3"] = dz.sum(axis=0)
+        dpre = (dz @ P["W3"]) * dsilu(c.hpre)
+        g["W2"] = dpre.T @ c.yt
+        g["b2"] = dpre.sum(axis=0)
+        dyt = dpre @ P["W2"]
+    else:
+        # z = yt W2^T + b2 + x
+        g["W2"] = dz.T @ c.yt
+        g["b2"] = dz.sum(axis=0)
+        dyt = dz @ P["W2"]
     # yt = GLN2(y)
     dy, g["gamma2"], g["beta2"] = gln_bwd(dyt, c.y, c.gid, c.mu2, c.r2, P["gamma2"])
     # y = o * u

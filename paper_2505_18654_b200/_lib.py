@@ -36,10 +36,10 @@ class Jagged(ctypes.Structure):
 class LayerCfg(ctypes.Structure):
     _fields_ = [("d_model", c_int32), ("n_heads", c_int32), ("num_groups", c_int32),
                 ("rab_buckets", c_int32), ("eps", c_float), ("qkvu_silu", c_int32),
-                ("mask_mode", c_int32)]
+                ("mask_mode", c_int32), ("post_mlp_layers", c_int32)]
 
 
-_PNAMES = ("w1", "b1", "w2", "b2", "gamma1", "beta1", "gamma2", "beta2", "rab_w")
+_PNAMES = ("w1", "b1", "w2", "b2", "gamma1", "beta1", "gamma2", "beta2", "rab_w", "w3", "b3")
 
 
 class LayerParams(ctypes.Structure):

@@ -114,9 +114,9 @@ MASK_MODES = {"dynamic": 0, "causal": 1}  # include/mtgr.h MTGR_MASK_*
 
 
 def layer_cfg(d_model, n_heads, num_groups=4, rab_buckets=0, eps=1e-6, qkvu_silu=True,
-              mask_mode="dynamic") -> LayerCfg:
+              mask_mode="dynamic", post_mlp_layers=1) -> LayerCfg:
     return LayerCfg(d_model, n_heads, num_groups, rab_buckets, eps, 1 if qkvu_silu else 0,
-                    MASK_MODES[mask_mode])
+                    MASK_MODES[mask_mode], post_mlp_layers)
 
 
 def validate_jagged(jb: JaggedBatch, num_groups: int):
@@ -190,9 +190,9 @@ def attn_bwd(cfg: LayerCfg, jb: JaggedBatch, dO, q, k, v, ld, rab_w=None, silu_p
 
 # ------------------------------------------------------------------ layer
 
-PARAM_KEYS = ("W1", "b1", "W2", "b2", "gamma1", "beta1", "gamma2", "beta2", "rab_w")
+PARAM_KEYS = ("W1", "b1", "W2", "b2", "gamma1", "beta1", "gamma2", "beta2", "rab_w", "W3", "b3")
 _C_NAMES = dict(W1="w1", b1="b1", W2="w2", b2="b2", gamma1="gamma1", beta1="beta1",
-                gamma2="gamma2", beta2="beta2", rab_w="rab_w")
+                gamma2="gamma2", beta2="beta2", rab_w="rab_w", W3="w3", b3="b3")
 
 
 def params_to_device(p: dict, dtype: torch.dtype, device) -> dict:
@@ -200,7 +200,7 @@ def params_to_device(p: dict, dtype: torch.dtype, device) -> dict:
     out = {}
     for k, v in p.items():
         t = torch.as_tensor(np.asarray(v, dtype=np.float32))
-        out[k] = t.to(device=device, dtype=dtype if k in ("W1", "W2") else torch.float32).contiguous()
+        out[k] = t.to(device=device, dtype=dtype if k in ("W1", "W2", "W3") else torch.float32).contiguous()
     return out
 
 
@@ -210,7 +210,8 @@ def _cparams(p: dict) -> LayerParams:
 
 def grad_numel(cfg: LayerCfg) -> int:
     d, G = cfg.d_model, cfg.num_groups
-    return 5 * d * d + 5 * d + 4 * G * d + (cfg.n_heads * cfg.rab_buckets if cfg.rab_buckets > 0 else 0)
+    return (5 * d * d + 5 * d + 4 * G * d + (cfg.n_heads * cfg.rab_buckets if cfg.rab_buckets > 0 else 0)
+            + (d * d + d if cfg.post_mlp_layers == 2 else 0))
 
 
 def alloc_grads(cfg: LayerCfg, device, flat: torch.Tensor | None = None) -> dict:
@@ -222,6 +223,8 @@ def alloc_grads(cfg: LayerCfg, device, flat: torch.Tensor | None = None) -> dict
                   gamma2=(G, d), beta2=(G, d))
     if cfg.rab_buckets > 0:
         shapes["rab_w"] = (cfg.n_heads, cfg.rab_buckets)
+    if cfg.post_mlp_layers == 2:
+        shapes["W3"], shapes["b3"] = (d, d), (d,)
     g, off = {}, 0
     for k, shp in shapes.items():
         n = int(np.prod(shp))

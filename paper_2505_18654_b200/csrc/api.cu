@@ -57,6 +57,7 @@ static mtgr_status_t check_cfg(const mtgr_layer_cfg_t* c) {
   MTGR_CHECK(c->eps > 0.f, MTGR_E_ARG, "eps must be positive");
   MTGR_CHECK(c->mask_mode == MTGR_MASK_DYNAMIC || c->mask_mode == MTGR_MASK_CAUSAL, MTGR_E_ARG,
              "mask_mode must be MTGR_MASK_DYNAMIC or MTGR_MASK_CAUSAL");
+  MTGR_CHECK(c->post_mlp_layers >= 0 && c->post_mlp_layers <= 2, MTGR_E_ARG, "post_mlp_layers must be 0, 1 or 2");
   return MTGR_OK;
 }
 
@@ -80,9 +81,10 @@ static size_t esize(mtgr_dtype_t d) { return d == MTGR_BF16 ? 2 : 4; }
 
 // ------------------------------------------------------------------ saved-buffer layout
 struct SavedLayout {
-  size_t xt, p, a, o, yt, mu1, r1, mu2, r2, total;
+  size_t xt, p, a, o, yt, mu1, r1, mu2, r2, h, hds, total;
 };
-static SavedLayout saved_layout(int d, int ntok, size_t es) {
+// post2: the 2-layer post-gate MLP also saves its hidden activation and SiLU' (R#6 variant)
+static SavedLayout saved_layout(int d, int ntok, size_t es, bool post2 = false) {
   SavedLayout s;
   size_t off = 0;
   auto take = [&](size_t bytes) { size_t o = off; off = align_up(off + bytes, 256); return o; };
@@ -96,6 +98,8 @@ static SavedLayout saved_layout(int d, int ntok, size_t es) {
   s.r1 = take(T * 4);
   s.mu2 = take(T * 4);
   s.r2 = take(T * 4);
+  s.h = post2 ? take(T * d * es) : 0;
+  s.hds = post2 ? take(T * d * es) : 0;
   s.total = off;
   return s;
 }
@@ -128,7 +132,7 @@ static size_t fwd_ws_bytes(const mtgr_layer_cfg_t* c, int ntok, mtgr_dtype_t dt,
   size_t b = attn_ws_bytes(ntok, c->n_heads);
   b += std::max(gemm_ws_bytes(ntok, 4 * c->d_model, c->d_model, EPI_QKVU, dt == MTGR_BF16),
                 gemm_ws_bytes(ntok, c->d_model, c->d_model, EPI_RESID, dt == MTGR_BF16));
-  if (inference) b += saved_layout(c->d_model, ntok, esize(dt)).total;
+  if (inference) b += saved_layout(c->d_model, ntok, esize(dt), c->post_mlp_layers == 2).total;
   return b;
 }
 
@@ -169,7 +173,8 @@ static mtgr_status_t layer_fwd_t(const mtgr_layer_cfg_t* c, const mtgr_jagged_t*
                                  const mtgr_layer_params_t* P, const T* x, T* z, char* saved,
                                  char* ws, size_t wsb, cudaStream_t st) {
   const int d = c->d_model, ntok = j->total_tokens;
-  SavedLayout L = saved_layout(d, ntok, sizeof(T));
+  const bool post2 = c->post_mlp_layers == 2;
+  SavedLayout L = saved_layout(d, ntok, sizeof(T), post2);
   Carve cw(ws, wsb);
   char* sv = saved;
   if (!sv) sv = cw.take<char>(L.total);
@@ -200,6 +205,21 @@ static mtgr_status_t layer_fwd_t(const mtgr_layer_cfg_t* c, const mtgr_jagged_t*
   // Y~ = GroupLN2(O (.) U)  (Eq.6)
   MTGR_TRY(gln_fwd_launch<T>(o, j->group_id, P->gamma2, P->beta2, yt, mu2, r2, ntok, d, c->eps, st,
                              a + 3 * d, 4 * d));
+  if (post2) {  // H = silu(Y~ W2^T + b2) (and SiLU'), Z = H W3^T + b3 + X  (R#6 variant)
+    T* hh = (T*)(sv + L.h); T* hds = (T*)(sv + L.hds);
+    GemmIO h1{};
+    h1.M = ntok; h1.N = d; h1.K = d;
+    h1.A = yt; h1.lda = d; h1.a_kmajor = 1;
+    h1.B = P->w2; h1.ldb = d; h1.b_kmajor = 1;
+    h1.C = hds; h1.ldc = d; h1.C2 = hh; h1.bias = P->b2; h1.silu = 1; h1.c_dsilu = 1;
+    MTGR_TRY(run_gemm<T>(h1, EPI_QKVU, gws, gws_bytes, st));
+    GemmIO h2{};
+    h2.M = ntok; h2.N = d; h2.K = d;
+    h2.A = hh; h2.lda = d; h2.a_kmajor = 1;
+    h2.B = P->w3; h2.ldb = d; h2.b_kmajor = 1;
+    h2.C = z; h2.ldc = d; h2.bias = P->b3; h2.R = x; h2.ldr = d;
+    return run_gemm<T>(h2, EPI_RESID, gws, gws_bytes, st);
+  }
   // Z = Y~ W2^T + b2 + X  (Eq.6)
   GemmIO h{};
   h.M = ntok; h.N = d; h.K = d;
@@ -216,7 +236,8 @@ static mtgr_status_t layer_bwd_t(const mtgr_layer_cfg_t* c, const mtgr_jagged_t*
                                  const T* dz, T* dx, const mtgr_layer_grads_t* G, int acc,
                                  char* ws, size_t wsb, cudaStream_t st) {
   const int d = c->d_model, ntok = j->total_tokens, H = c->n_heads;
-  SavedLayout L = saved_layout(d, ntok, sizeof(T));
+  const bool post2 = c->post_mlp_layers == 2;
+  SavedLayout L = saved_layout(d, ntok, sizeof(T), post2);
   const T* xt = (const T*)(sv + L.xt); const T* p = (const T*)(sv + L.p);
   const T* a = (const T*)(sv + L.a); const T* o = (const T*)(sv + L.o);
   const T* yt = (const T*)(sv + L.yt);
@@ -236,6 +257,7 @@ static mtgr_status_t layer_bwd_t(const mtgr_layer_cfg_t* c, const mtgr_jagged_t*
   if (!acc && ntok > 0) {
     cudaMemsetAsync(G->b1, 0, sizeof(float) * 4 * d, st);
     cudaMemsetAsync(G->b2, 0, sizeof(float) * d, st);
+    if (post2) cudaMemsetAsync(G->b3, 0, sizeof(float) * d, st);
   }
   const bool tc_attn = std::is_same<T, __nv_bfloat16>::value && c->rab_buckets == 0 &&
                        attn_tc_supported(d / H);
@@ -246,12 +268,48 @@ static mtgr_status_t layer_bwd_t(const mtgr_layer_cfg_t* c, const mtgr_jagged_t*
       cudaMemsetAsync(G->b1, 0, sizeof(float) * 4 * d, st);
       cudaMemsetAsync(G->w2, 0, sizeof(float) * d * d, st);
       cudaMemsetAsync(G->b2, 0, sizeof(float) * d, st);
+      if (post2) {
+        cudaMemsetAsync(G->w3, 0, sizeof(float) * d * d, st);
+        cudaMemsetAsync(G->b3, 0, sizeof(float) * d, st);
+      }
       for (float* q : {G->gamma1, G->beta1, G->gamma2, G->beta2})
         cudaMemsetAsync(q, 0, sizeof(float) * c->num_groups * d, st);
     }
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? MTGR_OK : set_error(MTGR_E_CUDA, "layer_bwd: %s", cudaGetErrorString(e));
   }
+  if (post2) {
+    // Z = H W3^T + b3 + X, H = silu(Y~ W2^T + b2):  dW3 = dZ^T H, db3 = sum dZ (GLN1 backward),
+    // dPre = (dZ W3) (.) silu', dW2 = dPre^T Y~, db2 = sum dPre, dY~ = dPre W2.  dPre lives in
+    // the dO buffer until the GLN2 backward overwrites it.
+    const T* hh = (const T*)(sv + L.h); const T* hds = (const T*)(sv + L.hds);
+    GemmIO g3{};
+    g3.M = d; g3.N = d; g3.K = ntok;
+    g3.A = dz; g3.lda = d; g3.a_kmajor = 0;
+    g3.B = hh; g3.ldb = d; g3.b_kmajor = 0;
+    g3.C = G->w3; g3.ldc = d; g3.accumulate = acc;
+    MTGR_TRY(run_gemm<T>(g3, EPI_F32, scratch, scratch_bytes, st));
+    GemmIO h3{};
+    h3.M = ntok; h3.N = d; h3.K = d;
+    h3.A = dz; h3.lda = d; h3.a_kmajor = 1;
+    h3.B = P->w3; h3.ldb = d; h3.b_kmajor = 0;
+    h3.C = dO; h3.ldc = d;
+    MTGR_TRY(run_gemm<T>(h3, EPI_STORE, scratch, scratch_bytes, st));
+    MTGR_TRY(mul_launch<T>(dO, hds, dO, (int64_t)ntok * d, st));
+    GemmIO g2{};
+    g2.M = d; g2.N = d; g2.K = ntok;
+    g2.A = dO; g2.lda = d; g2.a_kmajor = 0;
+    g2.B = yt; g2.ldb = d; g2.b_kmajor = 0;
+    g2.C = G->w2; g2.ldc = d; g2.accumulate = acc;
+    MTGR_TRY(run_gemm<T>(g2, EPI_F32, scratch, scratch_bytes, st));
+    MTGR_TRY(colsum_launch<T>(dO, d, ntok, d, G->b2, (float*)scratch, 1, st));
+    GemmIO h2{};
+    h2.M = ntok; h2.N = d; h2.K = d;
+    h2.A = dO; h2.lda = d; h2.a_kmajor = 1;
+    h2.B = P->w2; h2.ldb = d; h2.b_kmajor = 0;
+    h2.C = buf; h2.ldc = d;
+    MTGR_TRY(run_gemm<T>(h2, EPI_STORE, scratch, scratch_bytes, st));
+  } else {
   // dW2 = dZ^T Y~, db2 = sum dZ, dY~ = dZ W2
   GemmIO g{};
   g.M = d; g.N = d; g.K = ntok;
@@ -265,6 +323,7 @@ static mtgr_status_t layer_bwd_t(const mtgr_layer_cfg_t* c, const mtgr_jagged_t*
   h.B = P->w2; h.ldb = d; h.b_kmajor = 0;
   h.C = buf; h.ldc = d;
   MTGR_TRY(run_gemm<T>(h, EPI_STORE, scratch, scratch_bytes, st));
+  }
   // GLN2 backward fused with the gate: dO = dY (.) U, dp_U = dY (.) O (.) silu'(p_U)
   GlnBwdIO gi{};
   gi.dy = buf; gi.x = nullptr;  // norm input x = O (.) U, recomputed from o and u
@@ -301,7 +360,7 @@ static mtgr_status_t layer_bwd_t(const mtgr_layer_cfg_t* c, const mtgr_jagged_t*
   GlnBwdIO gj{};
   gj.dy = buf; gj.x = x; gj.mean = mu1; gj.rstd = r1; gj.gamma = P->gamma1; gj.gid = j->group_id;
   gj.dx = dx; gj.ntok = ntok; gj.d = d; gj.G = c->num_groups; gj.dz = dz;
-  gj.dcol = G->b2;  // db2 = sum_t dZ fused into the GLN1 backward (which reads dZ anyway)
+  gj.dcol = post2 ? G->b3 : G->b2;  // the last bias: sum_t dZ fused into the GLN1 backward
   return gln_bwd_launch<T>(gj, GLNB_RESID, (float*)scratch, G->gamma1, G->beta1, acc, st);
 }
 
@@ -466,7 +525,7 @@ MTGR_API mtgr_status_t mtgr_hstu_attn_bwd(const mtgr_layer_cfg_t* cfg, const mtg
 MTGR_API size_t mtgr_layer_saved_bytes(const mtgr_layer_cfg_t* cfg, int32_t total_tokens,
                                        mtgr_dtype_t dtype) {
   if (!cfg || total_tokens < 0) return 0;
-  return saved_layout(cfg->d_model, total_tokens, esize(dtype)).total;
+  return saved_layout(cfg->d_model, total_tokens, esize(dtype), cfg->post_mlp_layers == 2).total;
 }
 
 MTGR_API size_t mtgr_layer_workspace_bytes(const mtgr_layer_cfg_t* cfg, const mtgr_jagged_t* jag,

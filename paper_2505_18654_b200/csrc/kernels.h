@@ -88,6 +88,8 @@ mtgr_status_t colsum_launch(const T* X, int64_t ld, int ntok, int n, float* out,
                             int accumulate, cudaStream_t st);
 size_t colsum_ws_bytes(int ntok, int n);
 mtgr_status_t scale_launch(float* g, int64_t n, float s, cudaStream_t st);
+template <class T>
+mtgr_status_t mul_launch(const T* a, const T* b, T* y, int64_t n, cudaStream_t st);  // y = a (.) b
 mtgr_status_t gate_mul_launch(const void* o, int64_t ldo, const void* u, int64_t ldu, void* y,
                               int64_t ldy, int ntok, int d, cudaStream_t st);
 mtgr_status_t mask_dense_launch(const mtgr_jagged_t& j, int user, uint8_t* out, cudaStream_t st);

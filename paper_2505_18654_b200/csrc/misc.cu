@@ -1,3 +1,4 @@
+#include <algorithm>
 // Small HBM-bound kernels: bias-gradient column sums, gradient scaling (P:360 aggregation),
 // the dense mask export and the jagged metadata validator.
 #include "common.cuh"
@@ -131,6 +132,23 @@ mtgr_status_t gate_mul_launch(const void* o, int64_t ldo, const void* u, int64_t
                                           (__nv_bfloat16*)y, ldy, ntok, d);
   return check_launch("gate_mul");
 }
+
+// ------------------------------------------------------------------ elementwise product
+template <class T>
+__global__ void mul_kernel(const T* a, const T* b, T* y, int64_t n) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+    y[e] = from_f<T>(to_f(a[e]) * to_f(b[e]));
+}
+template <class T>
+mtgr_status_t mul_launch(const T* a, const T* b, T* y, int64_t n, cudaStream_t st) {
+  if (n == 0) return MTGR_OK;
+  const int blocks = (int)std::min<int64_t>(ceil_div64(n, 256), 8 * num_sms());
+  mul_kernel<T><<<blocks, 256, 0, st>>>(a, b, y, n);
+  return check_launch("mul");
+}
+template mtgr_status_t mul_launch<float>(const float*, const float*, float*, int64_t, cudaStream_t);
+template mtgr_status_t mul_launch<__nv_bfloat16>(const __nv_bfloat16*, const __nv_bfloat16*, __nv_bfloat16*,
+                                                 int64_t, cudaStream_t);
 
 // ------------------------------------------------------------------ dense mask export
 // The exact composition the attention kernels use: the off-diagonal predicate on the key range

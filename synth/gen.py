@@ -149,6 +149,10 @@ def gen_layer_params(cfg: dict, layer: int, rab_buckets: int = 0) -> dict:
     }
     if rab_buckets:
         p["rab_w"] = (0.1 * rng.standard_normal((H, rab_buckets))).astype(np.float32)
+    if cfg.get("post_mlp_layers", 1) == 2:  # second post-gate Linear (its own stream)
+        r3 = _rng(cfg["seed"], _S_PARAM, layer, 3)
+        p["W3"] = _vals(cfg, r3.standard_normal((d, d)) * sd)
+        p["b3"] = (r3.standard_normal(d) * 0.02).astype(np.float32)
     return p
 
 

@@ -155,7 +155,7 @@ def _run_layer(dev, cfg, seg, ts, X, dZ, P, n_layers=1, Ps=None, inv_norm=None):
     dt = _dt(cfg)
     jb = m.JaggedBatch.build(seg, ts, dev, inv_norm=inv_norm)
     lc = m.layer_cfg(cfg["d"], cfg["H"], cfg["groups"], cfg.get("rab_buckets", 0),
-                     mask_mode=cfg.get("mask_mode", "dynamic"))
+                     mask_mode=cfg.get("mask_mode", "dynamic"), post_mlp_layers=cfg.get("post_mlp_layers", 1))
     Ps = Ps or [P]
     stack = m.HstuStack(lc, [m.params_to_device(p, dt, dev) for p in Ps], dt, dev)
     stack.bind(jb)
@@ -167,7 +167,8 @@ def _run_layer(dev, cfg, seg, ts, X, dZ, P, n_layers=1, Ps=None, inv_norm=None):
 
 def _oracle_stack(cfg, seg, ts, X, dZ, Ps, inv_norm=None, users=None):
     h = oracle.build_jagged(seg)
-    ocfg = dict(d=cfg["d"], H=cfg["H"], mask_mode=cfg.get("mask_mode", "dynamic"))
+    ocfg = dict(d=cfg["d"], H=cfg["H"], mask_mode=cfg.get("mask_mode", "dynamic"),
+                post_mlp_layers=cfg.get("post_mlp_layers", 1))
     Z = np.full(X.shape, np.nan)
     dX = np.full(X.shape, np.nan)
     tot = [None] * len(Ps)
@@ -216,6 +217,17 @@ def test_layer_causal_mask(dev, name, bwd_path):
     z, dx, grads = _run_layer(dev, cfg, seg, ts, X, dZ, P)
     Z, dX, G = _oracle_stack(cfg, seg, ts, X, dZ, [P])
     print(_compare(z, dx, grads, Z, dX, G, TOL[_dt(cfg)]))
+
+
+@pytest.mark.parametrize("name", ["toy", "parity", "parity768"])
+def test_layer_post_mlp2(dev, name):
+    """f3 variant: the 2-layer post-gate MLP (Linear-SiLU-Linear) through the C ABI."""
+    cfg, seg, ts, X, dZ, P = make_batch(name, post_mlp_layers=2)
+    z, dx, grads = _run_layer(dev, cfg, seg, ts, X, dZ, P)
+    Z, dX, G = _oracle_stack(cfg, seg, ts, X, dZ, [P])
+    errs = _compare(z, dx, grads, Z, dX, G, TOL[_dt(cfg)])
+    assert "L0.dW3" in errs and "L0.db3" in errs
+    print(errs)
 
 
 @pytest.mark.parametrize("name", ["toy", "parity"])

@@ -253,3 +253,57 @@ def test_mask_is_shared_by_layers():
     _, caches = stack_fwd_user(x, gid, 4, 5, 5, ts, Ps, CFG)
     np.testing.assert_array_equal(caches[0].M, caches[1].M)
     np.testing.assert_array_equal(caches[0].M, mask_dense(4, 5, 5, ts))
+
+
+# ---------------------------------------------------------------- 2-layer post-gate MLP (R#6 variant)
+
+def _params2(rng, d, H):
+    P = tiny_params(rng, d, H)
+    P["W3"] = rng.standard_normal((d, d)) / np.sqrt(d)
+    P["b3"] = rng.standard_normal(d) * 0.1
+    return P
+
+
+def test_post_mlp2_matches_torch_and_residual():
+    """post_mlp_layers=2: z - x = Linear(W3,b3)(SiLU(Linear(W2,b2)(GLN2(y)))) (torch.nn on the
+    layer's own yt); W3 = b3 = 0 gives the residual identity z = x."""
+    rng = np.random.default_rng(21)
+    d, H = 8, 2
+    x, gid, ts = tiny_user(rng, 3, 3, 2, d)
+    P = _params2(rng, d, H)
+    cfg2 = dict(CFG, post_mlp_layers=2)
+    z, c = layer_fwd_user(x, gid, 3, 3, 2, ts, P, cfg2)
+    net = torch.nn.Sequential(torch.nn.Linear(d, d), torch.nn.SiLU(), torch.nn.Linear(d, d)).double()
+    with torch.no_grad():
+        net[0].weight.copy_(torch.from_numpy(P["W2"])); net[0].bias.copy_(torch.from_numpy(P["b2"]))
+        net[2].weight.copy_(torch.from_numpy(P["W3"])); net[2].bias.copy_(torch.from_numpy(P["b3"]))
+        ref = net(torch.from_numpy(c.yt)).numpy()
+    np.testing.assert_allclose(z - x, ref, rtol=1e-12, atol=1e-12)
+    P0 = dict(P, W3=np.zeros((d, d)), b3=np.zeros(d))
+    np.testing.assert_array_equal(layer_fwd_user(x, gid, 3, 3, 2, ts, P0, cfg2)[0], x)
+
+
+def test_post_mlp2_backward_finite_differences():
+    rng = np.random.default_rng(22)
+    d, H = 8, 2
+    x, gid, ts = tiny_user(rng, 3, 3, 2, d)
+    P = _params2(rng, d, H)
+    cfg2 = dict(CFG, post_mlp_layers=2)
+    w = rng.standard_normal(x.shape)
+    z, c = layer_fwd_user(x, gid, 3, 3, 2, ts, P, cfg2)
+    dx, g = layer_bwd_user(w, c, P, cfg2)
+    f = lambda xx, PP: (layer_fwd_user(xx, gid, 3, 3, 2, ts, PP, cfg2)[0] * w).sum()
+    h = 1e-6
+    num = np.zeros_like(x)
+    for idx in np.ndindex(x.shape):
+        xp = x.copy(); xp[idx] += h
+        xm = x.copy(); xm[idx] -= h
+        num[idx] = (f(xp, P) - f(xm, P)) / (2 * h)
+    np.testing.assert_allclose(dx, num, rtol=1e-5, atol=1e-6)
+    for key in ("W2", "b2", "W3", "b3", "W1"):
+        num = np.zeros_like(P[key])
+        for idx in np.ndindex(P[key].shape):
+            Pp = dict(P); Pp[key] = P[key].copy(); Pp[key][idx] += h
+            Pm = dict(P); Pm[key] = P[key].copy(); Pm[key][idx] -= h
+            num[idx] = (f(x, Pp) - f(x, Pm)) / (2 * h)
+        np.testing.assert_allclose(g[key], num, rtol=1e-5, atol=1e-6, err_msg=key)
