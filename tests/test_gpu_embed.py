@@ -72,7 +72,11 @@ def test_sgd_evict_expand(dev):
     model.sgd(ids, g, 0.01)
     got = t.gather(slots).cpu().numpy()
     ref = model.lookup(ids, now=100)
-    np.testing.assert_allclose(got, ref, rtol=0, atol=2e-6)
+    _, inv, cnt = np.unique(ids, return_inverse=True, return_counts=True)
+    absum = np.zeros((len(cnt), 16))
+    np.add.at(absum, inv, np.abs(g))
+    bound = 0.01 * (cnt[:, None] * 2.0 ** -23) * absum + 1e-6  # fp32 atomics in any order
+    assert (np.abs(got - ref) <= bound[inv]).all()
     # touch half of the keys later, evict the rest
     u = np.unique(ids)
     late = u[::2]
@@ -119,9 +123,17 @@ def test_sharded_lookup_single_rank(dev):
     np.testing.assert_array_equal(rows.cpu().numpy(), model.lookup(ids).astype(np.float32))
     g = torch.randn(len(ids), 32, device=dev)
     emb.backward_sgd(g, ctx, lr=0.05)
-    model.sgd(ids, g.cpu().numpy(), 0.05)
+    gn = g.cpu().numpy()
+    model.sgd(ids, gn, 0.05)
     rows2, _ = emb.lookup(torch.from_numpy(ids).to(dev), now=2)
-    np.testing.assert_allclose(rows2.cpu().numpy(), model.lookup(ids), rtol=0, atol=1e-5)
+    # fp32 sums of n occurrences in an unspecified order: |error| <= lr * n * 2^-23 * sum|g| per
+    # column (the standard recursive-summation bound), plus the rounding of the row itself
+    _, inv, cnt = np.unique(ids, return_inverse=True, return_counts=True)
+    absum = np.zeros((len(cnt), 32))
+    np.add.at(absum, inv, np.abs(gn))
+    bound = 0.05 * (cnt[:, None] * 2.0 ** -23) * absum + 1e-6
+    err = np.abs(rows2.cpu().numpy() - model.lookup(ids))
+    assert (err <= bound[inv]).all(), float((err / bound[inv]).max())
 
 
 @pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2, reason="needs 2 GPUs")
