@@ -104,7 +104,10 @@ static SavedLayout saved_layout(int d, int ntok, size_t es, bool post2 = false) 
   return s;
 }
 
-size_t attn_ws_bytes(int ntok, int H) { return 2 * align_up((size_t)ntok * H * sizeof(float), 256); }
+// diag_a [T][H] | diag_ds [T][H] | 64 work-queue counters (public attention calls; the layer
+// calls carve the same pieces from their own workspace)
+size_t attn_ws_bytes(int ntok, int H) { return 2 * align_up((size_t)ntok * H * sizeof(float), 256) + 256; }
+static size_t attn_diag_half(int ntok, int H) { return align_up((size_t)ntok * H * sizeof(float), 256); }
 
 static bool tc_attn_path(const mtgr_layer_cfg_t* c, mtgr_dtype_t dt) {
   return dt == MTGR_BF16 && c->rab_buckets == 0 && c->n_heads > 0 && attn_tc_supported(c->d_model / c->n_heads);
@@ -179,6 +182,7 @@ static mtgr_status_t layer_fwd_t(const mtgr_layer_cfg_t* c, const mtgr_jagged_t*
   char* sv = saved;
   if (!sv) sv = cw.take<char>(L.total);
   float* diag = cw.take<float>((size_t)ntok * c->n_heads);
+  int* ctr = cw.take<int>(64);
   size_t gws_bytes = cw.cap > cw.used ? cw.cap - align_up(cw.used, 256) : 0;
   void* gws = cw.take<char>(0);
   T* xt = (T*)(sv + L.xt); T* p = (T*)(sv + L.p); T* a = (T*)(sv + L.a);
@@ -201,6 +205,7 @@ static mtgr_status_t layer_fwd_t(const mtgr_layer_cfg_t* c, const mtgr_jagged_t*
   at.jag = *j; at.causal = c->mask_mode == MTGR_MASK_CAUSAL; at.H = c->n_heads; at.dh = d / c->n_heads; at.d = d; at.nb = c->rab_buckets;
   at.q = a; at.k = a + d; at.v = a + 2 * d; at.ld = 4 * d;
   at.o = o; at.u = nullptr; at.y = nullptr; at.rab_w = P->rab_w;  // gate folded into GLN2
+  at.ctr = ctr;
   MTGR_TRY(run_attn_fwd<T>(at, diag, st));
   // Y~ = GroupLN2(O (.) U)  (Eq.6)
   MTGR_TRY(gln_fwd_launch<T>(o, j->group_id, P->gamma2, P->beta2, yt, mu2, r2, ntok, d, c->eps, st,
@@ -249,6 +254,7 @@ static mtgr_status_t layer_bwd_t(const mtgr_layer_cfg_t* c, const mtgr_jagged_t*
   T* dp = cw.take<T>((size_t)ntok * 4 * d);
   float* diag_a = cw.take<float>((size_t)ntok * H);
   float* diag_ds = cw.take<float>((size_t)ntok * H);
+  int* ctr = cw.take<int>(64);
   void* scratch = cw.take<char>(0);
   size_t scratch_bytes = cw.cap > cw.used ? cw.cap - align_up(cw.used, 256) : 0;
   if (c->rab_buckets > 0 && G->rab_w && !acc)
@@ -341,6 +347,7 @@ static mtgr_status_t layer_bwd_t(const mtgr_layer_cfg_t* c, const mtgr_jagged_t*
   at.rab_w = P->rab_w; at.drab = c->rab_buckets > 0 ? G->rab_w : nullptr;
   at.dbias = tc_attn ? G->b1 : nullptr;  // db1 of the Q|K|V blocks fused into the epilogues
   at.mm_ws = scratch; at.mm_ws_bytes = scratch_bytes;  // stored scores (free until the wgrad GEMM)
+  at.ctr = ctr;
   MTGR_TRY(run_attn_bwd<T>(at, diag_a, diag_ds, st));
   if (!tc_attn) MTGR_TRY(colsum_launch<T>(dp, 4 * d, ntok, 3 * d, G->b1, (float*)scratch, 1, st));
   // dW1 = dp^T X~, db1 = sum dp, dX~ = dp W1
@@ -487,6 +494,7 @@ MTGR_API mtgr_status_t mtgr_hstu_attn_fwd(const mtgr_layer_cfg_t* cfg, const mtg
   at.jag = *jag; at.causal = cfg->mask_mode == MTGR_MASK_CAUSAL; at.H = cfg->n_heads; at.dh = cfg->d_model / cfg->n_heads; at.d = cfg->d_model;
   at.nb = cfg->rab_buckets; at.q = q; at.k = k; at.v = v; at.ld = ld; at.u = u; at.o = o; at.y = y;
   at.rab_w = rab_w;
+  at.ctr = (int*)((char*)ws + 2 * attn_diag_half(jag->total_tokens, cfg->n_heads));
   cudaStream_t st = (cudaStream_t)stream;
   if (dtype == MTGR_BF16) return run_attn_fwd<__nv_bfloat16>(at, (float*)ws, st);
   return run_attn_fwd<float>(at, (float*)ws, st);
@@ -508,7 +516,7 @@ MTGR_API mtgr_status_t mtgr_hstu_attn_bwd(const mtgr_layer_cfg_t* cfg, const mtg
   MTGR_CHECK(aligned16(dO) && aligned16(q) && aligned16(k) && aligned16(v) && aligned16(dq) &&
                  aligned16(dk) && aligned16(dv),
              MTGR_E_LAYOUT, "attn_bwd: pointers must be 16-byte aligned");
-  const size_t half = attn_ws_bytes(jag->total_tokens, cfg->n_heads) / 2;
+  const size_t half = attn_diag_half(jag->total_tokens, cfg->n_heads);
   AttnIO at{};
   at.jag = *jag; at.causal = cfg->mask_mode == MTGR_MASK_CAUSAL; at.H = cfg->n_heads; at.dh = cfg->d_model / cfg->n_heads; at.d = cfg->d_model;
   at.nb = cfg->rab_buckets; at.q = q; at.k = k; at.v = v; at.ld = ld; at.dO = dO;
@@ -516,8 +524,9 @@ MTGR_API mtgr_status_t mtgr_hstu_attn_bwd(const mtgr_layer_cfg_t* cfg, const mtg
   at.rab_w = rab_w; at.drab = drab_w;
   float* da = (float*)ws;
   float* dd = (float*)((char*)ws + half);
-  at.mm_ws = (char*)ws + 2 * half;
-  at.mm_ws_bytes = ws_bytes > 2 * half ? ws_bytes - 2 * half : 0;
+  at.ctr = (int*)((char*)ws + 2 * half);
+  at.mm_ws = (char*)ws + 2 * half + 256;
+  at.mm_ws_bytes = ws_bytes > 2 * half + 256 ? ws_bytes - 2 * half - 256 : 0;
   if (dtype == MTGR_BF16) return run_attn_bwd<__nv_bfloat16>(at, da, dd, st);
   return run_attn_bwd<float>(at, da, dd, st);
 }

@@ -67,6 +67,7 @@ struct AttnIO {
   float* dbias;                // optional: column sums of the (bwd) outputs, red.add into
                                // dbias[col] for the Q|K|V blocks (tensor-core path only)
   void* mm_ws; size_t mm_ws_bytes;  // stored-score backward scratch (attn_store_ws_bytes), or NULL
+  int* ctr;                    // >= 8 device ints of workspace: the tensor-core work-queue counters
 };
 // scratch of the stored-score tensor-core backward for this batch (0: recompute path)
 size_t attn_store_ws_bytes(const mtgr_jagged_t& j, int H);

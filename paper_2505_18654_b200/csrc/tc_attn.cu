@@ -1615,11 +1615,8 @@ static mtgr_status_t launch_mode(const AttnIO& io, const void* c1, int64_t ld_c1
   a2.pre_dsilu = io.pre_dsilu;
   a2.pmax = ceil_div(io.jag.max_len, 2 * BR);
   a2.nitems = io.jag.num_users * a2.pmax * io.H;
-  static int* ctr = nullptr;
-  if (ctr == nullptr) {
-    if (cudaMalloc(&ctr, 4 * sizeof(int)) != cudaSuccess) return set_error(MTGR_E_CUDA, "attention work counter");
-  }
-  a2.ctr = ctr + MODE;
+  MTGR_CHECK(io.ctr != nullptr, MTGR_E_ARG, "attention: work-queue counters (workspace) missing");
+  a2.ctr = io.ctr + MODE;  // per-call counters in the caller's workspace (stream-safe)
   cudaMemsetAsync(a2.ctr, 0, sizeof(int), st);
   const int pairs = std::max(1, std::min(num_sms_cached() / 2, a2.nitems));
   dim3 grid(2 * pairs, 1, 1);  // persistent CTA pairs
@@ -1681,11 +1678,8 @@ static mtgr_status_t launch_mm(const AttnIO& io, const void* amat, const void* b
   a2.nitems = io.jag.num_users * a2.pmax * io.H;
   a2.st_pitch = l.pitch; a2.st_rows = l.rows;
   a2.c_align = 1;
-  static int* ctr = nullptr;
-  if (ctr == nullptr) {
-    if (cudaMalloc(&ctr, 2 * sizeof(int)) != cudaSuccess) return set_error(MTGR_E_CUDA, "attention work counter");
-  }
-  a2.ctr = ctr + M2;
+  MTGR_CHECK(io.ctr != nullptr, MTGR_E_ARG, "attention: work-queue counters (workspace) missing");
+  a2.ctr = io.ctr + 4 + M2;
   cudaMemsetAsync(a2.ctr, 0, sizeof(int), st);
   const int pairs = std::max(1, std::min(num_sms_cached() / 2, a2.nitems));
   ProfScope ps(prof, st);
@@ -1707,11 +1701,8 @@ static mtgr_status_t launch_sc(const AttnIO& io, const MmLayout& l, const Args& 
   a2.nitems = io.jag.num_users * a2.pmax * io.H;
   a2.st_pitch = l.pitch; a2.st_rows = l.rows;
   a2.c_align = 1;
-  static int* ctr = nullptr;
-  if (ctr == nullptr) {
-    if (cudaMalloc(&ctr, sizeof(int)) != cudaSuccess) return set_error(MTGR_E_CUDA, "attention work counter");
-  }
-  a2.ctr = ctr;
+  MTGR_CHECK(io.ctr != nullptr, MTGR_E_ARG, "attention: work-queue counters (workspace) missing");
+  a2.ctr = io.ctr + 6;
   cudaMemsetAsync(a2.ctr, 0, sizeof(int), st);
   const int pairs = std::max(1, std::min(num_sms_cached() / 2, a2.nitems));
   ProfScope ps(PROF_ATTN_SC, st);
