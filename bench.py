@@ -47,6 +47,9 @@ def parse():
                     help="post-gate MLP: one Linear (R#6) or Linear-SiLU-Linear (S:354 variant)")
     ap.add_argument("--mask", default="dynamic", choices=["dynamic", "causal"],
                     help="mask mode: MTGR's dynamic mask, or the causal mask of the Table 4 ablation")
+    ap.add_argument("--full-model", action="store_true",
+                    help="step = the whole training step: sparse IDs -> sharded hash-embedding lookup -> "
+                         "tokens -> stack -> head/BCE -> backward -> sparse SGD (paper_2505_18654_b200.model)")
     ap.add_argument("--tokens", action="store_true",
                     help="step also runs the Eq.4 token construction (SURVEY f2) before the stack and its backward after")
     ap.add_argument("--head", action="store_true",
@@ -327,7 +330,30 @@ def run_mtgr(args, cfg, rank, world, local_rank):
         emb.bind(jb, wl["seg"][users])
         tok = dict(emb=emb, feats=feats)
 
+    full = {}
+    if args.full_model:
+        ids = [synth.gen_user_feature_ids(cfg, int(u), wl["seg"][u]) for u in users]
+        lab = np.concatenate([synth.gen_user_labels(cfg, int(u), int(l)) for u, l in zip(users, Ls)])
+        uids = np.concatenate([i["u"].reshape(-1) for i in ids])
+        iids = np.concatenate([np.concatenate([i[t].reshape(-1) for i in ids]) for t in "src"])
+        model = m.MTGRModel(cfg, lc, [synth.gen_layer_params(cfg, li) for li in range(cfg["n_layers"])],
+                            synth.gen_token_params(cfg), synth.gen_head_params(cfg), synth.token_widths(cfg),
+                            synth.EMB_DIM, dt, dev, cap_user=1 << 20, cap_item=1 << 23)
+        model.bind(jb, wl["seg"][users])
+        stack = model.stack
+        full = dict(model=model, uids=torch.from_numpy(uids).to(dev), iids=torch.from_numpy(iids).to(dev),
+                    labels=torch.from_numpy(lab).to(dev), n_ids=len(uids) + len(iids), t=[0])
+
     def step(xin=x_dev, dzin=dz_dev):
+        if args.full_model:
+            full["t"][0] += 1
+            _, g = full["model"].step(full["uids"], full["iids"], full["labels"], now=full["t"][0],
+                                      on_layer_done=agg.on_layer_done)
+            if world > 1:
+                dist.all_reduce(torch.cat([t.reshape(-1) for t in g["head"].values()] +
+                                          [t.reshape(-1) for q in g["tokens"].values() for t in q.values()]))
+            agg.finish(full["model"].stack.grad_flat)
+            return
         if args.tokens:
             xin = tok["emb"].forward(tok["feats"]).contiguous()
         z = stack.forward(xin)
@@ -438,6 +464,10 @@ def run_mtgr(args, cfg, rank, world, local_rank):
                 "algorithmic_tflops_per_gpu": flops_rank * args.steps / (ms_max / 1000.0) / 1e12,
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
                 "gpu_launches": int(launches), "kernels": kernels, "impl": "mtgr"}
+        if args.full_model:
+            line["config"]["step"] = ("full training step: sharded hash-embedding lookup (two-stage unique, "
+                                      "all-to-all) -> Eq.4 tokens -> stack -> head/BCE -> backward -> sparse SGD")
+            line["config"]["sparse_ids_per_rank"] = full["n_ids"]
         if args.tokens:
             line["config"]["tokens"] = "Eq.4 token construction (U embeddings + per-type MLPs) fwd/bwd in the step"
         if args.head:

@@ -16,3 +16,4 @@ __all__ = ["MtgrError", "LIB_PATH", "lib", "SIGNATURES", "JaggedBatch", "HstuSta
            "layer_workspace_bytes", "params_to_device", "alloc_grads", "grad_numel", "scale_", "gemm", "launch_count", "prof_enable",
            "prof_reset", "prof_query", "head_params_to_device", "head_fwd_bwd", "TokenEmbed"]
 from .embed import HashEmbedding, ShardedEmbedding, unique, segment_sum, take_rows  # noqa: E402
+from .model import MTGRModel  # noqa: E402

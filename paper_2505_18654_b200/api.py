@@ -431,14 +431,18 @@ class TokenEmbed:
                                    _p(x), _p(self.saved), _p(self.ws), self.ws.numel(), _stream()))
         return x[:self.jb.total_tokens]
 
-    def backward(self, dx: torch.Tensor, want_dfeats: bool = True):
-        """Returns (dfeats dict or None, grads {"s","r","c"} -> {"w1","b1","w2","b2"} fp32 sums)."""
+    def backward(self, dx: torch.Tensor, want_dfeats: bool = True, out: dict | None = None):
+        """Returns (dfeats dict or None, grads {"s","r","c"} -> {"w1","b1","w2","b2"} fp32 sums).
+        `out`: optional preallocated feature-gradient tensors (e.g. views of one buffer)."""
         f = lambda *s: torch.empty(s, dtype=torch.float32, device=self.device)
         grads = {t: {"w1": f(*self.params[t]["w1"].shape), "b1": f(self.d), "w2": f(self.d, self.d), "b2": f(self.d)}
                  for t in ("s", "r", "c")}
         cg = TokenGrads(*(MlpParams(*(grads[t][k].data_ptr() for k in ("w1", "b1", "w2", "b2")))
                           for t in ("s", "r", "c")))
-        dfe = {t: torch.empty_like(v) for t, v in self.feats.items() if v is not None} if want_dfeats else {}
+        dfe = {}
+        if want_dfeats:
+            dfe = {t: (out[t] if out is not None and t in out else torch.empty_like(v))
+                   for t, v in self.feats.items() if v is not None}
         j = self.jb.c()
         check(lib().mtgr_token_bwd(ctypes.byref(self.cfg), ctypes.byref(j), _p(self.n_user), self.n_tot,
                                    _dt(self.dtype), ctypes.byref(self._cp),

@@ -1,0 +1,72 @@
+"""The whole MTGR training step on one rank (Fig.2(a), Eq.4, §5
+P:352-362): sparse feature IDs -> sharded dynamic-hash embedding lookup (two-stage unique +
+all-to-all) -> Eq.4 token construction -> HSTU encoder stack -> candidate head and the
+CTR/CTCVR loss, and back: dense gradients aggregated over the ranks, embedding rows
+updated by SGD on their owner shard.  Orchestration only: every step runs in libmtgr kernels;
+torch.distributed moves buffers between ranks.
+
+Two tables: U features (one d-wide embedding per profile token) and item features
+(EMB_DIM-wide embeddings, k_t / EMB_DIM of them concatenated per S / R / candidate token,
+P:297-301).  A token's feature IDs are laid out token-major, so the looked-up rows of a type are
+already its [n_t][k_t] feature matrix (a view, no copy).
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from .api import HstuStack, JaggedBatch, TokenEmbed, head_fwd_bwd, params_to_device, head_params_to_device
+from .embed import HashEmbedding, ShardedEmbedding
+
+
+class MTGRModel:
+    def __init__(self, cfg: dict, layer_cfg, layer_params: list, token_params: dict, head_params: dict,
+                 widths: dict, emb_dim: int, dtype: torch.dtype, device, cap_user: int, cap_item: int,
+                 lr_sparse: float = 1e-3, seed: int = 0, group=None):
+        self.cfg, self.dtype, self.device = cfg, dtype, torch.device(device)
+        self.d, self.emb_dim, self.lr_sparse = cfg["d"], emb_dim, lr_sparse
+        self.widths = widths
+        self.stack = HstuStack(layer_cfg, [params_to_device(p, dtype, device) for p in layer_params], dtype, device)
+        self.tokens = TokenEmbed(self.d, widths, TokenEmbed.params_to_device(token_params, dtype, device), dtype, device)
+        self.head = head_params_to_device(head_params, dtype, device)
+        self.user_table = ShardedEmbedding(HashEmbedding(self.d, cap_user, seed=seed, init_scale=0.5, device=device),
+                                           group)
+        self.item_table = ShardedEmbedding(HashEmbedding(emb_dim, cap_item, seed=seed + 1, init_scale=0.5,
+                                                         device=device), group)
+
+    def bind(self, jb: JaggedBatch, seg4: np.ndarray):
+        self.jb = jb
+        self.n = {t: int(np.asarray(seg4)[:, i].sum()) for i, t in enumerate("usrc")}
+        self.stack.bind(jb)
+        self.tokens.bind(jb, seg4)
+
+    def _item_views(self, buf: torch.Tensor) -> dict:
+        """Per-type [n_t][k_t] views of one [n_item_ids][emb_dim] buffer (S | R | candidates)."""
+        views, off = {}, 0
+        for t in "src":
+            n_ids = self.n[t] * (self.widths[t] // self.emb_dim)
+            views[t] = buf[off:off + n_ids].view(self.n[t], self.widths[t])
+            off += n_ids
+        return views
+
+    def step(self, user_ids: torch.Tensor, item_ids: torch.Tensor, labels: torch.Tensor, now: int = 0,
+             on_layer_done=None):
+        """user_ids: int64 [n_U] (one per profile token); item_ids: int64 [n_S F_s + n_r F_r +
+        n_C F_c] = the S, R and candidate tokens' feature IDs (user-major, token-major, feature
+        fastest), as the data loader packs them; labels: uint8 [T].
+        Returns (loss [2] sums, dense gradient sums)."""
+        # sparse lookups (one two-stage-unique all-to-all per table)
+        urows, uctx = self.user_table.lookup(user_ids, now, self.dtype)
+        irows, ictx = self.item_table.lookup(item_ids, now, self.dtype)
+        feats = dict(self._item_views(irows), u=urows)
+        # dense forward / loss / backward
+        x = self.tokens.forward(feats)
+        z = self.stack.forward(x.contiguous())
+        _, loss, dz, head_grads = head_fwd_bwd(self.jb, self.head, z, labels)
+        dx = self.stack.backward(dz, on_layer_done=on_layer_done)
+        ditem = torch.empty_like(irows)
+        dfeats, token_grads = self.tokens.backward(dx, out=self._item_views(ditem))
+        # sparse updates on the owners
+        self.user_table.backward_sgd(dfeats["u"], uctx, self.lr_sparse)
+        self.item_table.backward_sgd(ditem, ictx, self.lr_sparse)
+        return loss, {"head": head_grads, "tokens": token_grads, "layers": self.stack.grads}

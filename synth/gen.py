@@ -24,7 +24,7 @@ import numpy as np
 T0 = 1_700_000_000
 
 # stream ids
-_S_SEG, _S_TS, _S_X, _S_DZ, _S_PARAM, _S_LABEL, _S_HEAD, _S_FEAT, _S_TOK = 11, 12, 13, 14, 15, 16, 17, 18, 19
+_S_SEG, _S_TS, _S_X, _S_DZ, _S_PARAM, _S_LABEL, _S_HEAD, _S_FEAT, _S_TOK, _S_IDS = 11, 12, 13, 14, 15, 16, 17, 18, 19, 20
 
 CONFIGS = {
     # name: layers, d_model, heads, users (per rank), segment recipe, dtype, seed
@@ -211,4 +211,30 @@ def gen_token_params(cfg: dict) -> dict:
                   "b1": (rng.standard_normal(d) * 0.02).astype(np.float32),
                   "w2": _vals(cfg, rng.standard_normal((d, d)) / np.sqrt(d)),
                   "b2": (rng.standard_normal(d) * 0.02).astype(np.float32)}
+    return out
+
+
+EMB_DIM = 16  # item-feature embedding width (a token of k features has k ~ d / EMB_DIM)
+
+
+def features_per_token(cfg: dict) -> dict:
+    """Feature count per token type: U tokens are one d-wide feature each; item tokens
+    concatenate k_t / EMB_DIM feature embeddings (token_widths)."""
+    k = token_widths(cfg)
+    return {"u": 1, "s": k["s"] // EMB_DIM, "r": k["r"] // EMB_DIM, "c": k["c"] // EMB_DIM}
+
+
+def gen_user_feature_ids(cfg: dict, user: int, seg) -> dict:
+    """Sparse feature IDs of one user's tokens, int64 [n_t][F_t] per type: feature slot f of a
+    token carries (f << 40) | value, values Zipf(1.2)-distributed over a 2^24 vocabulary per slot
+    (long-tail popularity), so IDs of different slots never collide; U IDs live in slots >= 4096."""
+    rng = _rng(cfg["seed"], _S_IDS, user)
+    F = features_per_token(cfg)
+    n = dict(zip(TOKEN_TYPES, (int(v) for v in seg)))
+    out = {}
+    for t in TOKEN_TYPES:
+        vals = (rng.zipf(1.2, (n[t], F[t])) % (1 << 24)).astype(np.int64)
+        base = 4096 if t == "u" else 0
+        slots = (np.arange(F[t], dtype=np.int64) + base + {"u": 0, "s": 0, "r": 64, "c": 128}[t]) << 40
+        out[t] = vals + slots[None, :]
     return out
