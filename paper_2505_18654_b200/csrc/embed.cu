@@ -119,20 +119,16 @@ __global__ void hash_find_or_insert_kernel(mtgr_hash_table_t t, const long long*
   }
 }
 
+// Row kernels map one thread to one (row, column) element: rows are narrow (16-32 values), so
+// a warp per row would leave most lanes idle; consecutive threads walk a row, then the next.
 template <class T>
 __global__ void hash_gather_kernel(mtgr_hash_table_t t, const int* __restrict__ slots, int n, T* __restrict__ out) {
-  const int lane = threadIdx.x & 31;
-  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int nw = (gridDim.x * blockDim.x) >> 5;
-  for (int i = w; i < n; i += nw) {
+  const int64_t total = (int64_t)n * t.dim;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / t.dim;
+    const int c = (int)(e - i * t.dim);
     const int s = slots[i];
-    T* o = out + (int64_t)i * t.dim;
-    if (s < 0) {
-      for (int c = lane; c < t.dim; c += 32) o[c] = from_f<T>(0.f);
-    } else {
-      const float* r = t.values + (int64_t)s * t.dim;
-      for (int c = lane; c < t.dim; c += 32) o[c] = from_f<T>(r[c]);
-    }
+    out[e] = from_f<T>(s < 0 ? 0.f : t.values[(int64_t)s * t.dim + c]);
   }
 }
 
@@ -140,15 +136,12 @@ __global__ void hash_gather_kernel(mtgr_hash_table_t t, const int* __restrict__ 
 template <class T>
 __global__ void hash_sgd_kernel(mtgr_hash_table_t t, const int* __restrict__ slots, int n,
                                 const T* __restrict__ g, float lr) {
-  const int lane = threadIdx.x & 31;
-  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int nw = (gridDim.x * blockDim.x) >> 5;
-  for (int i = w; i < n; i += nw) {
+  const int64_t total = (int64_t)n * t.dim;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / t.dim;
+    const int c = (int)(e - i * t.dim);
     const int s = slots[i];
-    if (s < 0) continue;
-    float* r = t.values + (int64_t)s * t.dim;
-    const T* gi = g + (int64_t)i * t.dim;
-    for (int c = lane; c < t.dim; c += 32) atomicAdd(r + c, -lr * to_f(gi[c]));
+    if (s >= 0) atomicAdd(t.values + (int64_t)s * t.dim + c, -lr * to_f(g[e]));
   }
 }
 
@@ -230,43 +223,32 @@ __global__ void unique_kernel(const long long* __restrict__ ids, int n, long lon
 template <class T>
 __global__ void segsum_kernel(const T* __restrict__ g, const int* __restrict__ inverse, int n, int dim,
                               float* __restrict__ out) {
-  const int lane = threadIdx.x & 31;
-  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int nw = (gridDim.x * blockDim.x) >> 5;
-  for (int i = w; i < n; i += nw) {
-    float* o = out + (int64_t)inverse[i] * dim;
-    const T* gi = g + (int64_t)i * dim;
-    for (int c = lane; c < dim; c += 32) atomicAdd(o + c, to_f(gi[c]));
+  const int64_t total = (int64_t)n * dim;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / dim;
+    const int c = (int)(e - i * dim);
+    atomicAdd(out + (int64_t)inverse[i] * dim + c, to_f(g[e]));
   }
 }
 
-// rows out[i] = src[idx[i]] (dim columns)
-template <class T>
-__global__ void take_rows_kernel(const T* __restrict__ src, const int* __restrict__ idx, int n, int dim,
-                                 T* __restrict__ out) {
-  const int lane = threadIdx.x & 31;
-  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int nw = (gridDim.x * blockDim.x) >> 5;
-  for (int i = w; i < n; i += nw) {
-    const T* s = src + (int64_t)idx[i] * dim;
-    T* o = out + (int64_t)i * dim;
-    for (int c = lane; c < dim; c += 32) o[c] = s[c];
+// row moves, 16 bytes per thread when the row allows it (else one element):
+//   gather (PUT = 0): out[i] = src[idx[i]];   scatter (PUT = 1): out[idx[i]] = src[i]
+template <class V, int PUT>
+__global__ void move_rows_kernel(const V* __restrict__ src, const int* __restrict__ idx, int n, int vpr,
+                                 V* __restrict__ out) {
+  const int64_t total = (int64_t)n * vpr;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / vpr;
+    const int c = (int)(e - i * vpr);
+    const int64_t j = idx[i];
+    if (PUT) out[j * vpr + c] = src[e];
+    else out[e] = src[j * vpr + c];
   }
 }
 
-// rows out[idx[i]] = src[i] (dim columns; idx a permutation or injective)
-template <class T>
-__global__ void put_rows_kernel(const T* __restrict__ src, const int* __restrict__ idx, int n, int dim,
-                                T* __restrict__ out) {
-  const int lane = threadIdx.x & 31;
-  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int nw = (gridDim.x * blockDim.x) >> 5;
-  for (int i = w; i < n; i += nw) {
-    const T* s = src + (int64_t)i * dim;
-    T* o = out + (int64_t)idx[i] * dim;
-    for (int c = lane; c < dim; c += 32) o[c] = s[c];
-  }
-}
+template <int PUT>
+mtgr_status_t move_rows(const void* src, const int32_t* idx, int32_t n, int64_t row_bytes, void* out,
+                        cudaStream_t st);
 
 // owner partition for the all-to-all: dest(k) = mix64(k ^ salt) % world; per-destination counts
 // and each id's position in the destination-grouped send buffer (order within a destination:
@@ -295,7 +277,22 @@ __global__ void scan_small_kernel(const int* counts, int n, int* starts) {
 }
 
 int grid_for(int64_t work_items, int per_block) {
-  return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div64(work_items, per_block), 8 * 148));
+  return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div64(work_items, per_block), 16 * 148));
+}
+
+template <int PUT>
+mtgr_status_t move_rows(const void* src, const int32_t* idx, int32_t n, int64_t row_bytes, void* out,
+                        cudaStream_t st) {
+  if (row_bytes % 16 == 0) {
+    const int vpr = (int)(row_bytes / 16);
+    move_rows_kernel<uint4, PUT><<<grid_for((int64_t)n * vpr, 256), 256, 0, st>>>(
+        (const uint4*)src, idx, n, vpr, (uint4*)out);
+  } else {
+    const int vpr = (int)(row_bytes / 2);
+    move_rows_kernel<uint16_t, PUT><<<grid_for((int64_t)n * vpr, 256), 256, 0, st>>>(
+        (const uint16_t*)src, idx, n, vpr, (uint16_t*)out);
+  }
+  return check_launch(PUT ? "put_rows" : "take_rows");
 }
 
 mtgr_status_t check_table(const mtgr_hash_table_t* t) {
@@ -338,7 +335,7 @@ MTGR_API mtgr_status_t mtgr_hash_gather(const mtgr_hash_table_t* t, const int32_
   MTGR_CHECK(dtype == MTGR_F32 || dtype == MTGR_BF16, MTGR_E_DTYPE, "hash_gather: dtype");
   if (n == 0) return MTGR_OK;
   ProfScope ps(PROF_EMBED, (cudaStream_t)stream);
-  const int g = grid_for((int64_t)n * 32, 256);
+  const int g = grid_for((int64_t)n * t->dim, 256);
   if (dtype == MTGR_BF16)
     hash_gather_kernel<__nv_bfloat16><<<g, 256, 0, (cudaStream_t)stream>>>(*t, slots, n, (__nv_bfloat16*)out);
   else
@@ -353,7 +350,7 @@ MTGR_API mtgr_status_t mtgr_hash_sgd(const mtgr_hash_table_t* t, const int32_t* 
   MTGR_CHECK(dtype == MTGR_F32 || dtype == MTGR_BF16, MTGR_E_DTYPE, "hash_sgd: dtype");
   if (n == 0) return MTGR_OK;
   ProfScope ps(PROF_EMBED, (cudaStream_t)stream);
-  const int g = grid_for((int64_t)n * 32, 256);
+  const int g = grid_for((int64_t)n * t->dim, 256);
   if (dtype == MTGR_BF16)
     hash_sgd_kernel<__nv_bfloat16><<<g, 256, 0, (cudaStream_t)stream>>>(*t, slots, n, (const __nv_bfloat16*)grads, lr);
   else
@@ -416,7 +413,7 @@ MTGR_API mtgr_status_t mtgr_segment_sum(mtgr_dtype_t dtype, const void* g, const
   cudaMemsetAsync(out, 0, sizeof(float) * (size_t)n_out * dim, st);
   if (n == 0) return MTGR_OK;
   ProfScope ps(PROF_EMBED, st);
-  const int gr = grid_for((int64_t)n * 32, 256);
+  const int gr = grid_for((int64_t)n * dim, 256);
   if (dtype == MTGR_BF16) segsum_kernel<__nv_bfloat16><<<gr, 256, 0, st>>>((const __nv_bfloat16*)g, inverse, n, dim, out);
   else segsum_kernel<float><<<gr, 256, 0, st>>>((const float*)g, inverse, n, dim, out);
   return check_launch("segment_sum");
@@ -429,10 +426,7 @@ MTGR_API mtgr_status_t mtgr_take_rows(mtgr_dtype_t dtype, const void* src, const
   if (n == 0) return MTGR_OK;
   cudaStream_t st = (cudaStream_t)stream;
   ProfScope ps(PROF_EMBED, st);
-  const int gr = grid_for((int64_t)n * 32, 256);
-  if (dtype == MTGR_BF16) take_rows_kernel<__nv_bfloat16><<<gr, 256, 0, st>>>((const __nv_bfloat16*)src, idx, n, dim, (__nv_bfloat16*)out);
-  else take_rows_kernel<float><<<gr, 256, 0, st>>>((const float*)src, idx, n, dim, (float*)out);
-  return check_launch("take_rows");
+  return move_rows<0>(src, idx, n, (int64_t)dim * (dtype == MTGR_BF16 ? 2 : 4), out, st);
 }
 
 MTGR_API mtgr_status_t mtgr_put_rows(mtgr_dtype_t dtype, const void* src, const int32_t* idx, int32_t n,
@@ -442,10 +436,7 @@ MTGR_API mtgr_status_t mtgr_put_rows(mtgr_dtype_t dtype, const void* src, const 
   if (n == 0) return MTGR_OK;
   cudaStream_t st = (cudaStream_t)stream;
   ProfScope ps(PROF_EMBED, st);
-  const int gr = grid_for((int64_t)n * 32, 256);
-  if (dtype == MTGR_BF16) put_rows_kernel<__nv_bfloat16><<<gr, 256, 0, st>>>((const __nv_bfloat16*)src, idx, n, dim, (__nv_bfloat16*)out);
-  else put_rows_kernel<float><<<gr, 256, 0, st>>>((const float*)src, idx, n, dim, (float*)out);
-  return check_launch("put_rows");
+  return move_rows<1>(src, idx, n, (int64_t)dim * (dtype == MTGR_BF16 ? 2 : 4), out, st);
 }
 
 MTGR_API mtgr_status_t mtgr_partition_ids(const int64_t* ids, int32_t n, int32_t world, uint64_t salt,
