@@ -747,6 +747,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       const bool full_chunk = q * 32 + 32 <= nrows;
       const int row0 = us.off + it.r0;
       uint8_t* epi = smem + OFF_EPI;
+      // FWD has no SiLU' source: compile the element loop without it
+      const bool use_u = MODE != FWD && a.uu != nullptr;
+      const bool pre_ds = a.pre_dsilu != 0;
+      const bool any_e = __any_sync(0xffffffffu, has_e);  // warp-uniform: skip the E loads
       if (a.uu != nullptr) mbar_wait(eu_full, idx & 1);
       const bool do_bias = MODE != FWD && a.dbias != nullptr;
       uint32_t r[2][32];
@@ -769,9 +773,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
         for (int i = 0; i < 4; ++i) {
           const uint32_t off = sw128(row, j0 + i);
           uint4 ew = make_uint4(0u, 0u, 0u, 0u);
-          if (has_e) ew = __ldg(reinterpret_cast<const uint4*>(erow + cc * 32 + 8 * i));
+          if (any_e && has_e) ew = __ldg(reinterpret_cast<const uint4*>(erow + cc * 32 + 8 * i));
           uint4 uw = make_uint4(0u, 0u, 0u, 0u);
-          if (a.uu != nullptr) uw = *reinterpret_cast<const uint4*>(box + off);
+          if (use_u) uw = *reinterpret_cast<const uint4*>(box + off);
           const __nv_bfloat162* eh = reinterpret_cast<const __nv_bfloat162*>(&ew);
           const __nv_bfloat162* uh = reinterpret_cast<const __nv_bfloat162*>(&uw);
 #pragma unroll
@@ -779,10 +783,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
             const float2 fe = __bfloat1622float2(eh[kk]);
             float x0 = fmaf(us.nu, __uint_as_float(rc[8 * i + 2 * kk]), dg * fe.x);
             float x1 = fmaf(us.nu, __uint_as_float(rc[8 * i + 2 * kk + 1]), dg * fe.y);
-            if (a.uu != nullptr) {
+            if (use_u) {
               const float2 fu = __bfloat1622float2(uh[kk]);
-              x0 *= a.pre_dsilu ? fu.x : dsilu_fast(fu.x);
-              x1 *= a.pre_dsilu ? fu.y : dsilu_fast(fu.y);
+              x0 *= pre_ds ? fu.x : dsilu_fast(fu.x);
+              x1 *= pre_ds ? fu.y : dsilu_fast(fu.y);
             }
             v[8 * i + 2 * kk] = x0;
             v[8 * i + 2 * kk + 1] = x1;
