@@ -661,7 +661,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
               float p0 = s0 * g0, p1 = s1 * g1;
               float v0 = __uint_as_float(dp[e]) * fmaf(p0, 1.0f - g0, g0);
               float v1 = __uint_as_float(dp[e + 1]) * fmaf(p1, 1.0f - g1, g1);
-              if (vis != 0xffffffffu) {
+              {  // selects, no branch (masked entries are exact zeros, R#2)
                 const bool m0 = (vis >> e) & 1u, m1 = (vis >> (e + 1)) & 1u;
                 v0 = m0 ? v0 : 0.f; p0 = m0 ? p0 : 0.f;
                 v1 = m1 ? v1 : 0.f; p1 = m1 ? p1 : 0.f;
@@ -681,10 +681,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
               v0 = silu_fast(s0);
               v1 = silu_fast(s1);
             }
-            if (vis != 0xffffffffu) {
-              v0 = ((vis >> e) & 1u) ? v0 : 0.f;
-              v1 = ((vis >> (e + 1)) & 1u) ? v1 : 0.f;
-            }
+            v0 = ((vis >> e) & 1u) ? v0 : 0.f;  // selects, no branch (masked: exact zeros, R#2)
+            v1 = ((vis >> (e + 1)) & 1u) ? v1 : 0.f;
             pk[e >> 1] = pack2(v0, v1);
           }
           }
@@ -1168,7 +1166,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
           float p0 = s0 * g0, p1 = s1 * g1;
           float v0 = __uint_as_float(dp[e]) * fmaf(p0, 1.0f - g0, g0);
           float v1 = __uint_as_float(dp[e + 1]) * fmaf(p1, 1.0f - g1, g1);
-          if (vis != 0xffffffffu) {
+          {  // selects, no branch (masked entries are exact zeros, R#2)
             const bool m0 = (vis >> e) & 1u, m1 = (vis >> (e + 1)) & 1u;
             v0 = m0 ? v0 : 0.f; p0 = m0 ? p0 : 0.f;
             v1 = m1 ? v1 : 0.f; p1 = m1 ? p1 : 0.f;
