@@ -1759,8 +1759,13 @@ mtgr_status_t attn_tc_bwd_launch(const AttnIO& io, cudaStream_t st) {
     bf* sds = (bf*)(ws + l.ds);
     attn_koff_kernel<<<1, 1024, 0, st>>>(io.jag, io.causal, koff);
     MTGR_TRY(check_launch("attn_koff"));
-    const char* fenv = getenv("MTGR_ATTN_FUSED_DK");  // A/B and tests: the fused DK kernel + stores
-    const bool fused_dk = fenv != nullptr && fenv[0] == '1';
+    // score kernel + dK GEMM for short users, the fused DK kernel (which also writes the scores)
+    // for long ones, where its per-item epilogue is amortised: measured crossover between
+    // `small` (mean 1.0k tokens: score kernel 3% faster) and `large` (4.5k: fused 2% faster).
+    // MTGR_ATTN_FUSED_DK=1 / =0 forces either (A/B and tests)
+    const char* fenv = getenv("MTGR_ATTN_FUSED_DK");
+    const bool fused_dk = fenv != nullptr ? fenv[0] == '1'
+                                          : (int64_t)io.jag.total_tokens >= (int64_t)2048 * io.jag.num_users;
     if (fused_dk) {  // dK = nu dS^T Q (+ diag), * silu'(p_K); also stores P^T, dS^T
       Args a{};
       a.jag = io.jag; a.H = io.H; a.d = io.d;

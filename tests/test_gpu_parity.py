@@ -111,7 +111,7 @@ def bwd_path(request, monkeypatch):
     MTGR_ATTN_FUSED_DK=1 makes the fused DK kernel write the scores instead; MTGR_ATTN_RECOMPUTE=1
     selects the kernels that recompute the scores (the path used when the scratch would not fit)."""
     monkeypatch.delenv("MTGR_ATTN_RECOMPUTE", raising=False)
-    monkeypatch.delenv("MTGR_ATTN_FUSED_DK", raising=False)
+    monkeypatch.setenv("MTGR_ATTN_FUSED_DK", "0")  # the score kernel, whatever the user lengths
     if request.param == "recompute":
         monkeypatch.setenv("MTGR_ATTN_RECOMPUTE", "1")
     elif request.param == "stored_fused_dk":
