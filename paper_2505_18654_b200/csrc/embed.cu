@@ -61,61 +61,56 @@ __device__ int alloc_slot(const mtgr_hash_table_t& t) {
   return (int64_t)s < t.cap_v ? s : -2;
 }
 
-// warp per key: lane 0 probes; the claiming warp initialises the row with all lanes
+// thread per key: probe; a missing key is claimed with a CAS, the claiming thread allocates a
+// slot, initialises the row and publishes the slot (threads meeting a claimed bucket wait for
+// the publication; independent thread scheduling lets a waiting lane and the claiming lane of
+// the same warp both progress)
 __global__ void hash_find_or_insert_kernel(mtgr_hash_table_t t, const long long* __restrict__ ids, int n,
                                            long long now, int insert, int* __restrict__ out_slots) {
-  const int lane = threadIdx.x & 31;
-  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int nw = (gridDim.x * blockDim.x) >> 5;
   const uint64_t mask = (uint64_t)t.cap_k - 1;
-  for (int i = w; i < n; i += nw) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const long long k = ids[i];
-    int slot = -1, claimed = 0;
+    int slot = -1;
+    bool claimed = false;
     uint64_t b = mix64((uint64_t)k) & mask;
-    if (lane == 0) {
-      for (int64_t probe = 0; probe < t.cap_k; ++probe, b = (b + 1) & mask) {
-        long long cur = *reinterpret_cast<volatile long long*>(&t.keys[b]);
+    for (int64_t probe = 0; probe < t.cap_k; ++probe, b = (b + 1) & mask) {
+      long long cur = *reinterpret_cast<volatile long long*>(&t.keys[b]);
+      if (cur == KEY_EMPTY) {
+        if (!insert) break;
+        cur = (long long)atomicCAS(reinterpret_cast<unsigned long long*>(&t.keys[b]),
+                                   (unsigned long long)KEY_EMPTY, (unsigned long long)k);
         if (cur == KEY_EMPTY) {
-          if (!insert) { slot = -1; break; }
-          cur = (long long)atomicCAS(reinterpret_cast<unsigned long long*>(&t.keys[b]),
-                                     (unsigned long long)KEY_EMPTY, (unsigned long long)k);
-          if (cur == KEY_EMPTY) {  // claimed: allocate and publish below
-            slot = alloc_slot(t);
-            claimed = 1;
-            break;
-          }
-        }
-        if (cur == k) {  // present (possibly being published by another warp)
-          int s;
-          while ((s = *reinterpret_cast<volatile int*>(&t.slots[b])) == -1) {
-          }
-          slot = s;
+          slot = alloc_slot(t);
+          claimed = true;
           break;
         }
-        // another key or a tombstone: keep probing
       }
-      if (claimed) {
-        // remember the bucket in the slot's metadata before publishing
-        if (slot >= 0) t.slot_key[slot] = k;
-        else atomicAdd(&t.alloc[2], 1);  // value structure full: counted failure
+      if (cur == k) {  // present (possibly being published)
+        int s;
+        while ((s = *reinterpret_cast<volatile int*>(&t.slots[b])) == -1) {
+        }
+        slot = s;
+        break;
       }
+      // another key or a tombstone: keep probing
     }
-    slot = __shfl_sync(0xffffffffu, slot, 0);
-    claimed = __shfl_sync(0xffffffffu, claimed, 0);
-    if (claimed && slot >= 0) {
-      float* row = t.values + (int64_t)slot * t.dim;
-      for (int c = lane; c < t.dim; c += 32) row[c] = init_value(t.seed, k, c, t.init_scale);
-      if (lane == 0) t.counter[slot] = 0;
-      __threadfence();
-    }
-    if (lane == 0) {
-      if (claimed) *reinterpret_cast<volatile int*>(&t.slots[b]) = slot;  // publish (b = claimed bucket)
+    if (claimed) {
       if (slot >= 0) {
-        atomicAdd(&t.counter[slot], 1u);
-        t.ts[slot] = now;
+        t.slot_key[slot] = k;
+        float* row = t.values + (int64_t)slot * t.dim;
+        for (int c = 0; c < t.dim; ++c) row[c] = init_value(t.seed, k, c, t.init_scale);
+        t.counter[slot] = 0;
+        __threadfence();
+      } else {
+        atomicAdd(&t.alloc[2], 1);  // value structure full: counted failure
       }
-      out_slots[i] = slot;
+      *reinterpret_cast<volatile int*>(&t.slots[b]) = slot;  // publish
     }
+    if (slot >= 0) {
+      atomicAdd(&t.counter[slot], 1u);
+      t.ts[slot] = now;
+    }
+    out_slots[i] = slot;
   }
 }
 
@@ -323,7 +318,7 @@ MTGR_API mtgr_status_t mtgr_hash_find_or_insert(const mtgr_hash_table_t* t, cons
   MTGR_CHECK(n >= 0 && (n == 0 || (ids && slots)), MTGR_E_ARG, "hash_find_or_insert: bad ids / slots");
   if (n == 0) return MTGR_OK;
   ProfScope ps(PROF_EMBED, (cudaStream_t)stream);
-  hash_find_or_insert_kernel<<<grid_for((int64_t)n * 32, 256), 256, 0, (cudaStream_t)stream>>>(
+  hash_find_or_insert_kernel<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(
       *t, (const long long*)ids, n, (long long)now, insert ? 1 : 0, slots);
   return check_launch("hash_find_or_insert");
 }
