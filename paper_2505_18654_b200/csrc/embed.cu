@@ -226,6 +226,32 @@ __global__ void segsum_kernel(const T* __restrict__ g, const int* __restrict__ i
   }
 }
 
+// the same sums with per-block privatisation of the first `hot` unique rows in shared memory:
+// the unique index of an ID is its first-arrival order, so the hottest IDs of a Zipf stream
+// (which appear early) get small indices, and their many occurrences accumulate in shared
+// memory instead of serialising on the same global addresses; each block then adds its partial
+// rows once.  Blocks own contiguous row ranges.
+template <class T>
+__global__ void segsum_priv_kernel(const T* __restrict__ g, const int* __restrict__ inverse, int n, int dim,
+                                   int hot, float* __restrict__ out) {
+  extern __shared__ float acc[];  // [hot][dim]
+  for (int e = threadIdx.x; e < hot * dim; e += blockDim.x) acc[e] = 0.f;
+  __syncthreads();
+  const int64_t rows_per = ((int64_t)n + gridDim.x - 1) / gridDim.x;
+  const int64_t r0 = blockIdx.x * rows_per, r1 = min((int64_t)n, r0 + rows_per);
+  for (int64_t e = r0 * dim + threadIdx.x; e < r1 * dim; e += blockDim.x) {
+    const int64_t i = e / dim;
+    const int c = (int)(e - i * dim);
+    const int key = inverse[i];
+    const float v = to_f(g[e]);
+    if (key < hot) atomicAdd(&acc[key * dim + c], v);
+    else atomicAdd(out + (int64_t)key * dim + c, v);
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < hot * dim; e += blockDim.x)
+    if (acc[e] != 0.f) atomicAdd(out + e, acc[e]);
+}
+
 // row moves, 16 bytes per thread when the row allows it (else one element):
 //   gather (PUT = 0): out[i] = src[idx[i]];   scatter (PUT = 1): out[idx[i]] = src[i]
 template <class V, int PUT>
@@ -408,9 +434,21 @@ MTGR_API mtgr_status_t mtgr_segment_sum(mtgr_dtype_t dtype, const void* g, const
   cudaMemsetAsync(out, 0, sizeof(float) * (size_t)n_out * dim, st);
   if (n == 0) return MTGR_OK;
   ProfScope ps(PROF_EMBED, st);
-  const int gr = grid_for((int64_t)n * dim, 256);
-  if (dtype == MTGR_BF16) segsum_kernel<__nv_bfloat16><<<gr, 256, 0, st>>>((const __nv_bfloat16*)g, inverse, n, dim, out);
-  else segsum_kernel<float><<<gr, 256, 0, st>>>((const float*)g, inverse, n, dim, out);
+  // privatise the first `hot` unique rows per block (16 KB of shared memory); 8 blocks per SM,
+  // each over a contiguous range of rows so its flush is amortised
+  if (n >= 2 * n_out && dim <= 128) {  // many occurrences per row (stage 1 of a skewed stream)
+    const int hot = std::min(n_out, std::max(1, 4096 / dim));  // 16 KB of shared memory
+    const int gr = std::max(1, std::min(ceil_div(n, 32), 8 * 148));
+    const size_t sm = (size_t)hot * dim * sizeof(float);
+    if (dtype == MTGR_BF16)
+      segsum_priv_kernel<__nv_bfloat16><<<gr, 256, sm, st>>>((const __nv_bfloat16*)g, inverse, n, dim, hot, out);
+    else
+      segsum_priv_kernel<float><<<gr, 256, sm, st>>>((const float*)g, inverse, n, dim, hot, out);
+  } else {
+    const int gr = grid_for((int64_t)n * dim, 256);
+    if (dtype == MTGR_BF16) segsum_kernel<__nv_bfloat16><<<gr, 256, 0, st>>>((const __nv_bfloat16*)g, inverse, n, dim, out);
+    else segsum_kernel<float><<<gr, 256, 0, st>>>((const float*)g, inverse, n, dim, out);
+  }
   return check_launch("segment_sum");
 }
 
