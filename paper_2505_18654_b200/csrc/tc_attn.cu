@@ -252,10 +252,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     mbar_init(s_free, 2 * NSM);
     mbar_init(r1_full, 1);
     mbar_init(r1_done, 2 * NSM);
-    mbar_init(r1_copied, 32 * NSM);
+    mbar_init(r1_copied, NSM);
     mbar_init(r2a_full, 1);
     mbar_init(r2a_done, 2 * NSM);
-    mbar_init(r2a_copied, 32 * NSM);
+    mbar_init(r2a_copied, NSM);
     mbar_init(r2_full, 1);
     mbar_init(r1s_full, 1);
     mbar_init(o_full, 1);
@@ -308,10 +308,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     // ---------------------------------------------------------------- producer A: R1 / R2, C1
     if (lane == 0) {
       int gt = 0, mi = 0, idx = 0;
+      // the leader publishes one item ahead, so every role (the row-operand loader, the softmax
+      // warps' end-of-loop peek) learns the next item before this item's column tiles are issued
+      int k_next = leader ? q_push(0) : 0;
       for (int n = 0;; ++n) {
         int k;
         if (leader) {
-          k = q_push(n);
+          k = k_next;
+          if (k >= 0) k_next = q_push(n + 1);
         } else {
           k = q_read(n);
           q_release(n);
@@ -329,13 +333,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
         };
         auto wait_epi = [&]() { if (idx > 0) mbar_wait(epi_free, (idx - 1) & 1); };
         if (it.ntiles > 0) {
-          if (!TWO) {
-            if (mi > 0) mbar_wait(r1_copied, (mi - 1) & 1);  // staging free again
-            mbar_expect_tx(r1_full, RT_BYTES);
-#pragma unroll
-            for (int c = 0; c < 4; ++c) tma_load_2d(smem + OFF_R1STAGE + c * (RT_BYTES / 4), &tmR1, r1_full, it.hcol + c * 64, row0);
-            DBG(7, idx);
-          }
+          // (!TWO: the row operand is staged by warp 2, ahead of this item's column tiles)
           // TWO: the row operands are loaded as soon as the previous item's score MMAs are done
           // (they overlap its epilogue); the column ring doubles as that epilogue's tile, so the
           // column tiles wait for the epilogue to release it
@@ -382,15 +380,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       }
     }
   } else if (!TWO && warp == 2) {
-    // ---------------------------------------------------------------- !TWO: epilogue tile loader
+    // ---------------------------------------------------------------- !TWO: row operand + epilogue
+    // tile loader.  The next item's row operand is staged as soon as the softmax warps copied the
+    // previous one into TMEM, independently of the column-tile producer (which reaches the next
+    // item only after issuing this item's last tiles), so it has landed when the softmax warps
+    // move it into TMEM at the end of this item's tile loop
     if (lane == 0) {
-      int idx = 0;
+      int idx = 0, mi = 0;
       for (int n = 0;; ++n) {
         const int k = q_read(n);
         q_release(n);
         if (k < 0) break;
         Item it;
         decode_item<TRANS>(a, k, crank, it);
+        if (it.ntiles > 0) {
+          if (mi > 0) mbar_wait(r1_copied, (mi - 1) & 1);  // staging free again
+          mbar_expect_tx(r1_full, RT_BYTES);
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            tma_load_2d(smem + OFF_R1STAGE + c * (RT_BYTES / 4), &tmR1, r1_full, it.hcol + c * 64, it.us.off + it.r0);
+          ++mi;
+        }
         if (a.uu != nullptr) {
           if (idx > 0) mbar_wait(epi_free, (idx - 1) & 1);
           mbar_expect_tx(eu_full, RT_BYTES);
@@ -566,7 +576,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       }
       tmem_st_wait();
       tc_fence_before();
-      mbar_arrive(TWO ? r2a_copied : r1_copied);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(TWO ? r2a_copied : r1_copied);  // one arrival per warp
       arrive_leader(TWO ? r2a_done : r1_done);
       ++copied;
     };
