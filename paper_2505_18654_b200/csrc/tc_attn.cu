@@ -73,6 +73,8 @@ struct Args {
   int64_t st_pitch, st_rows;
   const int* koff;                          // [B+1] padded key-row offsets (multiples of 256)
   int causal;                               // MTGR_MASK_CAUSAL: m_ij = [j <= i]
+  int sc_cp;                                // score kernel: row operands via tcgen05.cp
+  int row_cp;                               // FWD / DV: row operand via tcgen05.cp
   int c_align;                              // TRANS items of real-time keys start their query
                                             // range at the 256-aligned pair holding n_static
 };
@@ -252,7 +254,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     mbar_init(s_free, 2 * NSM);
     mbar_init(r1_full, 1);
     mbar_init(r1_done, 2 * NSM);
-    mbar_init(r1_copied, NSM);
+    mbar_init(r1_copied, (!TWO && a.row_cp) ? 1 : NSM);  // tcgen05.cp: one commit arrival
     mbar_init(r2a_full, 1);
     mbar_init(r2a_done, 2 * NSM);
     mbar_init(r2a_copied, NSM);
@@ -395,10 +397,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
         decode_item<TRANS>(a, k, crank, it);
         if (it.ntiles > 0) {
           if (mi > 0) mbar_wait(r1_copied, (mi - 1) & 1);  // staging free again
-          mbar_expect_tx(r1_full, RT_BYTES);
+          if (a.row_cp) {  // both CTAs' rows on the leader's barrier: the MMA warp copies them
+            if (leader) mbar_expect_tx(r1_full, 2 * RT_BYTES);
 #pragma unroll
-          for (int c = 0; c < 4; ++c)
-            tma_load_2d(smem + OFF_R1STAGE + c * (RT_BYTES / 4), &tmR1, r1_full, it.hcol + c * 64, it.us.off + it.r0);
+            for (int c = 0; c < 4; ++c)
+              tma_load_2d_2sm(smem + OFF_R1STAGE + c * (RT_BYTES / 4), &tmR1, r1_full, it.hcol + c * 64,
+                              it.us.off + it.r0);
+          } else {
+            mbar_expect_tx(r1_full, RT_BYTES);
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+              tma_load_2d(smem + OFF_R1STAGE + c * (RT_BYTES / 4), &tmR1, r1_full, it.hcol + c * 64, it.us.off + it.r0);
+          }
           ++mi;
         }
         if (a.uu != nullptr) {
@@ -461,6 +471,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       const uint32_t c2_base = smem_u32(smem + OFF_C2);
       const uint32_t x_base = smem_u32(smem + OFF_X);
       int gt = 0, mi = 0, idx = 0;
+      int cp_done = 0;  // !TWO with row_cp: items whose row operand has been copied into TMEM
+      const uint32_t r1s_base = smem_u32(smem + OFF_R1STAGE);
+      // R1 staging (both CTAs) -> TMEM by tcgen05.cp, ordered after the MMAs issued so far; the
+      // commit frees the staging for the loader
+      auto copy_r1 = [&]() {
+        mbar_wait(r1_full, cp_done & 1);
+        tc_fence_after();
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < DH / 16; ++kk)
+            tmem_cp_128x256b_2sm(tm + T_R1 + kk * 8,
+                                 desc_sw128(r1s_base + (kk >> 2) * (RT_BYTES / 4) + (kk & 3) * 32, 16, 1024));
+          mma_commit_2sm_mc(r1_copied, 0x3);
+        }
+        __syncwarp();
+        ++cp_done;
+      };
       for (int n = 0;; ++n) {
         const int k = q_read(n);
         if (lane == 0) q_release(n);
@@ -474,6 +501,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
           mbar_wait(r1s_full, mi & 1);
           mbar_wait(r2a_done, mi & 1);
           mbar_wait(r2_full, mi & 1);
+        } else if (a.row_cp) {
+          if (cp_done == mi) copy_r1();  // not prefetched at the end of the previous item
         } else {
           mbar_wait(r1_done, mi & 1);  // R1 of both CTAs copied into TMEM
         }
@@ -536,6 +565,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
         acc(nt - 1, gt + nt - 1);
         if (elect_one()) mma_commit_2sm_mc(o_full, 0x3);
         __syncwarp();
+        if (!TWO && a.row_cp) {  // the next item's row operand, right behind this item's MMAs
+          const int k2 = q_read(n + 1);  // peek (released when it is processed)
+          Item nx;
+          if (k2 >= 0 && decode_item<TRANS>(a, k2, crank, nx) && nx.ntiles > 0) copy_r1();
+        }
         if (lane == 0) DBG(6, idx);
         gt += nt;
         ++mi;
@@ -594,7 +628,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       const int64_t g = (int64_t)us.off + my;        // global token index
       if (dbgw) DBG(0, idx);
       if (it.ntiles > 0) {
-        if (copied == mi) copy_rows();  // not prefetched by the previous item
+        if (copied == mi && !(!TWO && a.row_cp)) copy_rows();  // not prefetched by the previous item
         const long long my_ts = (my < us.L && a.jag.ts) ? a.jag.ts[g] : 0;
         // stored-score row of this key (DK): [h][koff[u] + my][query]
         const int64_t st_row = store_scores ? ((int64_t)it.h * a.st_rows + a.koff[it.u] + my) * a.st_pitch : 0;
@@ -728,7 +762,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
         // !TWO: every S MMA of this item has completed: hand the next item's row operand (already
         // in the staging area) to the tensor pipe before draining this item's accumulator.
         // (TWO: the next item's rows are loaded only after this epilogue frees the region.)
-        if (!TWO) {
+        if (!TWO && !a.row_cp) {
           const int k2 = q_read(n + 1);  // peek (released when it is processed)
           Item nx;
           if (k2 >= 0 && decode_item<TRANS>(a, k2, crank, nx) && nx.ntiles > 0) copy_rows();
@@ -947,7 +981,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     }
     for (int s = 0; s < 2; ++s) { mbar_init(&s_full[s], 1); mbar_init(&s_free[s], 2 * NSM); }
     mbar_init(r_full, 1);
-    mbar_init(r_copied, NSM);
+    mbar_init(r_copied, a.sc_cp ? 1 : NSM);  // tcgen05.cp: one commit arrival
     mbar_init(r_done, 2 * NSM);
     mbar_init(r_free, 1);
     for (int s = 0; s < 4; ++s) {
@@ -1005,11 +1039,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
         if (it.ntiles == 0) continue;
         const int row0 = it.us.off + it.r0;
         if (mi > 0) mbar_wait(r_copied, (mi - 1) & 1);
-        mbar_expect_tx(r_full, 2 * RT_BYTES);
+        if (a.sc_cp) {  // both CTAs' rows land on the leader's barrier (the MMA warp copies them)
+          if (leader) mbar_expect_tx(r_full, 2 * 2 * RT_BYTES);
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          tma_load_2d(smem + SC_OFF_R1 + c * (RT_BYTES / 4), &tmR1, r_full, it.hcol + c * 64, row0);
-          tma_load_2d(smem + SC_OFF_R2 + c * (RT_BYTES / 4), &tmR2, r_full, it.hcol + c * 64, row0);
+          for (int c = 0; c < 4; ++c) {
+            tma_load_2d_2sm(smem + SC_OFF_R1 + c * (RT_BYTES / 4), &tmR1, r_full, it.hcol + c * 64, row0);
+            tma_load_2d_2sm(smem + SC_OFF_R2 + c * (RT_BYTES / 4), &tmR2, r_full, it.hcol + c * 64, row0);
+          }
+        } else {
+          mbar_expect_tx(r_full, 2 * RT_BYTES);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            tma_load_2d(smem + SC_OFF_R1 + c * (RT_BYTES / 4), &tmR1, r_full, it.hcol + c * 64, row0);
+            tma_load_2d(smem + SC_OFF_R2 + c * (RT_BYTES / 4), &tmR2, r_full, it.hcol + c * 64, row0);
+          }
         }
         ++mi;
       }
@@ -1060,7 +1103,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
         Item it;
         decode_item<TRANS>(a, k, crank, it);
         if (it.ntiles == 0) continue;
-        mbar_wait(r_done, mi & 1);  // both CTAs' K and V rows in TMEM
+        if (a.sc_cp) {
+          // K and V rows of both CTAs: staging -> TMEM by tcgen05.cp (ordered after the previous
+          // item's MMAs, before this item's); the commit frees the staging for the loaders
+          mbar_wait(r_full, mi & 1);
+          tc_fence_after();
+          const uint32_t r1b = smem_u32(smem + SC_OFF_R1), r2b = smem_u32(smem + SC_OFF_R2);
+          if (elect_one()) {
+#pragma unroll
+            for (int kk = 0; kk < DH / 16; ++kk) {
+              const uint32_t so = (kk >> 2) * (RT_BYTES / 4) + (kk & 3) * 32;
+              tmem_cp_128x256b_2sm(tm + T_R1 + kk * 8, desc_sw128(r1b + so, 16, 1024));
+              tmem_cp_128x256b_2sm(tm + T_R2 + kk * 8, desc_sw128(r2b + so, 16, 1024));
+            }
+            mma_commit_2sm_mc(r_copied, 0x3);
+          }
+          __syncwarp();
+        } else {
+          mbar_wait(r_done, mi & 1);  // both CTAs' K and V rows in TMEM
+        }
         for (int t = 0; t < it.ntiles; ++t, ++gt) {
           const int slot = gt % SC_NC, b = gt & 1;
           mbar_wait(&c1_full[slot], (gt / SC_NC) & 1);
@@ -1106,7 +1167,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       if (it.ntiles == 0) continue;
       const UserSpan& us = it.us;
       const int my = it.r0 + row;  // this thread's key (user-local)
-      // K and V rows of this item into TMEM (this warp: rows q*32.., head dims half*128..)
+      // K and V rows of this item into TMEM (this warp: rows q*32.., head dims half*128..);
+      // with tcgen05.cp the MMA warp does it
+      if (!a.sc_cp) {
       if (mi > 0) mbar_wait(r_free, (mi - 1) & 1);
       mbar_wait(r_full, mi & 1);
       tc_fence_after();
@@ -1128,6 +1191,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(r_copied);
       arrive_leader(r_done);
+      }
       const long long my_ts = (my < us.L && a.jag.ts) ? a.jag.ts[(int64_t)us.off + my] : 0;
       const bool need_ts = !a.causal && (it.r0 + BR > us.ns) && (it.r0 < it.kv_end);  // uniform
       const int64_t st_row = ((int64_t)it.h * a.st_rows + a.koff[it.u] + my) * a.st_pitch;
@@ -1623,6 +1687,9 @@ static mtgr_status_t launch_mode(const AttnIO& io, const void* c1, int64_t ld_c1
   MTGR_TRY(make_tmap_bf16(&m.o, args.out, d, T, args.ld_out, 64, 32));
   Args a2 = args;
   a2.causal = io.causal;
+  // row operand into TMEM by tcgen05.cp from the MMA warp (default) or through the softmax
+  // warps' registers (MTGR_ROW_CP=0)
+  { const char* x = getenv("MTGR_ROW_CP"); a2.row_cp = !(x != nullptr && x[0] == '0'); }
   a2.e = (const __nv_bfloat16*)e; a2.ld_e = ld_e;
   a2.uu = (const __nv_bfloat16*)uu; a2.ld_u = ld_u;
   a2.pre_dsilu = io.pre_dsilu;
@@ -1684,6 +1751,9 @@ static mtgr_status_t launch_mm(const AttnIO& io, const void* amat, const void* b
   MTGR_TRY(make_tmap_bf16(&to, args.out, d, T, args.ld_out, 64, 32));
   Args a2 = args;
   a2.causal = io.causal;
+  // row operand into TMEM by tcgen05.cp from the MMA warp (default) or through the softmax
+  // warps' registers (MTGR_ROW_CP=0)
+  { const char* x = getenv("MTGR_ROW_CP"); a2.row_cp = !(x != nullptr && x[0] == '0'); }
   a2.e = (const __nv_bfloat16*)e; a2.ld_e = ld_e;
   a2.uu = (const __nv_bfloat16*)uu; a2.ld_u = ld_u;
   a2.pre_dsilu = io.pre_dsilu;
@@ -1714,6 +1784,7 @@ static mtgr_status_t launch_sc(const AttnIO& io, const MmLayout& l, const Args& 
   a2.nitems = io.jag.num_users * a2.pmax * io.H;
   a2.st_pitch = l.pitch; a2.st_rows = l.rows;
   a2.c_align = 1;
+  { const char* x = getenv("MTGR_SC_CP"); a2.sc_cp = !(x != nullptr && x[0] == '0'); }  // as MTGR_ROW_CP
   MTGR_CHECK(io.ctr != nullptr, MTGR_E_ARG, "attention: work-queue counters (workspace) missing");
   a2.ctr = io.ctr + 6;
   cudaMemsetAsync(a2.ctr, 0, sizeof(int), st);

@@ -342,3 +342,16 @@ def test_layer_single_shared_ln(dev, name):
         Z[s:e], dX[s:e] = zz, dd
         G = [{k: v.copy() for k, v in gs[0].items()}] if G is None else [{k: G[0][k] + gs[0][k] for k in G[0]}]
     _compare(z, dx, grads, Z, dX, G, TOL[dt])
+
+
+@pytest.mark.parametrize("name", ["parity", "parity768"])
+def test_layer_register_row_copy(dev, name, monkeypatch):
+    """The row operands moved into TMEM through the softmax warps' registers (MTGR_ROW_CP=0,
+    MTGR_SC_CP=0) instead of tcgen05.cp: same results."""
+    monkeypatch.setenv("MTGR_ROW_CP", "0")
+    monkeypatch.setenv("MTGR_SC_CP", "0")
+    monkeypatch.setenv("MTGR_ATTN_FUSED_DK", "0")
+    cfg, seg, ts, X, dZ, P = make_batch(name)
+    z, dx, grads = _run_layer(dev, cfg, seg, ts, X, dZ, P)
+    Z, dX, G = _oracle_stack(cfg, seg, ts, X, dZ, [P])
+    _compare(z, dx, grads, Z, dX, G, TOL[_dt(cfg)])
