@@ -27,7 +27,16 @@
 // Warp roles (384 threads): w0 TMA producer (R1, R2, C1, E, U), w1 MMA issuer, w2 TMEM allocator,
 // w3 TMA producer (X or C2), w4-w11 softmax/epilogue (two warps per TMEM lane quadrant,
 // thread = row = TMEM lane).  TMEM: acc [0,256), S [256,384) (two buffers, or S and dP),
-// T [384,448) (two buffers of bf16 pairs).
+// T [384,448) (two buffers of bf16 pairs).  (The exact layouts per mode are in the kernel;
+// FWD/DV stage their row operand through warp 2 and move it into TMEM with tcgen05.cp from the
+// MMA warp, right behind the previous item's MMAs.)
+//
+// The default backward is the stored-score path (attn_tc_bwd_launch): attn_sc_kernel computes
+// S^T and dP^T per (key pair, head) and writes P^T and dS^T (bf16) into padded per-user key
+// blocks; attn_mm_kernel then forms dV = nu P^T dO, dK = nu dS^T Q and dQ = nu dS K as jagged
+// GEMMs (double-buffered TMEM accumulator, the same epilogue).  For long users (mean >= 2048
+// tokens) the DK mode above writes the scores while forming dK (fewer item transitions); the
+// recompute kernels (DV, DK, DQ modes) remain for batches whose score scratch would not fit.
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
