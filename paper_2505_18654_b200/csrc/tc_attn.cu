@@ -10,13 +10,13 @@
 //   DK   | K                  | V         | Q              | Q  (= C1)  | dS^T              | dK
 //   (DQ/DK also stream C2 = V / dO for dP = R2 C2^T.)
 //
-// Per column tile:  S = R1 C1^T (tcgen05.mma SS: A = R1 resident in smem, B = C1 K-major,
-// M=128 N=64 K=256) [and dP = R2 C2^T];  8 "softmax" warps tcgen05.ld S (and dP), apply the
-// mask predicate in registers and SiLU / SiLU' (tanh.approx), and tcgen05.st the bf16 T tile
-// into TMEM;  acc += T X (A = T from TMEM, B = X MN-major — the same TMA-loaded tile read with
-// an MN-major descriptor, M=128 N=256 K=64).  (Measured: with A from TMEM an N=64 MMA is bound
-// by the TMEM A-operand read, ~70 cycles instead of 32, so the N=64 score MMAs read A from smem
-// and only the N=256 accumulate MMAs read A from TMEM.)
+// Per column tile:  S = R1 C1^T (tcgen05.mma, M=256 on the CTA pair, N=64, K=256; A = R1 from
+// TMEM for FWD/DV, from smem for DQ/DK; B = C1 K-major) [and dP = R2 C2^T];  8 "softmax" warps
+// tcgen05.ld S (and dP), apply the mask predicate in registers and SiLU / SiLU' (tanh.approx),
+// and tcgen05.st the bf16 T tile into TMEM;  acc += T X (A = T from TMEM, B = X MN-major — the
+// same TMA-loaded tile read with an MN-major descriptor, N=256, K=64).  (Measured on B200,
+// tools/microbench/mma_rate.cu: SS N=64 is smem-bound at ~48 cycles per K=16 step, TS runs at
+// the ideal for every N, so the score MMAs read A from TMEM where TMEM has room.)
 // The 1/N factor, the diagonal term of non-static tokens (R#9: candidates and real-time tokens
 // see themselves), the gate (FWD: y = o*u) and the QKV activation backward (silu'(p)) are fused
 // into the epilogue, which stages E/U tiles and the outputs in shared memory (TMA in, coalesced
