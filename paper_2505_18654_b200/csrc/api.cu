@@ -113,6 +113,17 @@ static bool tc_attn_path(const mtgr_layer_cfg_t* c, mtgr_dtype_t dt) {
   return dt == MTGR_BF16 && c->rab_buckets == 0 && c->n_heads > 0 && attn_tc_supported(c->d_model / c->n_heads);
 }
 
+// bf16 attention = the tcgen05 kernels only: head dim 256 (every MTGR config, Table 2)
+// and no rab term (R#4: optional, not part of Eq.5; built on the fp32 path only)
+static mtgr_status_t check_attn_dtype(const mtgr_layer_cfg_t* c, mtgr_dtype_t dt) {
+  if (dt != MTGR_BF16) return MTGR_OK;
+  MTGR_CHECK(c->rab_buckets == 0, MTGR_E_UNSUPPORTED, "bf16 attention: rab is supported on the fp32 path only");
+  MTGR_CHECK(attn_tc_supported(c->d_model / c->n_heads), MTGR_E_UNSUPPORTED,
+             "bf16 attention: head dim %d unsupported (the tensor-core kernels need d_h = 256)",
+             c->d_model / c->n_heads);
+  return MTGR_OK;
+}
+
 static size_t bwd_ws_bytes(const mtgr_layer_cfg_t* c, const mtgr_jagged_t* j, mtgr_dtype_t dt) {
   const int ntok = j->total_tokens;
   const size_t es = esize(dt), T = ntok;
@@ -146,28 +157,31 @@ static mtgr_status_t run_gemm(const GemmIO& g, int epi, void* ws, size_t wsb, cu
   else return gemm_simt_launch<float>(g, epi, st);
 }
 
+// The bf16 attention runs only on the tensor-core kernels (d_h = 256, no rab); the SIMT kernels
+// are the fp32 parity path.  There is no dispatch between them: check_attn_dtype rejects every
+// other bf16 configuration with MTGR_E_UNSUPPORTED before anything is launched.
 template <class T>
 static mtgr_status_t run_attn_fwd(const AttnIO& a, float* diag, cudaStream_t st) {
-  const bool tc = std::is_same<T, __nv_bfloat16>::value && a.nb == 0 && attn_tc_supported(a.dh);
+  constexpr bool tc = std::is_same<T, __nv_bfloat16>::value;
   AttnIO b = a;
   b.diag_cand_only = tc;  // the tensor-core path adds real-time diagonals inside its tile loop
   // causal: every diagonal entry is inside the key range of the tile loops (no diagonal terms)
   if (!a.causal) MTGR_TRY(attn_diag_launch<T>(b, false, diag, nullptr, st));
   b.diag_a = diag;
-  if (tc) return attn_tc_fwd_launch(b, st);
-  return attn_simt_fwd_launch<T>(b, st);
+  if constexpr (tc) return attn_tc_fwd_launch(b, st);
+  else return attn_simt_fwd_launch<float>(b, st);
 }
 
 template <class T>
 static mtgr_status_t run_attn_bwd(const AttnIO& a, float* diag_a, float* diag_ds, cudaStream_t st) {
-  const bool tc = std::is_same<T, __nv_bfloat16>::value && a.nb == 0 && attn_tc_supported(a.dh);
+  constexpr bool tc = std::is_same<T, __nv_bfloat16>::value;
   AttnIO b = a;
   b.diag_cand_only = tc;
   if (!a.causal) MTGR_TRY(attn_diag_launch<T>(b, true, diag_a, diag_ds, st));
   b.diag_a = diag_a;
   b.diag_ds = diag_ds;
-  if (tc) return attn_tc_bwd_launch(b, st);
-  return attn_simt_bwd_launch<T>(b, st);
+  if constexpr (tc) return attn_tc_bwd_launch(b, st);
+  else return attn_simt_bwd_launch<float>(b, st);
 }
 
 // ------------------------------------------------------------------ layer forward
@@ -265,8 +279,7 @@ static mtgr_status_t layer_bwd_t(const mtgr_layer_cfg_t* c, const mtgr_jagged_t*
     cudaMemsetAsync(G->b2, 0, sizeof(float) * d, st);
     if (post2) cudaMemsetAsync(G->b3, 0, sizeof(float) * d, st);
   }
-  const bool tc_attn = std::is_same<T, __nv_bfloat16>::value && c->rab_buckets == 0 &&
-                       attn_tc_supported(d / H);
+  constexpr bool tc_attn = std::is_same<T, __nv_bfloat16>::value;  // check_attn_dtype
   if (ntok == 0) {
     // gradients of an empty batch are zero
     if (!acc) {
@@ -473,6 +486,7 @@ static mtgr_status_t attn_common_checks(const mtgr_layer_cfg_t* cfg, const mtgr_
   MTGR_TRY(check_cfg(cfg));
   MTGR_TRY(check_jag(jag, false));
   MTGR_TRY(check_dtype(dtype));
+  MTGR_TRY(check_attn_dtype(cfg, dtype));
   MTGR_CHECK(ld >= cfg->d_model && ld % 8 == 0, MTGR_E_LAYOUT, "ld must be >= d_model and a multiple of 8");
   MTGR_CHECK(cfg->rab_buckets == 0 || rab_w, MTGR_E_ARG, "rab on but rab_w is NULL");
   MTGR_CHECK(ws_bytes >= mtgr_attn_workspace_bytes(cfg, jag, dtype), MTGR_E_WORKSPACE,
@@ -562,6 +576,7 @@ MTGR_API mtgr_status_t mtgr_hstu_layer_fwd(const mtgr_layer_cfg_t* cfg, const mt
   MTGR_TRY(check_cfg(cfg));
   MTGR_TRY(check_jag(jag, true));
   MTGR_TRY(check_dtype(dtype));
+  MTGR_TRY(check_attn_dtype(cfg, dtype));
   MTGR_TRY(check_params(cfg, params));
   MTGR_CHECK(ws_bytes >= mtgr_layer_workspace_bytes(cfg, jag, dtype), MTGR_E_WORKSPACE,
              "layer workspace too small (%zu < %zu)", ws_bytes, mtgr_layer_workspace_bytes(cfg, jag, dtype));
@@ -587,6 +602,7 @@ MTGR_API mtgr_status_t mtgr_hstu_layer_bwd(const mtgr_layer_cfg_t* cfg, const mt
   MTGR_TRY(check_cfg(cfg));
   MTGR_TRY(check_jag(jag, true));
   MTGR_TRY(check_dtype(dtype));
+  MTGR_TRY(check_attn_dtype(cfg, dtype));
   MTGR_TRY(check_params(cfg, params));
   MTGR_CHECK(grads && grads->w1 && grads->b1 && grads->w2 && grads->b2 && grads->gamma1 &&
                  grads->beta1 && grads->gamma2 && grads->beta2,

@@ -465,8 +465,6 @@ mtgr_status_t attn_simt_bwd_launch(const AttnIO& a, cudaStream_t st) {
 }
 
 template mtgr_status_t attn_simt_fwd_launch<float>(const AttnIO&, cudaStream_t);
-template mtgr_status_t attn_simt_fwd_launch<__nv_bfloat16>(const AttnIO&, cudaStream_t);
 template mtgr_status_t attn_simt_bwd_launch<float>(const AttnIO&, cudaStream_t);
-template mtgr_status_t attn_simt_bwd_launch<__nv_bfloat16>(const AttnIO&, cudaStream_t);
 
 }  // namespace mtgr

@@ -75,3 +75,27 @@ def rel_err(got, ref):
     if ref.size == 0:
         return 0.0
     return float(np.abs(got - ref).max() / max(np.abs(ref).max(), 1e-30))
+
+
+def p999_rel_err(got, ref, floor=1e-2):
+    """99.9th percentile of the elementwise relative error |g - o| / max(|o|, floor * max|o|)
+    (reported beside the max-normalised error; the floor keeps entries that are
+    ~0 by cancellation from dominating)."""
+    got = np.asarray(got, dtype=np.float64).ravel()
+    ref = np.asarray(ref, dtype=np.float64).ravel()
+    if ref.size == 0:
+        return 0.0
+    den = np.maximum(np.abs(ref), floor * max(np.abs(ref).max(), 1e-30))
+    return float(np.percentile(np.abs(got - ref) / den, 99.9))
+
+
+def report(name, payload):
+    """Append a JSON line to $MTGR_REPORT_DIR/parity_report.jsonl (GPU runs keep the numbers the
+    tests print as evidence); no-op when the variable is unset."""
+    import json
+    d = os.environ.get("MTGR_REPORT_DIR")
+    if not d:
+        return
+    os.makedirs(d, exist_ok=True)
+    with open(os.path.join(d, "parity_report.jsonl"), "a") as f:
+        f.write(json.dumps({"test": name, **payload}) + "\n")
