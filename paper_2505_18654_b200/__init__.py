@@ -8,12 +8,12 @@ from .api import (JaggedBatch, HstuStack, layer_cfg, build_jagged, balance_lpt, 
                   mask_dense, gln_fwd, gln_bwd, attn_fwd, attn_bwd, hstu_layer_fwd,
                   hstu_layer_bwd, layer_saved_bytes, layer_workspace_bytes, params_to_device,
                   alloc_grads, grad_numel, scale_, gemm, launch_count, prof_enable, prof_reset,
-                  prof_query, head_params_to_device, head_fwd_bwd, TokenEmbed)
+                  prof_query, head_params_to_device, head_fwd_bwd, TokenEmbed, MASK_MODES)
 
 __all__ = ["MtgrError", "LIB_PATH", "lib", "SIGNATURES", "JaggedBatch", "HstuStack", "layer_cfg",
            "build_jagged", "balance_lpt", "validate_jagged", "mask_dense", "gln_fwd", "gln_bwd",
            "attn_fwd", "attn_bwd", "hstu_layer_fwd", "hstu_layer_bwd", "layer_saved_bytes",
            "layer_workspace_bytes", "params_to_device", "alloc_grads", "grad_numel", "scale_", "gemm", "launch_count", "prof_enable",
-           "prof_reset", "prof_query", "head_params_to_device", "head_fwd_bwd", "TokenEmbed"]
+           "prof_reset", "prof_query", "head_params_to_device", "head_fwd_bwd", "TokenEmbed", "MASK_MODES"]
 from .embed import HashEmbedding, ShardedEmbedding, unique, segment_sum, take_rows  # noqa: E402
 from .model import MTGRModel  # noqa: E402
