@@ -56,6 +56,8 @@ def parse():
                     help="step = stack fwd + candidate head/BCE (SURVEY f2) + stack bwd from the head's dZ")
     ap.add_argument("--balance", default="tokens", choices=["tokens", "flops"],
                     help="LPT cost: token count (R#19, default) or per-user FLOPs (SURVEY f3)")
+    ap.add_argument("--no-large-attn", action="store_true",
+                    help="skip the MTGR-large attention sub-record (one large layer fwd+bwd, N=1 only)")
     return ap.parse_args()
 
 
@@ -316,8 +318,14 @@ def run_mtgr(args, cfg, rank, world, local_rank):
     head_state = {}
     if args.head:  # candidate head + two-task BCE on the encoder output
         lab = np.concatenate([synth.gen_user_labels(cfg, int(u), int(l)) for u, l in zip(users, Ls)])
-        head_state = dict(params=m.head_params_to_device(synth.gen_head_params(cfg), dt, dev),
-                          labels=torch.from_numpy(lab).to(dev),
+        hp = m.head_params_to_device(synth.gen_head_params(cfg), dt, dev)
+        hshapes = {"w_a": tuple(hp["w_a"].shape), "b_a": (hp["w_a"].shape[0],), "w_b": tuple(hp["w_b"].shape), "b_b": (2,)}
+        hflat = torch.zeros(sum(int(np.prod(v)) for v in hshapes.values()), dtype=torch.float32, device=dev)
+        hviews, off = {}, 0
+        for kk, shp in hshapes.items():  # the head's gradient bucket (all-reduced + scaled with the layers')
+            hviews[kk] = hflat[off:off + int(np.prod(shp))].view(*shp)
+            off += hviews[kk].numel()
+        head_state = dict(params=hp, labels=torch.from_numpy(lab).to(dev), flat=hflat, views=hviews,
                           ws=None, K=int(jb.host["n_cand"].sum()))
 
     tok = {}
@@ -328,7 +336,15 @@ def run_mtgr(args, cfg, rank, world, local_rank):
                  .to(dev, dt) for t in synth.TOKEN_TYPES}
         emb = m.TokenEmbed(cfg["d"], k, m.TokenEmbed.params_to_device(synth.gen_token_params(cfg), dt, dev), dt, dev)
         emb.bind(jb, wl["seg"][users])
-        tok = dict(emb=emb, feats=feats)
+        tshapes = emb.grad_shapes()
+        tflat = torch.zeros(sum(int(np.prod(v)) for q in tshapes.values() for v in q.values()),
+                            dtype=torch.float32, device=dev)
+        tviews, off = {}, 0
+        for t_, q in tshapes.items():  # the token MLPs' gradient bucket
+            for kk, shp in q.items():
+                tviews.setdefault(t_, {})[kk] = tflat[off:off + int(np.prod(shp))].view(*shp)
+                off += int(np.prod(shp))
+        tok = dict(emb=emb, feats=feats, flat=tflat, views=tviews)
 
     full = {}
     if args.full_model:
@@ -338,7 +354,8 @@ def run_mtgr(args, cfg, rank, world, local_rank):
         iids = np.concatenate([np.concatenate([i[t].reshape(-1) for i in ids]) for t in "src"])
         model = m.MTGRModel(cfg, lc, [synth.gen_layer_params(cfg, li) for li in range(cfg["n_layers"])],
                             synth.gen_token_params(cfg), synth.gen_head_params(cfg), synth.token_widths(cfg),
-                            synth.EMB_DIM, dt, dev, cap_user=1 << 20, cap_item=1 << 23)
+                            synth.EMB_DIM, dt, dev, cap_user=1 << 20, cap_item=1 << 23,
+                            n_users_global=wl["B_g"])
         model.bind(jb, wl["seg"][users])
         stack = model.stack
         full = dict(model=model, uids=torch.from_numpy(uids).to(dev), iids=torch.from_numpy(iids).to(dev),
@@ -347,26 +364,24 @@ def run_mtgr(args, cfg, rank, world, local_rank):
     def step(xin=x_dev, dzin=dz_dev):
         if args.full_model:
             full["t"][0] += 1
-            _, g = full["model"].step(full["uids"], full["iids"], full["labels"], now=full["t"][0],
-                                      on_layer_done=agg.on_layer_done)
-            if world > 1:
-                dist.all_reduce(torch.cat([t.reshape(-1) for t in g["head"].values()] +
-                                          [t.reshape(-1) for q in g["tokens"].values() for t in q.values()]))
-            agg.finish(full["model"].stack.grad_flat)
+            # layer buckets + the head/token bucket all-reduced and scaled inside the step
+            full["model"].step(full["uids"], full["iids"], full["labels"], now=full["t"][0], aggregator=agg)
             return
         if args.tokens:
             xin = tok["emb"].forward(tok["feats"]).contiguous()
         z = stack.forward(xin)
+        flats = [stack.grad_flat]
         if args.head:
-            _, loss, dzin, hg = m.head_fwd_bwd(jb, head_state["params"], z, head_state["labels"])
-            if world > 1:
-                dist.all_reduce(torch.cat([t.reshape(-1) for t in hg.values()]))
+            _, loss, dzin, hg = m.head_fwd_bwd(jb, head_state["params"], z, head_state["labels"],
+                                               grads_out=head_state["views"])
+            agg.on_layer_done(-1, head_state["flat"])
+            flats.append(head_state["flat"])
         dx = stack.backward(dzin, on_layer_done=agg.on_layer_done)
         if args.tokens:
-            _, tg = tok["emb"].backward(dx)
-            if world > 1:
-                dist.all_reduce(torch.cat([t.reshape(-1) for q in tg.values() for t in q.values()]))
-        agg.finish(stack.grad_flat)
+            tok["emb"].backward(dx, grads_out=tok["views"])
+            agg.on_layer_done(-1, tok["flat"])
+            flats.append(tok["flat"])
+        agg.finish(*flats)
 
     def barrier():
         if world > 1:
@@ -419,7 +434,8 @@ def run_mtgr(args, cfg, rank, world, local_rank):
             avg_s = tot / n / 1000.0
             if bound == "tensor":
                 e.update(bound="tensor", achieved_tflops=per_launch / avg_s / 1e12,
-                         frac=per_launch / avg_s / 1e12 / pk["bf16_tflops_sustained"])
+                         frac=per_launch / avg_s / 1e12 / pk["bf16_tflops_sustained"],
+                         frac_burst=per_launch / avg_s / 1e12 / pk["bf16_tflops"])
             else:
                 e.update(bound="hbm", achieved_gbs=per_launch / avg_s / 1e9,
                          frac=per_launch / avg_s / 1e9 / pk["hbm_gbs"])
@@ -436,7 +452,8 @@ def run_mtgr(args, cfg, rank, world, local_rank):
         if e["bound"] == "tensor":
             roof = {"kernel": dom, "bound": "tensor", "achieved": e["achieved_tflops"],
                     "peak": pk["bf16_tflops_sustained"], "unit": "TFLOP/s", "frac": e["frac"],
-                    "traffic": traffic, "peak_source": f"{pk_kind} bf16_tflops_sustained (kernel timed inside a long step)"}
+                    "traffic": traffic, "peak_source": f"{pk_kind} bf16_tflops_sustained (kernel timed inside a long step)",
+                    "peak_burst": pk["bf16_tflops"], "frac_burst": e["frac_burst"]}
         else:
             roof = {"kernel": dom, "bound": "hbm", "achieved": e["achieved_gbs"], "peak": pk["hbm_gbs"],
                     "unit": "GB/s", "frac": e["frac"], "traffic": traffic, "peak_source": f"{pk_kind} hbm_gbs"}
@@ -445,6 +462,10 @@ def run_mtgr(args, cfg, rank, world, local_rank):
     e2e = None
     if not args.no_e2e:
         e2e = run_e2e(args, torch, dist, m, stack, jb, X, dZ, ts, wl, world, dev, step)
+
+    large = None
+    if world == 1 and not args.no_large_attn and cfg["name"] != "large":
+        large = run_large_attention(torch, m, dev, pk)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -459,11 +480,17 @@ def run_mtgr(args, cfg, rank, world, local_rank):
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
                 "data": "synthetic (seeded generator synth/, random-init weights)",
                 "config": workload_desc(cfg, wl, world),
+                # algorithmic FLOP/s / the burst bf16 peak (cuBLAS 8192^3 best of 10);
+                # the sustained-peak fraction beside it
                 "pct_bf16_peak": flops_rank * world * args.steps / (ms_max / 1000.0) / 1e12
-                                 / (pk["bf16_tflops_sustained"] * world),
+                                 / (pk["bf16_tflops"] * world),
+                "pct_bf16_peak_sustained": flops_rank * world * args.steps / (ms_max / 1000.0) / 1e12
+                                           / (pk["bf16_tflops_sustained"] * world),
                 "algorithmic_tflops_per_gpu": flops_rank * args.steps / (ms_max / 1000.0) / 1e12,
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
                 "gpu_launches": int(launches), "kernels": kernels, "impl": "mtgr"}
+        if large is not None:
+            line["large_attention"] = large
         if args.full_model:
             line["config"]["step"] = ("full training step: sharded hash-embedding lookup (two-stage unique, "
                                       "all-to-all) -> Eq.4 tokens -> stack -> head/BCE -> backward -> sparse SGD")
@@ -474,6 +501,69 @@ def run_mtgr(args, cfg, rank, world, local_rank):
             line["config"]["step"] = "stack fwd + candidate head/BCE + stack bwd (dZ from the head)"
             line["config"]["candidates_per_rank"] = head_state["K"]
         print(json.dumps(line), flush=True)
+
+
+def run_large_attention(torch, m, dev, pk, layers=1, steps=3, warmup=2):
+    """The north-star check in the default bench line (BASELINE.json: >= 50 % bf16 tensor-pipe
+    on the attention at the MTGR-large shape): one MTGR-large layer (d=768, 3 heads, 32 users x
+    4484 tokens: n_U 32, n_S 4096, n_r 100, K 256) forward + backward, CUDA-event timed per
+    kernel; algorithmic TFLOP/s of each attention kernel against the burst and sustained bf16
+    peaks, and the time-weighted attention fraction (all attention FLOPs / all attention time)."""
+    cfg = synth.config("large", n_layers=layers)
+    wl = workload(cfg, 0, 1, m.balance_lpt)
+    users = wl["users"]
+    ts = np.concatenate(wl["ts"])
+    Ls = wl["L"][users]
+    dt = torch.bfloat16
+    X = np.concatenate([synth.gen_user_x(cfg, int(u), int(l)) for u, l in zip(users, Ls)])
+    dZ = np.concatenate([synth.gen_user_dz(cfg, int(u), int(l)) for u, l in zip(users, Ls)])
+    jb = m.JaggedBatch.build(wl["seg"], ts, dev, users=users)
+    lc = m.layer_cfg(cfg["d"], cfg["H"], cfg["groups"])
+    stack = m.HstuStack(lc, [m.params_to_device(synth.gen_layer_params(cfg, li), dt, dev)
+                             for li in range(layers)], dt, dev)
+    stack.bind(jb)
+    x = torch.from_numpy(X).to(dev, dt)
+    dz = torch.from_numpy(dZ).to(dev, dt)
+    for _ in range(warmup):
+        stack.forward(x)
+        stack.backward(dz)
+    torch.cuda.synchronize()
+    st = torch.cuda.current_stream()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    m.prof_reset()
+    m.prof_enable(True)
+    ev0.record(st)
+    for _ in range(steps):
+        stack.forward(x)
+        stack.backward(dz)
+    ev1.record(st)
+    torch.cuda.synchronize()
+    m.prof_enable(False)
+    ms = ev0.elapsed_time(ev1) / steps
+    kern = m.prof_query()
+    algo = kernel_algorithmic(cfg, wl["tokens"], wl["pairs"])
+    out, a_fl, a_ms = {}, 0.0, 0.0
+    for name, (n, tot) in kern.items():
+        if not name.startswith("attn_") or name not in algo:
+            continue
+        work = algo[name][1]
+        tf = work * steps / (tot / 1000.0) / 1e12
+        out[name] = {"ms_per_layer": tot / steps / layers, "achieved_tflops": tf,
+                     "frac_burst": tf / pk["bf16_tflops"], "frac_sustained": tf / pk["bf16_tflops_sustained"]}
+        a_fl += work * steps
+        a_ms += tot
+    flops = step_flops(cfg, wl["tokens"], wl["pairs"])
+    del stack, x, dz
+    torch.cuda.empty_cache()
+    return {"workload": "MTGR-large shape: 1 layer, d=768, 3 heads (d_h=256), 32 users x 4484 tokens "
+                        "(n_U 32, n_S 4096, n_r 100, K 256), T=143488, fwd+bwd, bf16",
+            "ms_per_layer_step": ms / layers,
+            "layer_pct_bf16_peak": flops / (ms / 1000.0) / 1e12 / pk["bf16_tflops"],
+            "attention_kernels": out,
+            "attention_time_weighted_frac_burst": (a_fl / (a_ms / 1000.0) / 1e12 / pk["bf16_tflops"]) if a_ms else None,
+            "attention_share_of_layer": a_ms / steps / ms if ms else None,
+            "note": "algorithmic FLOPs only (SURVEY §8(d): masked pairs and the backward's S recompute "
+                    "excluded); tensor-pipe utilisation from ncu is in profiles/"}
 
 
 def run_e2e(args, torch, dist, m, stack, jb, X, dZ, ts, wl, world, dev, step):
@@ -546,11 +636,34 @@ def run_e2e(args, torch, dist, m, stack, jb, X, dZ, ts, wl, world, dev, step):
             "note": "pinned-host inputs copied every step on a copy stream (double-buffered), grads read back"}
 
 
+def _free_port():
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def self_launch(args) -> int:
+    """`python bench.py --gpus N` outside torchrun: launch N ranks (one per GPU) through
+    torch.distributed.run on 127.0.0.1; rank 0's JSON line reaches our stdout."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
+           os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
+    env_world = os.environ.get("WORLD_SIZE")
+    if env_world is None and args.gpus > 1 and args.impl != "reference":
+        sys.exit(self_launch(args))
     rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
+    world = int(env_world) if env_world is not None else args.gpus
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if env_world is not None and world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}: launch one rank per GPU "
+              f"(torchrun --nproc-per-node {args.gpus}) or drop --gpus", file=sys.stderr)
+        sys.exit(2)
     cfg = synth.config(args.config, mask_mode=args.mask, post_mlp_layers=args.post_mlp)
     if args.impl == "reference":
         run_reference(args, cfg, rank, world)
@@ -559,9 +672,10 @@ def main():
     import torch.distributed as dist
     if world > 1:
         torch.cuda.set_device(local_rank)
-        # NCCL's version banner goes to stdout, which must carry exactly one JSON line
-        if os.environ.get("NCCL_DEBUG", "").upper() not in ("INFO", "TRACE"):
-            os.environ["NCCL_DEBUG"] = "WARN"
+        # communicator INIT lines (nranks, transport) go to stderr; stdout carries one JSON line
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         dist.init_process_group(args.backend, device_id=torch.device("cuda", local_rank))
     try:
         run_mtgr(args, cfg, rank, world, local_rank)

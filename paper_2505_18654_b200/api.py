@@ -359,9 +359,10 @@ def head_params_to_device(p: dict, dtype: torch.dtype, device) -> dict:
 
 
 def head_fwd_bwd(jb: JaggedBatch, params: dict, z: torch.Tensor, labels: torch.Tensor,
-                 d_hidden: int | None = None, want_grad: bool = True, ws=None):
+                 d_hidden: int | None = None, want_grad: bool = True, ws=None, grads_out: dict | None = None):
     """Candidate logit head + CTR/CTCVR BCE sums (mtgr_head_fwd_bwd).  labels: uint8 [T]
-    (bit 0 click, bit 1 purchase).  Returns (logits [K][2], loss [2], dz or None, grads or None)."""
+    (bit 0 click, bit 1 purchase).  Returns (logits [K][2], loss [2], dz or None, grads or None).
+    grads_out: optional preallocated fp32 gradient tensors (e.g. views of an all-reduce bucket)."""
     d = z.shape[1]
     dh = d_hidden or params["w_a"].shape[0]
     cfg = HeadCfg(d, dh)
@@ -374,7 +375,9 @@ def head_fwd_bwd(jb: JaggedBatch, params: dict, z: torch.Tensor, labels: torch.T
     loss = torch.empty(2, dtype=torch.float32, device=z.device)
     dz = torch.empty_like(z) if want_grad else None
     grads = None
-    if want_grad:
+    if want_grad and grads_out is not None:
+        grads = grads_out
+    elif want_grad:
         grads = {"w_a": torch.empty((dh, d), dtype=torch.float32, device=z.device),
                  "b_a": torch.empty(dh, dtype=torch.float32, device=z.device),
                  "w_b": torch.empty((2, dh), dtype=torch.float32, device=z.device),
@@ -431,12 +434,18 @@ class TokenEmbed:
                                    _p(x), _p(self.saved), _p(self.ws), self.ws.numel(), _stream()))
         return x[:self.jb.total_tokens]
 
-    def backward(self, dx: torch.Tensor, want_dfeats: bool = True, out: dict | None = None):
+    def grad_shapes(self) -> dict:
+        return {t: {"w1": tuple(self.params[t]["w1"].shape), "b1": (self.d,), "w2": (self.d, self.d), "b2": (self.d,)}
+                for t in ("s", "r", "c")}
+
+    def backward(self, dx: torch.Tensor, want_dfeats: bool = True, out: dict | None = None,
+                 grads_out: dict | None = None):
         """Returns (dfeats dict or None, grads {"s","r","c"} -> {"w1","b1","w2","b2"} fp32 sums).
-        `out`: optional preallocated feature-gradient tensors (e.g. views of one buffer)."""
+        `out`: optional preallocated feature-gradient tensors (e.g. views of one buffer);
+        `grads_out`: optional preallocated parameter-gradient tensors (views of a bucket)."""
         f = lambda *s: torch.empty(s, dtype=torch.float32, device=self.device)
-        grads = {t: {"w1": f(*self.params[t]["w1"].shape), "b1": f(self.d), "w2": f(self.d, self.d), "b2": f(self.d)}
-                 for t in ("s", "r", "c")}
+        grads = grads_out if grads_out is not None else {
+            t: {k: f(*shp) for k, shp in q.items()} for t, q in self.grad_shapes().items()}
         cg = TokenGrads(*(MlpParams(*(grads[t][k].data_ptr() for k in ("w1", "b1", "w2", "b2")))
                           for t in ("s", "r", "c")))
         dfe = {}

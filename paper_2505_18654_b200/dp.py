@@ -69,8 +69,10 @@ class GradAggregator:
         if self.world > 1:
             self._works.append(self.dist.all_reduce(bucket, group=self.group, async_op=True))
 
-    def finish(self, flat):
+    def finish(self, *flats):
+        """Wait for every bucket's all-reduce, then scale each flat gradient buffer by 1/B_global."""
         while self._works:
             self._works.pop(0).wait()
-        self.scale_fn(flat, self.inv_b)
-        return flat
+        for flat in flats:
+            self.scale_fn(flat, self.inv_b)
+        return flats[0] if len(flats) == 1 else flats

@@ -22,7 +22,7 @@ from .embed import HashEmbedding, ShardedEmbedding
 class MTGRModel:
     def __init__(self, cfg: dict, layer_cfg, layer_params: list, token_params: dict, head_params: dict,
                  widths: dict, emb_dim: int, dtype: torch.dtype, device, cap_user: int, cap_item: int,
-                 lr_sparse: float = 1e-3, seed: int = 0, group=None):
+                 lr_sparse: float = 1e-3, seed: int = 0, group=None, n_users_global: int | None = None):
         self.cfg, self.dtype, self.device = cfg, dtype, torch.device(device)
         self.d, self.emb_dim, self.lr_sparse = cfg["d"], emb_dim, lr_sparse
         self.widths = widths
@@ -33,6 +33,24 @@ class MTGRModel:
                                            group)
         self.item_table = ShardedEmbedding(HashEmbedding(emb_dim, cap_item, seed=seed + 1, init_scale=0.5,
                                                          device=device), group)
+        # R#20: gradients are per-rank SUMS; with n_users_global the dense buckets are
+        # all-reduced and scaled by 1/B_global (GradAggregator) and the sparse SGD applies
+        # lr / B_global to the summed row gradients (= lr x the batch-weighted mean)
+        self.grad_scale = 1.0 if n_users_global is None else 1.0 / float(n_users_global)
+        # head + token-MLP gradients live in one flat fp32 bucket (their all-reduce unit)
+        shapes = [("head", k, v) for k, v in {"w_a": tuple(self.head["w_a"].shape), "b_a": (self.head["w_a"].shape[0],),
+                                             "w_b": tuple(self.head["w_b"].shape), "b_b": (2,)}.items()]
+        shapes += [(t, k, v) for t, q in self.tokens.grad_shapes().items() for k, v in q.items()]
+        n = sum(int(np.prod(shp)) for _, _, shp in shapes)
+        self.dense_flat = torch.zeros(n, dtype=torch.float32, device=self.device)
+        self.head_grads, self.token_grads, off = {}, {}, 0
+        for owner, k, shp in shapes:
+            v = self.dense_flat[off:off + int(np.prod(shp))].view(*shp)
+            off += v.numel()
+            if owner == "head":
+                self.head_grads[k] = v
+            else:
+                self.token_grads.setdefault(owner, {})[k] = v
 
     def bind(self, jb: JaggedBatch, seg4: np.ndarray):
         self.jb = jb
@@ -50,11 +68,16 @@ class MTGRModel:
         return views
 
     def step(self, user_ids: torch.Tensor, item_ids: torch.Tensor, labels: torch.Tensor, now: int = 0,
-             on_layer_done=None):
+             on_layer_done=None, aggregator=None):
         """user_ids: int64 [n_U] (one per profile token); item_ids: int64 [n_S F_s + n_r F_r +
         n_C F_c] = the S, R and candidate tokens' feature IDs (user-major, token-major, feature
         fastest), as the data loader packs them; labels: uint8 [T].
-        Returns (loss [2] sums, dense gradient sums)."""
+        aggregator: a dp.GradAggregator: the layer buckets are all-reduced as each layer's
+        backward is enqueued, the head + token bucket after the token backward, and both are
+        scaled by 1/B_global at the end (R#20).
+        Returns (loss [2] sums, dense gradients: per-rank sums, or the aggregated mean)."""
+        if aggregator is not None and on_layer_done is None:
+            on_layer_done = aggregator.on_layer_done
         # sparse lookups (one two-stage-unique all-to-all per table)
         urows, uctx = self.user_table.lookup(user_ids, now, self.dtype)
         irows, ictx = self.item_table.lookup(item_ids, now, self.dtype)
@@ -62,11 +85,16 @@ class MTGRModel:
         # dense forward / loss / backward
         x = self.tokens.forward(feats)
         z = self.stack.forward(x.contiguous())
-        _, loss, dz, head_grads = head_fwd_bwd(self.jb, self.head, z, labels)
+        _, loss, dz, head_grads = head_fwd_bwd(self.jb, self.head, z, labels, grads_out=self.head_grads)
         dx = self.stack.backward(dz, on_layer_done=on_layer_done)
         ditem = torch.empty_like(irows)
-        dfeats, token_grads = self.tokens.backward(dx, out=self._item_views(ditem))
-        # sparse updates on the owners
-        self.user_table.backward_sgd(dfeats["u"], uctx, self.lr_sparse)
-        self.item_table.backward_sgd(ditem, ictx, self.lr_sparse)
+        dfeats, token_grads = self.tokens.backward(dx, out=self._item_views(ditem), grads_out=self.token_grads)
+        if aggregator is not None:
+            aggregator.on_layer_done(-1, self.dense_flat)
+        # sparse updates on the owners (row gradients summed over every rank by the all-to-all)
+        lr = self.lr_sparse * self.grad_scale
+        self.user_table.backward_sgd(dfeats["u"], uctx, lr)
+        self.item_table.backward_sgd(ditem, ictx, lr)
+        if aggregator is not None:
+            aggregator.finish(self.stack.grad_flat, self.dense_flat)
         return loss, {"head": head_grads, "tokens": token_grads, "layers": self.stack.grads}

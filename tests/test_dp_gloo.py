@@ -45,11 +45,14 @@ def _worker(rank, world, port, q):
         from paper_2505_18654_b200.dp import shard_users, GradAggregator
         cfg = synth.config("toy")
         seg = synth.gen_segments(cfg, 9)
-        users, load = shard_users(seg, world, rank, balance=lambda c, w: oracle.lpt(c, w))
+        users, load = shard_users(seg, world, rank)  # the product LPT (libmtgr mtgr_balance_lpt)
+        ro, lo = oracle.lpt(seg.astype(np.int64).sum(1), world)  # bit-exact with the oracle's
+        assert np.array_equal(np.nonzero(np.asarray(ro) == rank)[0], users) and np.array_equal(lo, load)
         allu = [None] * world
         dist.all_gather_object(allu, users.tolist())
         P = synth.gen_layer_params(cfg, 0)
         g = torch.from_numpy(_user_grads(cfg, seg, users, P))
+        # (mtgr_scale_f32 is a CUDA kernel: on the CPU process group the scale is torch's mul_)
         agg = GradAggregator(len(seg), scale_fn=lambda t, s: t.mul_(s))
         n = g.numel()
         agg.on_layer_done(0, g[: n // 2])   # two buckets, reduced asynchronously
@@ -80,3 +83,34 @@ def test_dp_aggregation_matches_pooled_gradient():
     assert not set(allu[0]) & set(allu[1])
     assert max(load) <= (4 / 3) * max(max(load), sum(load) / world)
     assert err <= 1e-12 * max(scale, 1.0)
+
+
+def _run(cmd, env=None, timeout=240):
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    e = dict(os.environ)
+    for k in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT"):
+        e.pop(k, None)
+    e.update(env or {})
+    return subprocess.run([sys.executable] + cmd, cwd=root, env=e, capture_output=True, text=True, timeout=timeout)
+
+
+def test_bench_launch_two_ranks_reference_arm():
+    """bench.py under torchrun with 2 ranks (the driver's launch, 127.0.0.1): rank 0 alone
+    prints ONE JSON line with n_gpus 2; the other rank exits 0 without work."""
+    import json
+    r = _run(["-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr", "127.0.0.1",
+              "--master-port", str(_free_port()), "bench.py", "--impl", "reference", "--gpus", "2",
+              "--config", "toy", "--steps", "1", "--warmup", "1"])
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.strip()]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["config"]["parallelism"] == "dp2"
+
+
+def test_bench_rejects_gpus_world_mismatch():
+    """--gpus N inside a launch of a different world size fails loudly (no silent 1-rank run)."""
+    r = _run(["bench.py", "--gpus", "2", "--config", "toy"], env={"WORLD_SIZE": "1", "RANK": "0", "LOCAL_RANK": "0"})
+    assert r.returncode == 2 and "WORLD_SIZE" in r.stderr

@@ -113,7 +113,8 @@ def _check_all(name, cfg, z, dx, gflat, Z, dX, G, dev, rows=None):
         rep["d" + k] = (rel_err(gv[k], G[k]), p999_rel_err(gv[k], G[k]))
     report(name, rep)
     print(name, rep)
-    bad = {k: v for k, v in rep.items() if not v[0] <= 2e-2}
+    # max-normalised <= 2e-2 (north_star); elementwise p99.9 <= 0.5 (measured <= 0.24)
+    bad = {k: v for k, v in rep.items() if not (v[0] <= 2e-2 and v[1] <= 0.5)}
     assert not bad, bad
 
 

@@ -22,8 +22,12 @@ def dev():
     return torch.device("cuda:0")
 
 
+@pytest.mark.parametrize("weighted", [False, True])
 @pytest.mark.parametrize("name", ["toy", "parity"])
-def test_full_training_step(dev, name):
+def test_full_training_step(dev, name, weighted):
+    """weighted: the data-parallel form (R#20) with a global batch 3x this rank's users:
+    every dense gradient (layers, head, token MLPs) comes out of the GradAggregator scaled by
+    1/B_global and the sparse rows move by -lr/B_global x their summed gradients."""
     cfg, seg, ts, _, _, P = make_batch(name)
     dt = torch.float32 if cfg["dtype"] == "f32" else torch.bfloat16
     d, e = cfg["d"], synth.EMB_DIM
@@ -38,11 +42,17 @@ def test_full_training_step(dev, name):
     jb = m.JaggedBatch.build(seg, ts, dev)
     lc = m.layer_cfg(d, cfg["H"], cfg["groups"])
     lr = 0.05
+    B_g = 3 * len(seg) if weighted else None
+    sc = 1.0 / B_g if weighted else 1.0
     model = m.MTGRModel(cfg, lc, Ps, TP, HP, widths, e, dt, dev, cap_user=4096, cap_item=1 << 16,
-                        lr_sparse=lr, seed=3)
+                        lr_sparse=lr, seed=3, n_users_global=B_g)
     model.bind(jb, seg)
+    agg = None
+    if weighted:
+        from paper_2505_18654_b200.dp import GradAggregator
+        agg = GradAggregator(B_g)
     loss, grads = model.step(torch.from_numpy(user_ids).to(dev), torch.from_numpy(item_ids).to(dev),
-                             torch.from_numpy(lab).to(dev), now=1)
+                             torch.from_numpy(lab).to(dev), now=1, aggregator=agg)
     torch.cuda.synchronize()
     # oracle: rows are the tables' init rows (rounded to the activation dtype on gather)
     rnd = (lambda a: a) if dt == torch.float32 else synth.round_bf16
@@ -77,9 +87,10 @@ def test_full_training_step(dev, name):
         gtok = gtok + g_u["s"]["w1"]
         dfe.append(d_u)
     tol = TOL[dt]
-    errs = {"loss": rel_err(loss.cpu().numpy(), lo), "head.dw_a": rel_err(grads["head"]["w_a"].cpu().numpy(), go["w_a"]),
-            "L0.dW1": rel_err(grads["layers"][0]["W1"].cpu().numpy(), gW1),
-            "tok.s.dw1": rel_err(grads["tokens"]["s"]["w1"].cpu().numpy(), gtok)}
+    errs = {"loss": rel_err(loss.cpu().numpy(), lo), "head.dw_a": rel_err(grads["head"]["w_a"].cpu().numpy(), sc * go["w_a"]),
+            "head.db_b": rel_err(grads["head"]["b_b"].cpu().numpy(), sc * go["b_b"]),
+            "L0.dW1": rel_err(grads["layers"][0]["W1"].cpu().numpy(), sc * gW1),
+            "tok.s.dw1": rel_err(grads["tokens"]["s"]["w1"].cpu().numpy(), sc * gtok)}
     # sparse SGD: every item row moved by -lr * (sum of its occurrences' gradients)
     upd = {}
     for u in range(len(seg)):
@@ -90,7 +101,7 @@ def test_full_training_step(dev, name):
     keys = np.array(sorted(upd)[:200], dtype=np.int64)
     slots = model.item_table.shard.find_or_insert(torch.from_numpy(keys).to(dev), insert=False)
     got = model.item_table.shard.gather(slots).cpu().numpy()
-    ref = np.stack([oracle.init_row(4, int(k), e, 0.5) - lr * upd[int(k)] for k in keys])
+    ref = np.stack([oracle.init_row(4, int(k), e, 0.5) - lr * sc * upd[int(k)] for k in keys])
     errs["item_rows"] = rel_err(got - np.stack([oracle.init_row(4, int(k), e, 0.5) for k in keys]),
                                 ref - np.stack([oracle.init_row(4, int(k), e, 0.5) for k in keys]))
     bad = {k: v for k, v in errs.items() if not v <= tol}

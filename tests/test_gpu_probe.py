@@ -251,6 +251,9 @@ def test_zero_mean_scores_attention(dev, bwd_path):
         e = rel_err(got[name], ref[name])
         rep[name] = (e, p999_rel_err(got[name], ref[name]))
         assert e <= 2e-2, (name, e)
+        # elementwise: bf16 P / dS and output rounding (2^-9 each) on sums with cancellation;
+        # measured 0.07 (floor 1e-2 max|o|, tests/fixtures.p999_rel_err)
+        assert rep[name][1] <= 0.15, (name, rep[name])
     report("zero_mean_attention[%s]" % bwd_path, rep)
     print("zero-mean attention (max-normalised, p99.9 elementwise):", rep)
 
@@ -285,5 +288,7 @@ def test_zero_mean_scores_layer(dev, bwd_path):
         rep["d" + k] = (rel_err(grads[k], go[k]), p999_rel_err(grads[k], go[k]))
     report("zero_mean_layer[%s]" % bwd_path, rep)
     print("zero-mean layer (max-normalised, p99.9 elementwise):", rep)
-    bad = {k: v for k, v in rep.items() if not v[0] <= 2e-2}
+    # max-normalised <= 2e-2 (north_star); elementwise p99.9 <= 0.5 (bf16 storage of every
+    # intermediate - X~, p, a, O, Y~ - each rounded at 2^-9 of its own scale; measured <= 0.25)
+    bad = {k: v for k, v in rep.items() if not (v[0] <= 2e-2 and v[1] <= 0.5)}
     assert not bad, bad
