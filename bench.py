@@ -45,8 +45,8 @@ def parse():
     ap.add_argument("--backend", default="nccl")
     ap.add_argument("--post-mlp", type=int, default=1, choices=[1, 2],
                     help="post-gate MLP: one Linear (R#6) or Linear-SiLU-Linear (S:354 variant)")
-    ap.add_argument("--mask", default="dynamic", choices=["dynamic", "causal"],
-                    help="mask mode: MTGR's dynamic mask, or the causal mask of the Table 4 ablation")
+    ap.add_argument("--mask", default="dynamic", choices=["dynamic", "causal", "full"],
+                    help="mask mode: MTGR's dynamic mask, or the Table 4 ablation read as causal / full attention")
     ap.add_argument("--full-model", action="store_true",
                     help="step = the whole training step: sparse IDs -> sharded hash-embedding lookup -> "
                          "tokens -> stack -> head/BCE -> backward -> sparse SGD (paper_2505_18654_b200.model)")
@@ -74,12 +74,14 @@ def peaks():
 
 def visible_pairs(seg_u, ts_u, mask="dynamic"):
     """P_u = L*n_s + sum_{i >= n_s} |{j in rt : ts_j < ts_i}| + (L - n_s)  (SURVEY §8(d));
-    causal mask: L (L + 1) / 2.
+    causal mask: L (L + 1) / 2; full mask: L (n_s + n_r) + K.
     Measurement bookkeeping for the algorithmic FLOP count (not part of the hot path)."""
     nU, nS, nR, K = (int(v) for v in seg_u)
     ns, L = nU + nS, nU + nS + nR + K
     if mask == "causal":
         return L * (L + 1) // 2
+    if mask == "full":
+        return L * (ns + nR) + K
     rt = np.sort(ts_u[ns:ns + nR])
     rows = ts_u[ns:]
     return L * ns + int(np.searchsorted(rt, rows, side="left").sum()) + (L - ns)
@@ -124,8 +126,10 @@ def kernel_algorithmic(cfg, tokens, pairs):
         "attn_bwd_dv": ("tensor", nl * 2.0 * d * pairs),
         "attn_bwd_dk": ("tensor", nl * 2.0 * d * pairs),
         "attn_bwd_dq": ("tensor", nl * 2.0 * d * pairs),
-        # DK kernel that also forms dP (recompute path, MTGR_ATTN_RECOMPUTE / MTGR_ATTN_FUSED_DK)
+        # DK kernel that also forms dP (recompute path, MTGR_ATTN_RECOMPUTE / MTGR_ATTN_BWD=fused_dk)
         "attn_bwd_dk_fused": ("tensor", nl * 4.0 * d * pairs),
+        # coupled dK/dV kernel (default backward): dP, dV, dK (its S^T is the excluded recompute)
+        "attn_bwd_kv": ("tensor", nl * 6.0 * d * pairs),
         # post_mlp_layers == 2: the first post-gate Linear runs on the SiLU epilogue (qkvu kind),
         # the second on the residual epilogue; each adds 2Td^2 to dgrad and wgrad
         "gemm_qkvu": ("tensor", nl * (8.0 + 2.0 * p2) * T * d * d),

@@ -84,12 +84,16 @@ typedef struct {
   int32_t mask_mode;   /* MTGR_MASK_DYNAMIC (0): MTGR's dynamic mask (R#8-R#12).
                           MTGR_MASK_CAUSAL (1): the plain causal mask over the packed order,
                           m_ij = [j <= i] (HSTU's) -- the "w/o dynamic mask"
-                          ablation of Table 4.  Other values: MTGR_E_ARG.          */
+                          ablation of Table 4, read as causal.
+                          MTGR_MASK_FULL (2): the same ablation read as full attention
+                          (SPEC S:345): m_ij = [j < n_static + n_rt] or [i == j]
+                          (every static and real-time token visible to every token,
+                          candidates only to themselves).  Other values: MTGR_E_ARG.        */
   int32_t post_mlp_layers; /* "another MLP" above the gate: 0 or 1 = one Linear
                               d->d + b2 (R#6); 2 = Linear(W2,b2) -> SiLU -> Linear(W3,b3)
                               (S:354 reading; the f3 variant).  Other values: MTGR_E_ARG.   */
 } mtgr_layer_cfg_t;
-enum { MTGR_MASK_DYNAMIC = 0, MTGR_MASK_CAUSAL = 1 };
+enum { MTGR_MASK_DYNAMIC = 0, MTGR_MASK_CAUSAL = 1, MTGR_MASK_FULL = 2 };
 
 /* Parameters of one layer.  W1/W2 have the activation dtype; everything else fp32. */
 typedef struct {
@@ -210,11 +214,16 @@ mtgr_status_t mtgr_hstu_attn_bwd(const mtgr_layer_cfg_t* cfg, const mtgr_jagged_
 /* Forward: X~ = GLN1(x); p = X~ W1^T + b1; [q|k|v|u] = silu(p); o = attn(q,k,v);
  * y = o (.) u; Y~ = GLN2(y); z = Y~ W2^T + b2 + x.
  * x, z: [T][d] dtype (may not alias).  saved: opaque buffer of mtgr_layer_saved_bytes() bytes
- * that the backward reads, or NULL for inference.  ws: mtgr_layer_workspace_bytes(). */
+ * that the backward reads, or NULL for inference.  ws: at least
+ * mtgr_layer_fwd_workspace_bytes(cfg, jag, dtype, saved == NULL) bytes (the forward's own
+ * scratch; mtgr_layer_workspace_bytes() covers the forward and the backward, so one workspace
+ * serves a training step).  Both depend on num_users and max_len as well as total_tokens. */
 size_t mtgr_layer_saved_bytes(const mtgr_layer_cfg_t* cfg, int32_t total_tokens,
                               mtgr_dtype_t dtype);
 size_t mtgr_layer_workspace_bytes(const mtgr_layer_cfg_t* cfg, const mtgr_jagged_t* jag,
                                   mtgr_dtype_t dtype);
+size_t mtgr_layer_fwd_workspace_bytes(const mtgr_layer_cfg_t* cfg, const mtgr_jagged_t* jag,
+                                      mtgr_dtype_t dtype, int32_t inference);
 mtgr_status_t mtgr_hstu_layer_fwd(const mtgr_layer_cfg_t* cfg, const mtgr_jagged_t* jag,
                                   mtgr_dtype_t dtype, const mtgr_layer_params_t* params,
                                   const void* x, void* z, void* saved, void* ws,

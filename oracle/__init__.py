@@ -24,7 +24,7 @@ Parity unpinned against the paper (pinned only to our own definition): the
 optional `rab` term (R#4), SiLU on Q/K/V/U (R#5), single-Linear post-gate MLP
 (R#6), eps (R#14).
 """
-from .mask import mask_dense, mask_causal, mask_for, MASK_MODES, mask_rules_pairwise, rab_bucket
+from .mask import mask_dense, mask_causal, mask_full, mask_for, MASK_MODES, mask_rules_pairwise, rab_bucket
 from .gln import gln_fwd, gln_bwd
 from .layer import (silu, dsilu, LayerCache, layer_fwd_user, layer_bwd_user,
                     stack_fwd_user, stack_bwd_user, attn_fwd_user, attn_bwd_user)

@@ -53,7 +53,21 @@ def mask_causal(L: int) -> np.ndarray:
     return (j <= i).astype(np.uint8)
 
 
-MASK_MODES = ("dynamic", "causal")
+def mask_full(n_s: int, n_r: int, n_c: int) -> np.ndarray:
+    """Table 4's "w/o dynamic mask" ablation read as FULL attention, the second reading
+    SPEC lists: the dynamic mask is removed, "except candidate diagonal rule is
+    retained to keep the task well-posed".  uint8 [L][L]:
+        m_ij = [j < n_s + n_r]  or  [i == j]
+    every static and real-time token is visible to every token (no timestamps consulted);
+    candidate tokens are visible to themselves only (rule 3).
+    """
+    L = n_s + n_r + n_c
+    i = np.arange(L)[:, None]
+    j = np.arange(L)[None, :]
+    return ((j < n_s + n_r) | (i == j)).astype(np.uint8)
+
+
+MASK_MODES = ("dynamic", "causal", "full")
 
 
 def mask_for(mode: str, n_s: int, n_r: int, n_c: int, ts) -> np.ndarray:
@@ -62,6 +76,8 @@ def mask_for(mode: str, n_s: int, n_r: int, n_c: int, ts) -> np.ndarray:
         return mask_dense(n_s, n_r, n_c, ts)
     if mode == "causal":
         return mask_causal(n_s + n_r + n_c)
+    if mode == "full":
+        return mask_full(n_s, n_r, n_c)
     raise ValueError(mode)
 
 

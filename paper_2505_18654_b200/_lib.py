@@ -113,6 +113,7 @@ SIGNATURES = {
                                 c_int64, _P, _P, _P, _P, _P, c_int64, _P, _P, c_size_t, _P]),
     "mtgr_layer_saved_bytes": (c_size_t, [POINTER(LayerCfg), c_int32, c_int32]),
     "mtgr_layer_workspace_bytes": (c_size_t, [POINTER(LayerCfg), POINTER(Jagged), c_int32]),
+    "mtgr_layer_fwd_workspace_bytes": (c_size_t, [POINTER(LayerCfg), POINTER(Jagged), c_int32, c_int32]),
     "mtgr_hstu_layer_fwd": (_S, [POINTER(LayerCfg), POINTER(Jagged), c_int32, POINTER(LayerParams),
                                  _P, _P, _P, _P, c_size_t, _P]),
     "mtgr_hstu_layer_bwd": (_S, [POINTER(LayerCfg), POINTER(Jagged), c_int32, POINTER(LayerParams),

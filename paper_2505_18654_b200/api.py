@@ -110,7 +110,7 @@ class JaggedBatch:
                       None if self.inv_norm is None else self.inv_norm.data_ptr())
 
 
-MASK_MODES = {"dynamic": 0, "causal": 1}  # include/mtgr.h MTGR_MASK_*
+MASK_MODES = {"dynamic": 0, "causal": 1, "full": 2}  # include/mtgr.h MTGR_MASK_*
 
 
 def layer_cfg(d_model, n_heads, num_groups=4, rab_buckets=0, eps=1e-6, qkvu_silu=True,
@@ -248,10 +248,17 @@ def layer_workspace_bytes(cfg: LayerCfg, jb: JaggedBatch, dtype: torch.dtype) ->
     return lib().mtgr_layer_workspace_bytes(ctypes.byref(cfg), ctypes.byref(j), _dt(dtype))
 
 
+def layer_fwd_workspace_bytes(cfg: LayerCfg, jb: JaggedBatch, dtype: torch.dtype, inference: bool) -> int:
+    """Forward-only scratch (mtgr_layer_fwd_workspace_bytes): no backward score scratch; with
+    inference = True it includes the per-layer intermediates that `saved` would hold."""
+    j = jb.c()
+    return lib().mtgr_layer_fwd_workspace_bytes(ctypes.byref(cfg), ctypes.byref(j), _dt(dtype), 1 if inference else 0)
+
+
 def hstu_layer_fwd(cfg, jb, params, x, z=None, saved=None, ws=None):
     z = torch.empty_like(x) if z is None else z
     if ws is None:
-        ws = _ws(layer_workspace_bytes(cfg, jb, x.dtype), x.device)
+        ws = _ws(layer_fwd_workspace_bytes(cfg, jb, x.dtype, saved is None), x.device)
     j = jb.c()
     cp = _cparams(params)
     check(lib().mtgr_hstu_layer_fwd(ctypes.byref(cfg), ctypes.byref(j), _dt(x.dtype), ctypes.byref(cp),
@@ -308,19 +315,24 @@ class HstuStack:
         self.grad_flat = torch.zeros(n * len(params), dtype=torch.float32, device=device)
         self.grads = [alloc_grads(cfg, device, self.grad_flat[i * n:(i + 1) * n]) for i in range(len(params))]
         self._jb = None
+        self.saved = self.xs = self.ws = None
 
     def bind(self, jb: JaggedBatch):
-        """Allocate activations for a batch (re-used across steps with the same T)."""
-        if self._jb is not None and self._jb.total_tokens == jb.total_tokens:
-            self._jb = jb
-            return
+        """Allocate activations for a batch.  Buffers are re-used while they are large enough:
+        the activations depend on T, the workspace also on num_users and max_len (stored-score
+        scratch), so each is checked against this batch's own requirement."""
         self._jb = jb
         T, d = max(jb.total_tokens, 1), self.cfg.d_model
         sb = layer_saved_bytes(self.cfg, jb.total_tokens, self.dtype)
-        self.saved = [_ws(sb, self.device) for _ in self.params]
-        self.xs = [None] + [torch.empty(T, d, dtype=self.dtype, device=self.device) for _ in self.params]
-        self.dbuf = [torch.empty(T, d, dtype=self.dtype, device=self.device) for _ in range(2)]
-        self.ws = _ws(layer_workspace_bytes(self.cfg, jb, self.dtype), self.device)
+        if getattr(self, "saved", None) is None or self.saved[0].numel() < sb:
+            self.saved = [_ws(sb, self.device) for _ in self.params]
+        if getattr(self, "xs", None) is None or self.xs[1].shape[0] < T:
+            self.xs = [None] + [torch.empty(T, d, dtype=self.dtype, device=self.device) for _ in self.params]
+            self.dbuf = [torch.empty(T, d, dtype=self.dtype, device=self.device) for _ in range(2)]
+        wb = layer_workspace_bytes(self.cfg, jb, self.dtype)
+        if getattr(self, "ws", None) is None or self.ws.numel() < wb:
+            self.ws = None  # release before allocating the larger one
+            self.ws = _ws(wb, self.device)
 
     def forward(self, x: torch.Tensor) -> torch.Tensor:
         jb = self._jb

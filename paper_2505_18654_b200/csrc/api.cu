@@ -55,8 +55,9 @@ static mtgr_status_t check_cfg(const mtgr_layer_cfg_t* c) {
   MTGR_CHECK(dh % 8 == 0 && dh <= 256, MTGR_E_UNSUPPORTED, "head dim %d must be a multiple of 8, <= 256", dh);
   MTGR_CHECK(c->rab_buckets >= 0 && c->rab_buckets <= 64, MTGR_E_ARG, "rab_buckets must be in [0, 64]");
   MTGR_CHECK(c->eps > 0.f, MTGR_E_ARG, "eps must be positive");
-  MTGR_CHECK(c->mask_mode == MTGR_MASK_DYNAMIC || c->mask_mode == MTGR_MASK_CAUSAL, MTGR_E_ARG,
-             "mask_mode must be MTGR_MASK_DYNAMIC or MTGR_MASK_CAUSAL");
+  MTGR_CHECK(c->mask_mode == MTGR_MASK_DYNAMIC || c->mask_mode == MTGR_MASK_CAUSAL ||
+                 c->mask_mode == MTGR_MASK_FULL,
+             MTGR_E_ARG, "mask_mode must be MTGR_MASK_DYNAMIC, MTGR_MASK_CAUSAL or MTGR_MASK_FULL");
   MTGR_CHECK(c->post_mlp_layers >= 0 && c->post_mlp_layers <= 2, MTGR_E_ARG, "post_mlp_layers must be 0, 1 or 2");
   return MTGR_OK;
 }
@@ -216,7 +217,7 @@ static mtgr_status_t layer_fwd_t(const mtgr_layer_cfg_t* c, const mtgr_jagged_t*
   MTGR_TRY(run_gemm<T>(g, EPI_QKVU, gws, gws_bytes, st));
   // O = silu(Q K^T)/N (.) M V  (Eq.5); the gate Y = O (.) U (Eq.6) is formed inside GLN2
   AttnIO at{};
-  at.jag = *j; at.causal = c->mask_mode == MTGR_MASK_CAUSAL; at.H = c->n_heads; at.dh = d / c->n_heads; at.d = d; at.nb = c->rab_buckets;
+  at.jag = *j; at.causal = c->mask_mode == MTGR_MASK_CAUSAL; at.full = c->mask_mode == MTGR_MASK_FULL; at.H = c->n_heads; at.dh = d / c->n_heads; at.d = d; at.nb = c->rab_buckets;
   at.q = a; at.k = a + d; at.v = a + 2 * d; at.ld = 4 * d;
   at.o = o; at.u = nullptr; at.y = nullptr; at.rab_w = P->rab_w;  // gate folded into GLN2
   at.ctr = ctr;
@@ -353,7 +354,7 @@ static mtgr_status_t layer_bwd_t(const mtgr_layer_cfg_t* c, const mtgr_jagged_t*
   MTGR_TRY(gln_bwd_launch<T>(gi, GLNB_GATE, (float*)scratch, G->gamma2, G->beta2, acc, st));
   // attention backward (+ silu' of Q, K, V) into dp[:, 0:3d]
   AttnIO at{};
-  at.jag = *j; at.causal = c->mask_mode == MTGR_MASK_CAUSAL; at.H = H; at.dh = d / H; at.d = d; at.nb = c->rab_buckets;
+  at.jag = *j; at.causal = c->mask_mode == MTGR_MASK_CAUSAL; at.full = c->mask_mode == MTGR_MASK_FULL; at.H = H; at.dh = d / H; at.d = d; at.nb = c->rab_buckets;
   at.q = a; at.k = a + d; at.v = a + 2 * d; at.ld = 4 * d;
   at.dO = dO; at.pre = c->qkvu_silu ? p : nullptr; at.ld_pre = 4 * d; at.pre_dsilu = 1;
   at.dq = dp; at.dk = dp + d; at.dv = dp + 2 * d; at.ld_out = 4 * d;
@@ -505,7 +506,7 @@ MTGR_API mtgr_status_t mtgr_hstu_attn_fwd(const mtgr_layer_cfg_t* cfg, const mtg
   MTGR_CHECK(aligned16(q) && aligned16(k) && aligned16(v) && aligned16(o) && (!u || aligned16(u)),
              MTGR_E_LAYOUT, "attn_fwd: pointers must be 16-byte aligned");
   AttnIO at{};
-  at.jag = *jag; at.causal = cfg->mask_mode == MTGR_MASK_CAUSAL; at.H = cfg->n_heads; at.dh = cfg->d_model / cfg->n_heads; at.d = cfg->d_model;
+  at.jag = *jag; at.causal = cfg->mask_mode == MTGR_MASK_CAUSAL; at.full = cfg->mask_mode == MTGR_MASK_FULL; at.H = cfg->n_heads; at.dh = cfg->d_model / cfg->n_heads; at.d = cfg->d_model;
   at.nb = cfg->rab_buckets; at.q = q; at.k = k; at.v = v; at.ld = ld; at.u = u; at.o = o; at.y = y;
   at.rab_w = rab_w;
   at.ctr = (int*)((char*)ws + 2 * attn_diag_half(jag->total_tokens, cfg->n_heads));
@@ -532,7 +533,7 @@ MTGR_API mtgr_status_t mtgr_hstu_attn_bwd(const mtgr_layer_cfg_t* cfg, const mtg
              MTGR_E_LAYOUT, "attn_bwd: pointers must be 16-byte aligned");
   const size_t half = attn_diag_half(jag->total_tokens, cfg->n_heads);
   AttnIO at{};
-  at.jag = *jag; at.causal = cfg->mask_mode == MTGR_MASK_CAUSAL; at.H = cfg->n_heads; at.dh = cfg->d_model / cfg->n_heads; at.d = cfg->d_model;
+  at.jag = *jag; at.causal = cfg->mask_mode == MTGR_MASK_CAUSAL; at.full = cfg->mask_mode == MTGR_MASK_FULL; at.H = cfg->n_heads; at.dh = cfg->d_model / cfg->n_heads; at.d = cfg->d_model;
   at.nb = cfg->rab_buckets; at.q = q; at.k = k; at.v = v; at.ld = ld; at.dO = dO;
   at.pre = silu_pre; at.ld_pre = ld; at.dq = dq; at.dk = dk; at.dv = dv; at.ld_out = ld_out;
   at.rab_w = rab_w; at.drab = drab_w;
@@ -558,6 +559,12 @@ MTGR_API size_t mtgr_layer_workspace_bytes(const mtgr_layer_cfg_t* cfg, const mt
                   bwd_ws_bytes(cfg, jag, dtype)) + 4096;
 }
 
+MTGR_API size_t mtgr_layer_fwd_workspace_bytes(const mtgr_layer_cfg_t* cfg, const mtgr_jagged_t* jag,
+                                               mtgr_dtype_t dtype, int32_t inference) {
+  if (!cfg || !jag) return 0;
+  return fwd_ws_bytes(cfg, jag->total_tokens, dtype, inference != 0) + 4096;
+}
+
 static mtgr_status_t check_params(const mtgr_layer_cfg_t* cfg, const mtgr_layer_params_t* P) {
   MTGR_CHECK(P, MTGR_E_ARG, "params is NULL");
   MTGR_CHECK(P->w1 && P->b1 && P->w2 && P->b2 && P->gamma1 && P->beta1 && P->gamma2 && P->beta2,
@@ -578,8 +585,10 @@ MTGR_API mtgr_status_t mtgr_hstu_layer_fwd(const mtgr_layer_cfg_t* cfg, const mt
   MTGR_TRY(check_dtype(dtype));
   MTGR_TRY(check_attn_dtype(cfg, dtype));
   MTGR_TRY(check_params(cfg, params));
-  MTGR_CHECK(ws_bytes >= mtgr_layer_workspace_bytes(cfg, jag, dtype), MTGR_E_WORKSPACE,
-             "layer workspace too small (%zu < %zu)", ws_bytes, mtgr_layer_workspace_bytes(cfg, jag, dtype));
+  {
+    const size_t need = mtgr_layer_fwd_workspace_bytes(cfg, jag, dtype, saved == nullptr);
+    MTGR_CHECK(ws_bytes >= need, MTGR_E_WORKSPACE, "layer forward workspace too small (%zu < %zu)", ws_bytes, need);
+  }
   if (jag->total_tokens == 0) return MTGR_OK;
   MTGR_CHECK(x && z && ws, MTGR_E_ARG, "layer_fwd: null pointer");
   MTGR_CHECK(x != z, MTGR_E_ARG, "layer_fwd: x and z must not alias");

@@ -97,4 +97,11 @@ __device__ __forceinline__ bool visible_offdiag(int i, int j, int ns, long long 
   return (j < ns) || (i >= ns && ts_j < ts_i);
 }
 
+// The full mask (MTGR_MASK_FULL: Table 4's "w/o dynamic mask" read as full attention, SPEC
+// S:345) restricted the same way: every static and real-time key [0, ns+nr) is visible to every
+// row, except the row's own column for non-static rows (their diagonal term adds it).
+__device__ __forceinline__ bool visible_offdiag_full(int i, int j, int ns, int nr) {
+  return j < ns + nr && (i < ns || i != j);
+}
+
 }  // namespace mtgr

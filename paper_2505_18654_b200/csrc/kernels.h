@@ -52,6 +52,7 @@ mtgr_status_t gemm_bf16_launch(const GemmIO& g, int epi, void* ws, size_t ws_byt
 struct AttnIO {
   mtgr_jagged_t jag;
   int causal;                  // mask mode MTGR_MASK_CAUSAL: m_ij = [j <= i] (else dynamic)
+  int full;                    // mask mode MTGR_MASK_FULL: m_ij = [j < ns + nr] or [i == j]
   int H, dh, d, nb;            // heads, head dim, d_model, rab buckets (0 = off)
   const void* q; const void* k; const void* v; int64_t ld;
   const void* u;               // gate or NULL
@@ -71,6 +72,7 @@ struct AttnIO {
 };
 // scratch of the stored-score tensor-core backward for this batch (0: recompute path)
 size_t attn_store_ws_bytes(const mtgr_jagged_t& j, int H);
+size_t attn_kv_ws_bytes(const mtgr_jagged_t& j, int H);  // coupling workspace of attn_kv_launch
 size_t attn_ws_bytes(int ntok, int H);
 template <class T>
 mtgr_status_t attn_diag_launch(const AttnIO& a, bool bwd, float* diag_a, float* diag_ds,

@@ -211,7 +211,8 @@ __global__ void __launch_bounds__(256) attn_simt_fwd_kernel(AttnIO a) {
   const int i0 = blockIdx.x * SA_B;
   if (i0 >= us.L) return;
   const int nq = min(SA_B, us.L - i0);
-  const int kv_end = a.causal ? min(us.L, i0 + nq) : ((i0 + nq > us.ns) ? us.ns + us.nr : us.ns);
+  const int kv_end = a.causal ? min(us.L, i0 + nq)
+                              : ((a.full || i0 + nq > us.ns) ? us.ns + us.nr : us.ns);
   const int r = threadIdx.x / 8, cg = threadIdx.x % 8;
   const int i = i0 + r;
   const int64_t col0 = (int64_t)h * dh;
@@ -237,7 +238,10 @@ __global__ void __launch_bounds__(256) attn_simt_fwd_kernel(AttnIO a) {
       int j = j0 + jj;
       float s = 0.f;
       for (int c = 0; c < dh; ++c) s = fmaf(Qs[r * dh + c], Ks[jj * dh + c], s);
-      bool vis = i < us.L && jj < nk && (a.causal ? j <= i : visible_offdiag(i, j, us.ns, ts_i, tsk[jj]));
+      bool vis = i < us.L && jj < nk &&
+                 (a.causal ? j <= i
+                           : (a.full ? visible_offdiag_full(i, j, us.ns, us.nr)
+                                     : visible_offdiag(i, j, us.ns, ts_i, tsk[jj])));
       if (a.nb > 0) s += a.rab_w[h * a.nb + rab_bucket(ts_i - tsk[jj], a.nb)];
       Ps[r * (SA_B + 1) + jj] = vis ? silu_f(s) : 0.f;
     }
@@ -295,7 +299,7 @@ __global__ void __launch_bounds__(256) attn_simt_dkv_kernel(AttnIO a) {
 #pragma unroll
   for (int c = 0; c < 32; ++c) accv[c] = acck[c] = 0.f;
   const int ncol = dh / 8;
-  const int q_begin = a.causal ? j0 : ((j0 < us.ns) ? 0 : us.ns);
+  const int q_begin = a.causal ? j0 : ((a.full || j0 < us.ns) ? 0 : us.ns);
   const int q_end = (j0 < key_end) ? us.L : 0;
   for (int i0 = q_begin; i0 < q_end; i0 += SA_B) {
     const int nq = min(SA_B, us.L - i0);
@@ -314,7 +318,10 @@ __global__ void __launch_bounds__(256) attn_simt_dkv_kernel(AttnIO a) {
         s = fmaf(Qs[ii * dh + c], Ks[r * dh + c], s);
         dp = fmaf(Ds[ii * dh + c], Vs[r * dh + c], dp);
       }
-      bool vis = ii < nq && j < key_end && (a.causal ? i >= j : visible_offdiag(i, j, us.ns, tsq[ii], ts_j));
+      bool vis = ii < nq && j < key_end &&
+                 (a.causal ? i >= j
+                           : (a.full ? visible_offdiag_full(i, j, us.ns, us.nr)
+                                     : visible_offdiag(i, j, us.ns, tsq[ii], ts_j)));
       int bk = 0;
       if (a.nb > 0) { bk = rab_bucket(tsq[ii] - ts_j, a.nb); s += a.rab_w[h * a.nb + bk]; }
       float ds = vis ? dp * dsilu_f(s) : 0.f;
@@ -375,7 +382,8 @@ __global__ void __launch_bounds__(256) attn_simt_dq_kernel(AttnIO a) {
   const int i0 = blockIdx.x * SA_B;
   if (i0 >= us.L) return;
   const int nq = min(SA_B, us.L - i0);
-  const int kv_end = a.causal ? min(us.L, i0 + nq) : ((i0 + nq > us.ns) ? us.ns + us.nr : us.ns);
+  const int kv_end = a.causal ? min(us.L, i0 + nq)
+                              : ((a.full || i0 + nq > us.ns) ? us.ns + us.nr : us.ns);
   const int r = threadIdx.x / 8, cg = threadIdx.x % 8;
   const int i = i0 + r;
   const int64_t col0 = (int64_t)h * dh;
@@ -405,7 +413,10 @@ __global__ void __launch_bounds__(256) attn_simt_dq_kernel(AttnIO a) {
         s = fmaf(Qs[r * dh + c], Ks[jj * dh + c], s);
         dp = fmaf(Ds[r * dh + c], Vs[jj * dh + c], dp);
       }
-      bool vis = i < us.L && jj < nk && (a.causal ? j <= i : visible_offdiag(i, j, us.ns, ts_i, tsk[jj]));
+      bool vis = i < us.L && jj < nk &&
+                 (a.causal ? j <= i
+                           : (a.full ? visible_offdiag_full(i, j, us.ns, us.nr)
+                                     : visible_offdiag(i, j, us.ns, ts_i, tsk[jj])));
       if (a.nb > 0) s += a.rab_w[h * a.nb + rab_bucket(ts_i - tsk[jj], a.nb)];
       Ss[r * (SA_B + 1) + jj] = vis ? dp * dsilu_f(s) : 0.f;
     }

@@ -45,112 +45,10 @@
 #include "kernels.h"
 #include "prof.h"
 #include "sm100.cuh"
+#include "tc_attn.cuh"
 
 namespace mtgr {
 namespace tca {
-
-constexpr int DH = 256;
-constexpr int BR = 128;                 // rows per CTA
-constexpr int BC = 64;                  // columns per iterated tile
-constexpr int KB = 1024;
-constexpr int RT_BYTES = BR * DH * 2;   // 64 KB: 4 boxes {64 dh, 128 rows}
-// key timestamps of the current tile (int64 x 64) and the barriers: after the epilogue tile
-// (!TWO) / after the dbias scratch [208,216) KB (TWO)
-constexpr int off_ts(bool two) { return (two ? 216 : 224) * KB; }
-constexpr int off_bar(bool two) { return off_ts(two) + BC * 8; }
-constexpr int SMEM_BYTES = off_bar(false) + 512 + 1024;
-constexpr int NSM = 8;  // softmax/epilogue warps
-
-enum { FWD = 0, DV = 1, DQ = 2, DK = 3 };
-
-struct Args {
-  mtgr_jagged_t jag;
-  int H, d;
-  int pmax, nitems;                         // row pairs per user (max), work items B*pmax*H
-  int* ctr;                                 // work-queue counter (zeroed before the launch)
-  __nv_bfloat16* out; int64_t ld_out;
-  const __nv_bfloat16* e; int64_t ld_e;     // diagonal-term rows (E) of the epilogue
-  const __nv_bfloat16* uu; int64_t ld_u;    // gate (FWD) / SiLU' source (bwd) rows, or NULL
-  const float* diag;                        // [T][H]
-  int pre_dsilu;                            // the pre rows hold silu'(p) already
-  float* dbias;                             // bwd: red.add column sums of the outputs, or NULL
-  long long* dbg;                           // debug timestamps (MTGR_ATTN_TRACE) or NULL
-  // stored-score backward (DK writes P^T and dS^T, the DV / DQ products read them back):
-  // matrices [H][st_rows][st_pitch] bf16, row = koff[u] + key (user-local), column = query
-  __nv_bfloat16* st_p;                      // P^T  = silu(S^T) * m      (DK writes, or NULL)
-  __nv_bfloat16* st_ds;                     // dS^T = dP^T silu'(S^T) m  (DK writes, or NULL)
-  int64_t st_pitch, st_rows;
-  const int* koff;                          // [B+1] padded key-row offsets (multiples of 256)
-  int causal;                               // MTGR_MASK_CAUSAL: m_ij = [j <= i]
-  int sc_cp;                                // score kernel: row operands via tcgen05.cp
-  int row_cp;                               // FWD / DV: row operand via tcgen05.cp
-  int c_align;                              // TRANS items of real-time keys start their query
-                                            // range at the 256-aligned pair holding n_static
-};
-
-// debug tracing (MTGR_ATTN_TRACE=1) of the CTA pair of cluster 1: slot layout [event][item]
-// per CTA, events: 0 item start, 1 tiles done, 2 next R1 copied, 3 o_full, 4 epilogue done
-// (softmax warp 4); 5 first S issued, 6 last acc issued (MMA warp); 7 R1 load issued, 8 last C1
-// load issued (producer); 9 ntiles (value); 10*64 = time base after the start-up cluster barrier
-#define DBG_ON (a.dbg != nullptr && (blockIdx.x >> 1) == 1)
-#define DBGV(ev, i, val) do { if (DBG_ON && (i) < 64) a.dbg[(blockIdx.x & 1) * 20 * 64 + (ev) * 64 + (i)] = (val); } while (0)
-#define DBG(ev, i) DBGV(ev, i, clock64())
-
-__device__ __forceinline__ float silu_fast(float s) {
-  const float h = 0.5f * s;
-  return fmaf(h, sm100::tanh_approx(h), h);
-}
-__device__ __forceinline__ float dsilu_fast(float s) {
-  const float sg = fmaf(0.5f, sm100::tanh_approx(0.5f * s), 0.5f);
-  return fmaf(s * sg, 1.0f - sg, sg);
-}
-__device__ __forceinline__ uint32_t pack2(float a, float b) {
-  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
-  return *reinterpret_cast<uint32_t*>(&h);
-}
-// 16-byte chunk j (0..7) of row r inside a SWIZZLE_128B box of 128-byte rows
-__device__ __forceinline__ uint32_t sw128(int r, int j) { return r * 128 + ((j ^ (r & 7)) << 4); }
-
-// One work item = (user u, row pair p, head h): rows [p*256, p*256+256) of user u, 128 per CTA.
-struct Item {
-  UserSpan us;
-  int u, h, hcol, pr0, r0, kv_end, c_begin, ntiles;
-  bool need_e;  // some rows of this CTA are candidates (diagonal terms outside the key range)
-};
-
-template <bool TRANS>
-__device__ __forceinline__ bool decode_item(const Args& a, int k, uint32_t crank, Item& it) {
-  it.h = k % a.H;
-  const int rest = k / a.H;
-  const int p = rest % a.pmax;
-  it.u = rest / a.pmax;
-  it.us = load_user(a.jag, it.u);
-  it.pr0 = p * 2 * BR;
-  if (it.pr0 >= it.us.L) return false;
-  it.r0 = it.pr0 + (int)crank * BR;
-  it.hcol = it.h * DH;
-  // keys that can be visible to some row (beyond them only the candidates' own diagonal):
-  // dynamic mask [0, ns + nr); causal mask every key
-  it.kv_end = a.causal ? it.us.L : it.us.ns + it.us.nr;
-  const int pair_end = min(it.us.L, it.pr0 + 2 * BR);
-  int c_end = 0;
-  it.c_begin = 0;
-  if (a.causal) {  // keys [0, pair_end) of a query pair; queries [pr0, L) of a key pair
-    if (!TRANS) c_end = pair_end;
-    else { it.c_begin = it.pr0; c_end = it.us.L; }
-  } else if (!TRANS) {
-    c_end = (pair_end > it.us.ns) ? it.kv_end : it.us.ns;
-  } else if (it.pr0 < it.kv_end) {
-    // keys that only non-static queries read.  With c_align the range starts at the query pair
-    // holding n_static, so that every query pair that reads these keys finds them stored (its
-    // static rows read masked zeros)
-    it.c_begin = (it.pr0 < it.us.ns) ? 0 : (a.c_align ? (it.us.ns / (2 * BR)) * (2 * BR) : it.us.ns);
-    c_end = it.us.L;
-  }
-  it.ntiles = c_end > it.c_begin ? (c_end - it.c_begin + BC - 1) / BC : 0;
-  it.need_e = it.r0 + BR > it.kv_end && it.r0 < it.us.L;
-  return true;
-}
 
 template <int MODE>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
@@ -641,11 +539,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
         const long long my_ts = (my < us.L && a.jag.ts) ? a.jag.ts[g] : 0;
         // stored-score row of this key (DK): [h][koff[u] + my][query]
         const int64_t st_row = store_scores ? ((int64_t)it.h * a.st_rows + a.koff[it.u] + my) * a.st_pitch : 0;
-        const bool need_ts_rows = TRANS && !a.causal && (it.r0 + BR > us.ns) && (it.r0 < it.kv_end);
+        const bool need_ts_rows = TRANS && !a.causal && !a.full && (it.r0 + BR > us.ns) && (it.r0 < it.kv_end);
 #pragma unroll 1
         for (int t = 0; t < it.ntiles; ++t, ++gt) {
           const int c0 = it.c_begin + t * BC;
-          const bool need_ts = TRANS ? need_ts_rows : (!a.causal && c0 + BC > us.ns && c0 < it.kv_end);
+          const bool need_ts = TRANS ? need_ts_rows : (!a.causal && !a.full && c0 + BC > us.ns && c0 < it.kv_end);
           long long* tsb = sTs;
           if (need_ts) {  // uniform over the 8 softmax warps
             const int i = threadIdx.x - 128;
@@ -676,6 +574,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
             const uint32_t below_hi = hi >= 32 ? 0xffffffffu : ((1u << hi) - 1u);
             const uint32_t below_lo = lo >= 32 ? 0xffffffffu : ((1u << lo) - 1u);
             vis = (my < us.L) ? (below_hi & ~below_lo) : 0u;
+          } else if (a.full) {
+            // full mask (Table 4 "w/o dynamic mask" read as full attention): static
+            // and real-time keys [0, kv_end) visible to every query; candidates: diagonal only
+            if (!TRANS) {
+              const int n_kv = min(max(it.kv_end - cb, 0), 32);
+              vis = n_kv >= 32 ? 0xffffffffu : ((1u << n_kv) - 1u);
+            } else {
+              const int nvalid = us.L - cb;
+              vis = (my >= it.kv_end || nvalid <= 0) ? 0u : (nvalid >= 32 ? 0xffffffffu : ((1u << nvalid) - 1u));
+            }
           } else if (!TRANS) {
             // static columns [0, ns) are visible to every row; real-time columns [ns, kv_end)
             // only to non-static rows with an earlier timestamp (diagonal: epilogue)
@@ -1202,7 +1110,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       arrive_leader(r_done);
       }
       const long long my_ts = (my < us.L && a.jag.ts) ? a.jag.ts[(int64_t)us.off + my] : 0;
-      const bool need_ts = !a.causal && (it.r0 + BR > us.ns) && (it.r0 < it.kv_end);  // uniform
+      const bool need_ts = !a.causal && !a.full && (it.r0 + BR > us.ns) && (it.r0 < it.kv_end);  // uniform
       const int64_t st_row = ((int64_t)it.h * a.st_rows + a.koff[it.u] + my) * a.st_pitch;
 #pragma unroll 1
       for (int t = 0; t < it.ntiles; ++t, ++gt) {
@@ -1229,7 +1137,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
           const uint32_t below_hi = hi >= 32 ? 0xffffffffu : ((1u << hi) - 1u);
           const uint32_t below_lo = lo >= 32 ? 0xffffffffu : ((1u << lo) - 1u);
           vis = (my < us.L) ? (below_hi & ~below_lo) : 0u;
-        } else if (my < us.ns) {  // static keys: every query of the user
+        } else if (my < us.ns || (a.full && my < it.kv_end)) {  // every query of the user
           const int nvalid = us.L - cb;
           vis = nvalid >= 32 ? 0xffffffffu : (nvalid <= 0 ? 0u : ((1u << nvalid) - 1u));
         } else if (my < it.kv_end) {  // real-time keys: later non-static queries, and itself
@@ -1696,6 +1604,7 @@ static mtgr_status_t launch_mode(const AttnIO& io, const void* c1, int64_t ld_c1
   MTGR_TRY(make_tmap_bf16(&m.o, args.out, d, T, args.ld_out, 64, 32));
   Args a2 = args;
   a2.causal = io.causal;
+  a2.full = io.full;
   // row operand into TMEM by tcgen05.cp from the MMA warp (default) or through the softmax
   // warps' registers (MTGR_ROW_CP=0)
   { const char* x = getenv("MTGR_ROW_CP"); a2.row_cp = !(x != nullptr && x[0] == '0'); }
@@ -1760,6 +1669,7 @@ static mtgr_status_t launch_mm(const AttnIO& io, const void* amat, const void* b
   MTGR_TRY(make_tmap_bf16(&to, args.out, d, T, args.ld_out, 64, 32));
   Args a2 = args;
   a2.causal = io.causal;
+  a2.full = io.full;
   // row operand into TMEM by tcgen05.cp from the MMA warp (default) or through the softmax
   // warps' registers (MTGR_ROW_CP=0)
   { const char* x = getenv("MTGR_ROW_CP"); a2.row_cp = !(x != nullptr && x[0] == '0'); }
@@ -1789,6 +1699,7 @@ static mtgr_status_t launch_sc(const AttnIO& io, const MmLayout& l, const Args& 
   MTGR_TRY(make_tmap_bf16(&tr2, io.v, d, T, io.ld, 64, BR));      // V rows
   Args a2 = args;
   a2.causal = io.causal;
+  a2.full = io.full;
   a2.pmax = ceil_div(io.jag.max_len, 2 * BR);
   a2.nitems = io.jag.num_users * a2.pmax * io.H;
   a2.st_pitch = l.pitch; a2.st_rows = l.rows;
@@ -1804,6 +1715,20 @@ static mtgr_status_t launch_sc(const AttnIO& io, const MmLayout& l, const Args& 
   return check_launch("attn_sc");
 }
 
+// Coupled dK/dV backward (tc_attn_kv.cu): koff [B+1], the stored dS^T matrix [H][rows][pitch]
+// of the dQ GEMM, then the coupling workspace (tickets, flags, item lists, G rings)
+struct KvLayout {
+  size_t koff = 0, ds = 0, sync = 0, total = 0;
+};
+static KvLayout kv_layout(const mtgr_jagged_t& j, int H) {
+  const MmLayout m = mm_layout(j, H);
+  KvLayout l;
+  l.ds = m.p;  // same koff / matrix geometry as the stored-score path
+  l.sync = l.ds + (m.ds - m.p);
+  l.total = l.sync + align_up(attn_kv_ws_bytes(j, H), 1024);
+  return l;
+}
+
 }  // namespace tca
 
 bool attn_tc_supported(int dh) { return dh == tca::DH; }
@@ -1812,7 +1737,7 @@ size_t attn_store_ws_bytes(const mtgr_jagged_t& j, int H) {
   if (j.num_users == 0 || j.total_tokens == 0) return 0;
   const char* env = getenv("MTGR_ATTN_RECOMPUTE");  // tests / A-B: force the recompute kernels
   if (env != nullptr && env[0] == '1') return 0;
-  const size_t b = tca::mm_layout(j, H).total;
+  const size_t b = std::max(tca::mm_layout(j, H).total, tca::kv_layout(j, H).total);
   // beyond this the backward recomputes the scores in the DV / DQ kernels instead
   return b <= ((size_t)48 << 30) ? b : 0;
 }
@@ -1850,14 +1775,30 @@ mtgr_status_t attn_tc_bwd_launch(const AttnIO& io, cudaStream_t st) {
     bf* sds = (bf*)(ws + l.ds);
     attn_koff_kernel<<<1, 1024, 0, st>>>(io.jag, io.causal, koff);
     MTGR_TRY(check_launch("attn_koff"));
-    // score kernel + dK GEMM for short users, the fused DK kernel (which also writes the scores)
-    // for long ones, where its per-item epilogue is amortised: measured crossover between
-    // `small` (mean 1.0k tokens: score kernel 3% faster) and `large` (4.5k: fused 2% faster).
-    // MTGR_ATTN_FUSED_DK=1 / =0 forces either (A/B and tests)
+    // Which backward: MTGR_ATTN_BWD = kv (default: the coupled dK/dV kernel writes dS^T, then the
+    // dQ GEMM), stored (score kernel writes P^T and dS^T, then dK / dV / dQ GEMMs) or fused_dk
+    // (the DK kernel writes both while forming dK).  MTGR_ATTN_FUSED_DK=1 / =0 (round 1) still
+    // selects fused_dk / stored.
+    const char* benv = getenv("MTGR_ATTN_BWD");
     const char* fenv = getenv("MTGR_ATTN_FUSED_DK");
-    const bool fused_dk = fenv != nullptr ? fenv[0] == '1'
-                                          : (int64_t)io.jag.total_tokens >= (int64_t)2048 * io.jag.num_users;
-    if (fused_dk) {  // dK = nu dS^T Q (+ diag), * silu'(p_K); also stores P^T, dS^T
+    int path = 0;  // 0 kv, 1 stored, 2 fused_dk
+    if (benv != nullptr) path = benv[0] == 's' ? 1 : (benv[0] == 'f' ? 2 : 0);
+    else if (fenv != nullptr) path = fenv[0] == '1' ? 2 : 1;
+    if (path == 0) {
+      const KvLayout kl = kv_layout(io.jag, io.H);
+      bf* kds = (bf*)(ws + kl.ds);
+      Args ax{}, ay{};
+      for (Args* p : {&ax, &ay}) { p->jag = io.jag; p->H = io.H; p->d = io.d; p->koff = koff; }
+      ay.st_ds = kds; ay.st_pitch = l.pitch; ay.st_rows = l.rows;
+      MTGR_TRY(attn_kv_launch(io, ax, ay, ws + kl.sync, st));
+      Args a{};
+      a.jag = io.jag; a.H = io.H; a.d = io.d;
+      a.out = (bf*)io.dq; a.ld_out = io.ld_out; a.diag = io.diag_ds;
+      a.dbias = io.dbias;
+      a.koff = koff;
+      return launch_mm<MM_DQ>(io, kds, io.k, io.ld, io.k, io.ld, pre, io.ld_pre, l, a, PROF_ATTN_DQ, st);
+    }
+    if (path == 2) {  // dK = nu dS^T Q (+ diag), * silu'(p_K); also stores P^T, dS^T
       Args a{};
       a.jag = io.jag; a.H = io.H; a.d = io.d;
       a.out = (bf*)io.dk; a.ld_out = io.ld_out; a.diag = io.diag_ds;

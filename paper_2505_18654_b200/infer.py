@@ -41,7 +41,8 @@ class InferenceSession:
         self.T, self.d = self.jb.total_tokens, cfg.d_model
         self.x = torch.zeros(max(self.T, 1), self.d, dtype=dtype, device=device)
         self.bufs = [torch.empty_like(self.x) for _ in range(2)]
-        self.ws = api._ws(api.layer_workspace_bytes(cfg, self.jb, dtype), device)
+        # forward-only scratch (no backward score scratch)
+        self.ws = api._ws(api.layer_fwd_workspace_bytes(cfg, self.jb, dtype, inference=True), device)
         self.graph = None
         self.out = None
         # candidate rows of each user (the scored outputs): [offsets[u] + n_s + n_r, offsets[u+1])

@@ -43,7 +43,7 @@ def test_full_training_step(dev, name, weighted):
     lc = m.layer_cfg(d, cfg["H"], cfg["groups"])
     lr = 0.05
     B_g = 3 * len(seg) if weighted else None
-    sc = 1.0 / B_g if weighted else 1.0
+    wsc = 1.0 / B_g if weighted else 1.0
     model = m.MTGRModel(cfg, lc, Ps, TP, HP, widths, e, dt, dev, cap_user=4096, cap_item=1 << 16,
                         lr_sparse=lr, seed=3, n_users_global=B_g)
     model.bind(jb, seg)
@@ -87,10 +87,10 @@ def test_full_training_step(dev, name, weighted):
         gtok = gtok + g_u["s"]["w1"]
         dfe.append(d_u)
     tol = TOL[dt]
-    errs = {"loss": rel_err(loss.cpu().numpy(), lo), "head.dw_a": rel_err(grads["head"]["w_a"].cpu().numpy(), sc * go["w_a"]),
-            "head.db_b": rel_err(grads["head"]["b_b"].cpu().numpy(), sc * go["b_b"]),
-            "L0.dW1": rel_err(grads["layers"][0]["W1"].cpu().numpy(), sc * gW1),
-            "tok.s.dw1": rel_err(grads["tokens"]["s"]["w1"].cpu().numpy(), sc * gtok)}
+    errs = {"loss": rel_err(loss.cpu().numpy(), lo), "head.dw_a": rel_err(grads["head"]["w_a"].cpu().numpy(), wsc * go["w_a"]),
+            "head.db_b": rel_err(grads["head"]["b_b"].cpu().numpy(), wsc * go["b_b"]),
+            "L0.dW1": rel_err(grads["layers"][0]["W1"].cpu().numpy(), wsc * gW1),
+            "tok.s.dw1": rel_err(grads["tokens"]["s"]["w1"].cpu().numpy(), wsc * gtok)}
     # sparse SGD: every item row moved by -lr * (sum of its occurrences' gradients)
     upd = {}
     for u in range(len(seg)):
@@ -101,7 +101,7 @@ def test_full_training_step(dev, name, weighted):
     keys = np.array(sorted(upd)[:200], dtype=np.int64)
     slots = model.item_table.shard.find_or_insert(torch.from_numpy(keys).to(dev), insert=False)
     got = model.item_table.shard.gather(slots).cpu().numpy()
-    ref = np.stack([oracle.init_row(4, int(k), e, 0.5) - lr * sc * upd[int(k)] for k in keys])
+    ref = np.stack([oracle.init_row(4, int(k), e, 0.5) - lr * wsc * upd[int(k)] for k in keys])
     errs["item_rows"] = rel_err(got - np.stack([oracle.init_row(4, int(k), e, 0.5) for k in keys]),
                                 ref - np.stack([oracle.init_row(4, int(k), e, 0.5) for k in keys]))
     bad = {k: v for k, v in errs.items() if not v <= tol}

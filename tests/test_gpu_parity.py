@@ -105,21 +105,22 @@ def _attn_case(name, seed=0):
     return cfg, seg, ts, qkvu, dO
 
 
-@pytest.fixture(params=["stored", "stored_fused_dk", "recompute"])
+@pytest.fixture(params=["kv", "stored", "stored_fused_dk", "recompute"])
 def bwd_path(request, monkeypatch):
-    """The tensor-core backward stores P^T / dS^T (score kernel + three GEMMs) by default;
-    MTGR_ATTN_FUSED_DK=1 makes the fused DK kernel write the scores instead; MTGR_ATTN_RECOMPUTE=1
-    selects the kernels that recompute the scores (the path used when the scratch would not fit)."""
+    """The tensor-core backward paths (MTGR_ATTN_BWD): kv (default) = the coupled dK/dV kernel
+    stores dS^T, then the dQ GEMM; stored = the score kernel stores P^T / dS^T, then three GEMMs;
+    fused_dk = the DK kernel writes the scores; MTGR_ATTN_RECOMPUTE=1 = the kernels that recompute
+    the scores (the path used when the score scratch would not fit)."""
     monkeypatch.delenv("MTGR_ATTN_RECOMPUTE", raising=False)
-    monkeypatch.setenv("MTGR_ATTN_FUSED_DK", "0")  # the score kernel, whatever the user lengths
+    monkeypatch.delenv("MTGR_ATTN_FUSED_DK", raising=False)
+    monkeypatch.setenv("MTGR_ATTN_BWD", {"kv": "kv", "stored": "stored", "stored_fused_dk": "fused_dk",
+                                         "recompute": "kv"}[request.param])
     if request.param == "recompute":
         monkeypatch.setenv("MTGR_ATTN_RECOMPUTE", "1")
-    elif request.param == "stored_fused_dk":
-        monkeypatch.setenv("MTGR_ATTN_FUSED_DK", "1")
     return request.param
 
 
-@pytest.mark.parametrize("mask", ["dynamic", "causal"])
+@pytest.mark.parametrize("mask", ["dynamic", "causal", "full"])
 @pytest.mark.parametrize("name", ["toy", "parity", "parity768"])
 def test_attention_fwd_bwd(dev, name, bwd_path, mask):
     cfg, seg, ts, qkvu, dO = _attn_case(name)
@@ -210,10 +211,12 @@ def test_layer_fwd_bwd(dev, name, bwd_path):
     print(_compare(z, dx, grads, Z, dX, G, TOL[_dt(cfg)]))
 
 
+@pytest.mark.parametrize("mask", ["causal", "full"])
 @pytest.mark.parametrize("name", ["toy", "parity", "parity768"])
-def test_layer_causal_mask(dev, name, bwd_path):
-    """Table 4's "w/o dynamic mask" ablation: the plain causal mask."""
-    cfg, seg, ts, X, dZ, P = make_batch(name, mask_mode="causal")
+def test_layer_ablation_masks(dev, name, bwd_path, mask):
+    """Table 4's "w/o dynamic mask" ablation under both readings: the plain causal mask
+     and full attention with candidates isolated."""
+    cfg, seg, ts, X, dZ, P = make_batch(name, mask_mode=mask)
     z, dx, grads = _run_layer(dev, cfg, seg, ts, X, dZ, P)
     Z, dX, G = _oracle_stack(cfg, seg, ts, X, dZ, [P])
     print(_compare(z, dx, grads, Z, dX, G, TOL[_dt(cfg)]))
@@ -350,7 +353,7 @@ def test_layer_register_row_copy(dev, name, monkeypatch):
     MTGR_SC_CP=0) instead of tcgen05.cp: same results."""
     monkeypatch.setenv("MTGR_ROW_CP", "0")
     monkeypatch.setenv("MTGR_SC_CP", "0")
-    monkeypatch.setenv("MTGR_ATTN_FUSED_DK", "0")
+    monkeypatch.setenv("MTGR_ATTN_BWD", "stored")
     cfg, seg, ts, X, dZ, P = make_batch(name)
     z, dx, grads = _run_layer(dev, cfg, seg, ts, X, dZ, P)
     Z, dX, G = _oracle_stack(cfg, seg, ts, X, dZ, [P])

@@ -90,14 +90,18 @@ def _probe_inputs(kind, seg, H):
 PROBED = {"o_dv": ("o", "dv"), "dk": ("dk",), "dq": ("dq",)}
 
 
-@pytest.fixture(params=["stored", "stored_fused_dk", "recompute"])
+@pytest.fixture(params=["kv", "stored", "stored_fused_dk", "recompute"])
 def bwd_path(request, monkeypatch):
+    """The tensor-core backward paths (MTGR_ATTN_BWD): kv (default) = the coupled dK/dV kernel
+    stores dS^T, then the dQ GEMM; stored = the score kernel stores P^T / dS^T, then three GEMMs;
+    fused_dk = the DK kernel writes the scores; MTGR_ATTN_RECOMPUTE=1 = the kernels that recompute
+    the scores (the path used when the score scratch would not fit)."""
     monkeypatch.delenv("MTGR_ATTN_RECOMPUTE", raising=False)
-    monkeypatch.setenv("MTGR_ATTN_FUSED_DK", "0")
+    monkeypatch.delenv("MTGR_ATTN_FUSED_DK", raising=False)
+    monkeypatch.setenv("MTGR_ATTN_BWD", {"kv": "kv", "stored": "stored", "stored_fused_dk": "fused_dk",
+                                         "recompute": "kv"}[request.param])
     if request.param == "recompute":
         monkeypatch.setenv("MTGR_ATTN_RECOMPUTE", "1")
-    elif request.param == "stored_fused_dk":
-        monkeypatch.setenv("MTGR_ATTN_FUSED_DK", "1")
     return request.param
 
 
