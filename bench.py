@@ -324,11 +324,12 @@ def run_mtgr(args, cfg, rank, world, local_rank):
         lab = np.concatenate([synth.gen_user_labels(cfg, int(u), int(l)) for u, l in zip(users, Ls)])
         hp = m.head_params_to_device(synth.gen_head_params(cfg), dt, dev)
         hshapes = {"w_a": tuple(hp["w_a"].shape), "b_a": (hp["w_a"].shape[0],), "w_b": tuple(hp["w_b"].shape), "b_b": (2,)}
-        hflat = torch.zeros(sum(int(np.prod(v)) for v in hshapes.values()), dtype=torch.float32, device=dev)
+        al = lambda n: (n + 63) // 64 * 64  # 256-byte aligned views (16-byte TMA pointers)
+        hflat = torch.zeros(sum(al(int(np.prod(v))) for v in hshapes.values()), dtype=torch.float32, device=dev)
         hviews, off = {}, 0
         for kk, shp in hshapes.items():  # the head's gradient bucket (all-reduced + scaled with the layers')
             hviews[kk] = hflat[off:off + int(np.prod(shp))].view(*shp)
-            off += hviews[kk].numel()
+            off += al(hviews[kk].numel())
         head_state = dict(params=hp, labels=torch.from_numpy(lab).to(dev), flat=hflat, views=hviews,
                           ws=None, K=int(jb.host["n_cand"].sum()))
 
@@ -341,13 +342,14 @@ def run_mtgr(args, cfg, rank, world, local_rank):
         emb = m.TokenEmbed(cfg["d"], k, m.TokenEmbed.params_to_device(synth.gen_token_params(cfg), dt, dev), dt, dev)
         emb.bind(jb, wl["seg"][users])
         tshapes = emb.grad_shapes()
-        tflat = torch.zeros(sum(int(np.prod(v)) for q in tshapes.values() for v in q.values()),
+        al = lambda n: (n + 63) // 64 * 64
+        tflat = torch.zeros(sum(al(int(np.prod(v))) for q in tshapes.values() for v in q.values()),
                             dtype=torch.float32, device=dev)
         tviews, off = {}, 0
         for t_, q in tshapes.items():  # the token MLPs' gradient bucket
             for kk, shp in q.items():
                 tviews.setdefault(t_, {})[kk] = tflat[off:off + int(np.prod(shp))].view(*shp)
-                off += int(np.prod(shp))
+                off += al(int(np.prod(shp)))
         tok = dict(emb=emb, feats=feats, flat=tflat, views=tviews)
 
     full = {}

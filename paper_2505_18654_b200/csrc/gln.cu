@@ -71,6 +71,11 @@ __device__ __forceinline__ float warp_sum(float v) {
   return v;
 }
 
+// One warp per token over a CONTIGUOUS token range per warp (tokens of a group are contiguous
+// within a user, so gamma / beta of the current group stay in registers and are reloaded only on
+// a group change: the per-token traffic is the token's own rows, not 2d fp32 parameters through
+// L1).  Software pipelined: the next token's rows (and group id) are in flight while this one is
+// reduced, normalised and stored.
 template <class T, int NC>
 __global__ void __launch_bounds__(256) gln_fwd_kernel(const T* __restrict__ x,
                                                       const uint8_t* __restrict__ gid,
@@ -79,13 +84,13 @@ __global__ void __launch_bounds__(256) gln_fwd_kernel(const T* __restrict__ x,
                                                       T* __restrict__ y, float* __restrict__ mean,
                                                       float* __restrict__ rstd, int ntok, int d,
                                                       float eps, const T* __restrict__ gate,
-                                                      int64_t ld_gate) {
+                                                      int64_t ld_gate, int tok_per_warp) {
   const int lane = threadIdx.x & 31;
-  const int nwarps = gridDim.x * (blockDim.x >> 5);
   const int nch = d >> 3;
   const float inv_d = 1.0f / (float)d;
-  // software pipelined: the next token's rows (and group id) are in flight while this one is
-  // reduced, normalised and stored (two tokens' bytes in flight per warp)
+  const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int t_begin = w * tok_per_warp;
+  const int t_end = min(ntok, t_begin + tok_per_warp);
   Raw8<T> cx[NC], cg[NC], nx[NC], ng[NC];
   auto issue = [&](int tt, Raw8<T>* xa, Raw8<T>* ga) {
 #pragma unroll
@@ -97,13 +102,26 @@ __global__ void __launch_bounds__(256) gln_fwd_kernel(const T* __restrict__ x,
       }
     }
   };
-  int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  float gg[NC][8], bb[NC][8];
+  int g_loaded = -1;
+  int t = t_begin;
   int g_cur = 0;
-  if (t < ntok) { issue(t, cx, cg); g_cur = gid[t]; }
-  for (; t < ntok; t += nwarps) {
-    const int tn = t + nwarps;
+  if (t < t_end) { issue(t, cx, cg); g_cur = gid[t]; }
+  for (; t < t_end; ++t) {
+    const int tn = t + 1;
     int g_next = 0;
-    if (tn < ntok) { issue(tn, nx, ng); g_next = gid[tn]; }
+    if (tn < t_end) { issue(tn, nx, ng); g_next = gid[tn]; }
+    if (g_cur != g_loaded) {  // group change: this group's affine parameters into registers
+#pragma unroll
+      for (int k = 0; k < NC; ++k) {
+        const int c = lane + 32 * k;
+        if (c < nch) {
+          load8(gamma + (int64_t)g_cur * d + c * 8, gg[k]);
+          load8(beta + (int64_t)g_cur * d + c * 8, bb[k]);
+        }
+      }
+      g_loaded = g_cur;
+    }
     float v[NC][8];
     float s = 0.f;
 #pragma unroll
@@ -134,19 +152,14 @@ __global__ void __launch_bounds__(256) gln_fwd_kernel(const T* __restrict__ x,
       }
     const float var = warp_sum(q) * inv_d;
     const float r = 1.0f / sqrtf(var + eps);
-    const int g = g_cur;
-    const float* gr = gamma + (int64_t)g * d;
-    const float* br = beta + (int64_t)g * d;
     T* yr = y + (int64_t)t * d;
 #pragma unroll
     for (int k = 0; k < NC; ++k) {
       int c = lane + 32 * k;
       if (c < nch) {
-        float gg[8], bb[8], o[8];
-        load8(gr + c * 8, gg);
-        load8(br + c * 8, bb);
+        float o[8];
 #pragma unroll
-        for (int e = 0; e < 8; ++e) o[e] = gg[e] * ((v[k][e] - mu) * r) + bb[e];
+        for (int e = 0; e < 8; ++e) o[e] = gg[k][e] * ((v[k][e] - mu) * r) + bb[k][e];
         store8(yr + c * 8, o);
       }
     }
@@ -583,9 +596,12 @@ template <class T, int NC>
 static void gln_fwd_go(const T* x, const uint8_t* gid, const float* gamma, const float* beta, T* y,
                        float* mean, float* rstd, int ntok, int d, float eps, const T* gate,
                        int64_t ld_gate, cudaStream_t st) {
-  int blocks = min(ceil_div(ntok, 8), 16 * num_sms());
+  // ~8 resident 256-thread blocks per SM (64 warps), each warp a contiguous run of tokens
+  const int warps = 8 * 8 * num_sms();
+  const int tpw = std::max(1, ceil_div(ntok, warps));
+  const int blocks = ceil_div(ceil_div(ntok, tpw), 8);
   gln_fwd_kernel<T, NC><<<blocks, 256, 0, st>>>(x, gid, gamma, beta, y, mean, rstd, ntok, d, eps,
-                                                gate, ld_gate);
+                                                gate, ld_gate, tpw);
 }
 
 template <class T>

@@ -6,6 +6,7 @@
 #include "common.cuh"
 #include "kernels.h"
 #include "sm100.cuh"
+#include <cuda_fp16.h>
 
 namespace mtgr {
 namespace tca {
@@ -65,6 +66,34 @@ __device__ __forceinline__ float silu_fast(float s) {
 __device__ __forceinline__ float dsilu_fast(float s) {
   const float sg = fmaf(0.5f, sm100::tanh_approx(0.5f * s), 0.5f);
   return fmaf(s * sg, 1.0f - sg, sg);
+}
+// packed fp32 pairs (FFMA2 / FMUL2 / FADD2 on sm_100): half the issue slots of scalar math
+__device__ __forceinline__ unsigned long long f2u(float2 v) { return *reinterpret_cast<unsigned long long*>(&v); }
+__device__ __forceinline__ float2 u2f(unsigned long long v) { return *reinterpret_cast<float2*>(&v); }
+__device__ __forceinline__ float2 f2fma(float2 a, float2 b, float2 c) {
+  unsigned long long d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(f2u(a)), "l"(f2u(b)), "l"(f2u(c)));
+  return u2f(d);
+}
+__device__ __forceinline__ float2 f2mul(float2 a, float2 b) {
+  unsigned long long d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2u(a)), "l"(f2u(b)));
+  return u2f(d);
+}
+__device__ __forceinline__ float2 f2add(float2 a, float2 b) {
+  unsigned long long d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2u(a)), "l"(f2u(b)));
+  return u2f(d);
+}
+// sigma(s) = 0.5 + 0.5 tanh(s/2) for a pair, the tanh in f16x2 (one MUFU op for two values;
+// its 2^-11 relative error is below the bf16 rounding of the P / dS tiles it feeds)
+__device__ __forceinline__ float2 sigmoid2_fast(float2 s) {
+  const float2 h = f2mul(s, make_float2(0.5f, 0.5f));
+  __half2 hh = __float22half2_rn(h);
+  uint32_t t;
+  asm("tanh.approx.f16x2 %0, %1;" : "=r"(t) : "r"(*reinterpret_cast<uint32_t*>(&hh)));
+  const float2 tf = __half22float2(*reinterpret_cast<__half2*>(&t));
+  return f2fma(tf, make_float2(0.5f, 0.5f), make_float2(0.5f, 0.5f));
 }
 __device__ __forceinline__ uint32_t pack2(float a, float b) {
   __nv_bfloat162 h = __floats2bfloat162_rn(a, b);

@@ -36,9 +36,11 @@
 // smem and TMEM layouts are those of the FWD/DV modes of attn_tc_kernel (tc_attn.cu).
 #include <algorithm>
 #include <climits>
+#include <type_traits>
 #include <cstdio>
 #include <cstdlib>
 #include <cuda_fp16.h>
+#include <vector>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -49,7 +51,7 @@
 namespace mtgr {
 namespace tca {
 
-constexpr int KV_NG = 8;            // G ring depth (tiles) per CTA
+constexpr int KV_NG_MAX = 32;       // G ring depth (tiles) per CTA: ks.ng <= this (MTGR_KV_NG)
 constexpr int KV_THREADS = 384;     // 12 warps (13 would round the register budget to 16 warps')
 constexpr int KV_EXIT = 1 << 30;    // per-warp counter flag: the warp has left its item loop
 constexpr int KV_FLAG_STRIDE = 32;  // ints per couple in the flag block (own 128-byte line)
@@ -62,6 +64,8 @@ struct KvSync {
   int* items;      // [ncouples][item_cap] work items in X's claim order, -1 = end
   uint4* gbuf;     // [ncouples][2][KV_NG][8 warps][4 chunks][32 lanes] fp16 G pieces
   int ncouples, item_cap;
+  long long* trace;  // MTGR_KV_TRACE: [role][10 events][1024] globaltimer stamps of couple 0, rank 0
+  int ng;          // G ring depth in tiles
   int dbg;         // MTGR_KV_DEBUG (timing experiments only; results are wrong when set): 1 Y does
                    // not wait for G, 2 X writes no G, 4 Y stores no dS^T, 8 X ignores ring reuse
 };
@@ -91,6 +95,16 @@ __device__ __forceinline__ int ld_acquire_cta_smem(const int* p) {
   asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(sm100::smem_u32(p)) : "memory");
   return v;
 }
+__device__ __forceinline__ long long gtimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// trace events (MTGR_KV_TRACE): per item 0 start, 1 tiles done, 2 o_full, 3 epilogue done,
+// 4 ntiles, 5 first S issued, 6 last acc issued; per tile 7 s_full passed, 8 t_full arrived,
+// 9 S issued, 10 C1 load issued, 11 X load issued, 12 MMA saw c1_full, 13 MMA saw x_full
+#define KV_TR(ev, i, v) do { if (tr != nullptr && (i) < 1024) tr[(ev) * 1024 + (i)] = (v); } while (0)
+
 __device__ __forceinline__ uint32_t pack_h2(float a, float b) {
   __half2 h = __floats2half2_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&h);
@@ -110,7 +124,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KV_THREADS, 1)
   constexpr int X_BYTES = BC * (DH / 2) * 2;   // 16 KB: 2 boxes {64 dh, 64 cols}
   constexpr int NC1 = 3, NX = 3;
   constexpr int OFF_C1 = 0, OFF_X = 48 * KB, OFF_R1STAGE = 96 * KB, OFF_EPI = 160 * KB;
-  constexpr uint32_t T_R1 = 0, T_ACC = 128, T_S = 384, T_P = 448;
+  // TMEM: row operand [0,128), accumulator [128,384), score tiles S[b] = [384 + 64b, +64), b = tile & 1;
+  // the bf16 T tile is written in place: warp half h's 32 values into columns [32h, 32h + 16) of
+  // its own S[b] half, so the next tile's score MMA never waits for the softmax
+  constexpr uint32_t T_R1 = 0, T_ACC = 128, T_S = 384;
 
   const uint32_t crank = cluster_ctarank();
   const bool leader = crank == 0;
@@ -122,10 +139,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KV_THREADS, 1)
   uint64_t* c1_empty = bars + 3;      // [3]
   uint64_t* x_full = bars + 6;        // [3] leader
   uint64_t* x_empty = bars + 9;       // [3]
-  uint64_t* s_full = bars + 16;
-  uint64_t* s_free = bars + 17;       // leader, both CTAs' softmax warps
-  uint64_t* t_full = bars + 18;       // [2] leader, both CTAs
-  uint64_t* t_free = bars + 20;       // [2]
+  uint64_t* s_full = bars + 16;       // [2] score tile b complete (multicast commit)
+  uint64_t* t_full = bars + 18;       // [2] leader, both CTAs: T tile b written
   uint64_t* r1_full = bars + 22;      // leader: both CTAs' row operand staged
   uint64_t* r1_copied = bars + 24;    // own (tcgen05.cp done: staging reusable)
   uint64_t* o_full = bars + 30;
@@ -138,6 +153,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KV_THREADS, 1)
   int* ticket = reinterpret_cast<int*>(bars + 46);       // this cluster's ticket
   int* cons_ok = ticket + 1;                             // X: Y's consumed count (mirror)
   int* wcnt = ticket + 2;                                // [8] X: tiles written / Y: consumed
+  int* gready = ticket + 10;                             // Y: G tiles published by X (mirror)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   auto arrive_leader = [&](uint64_t* bar) {  // one arrival per warp (whole warp calls)
     __syncwarp();
@@ -152,9 +168,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KV_THREADS, 1)
       mbar_init(&c1_full[s], 1); mbar_init(&c1_empty[s], 1);
       mbar_init(&x_full[s], 1); mbar_init(&x_empty[s], 1);
     }
-    for (int s = 0; s < 2; ++s) { mbar_init(&t_full[s], 2 * NSM); mbar_init(&t_free[s], 1); }
-    mbar_init(s_full, 1);
-    mbar_init(s_free, 2 * NSM);
+    for (int s = 0; s < 2; ++s) { mbar_init(&t_full[s], 2 * NSM); mbar_init(&s_full[s], 1); }
     mbar_init(r1_full, 1);
     mbar_init(r1_copied, 1);
     mbar_init(o_full, 1);
@@ -165,6 +179,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KV_THREADS, 1)
       mbar_init(&q_empty[s], 2 * (NSM + 3));  // per CTA: X producer, row loader, 8 softmax, MMA | C1 producer
     }
     *cons_ok = 0;
+    *gready = 0;
     for (int w = 0; w < NSM; ++w) wcnt[w] = 0;
     if (leader) {  // role ticket, shared with the peer before the cluster barrier
       const int t = atomicAdd(ks.role_ctr, 1);
@@ -190,7 +205,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KV_THREADS, 1)
   int* cflags = ks.flags + (size_t)couple * KV_FLAG_STRIDE;
   int* items = ks.items + (size_t)couple * ks.item_cap;
   // this CTA's G ring: [KV_NG slots][8 warps][4 chunks][32 lanes] x 16 B
-  uint4* gring = ks.gbuf + (size_t)(couple * 2 + (int)crank) * KV_NG * NSM * 128;
+  uint4* gring = ks.gbuf + (size_t)(couple * 2 + (int)crank) * KV_NG_MAX * NSM * 128;
+  long long* tr = (ks.trace != nullptr && couple == 0 && crank == 0) ? ks.trace + (size_t)role * 18 * 1024 : nullptr;
 
   auto q_read = [&](int n) -> int {
     mbar_wait_cluster(&q_full[n & 3], (n >> 2) & 1);
@@ -245,6 +261,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KV_THREADS, 1)
           const int slot = gt % NC1;
           mbar_wait(&c1_empty[slot], ((gt / NC1) & 1) ^ 1);
           if (leader) mbar_expect_tx(&c1_full[slot], 2 * C1_BYTES);
+          KV_TR(10, gt, gtimer());
           const int row = it.us.off + it.c_begin + t * BC + 32 * crank;  // this CTA's 32 columns
           uint8_t* dst = smem + OFF_C1 + slot * C1_BYTES;
 #pragma unroll
@@ -254,7 +271,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KV_THREADS, 1)
     }
   } else if (warp == 2 && lane == 1) {
     // ---------------------------------------------------------------- sync thread
-    int done = 0;  // X: tiles published / Y: tiles reported consumed
+    int done = 0;   // X: tiles published / Y: tiles reported consumed
+    int seen = 0;   // Y: X's published count mirrored into shared memory
     for (;;) {
       int mn = INT_MAX;
       bool all_exit = true;
@@ -276,9 +294,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KV_THREADS, 1)
         }
         done = mn;
       }
-      if (role == 0) *reinterpret_cast<volatile int*>(cons_ok) = ld_relaxed_gpu(&cflags[3 + crank]);
+      if (role == 0) {
+        *reinterpret_cast<volatile int*>(cons_ok) = ld_relaxed_gpu(&cflags[3 + crank]);
+      } else {
+        // X's release -> this acquire -> the release below -> the softmax warps' acquire (smem)
+        const int p = ld_acquire_gpu(&cflags[1 + crank]);
+        if (p > seen) { st_release_cta_smem(gready, p); seen = p; }
+      }
       if (all_exit) break;
-      __nanosleep(64);
+      __nanosleep(32);
     }
   } else if (warp == 2) {
     // ---------------------------------------------------------------- row operand + epilogue tile
@@ -321,6 +345,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KV_THREADS, 1)
           const int slot = gt % NX;
           mbar_wait(&x_empty[slot], ((gt / NX) & 1) ^ 1);
           if (leader) mbar_expect_tx(&x_full[slot], 2 * X_BYTES);
+          KV_TR(11, gt, gtimer());
           const int row = it.us.off + it.c_begin + t * BC;
           uint8_t* dst = smem + OFF_X + slot * X_BYTES;
 #pragma unroll
@@ -363,19 +388,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KV_THREADS, 1)
         const int nt = it.ntiles;
         if (nt == 0) continue;
         if (cp_done == mi) copy_r1();  // not prefetched at the end of the previous item
+        const int item_n = n;
         // acc += T_j X_j  (A = T from each CTA's TMEM, B = X: each CTA's half of the head dim)
         auto acc = [&](int j, int g) {
           const int tb = g & 1;
           mbar_wait(&t_full[tb], (g >> 1) & 1);
           mbar_wait(&x_full[g % NX], (g / NX) & 1);
+          if (lane == 0) KV_TR(13, g, gtimer());
           const uint32_t x = x_base + (g % NX) * X_BYTES;
           tc_fence_after();
           if (elect_one()) {
 #pragma unroll
             for (int kk = 0; kk < BC / 16; ++kk)
-              mma_bf16_ts_2sm(tm + T_ACC, tm + T_P + tb * 32 + kk * 8,
+              mma_bf16_ts_2sm(tm + T_ACC, tm + T_S + 64 * tb + (kk >> 1) * 32 + (kk & 1) * 8,
                               desc_sw128(x + kk * 2048, X_BYTES / 2, 1024), idesc_acc, (j > 0 || kk > 0));
-            mma_commit_2sm_mc(&t_free[tb], 0x3);
             mma_commit_2sm_mc(&x_empty[g % NX], 0x3);
           }
           __syncwarp();
@@ -383,23 +409,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KV_THREADS, 1)
         for (int t = 0; t < nt; ++t) {
           const int g = gt + t;
           mbar_wait(&c1_full[g % NC1], (g / NC1) & 1);
-          mbar_wait(s_free, (g & 1) ^ 1);  // single score buffer, released on tcgen05.ld
+          if (lane == 0) KV_TR(12, g, gtimer());
+          // score tile (g & 1) was last read by the T MMA of tile g - 2, issued (in order) in
+          // the previous iteration after its softmax finished
           tc_fence_after();
           const uint32_t c1 = c1_base + (g % NC1) * C1_BYTES;
           if (elect_one()) {
 #pragma unroll
             for (int kk = 0; kk < DH / 16; ++kk)
-              mma_bf16_ts_2sm(tm + T_S, tm + T_R1 + kk * 8,
+              mma_bf16_ts_2sm(tm + T_S + 64 * (g & 1), tm + T_R1 + kk * 8,
                               desc_sw128(c1 + (kk >> 2) * (C1_BYTES / 4) + (kk & 3) * 32, 16, 1024), idesc_s, kk > 0);
-            mma_commit_2sm_mc(s_full, 0x3);
+            mma_commit_2sm_mc(&s_full[g & 1], 0x3);
             mma_commit_2sm_mc(&c1_empty[g % NC1], 0x3);
           }
           __syncwarp();
+          if (lane == 0) { const long long tt = gtimer(); KV_TR(9, g, tt); if (t == 0) KV_TR(5, item_n, tt); }
           if (t >= 1) acc(t - 1, g - 1);
         }
         acc(nt - 1, gt + nt - 1);
         if (elect_one()) mma_commit_2sm_mc(o_full, 0x3);
         __syncwarp();
+        if (lane == 0) KV_TR(6, item_n, gtimer());
         {  // the next item's row operand, right behind this item's MMAs
           const int k2 = q_read(n + 1);  // peek (released when it is processed)
           Item nx;
@@ -429,6 +459,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KV_THREADS, 1)
       const UserSpan& us = it.us;
       const int my = it.r0 + row;                    // this thread's key (user-local)
       const int64_t g = (int64_t)us.off + my;        // global token index
+      const bool trw = warp == 4 && lane == 0;
+      if (trw) { KV_TR(0, n, gtimer()); KV_TR(4, n, it.ntiles); }
       if (it.ntiles > 0) {
         const long long my_ts = (role == 0 && my < us.L && a.jag.ts) ? a.jag.ts[g] : 0;
         // stored dS^T row of this key (Y): [h][koff[u] + my][query]
@@ -438,7 +470,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KV_THREADS, 1)
         for (int t = 0; t < it.ntiles; ++t, ++gt) {
           const int c0 = it.c_begin + t * BC;
           const int cb = c0 + j_half;  // this warp's 32 query columns
-          uint4* gp = gring + ((size_t)(gt % KV_NG) * NSM + sw) * 128;  // this warp's G piece
+          uint4* gp = gring + ((size_t)(gt % ks.ng) * NSM + sw) * 128;  // this warp's G piece
           uint32_t pk[16];
           if (role == 0) {
             // ---------------- X: P^T = silu(S^T) m for the dV MMA, G = silu'(S^T) m for Y
@@ -448,13 +480,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KV_THREADS, 1)
               if (i < BC) sTs[i] = (c0 + i < us.L && a.jag.ts) ? a.jag.ts[us.off + c0 + i] : 0;
               named_bar_sync(1, 32 * NSM);
             }
-            mbar_wait(s_full, gt & 1);
+            const int tb = gt & 1;
+            mbar_wait(&s_full[tb], (gt >> 1) & 1);
+            if (trw) KV_TR(7, gt, gtimer());
             tc_fence_after();
             uint32_t s[32];
-            tmem_ld32(tmem + T_S + j_half + lane_off, s);
+            tmem_ld32(tmem + T_S + 64 * tb + j_half + lane_off, s);
             tmem_ld_wait();
-            tc_fence_before();
-            arrive_leader(s_free);
             uint32_t vis;
             if (a.causal) {  // queries i >= key j, i < L
               const int lo = min(max(my - cb, 0), 32), hi = min(max(us.L - cb, 0), 32);
@@ -474,71 +506,76 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KV_THREADS, 1)
               vis = 0;
             }
             uint32_t gw[16];
+            const bool all_vis = vis == 0xffffffffu;
+            if (ks.dbg & 16) {  // timing experiment: no softmax math
+#pragma unroll
+              for (int e = 0; e < 16; ++e) { pk[e] = s[2 * e]; gw[e] = s[2 * e + 1]; }
+            } else
 #pragma unroll
             for (int e = 0; e < 32; e += 2) {
-              const float s0 = __uint_as_float(s[e]), s1 = __uint_as_float(s[e + 1]);
-              // silu and silu' share sigma(s) = 0.5 + 0.5 tanh(s/2)
-              const float g0 = fmaf(0.5f, sm100::tanh_approx(0.5f * s0), 0.5f);
-              const float g1 = fmaf(0.5f, sm100::tanh_approx(0.5f * s1), 0.5f);
-              float p0 = s0 * g0, p1 = s1 * g1;
-              float d0 = fmaf(p0, 1.0f - g0, g0), d1 = fmaf(p1, 1.0f - g1, g1);
-              const bool m0 = (vis >> e) & 1u, m1 = (vis >> (e + 1)) & 1u;  // selects (R#2)
-              p0 = m0 ? p0 : 0.f; d0 = m0 ? d0 : 0.f;
-              p1 = m1 ? p1 : 0.f; d1 = m1 ? d1 : 0.f;
-              pk[e >> 1] = pack2(p0, p1);
-              gw[e >> 1] = pack_h2(d0, d1);
+              const float2 sv = make_float2(__uint_as_float(s[e]), __uint_as_float(s[e + 1]));
+              // silu and silu' share sigma(s): p = s sigma, g = sigma + p (1 - sigma)
+              const float2 sg = sigmoid2_fast(sv);
+              float2 p2 = f2mul(sv, sg);
+              float2 d2 = f2fma(p2, f2add(make_float2(1.f, 1.f), make_float2(-sg.x, -sg.y)), sg);
+              if (!all_vis) {  // selects, no branch per element (masked entries exact zeros, R#2)
+                const bool m0 = (vis >> e) & 1u, m1 = (vis >> (e + 1)) & 1u;
+                p2.x = m0 ? p2.x : 0.f; d2.x = m0 ? d2.x : 0.f;
+                p2.y = m1 ? p2.y : 0.f; d2.y = m1 ? d2.y : 0.f;
+              }
+              pk[e >> 1] = pack2(p2.x, p2.y);
+              gw[e >> 1] = pack_h2(d2.x, d2.y);
             }
-            const int tb = gt & 1;
-            mbar_wait(&t_free[tb], ((gt >> 1) & 1) ^ 1);
-            tc_fence_after();
-            tmem_st16(tmem + T_P + tb * 32 + half * 16 + lane_off, pk);
+            tmem_st16(tmem + T_S + 64 * tb + j_half + lane_off, pk);  // in place (this warp's S)
             tmem_st_wait();
             tc_fence_before();
             arrive_leader(&t_full[tb]);
+            if (trw) KV_TR(8, gt, gtimer());
+            // publish the PREVIOUS tile's G piece: its stores were issued a tile ago, so this
+            // release (which waits for them) does not stall; this tile's follow below
+            __syncwarp();
+            if (lane == 0 && t > 0) st_release_cta_smem(&wcnt[sw], gt);
             // G piece -> ring slot gt % NG (free once Y consumed tile gt - NG)
-            if (gt >= KV_NG && !(ks.dbg & 8))
-              while (*reinterpret_cast<volatile int*>(cons_ok) < gt - KV_NG + 1) __nanosleep(32);
+            if (gt >= ks.ng && !(ks.dbg & 8))
+              while (*reinterpret_cast<volatile int*>(cons_ok) < gt - ks.ng + 1) __nanosleep(32);
             if (!(ks.dbg & 2)) {
 #pragma unroll
               for (int c = 0; c < 4; ++c)
                 gp[c * 32 + lane] = make_uint4(gw[4 * c], gw[4 * c + 1], gw[4 * c + 2], gw[4 * c + 3]);
             }
-            __syncwarp();
-            if (lane == 0) st_release_cta_smem(&wcnt[sw], gt + 1);
+            if (t + 1 == it.ntiles) {  // the item's last tile: publish now (before the epilogue)
+              __syncwarp();
+              if (lane == 0) st_release_cta_smem(&wcnt[sw], gt + 1);
+            }
           } else {
             // ---------------- Y: dS^T = dP^T (.) G for the dK MMA and the dQ GEMM
-            if (ready < gt + 1 && !(ks.dbg & 1)) {
-              int v = 0;
-              if (lane == 0) {
-                while ((v = ld_acquire_gpu(&cflags[1 + crank])) < gt + 1) __nanosleep(64);
-              }
-              __syncwarp();
-              ready = __shfl_sync(0xffffffffu, v, 0);
+            if (ready < gt + 1 && !(ks.dbg & 1)) {  // X's count, mirrored by the sync thread
+              int v;
+              while ((v = ld_acquire_cta_smem(gready)) < gt + 1) __nanosleep(32);
+              ready = v;
             }
             uint4 gv[4];
 #pragma unroll
             for (int c = 0; c < 4; ++c) gv[c] = __ldcg(&gp[c * 32 + lane]);  // L2 (never a stale L1 line)
-            mbar_wait(s_full, gt & 1);
+            const int tb = gt & 1;
+            mbar_wait(&s_full[tb], (gt >> 1) & 1);
+            if (trw) KV_TR(7, gt, gtimer());
             tc_fence_after();
             uint32_t dp[32];
-            tmem_ld32(tmem + T_S + j_half + lane_off, dp);
+            tmem_ld32(tmem + T_S + 64 * tb + j_half + lane_off, dp);
             tmem_ld_wait();
-            tc_fence_before();
-            arrive_leader(s_free);
             const uint32_t* gw = reinterpret_cast<const uint32_t*>(gv);
 #pragma unroll
             for (int e = 0; e < 32; e += 2) {
               __half2 h = *reinterpret_cast<const __half2*>(&gw[e >> 1]);
-              const float2 gf = __half22float2(h);
-              pk[e >> 1] = pack2(__uint_as_float(dp[e]) * gf.x, __uint_as_float(dp[e + 1]) * gf.y);
+              const float2 ds = f2mul(make_float2(__uint_as_float(dp[e]), __uint_as_float(dp[e + 1])), __half22float2(h));
+              pk[e >> 1] = pack2(ds.x, ds.y);
             }
-            const int tb = gt & 1;
-            mbar_wait(&t_free[tb], ((gt >> 1) & 1) ^ 1);
-            tc_fence_after();
-            tmem_st16(tmem + T_P + tb * 32 + half * 16 + lane_off, pk);
+            tmem_st16(tmem + T_S + 64 * tb + j_half + lane_off, pk);  // in place (this warp's S)
             tmem_st_wait();
             tc_fence_before();
             arrive_leader(&t_full[tb]);
+            if (trw) KV_TR(8, gt, gtimer());
             // this tile's G is consumed
             __syncwarp();
             if (lane == 0) *reinterpret_cast<volatile int*>(&wcnt[sw]) = gt + 1;
@@ -558,7 +595,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KV_THREADS, 1)
             }
           }
         }
+        if (trw) KV_TR(1, n, gtimer());
         mbar_wait(o_full, mi & 1);
+        if (trw) KV_TR(2, n, gtimer());
         tc_fence_after();
         ++mi;
       }
@@ -579,6 +618,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KV_THREADS, 1)
       const bool pre_ds = a.pre_dsilu != 0;
       const bool any_e = __any_sync(0xffffffffu, has_e);
       if (use_u) mbar_wait(eu_full, idx & 1);
+      if (trw) KV_TR(14, n, gtimer());
       uint32_t r[2][32];
       if (it.ntiles > 0) tmem_ld32(tmem + T_ACC + half * 128 + lane_off, r[0]);
 #pragma unroll
@@ -595,32 +635,59 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KV_THREADS, 1)
         const int bx = acol >> 6, j0 = (acol & 63) >> 3;
         uint8_t* box = epi + bx * (RT_BYTES / 4);
         float v[32];
+        // one copy of the element loop per epilogue form (uniform branch outside the loop):
+        // 0 no SiLU' source, 1 the saved silu'(p), 2 pre-activations (silu' formed here)
+        auto elems = [&](auto form) {
+          constexpr int F = decltype(form)::value;
+          const float2 nu2 = make_float2(us.nu, us.nu), dg2 = make_float2(dg, dg);
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const uint32_t off = sw128(row, j0 + i);
-          uint4 ew = make_uint4(0u, 0u, 0u, 0u);
-          if (any_e && has_e) ew = __ldg(reinterpret_cast<const uint4*>(erow + cc * 32 + 8 * i));
-          uint4 uw = make_uint4(0u, 0u, 0u, 0u);
-          if (use_u) uw = *reinterpret_cast<const uint4*>(box + off);
-          const __nv_bfloat162* eh = reinterpret_cast<const __nv_bfloat162*>(&ew);
-          const __nv_bfloat162* uh = reinterpret_cast<const __nv_bfloat162*>(&uw);
+          for (int i = 0; i < 4; ++i) {
+            const uint32_t off = sw128(row, j0 + i);
+            uint4 ew = make_uint4(0u, 0u, 0u, 0u);
+            if (any_e && has_e) ew = __ldg(reinterpret_cast<const uint4*>(erow + cc * 32 + 8 * i));
+            uint4 uw = make_uint4(0u, 0u, 0u, 0u);
+            if (F != 0) uw = *reinterpret_cast<const uint4*>(box + off);
+            const __nv_bfloat162* eh = reinterpret_cast<const __nv_bfloat162*>(&ew);
+            const __nv_bfloat162* uh = reinterpret_cast<const __nv_bfloat162*>(&uw);
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk) {
-            const float2 fe = __bfloat1622float2(eh[kk]);
-            float x0 = fmaf(us.nu, __uint_as_float(rc[8 * i + 2 * kk]), dg * fe.x);
-            float x1 = fmaf(us.nu, __uint_as_float(rc[8 * i + 2 * kk + 1]), dg * fe.y);
-            if (use_u) {
-              const float2 fu = __bfloat1622float2(uh[kk]);
-              x0 *= pre_ds ? fu.x : dsilu_fast(fu.x);
-              x1 *= pre_ds ? fu.y : dsilu_fast(fu.y);
+            for (int kk = 0; kk < 4; ++kk) {
+              float2 x = f2mul(nu2, make_float2(__uint_as_float(rc[8 * i + 2 * kk]), __uint_as_float(rc[8 * i + 2 * kk + 1])));
+              if (any_e) x = f2fma(dg2, __bfloat1622float2(eh[kk]), x);
+              if constexpr (F == 1) x = f2mul(x, __bfloat1622float2(uh[kk]));
+              if constexpr (F == 2) {
+                const float2 fu = __bfloat1622float2(uh[kk]);
+                x = f2mul(x, make_float2(dsilu_fast(fu.x), dsilu_fast(fu.y)));
+              }
+              v[8 * i + 2 * kk] = x.x;
+              v[8 * i + 2 * kk + 1] = x.y;
             }
-            v[8 * i + 2 * kk] = x0;
-            v[8 * i + 2 * kk + 1] = x1;
+            *reinterpret_cast<uint4*>(box + off) =
+                make_uint4(pack2(v[8 * i], v[8 * i + 1]), pack2(v[8 * i + 2], v[8 * i + 3]),
+                           pack2(v[8 * i + 4], v[8 * i + 5]), pack2(v[8 * i + 6], v[8 * i + 7]));
           }
-          *reinterpret_cast<uint4*>(box + off) =
-              make_uint4(pack2(v[8 * i], v[8 * i + 1]), pack2(v[8 * i + 2], v[8 * i + 3]),
-                         pack2(v[8 * i + 4], v[8 * i + 5]), pack2(v[8 * i + 6], v[8 * i + 7]));
+        };
+        if (!use_u) elems(std::integral_constant<int, 0>{});
+        else if (pre_ds) elems(std::integral_constant<int, 1>{});
+        else elems(std::integral_constant<int, 2>{});
+        if (a.dbias != nullptr) {
+          // bias gradient of this projection block: column sums over the item's rows.  The 32
+          // columns of the chunk are summed over the warp's 32 rows by a butterfly
+          // reduce-scatter (lane l ends with column l), then one red.add per lane
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = row_ok ? v[i] : 0.f;
+#pragma unroll
+          for (int o = 16; o >= 1; o >>= 1) {
+            const bool up = (lane & o) != 0;
+#pragma unroll
+            for (int i = 0; i < o; ++i) {
+              const float send = up ? v[i] : v[i + o];
+              const float keep = up ? v[i + o] : v[i];
+              v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+            }
+          }
+          if (v[0] != 0.f) atomicAdd(a.dbias + it.hcol + acol + lane, v[0]);
         }
+        if (trw && cc == 1) KV_TR(15, n, gtimer());
         if (cc & 1) {  // box bx of this warp's 32 rows is complete: store it
           if (full_chunk) {
             fence_proxy_async_smem();
@@ -638,28 +705,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KV_THREADS, 1)
           }
         }
       }
-      if (a.dbias != nullptr) {
-        // bias gradient of this projection block: column sums of the stored outputs, read back
-        // from the epilogue tile; warp sw owns columns sw*32.., lane = one column
-        named_bar_sync(1, 32 * NSM);
-        const int col = sw * 32 + lane;
-        const uint8_t* cbox = epi + (col >> 6) * (RT_BYTES / 4);
-        const int cj = (col & 63) >> 3, ce = (col & 7) * 2;
-        float ps[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-        int rr = 0;
-        for (; rr + 8 <= nrows; rr += 8) {
-#pragma unroll
-          for (int k2 = 0; k2 < 8; ++k2)
-            ps[k2] += __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(cbox + sw128(rr + k2, cj) + ce));
-        }
-        for (; rr < nrows; ++rr)
-          ps[0] += __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(cbox + sw128(rr, cj) + ce));
-        const float sum = ((ps[0] + ps[1]) + (ps[2] + ps[3])) + ((ps[4] + ps[5]) + (ps[6] + ps[7]));
-        if (sum != 0.f) atomicAdd(a.dbias + it.hcol + col, sum);
-      }
+      if (trw) KV_TR(16, n, gtimer());
       if (lane == 0) tma_store_wait_read<0>();
       __syncwarp();
       if (lane == 0) mbar_arrive(epi_free);
+      if (trw) KV_TR(3, n, gtimer());
       ++idx;
     }
     // leave the item loop: the sync thread stops once every warp has (X: after publishing the
@@ -682,7 +732,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KV_THREADS, 1)
 size_t kv_sync_bytes(int ncouples, int item_cap) {
   return align_up(256 + (size_t)ncouples * KV_FLAG_STRIDE * 4, 256) +
          align_up((size_t)ncouples * item_cap * 4, 256) +
-         (size_t)ncouples * 2 * KV_NG * NSM * 128 * sizeof(uint4);
+         (size_t)ncouples * 2 * KV_NG_MAX * NSM * 128 * sizeof(uint4);
 }
 
 static int kv_couples() {
@@ -754,11 +804,27 @@ mtgr_status_t attn_kv_launch(const AttnIO& io, const tca::Args& ax_in, const tca
   ks.ncouples = nc;
   ks.item_cap = item_cap;
   { const char* e = getenv("MTGR_KV_DEBUG"); ks.dbg = e ? atoi(e) : 0; }
+  { const char* e = getenv("MTGR_KV_NG"); ks.ng = e ? std::max(2, std::min(KV_NG_MAX, atoi(e))) : 16; }
+  static const bool trace = getenv("MTGR_KV_TRACE") != nullptr;
+  const size_t trn = 2 * 18 * 1024;
+  if (trace) {  // debug only
+    cudaMalloc(&ks.trace, trn * sizeof(long long));
+    cudaMemsetAsync(ks.trace, 0, trn * sizeof(long long), st);
+  }
   cudaMemsetAsync(w, 0, flag_bytes, st);
   cudaMemsetAsync(ax.ctr, 0, sizeof(int), st);
   ProfScope ps(PROF_ATTN_KV, st);
   cudaFuncSetAttribute(attn_kv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, KV_SMEM_BYTES);
   attn_kv_kernel<<<4 * nc, KV_THREADS, KV_SMEM_BYTES, st>>>(xc1, xx, xr1, xu, xo, yc1, yx, yr1, yu, yo, ax, ay, ks);
+  if (trace) {
+    std::vector<long long> hb(trn);
+    cudaMemcpyAsync(hb.data(), ks.trace, trn * sizeof(long long), cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    cudaFree(ks.trace);
+    fprintf(stderr, "KV_TRACE");
+    for (size_t i = 0; i < trn; ++i) fprintf(stderr, " %lld", hb[i]);
+    fprintf(stderr, "\n");
+  }
   return check_launch("attn_kv");
 }
 

@@ -41,12 +41,15 @@ class MTGRModel:
         shapes = [("head", k, v) for k, v in {"w_a": tuple(self.head["w_a"].shape), "b_a": (self.head["w_a"].shape[0],),
                                              "w_b": tuple(self.head["w_b"].shape), "b_b": (2,)}.items()]
         shapes += [(t, k, v) for t, q in self.tokens.grad_shapes().items() for k, v in q.items()]
-        n = sum(int(np.prod(shp)) for _, _, shp in shapes)
+        # each view starts on a 256-byte boundary (the GEMMs' TMA descriptors need 16-byte
+        # aligned pointers)
+        al = lambda n: (n + 63) // 64 * 64
+        n = sum(al(int(np.prod(shp))) for _, _, shp in shapes)
         self.dense_flat = torch.zeros(n, dtype=torch.float32, device=self.device)
         self.head_grads, self.token_grads, off = {}, {}, 0
         for owner, k, shp in shapes:
             v = self.dense_flat[off:off + int(np.prod(shp))].view(*shp)
-            off += v.numel()
+            off += al(v.numel())
             if owner == "head":
                 self.head_grads[k] = v
             else:
