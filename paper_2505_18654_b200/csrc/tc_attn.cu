@@ -119,8 +119,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
   uint64_t* x_empty = bars + 9;       // [3]
   uint64_t* c2_full = bars + 12;      // [2] leader
   uint64_t* c2_empty = bars + 14;     // [2]
+  // !TWO: the score tile is double-buffered (S[b] = T_S + 64 b) and the P tile written in place,
+  // so s_full is [2] (bars 16 and 44) and neither s_free nor t_free is used; TWO: single S / dP
   uint64_t* s_full = bars + 16;
-  uint64_t* s_free = bars + 17;       // leader, both CTAs' softmax warps
+  uint64_t* s_free = bars + 17;       // leader, both CTAs' softmax warps (TWO)
+  uint64_t* s_full1 = bars + 46;      // !TWO: score tile 1 (after q_item [43, 45))
   uint64_t* t_full = bars + 18;       // [2] leader, both CTAs
   uint64_t* t_free = bars + 20;       // [2]
   uint64_t* r1_full = bars + 22;
@@ -158,6 +161,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       mbar_init(&t_full[s], 2 * NSM); mbar_init(&t_free[s], 1);
     }
     mbar_init(s_full, 1);
+    mbar_init(s_full1, 1);
     mbar_init(s_free, 2 * NSM);
     mbar_init(r1_full, 1);
     mbar_init(r1_done, 2 * NSM);
@@ -423,9 +427,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
           if (elect_one()) {
 #pragma unroll
             for (int kk = 0; kk < BC / 16; ++kk)
-              mma_bf16_ts_2sm(tm + T_ACC, tm + T_P + tb * 32 + kk * 8,
+              mma_bf16_ts_2sm(tm + T_ACC, TWO ? tm + T_P + tb * 32 + kk * 8
+                                                : tm + T_S + 64 * tb + (kk >> 1) * 32 + (kk & 1) * 8,
                               desc_sw128(x + kk * 2048, X_BYTES / 2, 1024), idesc_acc, (j > 0 || kk > 0));
-            mma_commit_2sm_mc(&t_free[tb], 0x3);
+            if (TWO) mma_commit_2sm_mc(&t_free[tb], 0x3);
             mma_commit_2sm_mc(&x_empty[g % NX], 0x3);
           }
           __syncwarp();
@@ -434,7 +439,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
           const int g = gt + t;
           mbar_wait(&c1_full[g % NC1], (g / NC1) & 1);
           if (TWO) mbar_wait(&c2_full[g % NC2], (g / NC2) & 1);
-          mbar_wait(s_free, (g & 1) ^ 1);  // single S (and dP) buffer, released on tcgen05.ld
+          // TWO: single S (and dP) buffer, released on tcgen05.ld; !TWO: score tile (g & 1) was
+          // last read by the accumulate MMA of tile g - 2, issued (in order) before this one
+          if (TWO) mbar_wait(s_free, (g & 1) ^ 1);
           tc_fence_after();
           const uint32_t c1 = c1_base + (g % NC1) * C1_BYTES;
           const uint32_t c2 = c2_base + (g % NC2) * C1_BYTES;
@@ -458,10 +465,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
             } else {
 #pragma unroll
               for (int kk = 0; kk < DH / 16; ++kk)
-                mma_bf16_ts_2sm(tm + T_S, tm + T_R1 + kk * 8,
+                mma_bf16_ts_2sm(tm + T_S + 64 * (g & 1), tm + T_R1 + kk * 8,
                                 desc_sw128(c1 + (kk >> 2) * (C1_BYTES / 4) + (kk & 3) * 32, 16, 1024), idesc_s, kk > 0);
             }
-            mma_commit_2sm_mc(s_full, 0x3);
+            mma_commit_2sm_mc((TWO || (g & 1) == 0) ? s_full : s_full1, 0x3);
             mma_commit_2sm_mc(&c1_empty[g % NC1], 0x3);
             if (TWO && t + 1 == nt) mma_commit_2sm_mc(sc_done, 0x3);
           }
@@ -551,18 +558,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
             if (i < BC) tsb[i] = (c0 + i < us.L && a.jag.ts) ? a.jag.ts[us.off + c0 + i] : 0;
             named_bar_sync(1, 32 * NSM);
           }
-          mbar_wait(s_full, gt & 1);
+          const uint32_t t_s = TWO ? T_S : T_S + 64 * (gt & 1);
+          if (TWO) mbar_wait(s_full, gt & 1);
+          else mbar_wait((gt & 1) ? s_full1 : s_full, (gt >> 1) & 1);
           tc_fence_after();
           uint32_t s[32];
           uint32_t dp[TWO ? 32 : 1];
-          tmem_ld32(tmem + T_S + j_half + lane_off, s);
+          tmem_ld32(tmem + t_s + j_half + lane_off, s);
           if constexpr (TWO) {
             uint32_t (&d0)[32] = *reinterpret_cast<uint32_t(*)[32]>(&dp[0]);
             tmem_ld32(tmem + T_DP + j_half + lane_off, d0);
           }
           tmem_ld_wait();
-          tc_fence_before();
-          arrive_leader(s_free);
+          if (TWO) {
+            tc_fence_before();
+            arrive_leader(s_free);
+          }
           // visibility of this warp's 32 columns for this row (dynamic mask, R#8-R#12)
           const int cb = c0 + j_half;
           uint32_t vis;
@@ -649,9 +660,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
           }
           }
           const int tb = gt & 1;
-          mbar_wait(&t_free[tb], ((gt >> 1) & 1) ^ 1);
-          tc_fence_after();
-          tmem_st16(tmem + T_P + tb * 32 + half * 16 + lane_off, pk);
+          if (TWO) {
+            mbar_wait(&t_free[tb], ((gt >> 1) & 1) ^ 1);
+            tc_fence_after();
+          }
+          // !TWO: in place, into this warp's own 32 columns of the score tile it just read
+          tmem_st16(tmem + (TWO ? T_P + tb * 32 + half * 16 : t_s + j_half) + lane_off, pk);
           tmem_st_wait();
           tc_fence_before();
           arrive_leader(&t_full[tb]);

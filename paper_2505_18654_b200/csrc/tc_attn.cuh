@@ -85,14 +85,11 @@ __device__ __forceinline__ float2 f2add(float2 a, float2 b) {
   asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2u(a)), "l"(f2u(b)));
   return u2f(d);
 }
-// sigma(s) = 0.5 + 0.5 tanh(s/2) for a pair, the tanh in f16x2 (one MUFU op for two values;
-// its 2^-11 relative error is below the bf16 rounding of the P / dS tiles it feeds)
+// sigma(s) = 0.5 + 0.5 tanh(s/2) for a pair (two MUFU.TANH; the f16x2 / bf16x2 forms split into
+// two MUFU ops on sm_100 as well, plus conversions)
 __device__ __forceinline__ float2 sigmoid2_fast(float2 s) {
   const float2 h = f2mul(s, make_float2(0.5f, 0.5f));
-  __half2 hh = __float22half2_rn(h);
-  uint32_t t;
-  asm("tanh.approx.f16x2 %0, %1;" : "=r"(t) : "r"(*reinterpret_cast<uint32_t*>(&hh)));
-  const float2 tf = __half22float2(*reinterpret_cast<__half2*>(&t));
+  const float2 tf = make_float2(sm100::tanh_approx(h.x), sm100::tanh_approx(h.y));
   return f2fma(tf, make_float2(0.5f, 0.5f), make_float2(0.5f, 0.5f));
 }
 __device__ __forceinline__ uint32_t pack2(float a, float b) {

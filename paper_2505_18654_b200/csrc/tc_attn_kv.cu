@@ -103,7 +103,12 @@ __device__ __forceinline__ long long gtimer() {
 // trace events (MTGR_KV_TRACE): per item 0 start, 1 tiles done, 2 o_full, 3 epilogue done,
 // 4 ntiles, 5 first S issued, 6 last acc issued; per tile 7 s_full passed, 8 t_full arrived,
 // 9 S issued, 10 C1 load issued, 11 X load issued, 12 MMA saw c1_full, 13 MMA saw x_full
+// (compiled in only with -DMTGR_KV_TRACE_BUILD, `make TRACE=1`: the stamps cost registers)
+#ifdef MTGR_KV_TRACE_BUILD
 #define KV_TR(ev, i, v) do { if (tr != nullptr && (i) < 1024) tr[(ev) * 1024 + (i)] = (v); } while (0)
+#else
+#define KV_TR(ev, i, v) do { } while (0)
+#endif
 
 __device__ __forceinline__ uint32_t pack_h2(float a, float b) {
   __half2 h = __floats2half2_rn(a, b);
@@ -484,9 +489,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KV_THREADS, 1)
             mbar_wait(&s_full[tb], (gt >> 1) & 1);
             if (trw) KV_TR(7, gt, gtimer());
             tc_fence_after();
-            uint32_t s[32];
-            tmem_ld32(tmem + T_S + 64 * tb + j_half + lane_off, s);
+            // the 32 columns in two halves: the second TMEM load is in flight while the first
+            // half's SiLU / SiLU' are formed
+            uint32_t sa[16], sb[16];
+            tmem_ld16(tmem + T_S + 64 * tb + j_half + lane_off, sa);
             tmem_ld_wait();
+            tmem_ld16(tmem + T_S + 64 * tb + j_half + 16 + lane_off, sb);
             uint32_t vis;
             if (a.causal) {  // queries i >= key j, i < L
               const int lo = min(max(my - cb, 0), 32), hi = min(max(us.L - cb, 0), 32);
@@ -507,24 +515,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KV_THREADS, 1)
             }
             uint32_t gw[16];
             const bool all_vis = vis == 0xffffffffu;
-            if (ks.dbg & 16) {  // timing experiment: no softmax math
+            auto half16 = [&](const uint32_t* sv, int e0) {
 #pragma unroll
-              for (int e = 0; e < 16; ++e) { pk[e] = s[2 * e]; gw[e] = s[2 * e + 1]; }
-            } else
-#pragma unroll
-            for (int e = 0; e < 32; e += 2) {
-              const float2 sv = make_float2(__uint_as_float(s[e]), __uint_as_float(s[e + 1]));
-              // silu and silu' share sigma(s): p = s sigma, g = sigma + p (1 - sigma)
-              const float2 sg = sigmoid2_fast(sv);
-              float2 p2 = f2mul(sv, sg);
-              float2 d2 = f2fma(p2, f2add(make_float2(1.f, 1.f), make_float2(-sg.x, -sg.y)), sg);
-              if (!all_vis) {  // selects, no branch per element (masked entries exact zeros, R#2)
-                const bool m0 = (vis >> e) & 1u, m1 = (vis >> (e + 1)) & 1u;
-                p2.x = m0 ? p2.x : 0.f; d2.x = m0 ? d2.x : 0.f;
-                p2.y = m1 ? p2.y : 0.f; d2.y = m1 ? d2.y : 0.f;
+              for (int e = 0; e < 16; e += 2) {
+                const float2 x = make_float2(__uint_as_float(sv[e]), __uint_as_float(sv[e + 1]));
+                // silu and silu' share sigma(s): p = s sigma, g = sigma + p (1 - sigma)
+                const float2 sg = sigmoid2_fast(x);
+                float2 p2 = f2mul(x, sg);
+                float2 d2 = f2fma(p2, f2add(make_float2(1.f, 1.f), make_float2(-sg.x, -sg.y)), sg);
+                if (!all_vis) {  // selects, no branch per element (masked entries exact zeros, R#2)
+                  const bool m0 = (vis >> (e0 + e)) & 1u, m1 = (vis >> (e0 + e + 1)) & 1u;
+                  p2.x = m0 ? p2.x : 0.f; d2.x = m0 ? d2.x : 0.f;
+                  p2.y = m1 ? p2.y : 0.f; d2.y = m1 ? d2.y : 0.f;
+                }
+                pk[(e0 + e) >> 1] = pack2(p2.x, p2.y);
+                gw[(e0 + e) >> 1] = pack_h2(d2.x, d2.y);
               }
-              pk[e >> 1] = pack2(p2.x, p2.y);
-              gw[e >> 1] = pack_h2(d2.x, d2.y);
+            };
+            if (ks.dbg & 16) {  // timing experiment: no softmax math
+              tmem_ld_wait();
+#pragma unroll
+              for (int e = 0; e < 16; ++e) { pk[e] = sa[e]; gw[e] = sb[e]; }
+            } else {
+              half16(sa, 0);
+              tmem_ld_wait();
+              half16(sb, 16);
             }
             tmem_st16(tmem + T_S + 64 * tb + j_half + lane_off, pk);  // in place (this warp's S)
             tmem_st_wait();
@@ -672,7 +687,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KV_THREADS, 1)
         if (a.dbias != nullptr) {
           // bias gradient of this projection block: column sums over the item's rows.  The 32
           // columns of the chunk are summed over the warp's 32 rows by a butterfly
-          // reduce-scatter (lane l ends with column l), then one red.add per lane
+          // reduce-scatter (lane l ends with column l), then one red.add per lane.  (Reading the
+          // column pairs back from the bf16 tile instead was 2x slower: measured.)
 #pragma unroll
           for (int i = 0; i < 32; ++i) v[i] = row_ok ? v[i] : 0.f;
 #pragma unroll
