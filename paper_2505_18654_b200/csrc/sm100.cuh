@@ -16,6 +16,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <cstdio>
 
 namespace mtgr {
 namespace sm100 {
@@ -39,6 +40,30 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+#ifdef MTGR_WATCHDOG_BUILD
+// Hang watchdog (`make WATCHDOG=1`): a wait that has not completed after ~2^24 suspended
+// try_wait polls (seconds) reports the barrier and traps instead of hanging the GPU.
+__device__ __forceinline__ bool mbar_try_wait_dbg(uint64_t* bar, uint32_t parity, bool cluster) {
+  uint32_t ok;
+  if (cluster)
+    asm volatile("{\n\t.reg .pred P1;\n\tmbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%1], %2;\n\t"
+                 "selp.u32 %0, 1, 0, P1;\n\t}" : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+  else
+    asm volatile("{\n\t.reg .pred P1;\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+                 "selp.u32 %0, 1, 0, P1;\n\t}" : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_watch(uint64_t* bar, uint32_t parity, bool cluster) {
+  for (long long n = 0; !mbar_try_wait_dbg(bar, parity, cluster); ++n) {
+    if (n == (1ll << 24)) {
+      printf("MTGR watchdog: block %d thread %d waits on mbarrier smem %#x parity %u\n", blockIdx.x,
+             threadIdx.x, smem_u32(bar), parity);
+      __trap();
+    }
+  }
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) { mbar_watch(bar, parity, false); }
+#else
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred P1;\n"
@@ -50,6 +75,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+#endif
 
 // ------------------------------------------------------------------ TMA
 __device__ __forceinline__ void tma_prefetch(const CUtensorMap* m) {
@@ -123,6 +149,9 @@ __device__ __forceinline__ void mbar_arrive_cluster_release(uint64_t* bar, uint3
       "r"(rank)
       : "memory");
 }
+#ifdef MTGR_WATCHDOG_BUILD
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) { mbar_watch(bar, parity, true); }
+#else
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred P1;\n"
@@ -134,6 +163,7 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity
       "r"(parity)
       : "memory");
 }
+#endif
 // 1-D bulk copy global -> shared (bytes multiple of 16, both addresses 16-byte aligned)
 __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile(

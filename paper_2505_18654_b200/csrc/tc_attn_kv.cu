@@ -128,11 +128,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KV_THREADS, 1)
   constexpr int C1_BYTES = 32 * DH * 2;        // 16 KB: 4 boxes {64 dh, 32 cols}
   constexpr int X_BYTES = BC * (DH / 2) * 2;   // 16 KB: 2 boxes {64 dh, 64 cols}
   constexpr int NC1 = 3, NX = 3;
-  constexpr int OFF_C1 = 0, OFF_X = 48 * KB, OFF_R1STAGE = 96 * KB, OFF_EPI = 160 * KB;
+  // smem: C1 ring, X ring, the row operand's head dims 0..127 staged for tcgen05.cp [96,128) KB,
+  // its head dims 128..255 resident for the item as the SS half of the score MMA [128,160) KB,
+  // the epilogue tile [160,224) KB
+  constexpr int OFF_C1 = 0, OFF_X = 48 * KB, OFF_R1STAGE = 96 * KB, OFF_R1U = 128 * KB, OFF_EPI = 160 * KB;
+  constexpr int NS = 3;  // score tiles in flight
   // TMEM: row operand [0,128), accumulator [128,384), score tiles S[b] = [384 + 64b, +64), b = tile & 1;
   // the bf16 T tile is written in place: warp half h's 32 values into columns [32h, 32h + 16) of
   // its own S[b] half, so the next tile's score MMA never waits for the softmax
-  constexpr uint32_t T_R1 = 0, T_ACC = 128, T_S = 384;
+  // TMEM: row operand head dims 0..127 [0,64), accumulator [64,320), score tiles S[b] =
+  // [320 + 64b, +64), b = tile % 3 (triple-buffered: the score MMA runs two tiles ahead of the
+  // softmax)
+  constexpr uint32_t T_R1 = 0, T_ACC = 64, T_S = 320;
 
   const uint32_t crank = cluster_ctarank();
   const bool leader = crank == 0;
@@ -144,10 +151,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KV_THREADS, 1)
   uint64_t* c1_empty = bars + 3;      // [3]
   uint64_t* x_full = bars + 6;        // [3] leader
   uint64_t* x_empty = bars + 9;       // [3]
-  uint64_t* s_full = bars + 16;       // [2] score tile b complete (multicast commit)
-  uint64_t* t_full = bars + 18;       // [2] leader, both CTAs: T tile b written
-  uint64_t* r1_full = bars + 22;      // leader: both CTAs' row operand staged
+  uint64_t* s_full = bars + 12;       // [3] score tile b complete (multicast commit)
+  uint64_t* t_full = bars + 16;       // [3] leader, both CTAs: T tile b written
+  uint64_t* r1_full = bars + 22;      // leader: both CTAs' row operand (dh 0..127) staged
   uint64_t* r1_copied = bars + 24;    // own (tcgen05.cp done: staging reusable)
+  uint64_t* r1u_full = bars + 25;     // leader: both CTAs' row operand dh 128..255 resident
+  uint64_t* r1u_free = bars + 26;     // own (multicast): the item's last score MMA is done
   uint64_t* o_full = bars + 30;
   uint64_t* q_full = bars + 32;       // [4] work queue: item index published (own)
   uint64_t* q_empty = bars + 36;      // [4] leader: every consumer of both CTAs has read it
@@ -173,9 +182,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KV_THREADS, 1)
       mbar_init(&c1_full[s], 1); mbar_init(&c1_empty[s], 1);
       mbar_init(&x_full[s], 1); mbar_init(&x_empty[s], 1);
     }
-    for (int s = 0; s < 2; ++s) { mbar_init(&t_full[s], 2 * NSM); mbar_init(&s_full[s], 1); }
+    for (int s = 0; s < NS; ++s) { mbar_init(&t_full[s], 2 * NSM); mbar_init(&s_full[s], 1); }
     mbar_init(r1_full, 1);
     mbar_init(r1_copied, 1);
+    mbar_init(r1u_full, 1);
+    mbar_init(r1u_free, 1);
     mbar_init(o_full, 1);
     mbar_init(eu_full, 1);
     mbar_init(epi_free, NSM);
@@ -321,10 +332,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KV_THREADS, 1)
         decode_item<TRANS>(a, k, crank, it);
         if (it.ntiles > 0) {
           if (mi > 0) mbar_wait(r1_copied, (mi - 1) & 1);  // staging free again
-          if (leader) mbar_expect_tx(r1_full, 2 * RT_BYTES);
+          if (leader) mbar_expect_tx(r1_full, RT_BYTES);
 #pragma unroll
-          for (int c = 0; c < 4; ++c)
+          for (int c = 0; c < 2; ++c)  // head dims 0..127 -> staging (then TMEM)
             tma_load_2d_2sm(smem + OFF_R1STAGE + c * (RT_BYTES / 4), mR1, r1_full, it.hcol + c * 64, it.us.off + it.r0);
+          if (mi > 0) mbar_wait(r1u_free, (mi - 1) & 1);  // the previous item's score MMAs are done
+          if (leader) mbar_expect_tx(r1u_full, RT_BYTES);
+#pragma unroll
+          for (int c = 2; c < 4; ++c)  // head dims 128..255 -> resident (SS half of the score MMA)
+            tma_load_2d_2sm(smem + OFF_R1U + (c - 2) * (RT_BYTES / 4), mR1, r1u_full, it.hcol + c * 64, it.us.off + it.r0);
           ++mi;
         }
         if (a.uu != nullptr) {
@@ -376,7 +392,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KV_THREADS, 1)
         tc_fence_after();
         if (elect_one()) {
 #pragma unroll
-          for (int kk = 0; kk < DH / 16; ++kk)
+          for (int kk = 0; kk < DH / 32; ++kk)  // head dims 0..127
             tmem_cp_128x256b_2sm(tm + T_R1 + kk * 8,
                                  desc_sw128(r1s_base + (kk >> 2) * (RT_BYTES / 4) + (kk & 3) * 32, 16, 1024));
           mma_commit_2sm_mc(r1_copied, 0x3);
@@ -394,10 +410,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KV_THREADS, 1)
         if (nt == 0) continue;
         if (cp_done == mi) copy_r1();  // not prefetched at the end of the previous item
         const int item_n = n;
+        mbar_wait(r1u_full, mi & 1);  // head dims 128..255 of this item's rows in smem
+        const uint32_t r1u_base = smem_u32(smem + OFF_R1U);
         // acc += T_j X_j  (A = T from each CTA's TMEM, B = X: each CTA's half of the head dim)
         auto acc = [&](int j, int g) {
-          const int tb = g & 1;
-          mbar_wait(&t_full[tb], (g >> 1) & 1);
+          const int tb = g % NS;
+          mbar_wait(&t_full[tb], (g / NS) & 1);
           mbar_wait(&x_full[g % NX], (g / NX) & 1);
           if (lane == 0) KV_TR(13, g, gtimer());
           const uint32_t x = x_base + (g % NX) * X_BYTES;
@@ -411,27 +429,38 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KV_THREADS, 1)
           }
           __syncwarp();
         };
-        for (int t = 0; t < nt; ++t) {
+        // score tile g: head dims 0..127 with A from TMEM, 128..255 with A from smem.  Its buffer
+        // (g % 3) was last read by the T MMA of tile g - 3, issued (in order) before this one
+        auto score = [&](int t) {
           const int g = gt + t;
           mbar_wait(&c1_full[g % NC1], (g / NC1) & 1);
           if (lane == 0) KV_TR(12, g, gtimer());
-          // score tile (g & 1) was last read by the T MMA of tile g - 2, issued (in order) in
-          // the previous iteration after its softmax finished
           tc_fence_after();
           const uint32_t c1 = c1_base + (g % NC1) * C1_BYTES;
+          const uint32_t ts = tm + T_S + 64 * (g % NS);
           if (elect_one()) {
 #pragma unroll
-            for (int kk = 0; kk < DH / 16; ++kk)
-              mma_bf16_ts_2sm(tm + T_S + 64 * (g & 1), tm + T_R1 + kk * 8,
-                              desc_sw128(c1 + (kk >> 2) * (C1_BYTES / 4) + (kk & 3) * 32, 16, 1024), idesc_s, kk > 0);
-            mma_commit_2sm_mc(&s_full[g & 1], 0x3);
+            for (int kk = 0; kk < DH / 16; ++kk) {
+              const uint64_t bd = desc_sw128(c1 + (kk >> 2) * (C1_BYTES / 4) + (kk & 3) * 32, 16, 1024);
+              if (kk < 8)
+                mma_bf16_ts_2sm(ts, tm + T_R1 + kk * 8, bd, idesc_s, kk > 0);
+              else
+                mma_bf16_ss_2sm(ts, desc_sw128(r1u_base + ((kk >> 2) - 2) * (RT_BYTES / 4) + (kk & 3) * 32, 16, 1024),
+                                bd, idesc_s, 1);
+            }
+            mma_commit_2sm_mc(&s_full[g % NS], 0x3);
             mma_commit_2sm_mc(&c1_empty[g % NC1], 0x3);
+            if (t + 1 == nt) mma_commit_2sm_mc(r1u_free, 0x3);  // the resident half may be replaced
           }
           __syncwarp();
           if (lane == 0) { const long long tt = gtimer(); KV_TR(9, g, tt); if (t == 0) KV_TR(5, item_n, tt); }
-          if (t >= 1) acc(t - 1, g - 1);
+        };
+        score(0);
+        if (nt > 1) score(1);
+        for (int t = 0; t < nt; ++t) {
+          if (t + 2 < nt) score(t + 2);  // its buffer's T tile (t - 1) went to the pipe last iteration
+          acc(t, gt + t);
         }
-        acc(nt - 1, gt + nt - 1);
         if (elect_one()) mma_commit_2sm_mc(o_full, 0x3);
         __syncwarp();
         if (lane == 0) KV_TR(6, item_n, gtimer());
@@ -485,8 +514,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KV_THREADS, 1)
               if (i < BC) sTs[i] = (c0 + i < us.L && a.jag.ts) ? a.jag.ts[us.off + c0 + i] : 0;
               named_bar_sync(1, 32 * NSM);
             }
-            const int tb = gt & 1;
-            mbar_wait(&s_full[tb], (gt >> 1) & 1);
+            const int tb = gt % NS;
+            mbar_wait(&s_full[tb], (gt / NS) & 1);
             if (trw) KV_TR(7, gt, gtimer());
             tc_fence_after();
             // the 32 columns in two halves: the second TMEM load is in flight while the first
@@ -572,8 +601,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KV_THREADS, 1)
             uint4 gv[4];
 #pragma unroll
             for (int c = 0; c < 4; ++c) gv[c] = __ldcg(&gp[c * 32 + lane]);  // L2 (never a stale L1 line)
-            const int tb = gt & 1;
-            mbar_wait(&s_full[tb], (gt >> 1) & 1);
+            const int tb = gt % NS;
+            mbar_wait(&s_full[tb], (gt / NS) & 1);
             if (trw) KV_TR(7, gt, gtimer());
             tc_fence_after();
             uint32_t dp[32];
