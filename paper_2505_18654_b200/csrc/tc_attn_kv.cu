@@ -66,6 +66,7 @@ struct KvSync {
   int ncouples, item_cap;
   long long* trace;  // MTGR_KV_TRACE: [role][10 events][1024] globaltimer stamps of couple 0, rank 0
   int ng;          // G ring depth in tiles
+  int sleep_ns;    // sync thread poll period (MTGR_KV_SLEEP)
   int dbg;         // MTGR_KV_DEBUG (timing experiments only; results are wrong when set): 1 Y does
                    // not wait for G, 2 X writes no G, 4 Y stores no dS^T, 8 X ignores ring reuse
 };
@@ -318,7 +319,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KV_THREADS, 1)
         if (p > seen) { st_release_cta_smem(gready, p); seen = p; }
       }
       if (all_exit) break;
-      __nanosleep(32);
+      // the thread shares an SM sub-partition with two softmax warps: poll sparingly
+      __nanosleep(ks.sleep_ns);
     }
   } else if (warp == 2) {
     // ---------------------------------------------------------------- row operand + epilogue tile
@@ -483,6 +485,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KV_THREADS, 1)
     const int j_half = half * 32;
     int gt = 0, mi = 0, idx = 0;
     int ready = 0;  // Y: G tiles known published
+    uint4 gpre[4];  // Y: the next tile's G piece, prefetched
+    int gpre_t = -1;
     for (int n = 0;; ++n) {
       const int k = q_read(n);
       __syncwarp();
@@ -504,7 +508,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KV_THREADS, 1)
         for (int t = 0; t < it.ntiles; ++t, ++gt) {
           const int c0 = it.c_begin + t * BC;
           const int cb = c0 + j_half;  // this warp's 32 query columns
-          uint4* gp = gring + ((size_t)(gt % ks.ng) * NSM + sw) * 128;  // this warp's G piece
+          uint4* gp = gring + ((size_t)(gt & (ks.ng - 1)) * NSM + sw) * 128;  // this warp's G piece
           uint32_t pk[16];
           if (role == 0) {
             // ---------------- X: P^T = silu(S^T) m for the dV MMA, G = silu'(S^T) m for Y
@@ -599,8 +603,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KV_THREADS, 1)
               ready = v;
             }
             uint4 gv[4];
+            if (gpre_t == gt) {  // prefetched during the previous tile
 #pragma unroll
-            for (int c = 0; c < 4; ++c) gv[c] = __ldcg(&gp[c * 32 + lane]);  // L2 (never a stale L1 line)
+              for (int c = 0; c < 4; ++c) gv[c] = gpre[c];
+            } else {
+#pragma unroll
+              for (int c = 0; c < 4; ++c) gv[c] = __ldcg(&gp[c * 32 + lane]);  // L2 (never a stale L1 line)
+            }
             const int tb = gt % NS;
             mbar_wait(&s_full[tb], (gt / NS) & 1);
             if (trw) KV_TR(7, gt, gtimer());
@@ -636,6 +645,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KV_THREADS, 1)
             if (!(ks.dbg & 4)) {
               stg256(p0 - (int64_t)b * a.st_pitch, b ? oth : own);
               stg256(p0 + (int64_t)(1 - b) * a.st_pitch, b ? own : oth);
+            }
+            // prefetch the next tile's G when it is already published (its L2 latency then hides
+            // behind this tile's tail and the next score wait)
+            if (t + 1 < it.ntiles && !(ks.dbg & 1)) {
+              if (ready < gt + 2) ready = ld_acquire_cta_smem(gready);
+              if (ready >= gt + 2) {
+                const uint4* gn = gring + ((size_t)((gt + 1) & (ks.ng - 1)) * NSM + sw) * 128;
+#pragma unroll
+                for (int c = 0; c < 4; ++c) gpre[c] = __ldcg(&gn[c * 32 + lane]);
+                gpre_t = gt + 1;
+              }
             }
           }
         }
@@ -849,7 +869,13 @@ mtgr_status_t attn_kv_launch(const AttnIO& io, const tca::Args& ax_in, const tca
   ks.ncouples = nc;
   ks.item_cap = item_cap;
   { const char* e = getenv("MTGR_KV_DEBUG"); ks.dbg = e ? atoi(e) : 0; }
-  { const char* e = getenv("MTGR_KV_NG"); ks.ng = e ? std::max(2, std::min(KV_NG_MAX, atoi(e))) : 16; }
+  { const char* e = getenv("MTGR_KV_SLEEP"); ks.sleep_ns = e ? std::max(0, atoi(e)) : 256; }
+  {  // a power of two (slot = tile & (ng - 1))
+    const char* e = getenv("MTGR_KV_NG");
+    int ng = e ? std::max(2, std::min(KV_NG_MAX, atoi(e))) : 16;
+    while (ng & (ng - 1)) ng &= ng - 1;
+    ks.ng = ng;
+  }
   static const bool trace = getenv("MTGR_KV_TRACE") != nullptr;
   const size_t trn = 2 * 18 * 1024;
   if (trace) {  // debug only

@@ -2,11 +2,17 @@
 // Eq.6 output "MLP", and their backward): C[M][N] = A[M][K] * B[N][K]^T, fp32 accumulation
 // in TMEM.
 //
-// Persistent, warp-specialised, one CTA per SM:
-//   warp 0 : TMA producer  (4-stage ring of 128x64 A + 256x64 B bf16 tiles, SWIZZLE_128B)
-//   warp 1 : MMA issuer    (one thread, tcgen05.mma.cta_group::1 M=128 N=256 K=16)
-//   warp 2 : TMEM allocator (512 columns = two 128x256 fp32 accumulators, double-buffered)
-//   warps 4-7: epilogue    (tcgen05.ld 32x32b -> registers -> fused epilogue -> global)
+// Persistent, warp-specialised; the layer GEMMs run on CTA pairs (cta_group::2, clusters of 2):
+//   warp 0 : TMA producer  (4-stage ring: this CTA's 128x64 rows of A + its half, 128x64, of the
+//            256x64 B tile, SWIZZLE_128B, 2-SM TMA onto the leader's barriers)
+//   warp 1 : MMA issuer    (leader CTA, one elected thread, tcgen05.mma.cta_group::2 M=256
+//            N=256 K=16: each CTA's 128 rows of A against the whole B tile, B read half from
+//            each CTA's shared memory)
+//   warp 2 : TMEM allocator (512 columns = two 128x256 fp32 accumulators per CTA,
+//            double-buffered so an epilogue overlaps the next tile's MMAs)
+//   warps 4-11: epilogue   (two per TMEM lane quadrant: tcgen05.ld 32x32b -> registers -> fused
+//            epilogue -> SW128 staging -> TMA store)
+// (Geo<1, ...> is the one-CTA cta_group::1 M=128 variant, compiled in by CG_USE = 1.)
 // Either operand may be K-major or MN-major (the weight-gradient and data-gradient GEMMs read
 // activations [T][n] as MN-major operands directly — no transposes).  Small output grids
 // (weight gradients, K = T) are split along K with a deterministic second-pass reduction.
