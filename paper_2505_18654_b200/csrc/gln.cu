@@ -8,7 +8,6 @@
 // Parameter gradients are per-block partial sums (smem) reduced in block order by a second
 // kernel.
 #include <algorithm>
-#include <type_traits>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -75,10 +74,9 @@ __device__ __forceinline__ float warp_sum(float v) {
 // One warp per token over a CONTIGUOUS token range per warp (tokens of a group are contiguous
 // within a user, so gamma / beta of the current group stay in registers and are reloaded only on
 // a group change: the per-token traffic is the token's own rows, not 2d fp32 parameters through
-// L1).  Software pipelined D tokens deep: token t + D's rows (and group id) are issued as token t
-// is finished, so D tokens' bytes are in flight per warp (GLN1 moves 1 KB per token at d=512:
-// two in flight left it latency-bound at ~67 % of HBM, ncu).
-template <class T, int NC, int D>
+// L1).  Software pipelined: the next token's rows (and group id) are in flight while this one is
+// reduced, normalised and stored.
+template <class T, int NC>
 __global__ void __launch_bounds__(256) gln_fwd_kernel(const T* __restrict__ x,
                                                       const uint8_t* __restrict__ gid,
                                                       const float* __restrict__ gamma,
@@ -93,8 +91,7 @@ __global__ void __launch_bounds__(256) gln_fwd_kernel(const T* __restrict__ x,
   const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int t_begin = w * tok_per_warp;
   const int t_end = min(ntok, t_begin + tok_per_warp);
-  Raw8<T> bx[D][NC], bg[D][NC];
-  int bgid[D];
+  Raw8<T> cx[NC], cg[NC], nx[NC], ng[NC];
   auto issue = [&](int tt, Raw8<T>* xa, Raw8<T>* ga) {
 #pragma unroll
     for (int k = 0; k < NC; ++k) {
@@ -105,77 +102,74 @@ __global__ void __launch_bounds__(256) gln_fwd_kernel(const T* __restrict__ x,
       }
     }
   };
-#pragma unroll
-  for (int s = 0; s < D; ++s)
-    if (t_begin + s < t_end) { issue(t_begin + s, bx[s], bg[s]); bgid[s] = gid[t_begin + s]; }
   float gg[NC][8], bb[NC][8];
   int g_loaded = -1;
-  for (int t0 = t_begin; t0 < t_end; t0 += D) {
+  int t = t_begin;
+  int g_cur = 0;
+  if (t < t_end) { issue(t, cx, cg); g_cur = gid[t]; }
+  for (; t < t_end; ++t) {
+    const int tn = t + 1;
+    int g_next = 0;
+    if (tn < t_end) { issue(tn, nx, ng); g_next = gid[tn]; }
+    if (g_cur != g_loaded) {  // group change: this group's affine parameters into registers
 #pragma unroll
-    for (int s = 0; s < D; ++s) {
-      const int t = t0 + s;
-      if (t < t_end) {
-        const int g_cur = bgid[s];
-        if (g_cur != g_loaded) {  // group change: this group's affine parameters into registers
-#pragma unroll
-          for (int k = 0; k < NC; ++k) {
-            const int c = lane + 32 * k;
-            if (c < nch) {
-              load8(gamma + (int64_t)g_cur * d + c * 8, gg[k]);
-              load8(beta + (int64_t)g_cur * d + c * 8, bb[k]);
-            }
-          }
-          g_loaded = g_cur;
-        }
-        float v[NC][8];
-        float sm = 0.f;
-#pragma unroll
-        for (int k = 0; k < NC; ++k) {
-          int c = lane + 32 * k;
-          if (c < nch) {
-            unpack(bx[s][k], v[k]);
-            if (gate != nullptr) {  // input = x (.) gate (Eq.6 gate folded into the norm's load)
-              float gv[8];
-              unpack(bg[s][k], gv);
-#pragma unroll
-              for (int e = 0; e < 8; ++e) v[k][e] *= gv[e];
-            }
-#pragma unroll
-            for (int e = 0; e < 8; ++e) sm += v[k][e];
-          }
-        }
-        // the slot is free: issue the token D ahead (its latency hides behind D tokens' work)
-        if (t + D < t_end) { issue(t + D, bx[s], bg[s]); bgid[s] = gid[t + D]; }
-        const float mu = warp_sum(sm) * inv_d;
-        float q = 0.f;
-#pragma unroll
-        for (int k = 0; k < NC; ++k)
-          if (lane + 32 * k < nch) {
-#pragma unroll
-            for (int e = 0; e < 8; ++e) {
-              float dlt = v[k][e] - mu;
-              q += dlt * dlt;
-            }
-          }
-        const float var = warp_sum(q) * inv_d;
-        const float r = 1.0f / sqrtf(var + eps);
-        T* yr = y + (int64_t)t * d;
-#pragma unroll
-        for (int k = 0; k < NC; ++k) {
-          int c = lane + 32 * k;
-          if (c < nch) {
-            float o[8];
-#pragma unroll
-            for (int e = 0; e < 8; ++e) o[e] = gg[k][e] * ((v[k][e] - mu) * r) + bb[k][e];
-            store8(yr + c * 8, o);
-          }
-        }
-        if (lane == 0) {
-          if (mean) mean[t] = mu;
-          if (rstd) rstd[t] = r;
+      for (int k = 0; k < NC; ++k) {
+        const int c = lane + 32 * k;
+        if (c < nch) {
+          load8(gamma + (int64_t)g_cur * d + c * 8, gg[k]);
+          load8(beta + (int64_t)g_cur * d + c * 8, bb[k]);
         }
       }
+      g_loaded = g_cur;
     }
+    float v[NC][8];
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < NC; ++k) {
+      int c = lane + 32 * k;
+      if (c < nch) {
+        unpack(cx[k], v[k]);
+        if (gate != nullptr) {  // input = x (.) gate (Eq.6 gate folded into the norm's load)
+          float gv[8];
+          unpack(cg[k], gv);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) v[k][e] *= gv[e];
+        }
+#pragma unroll
+        for (int e = 0; e < 8; ++e) s += v[k][e];
+      }
+    }
+    const float mu = warp_sum(s) * inv_d;
+    float q = 0.f;
+#pragma unroll
+    for (int k = 0; k < NC; ++k)
+      if (lane + 32 * k < nch) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          float dlt = v[k][e] - mu;
+          q += dlt * dlt;
+        }
+      }
+    const float var = warp_sum(q) * inv_d;
+    const float r = 1.0f / sqrtf(var + eps);
+    T* yr = y + (int64_t)t * d;
+#pragma unroll
+    for (int k = 0; k < NC; ++k) {
+      int c = lane + 32 * k;
+      if (c < nch) {
+        float o[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) o[e] = gg[k][e] * ((v[k][e] - mu) * r) + bb[k][e];
+        store8(yr + c * 8, o);
+      }
+    }
+    if (lane == 0) {
+      if (mean) mean[t] = mu;
+      if (rstd) rstd[t] = r;
+    }
+#pragma unroll
+    for (int k = 0; k < NC; ++k) { cx[k] = nx[k]; cg[k] = ng[k]; }
+    g_cur = g_next;
   }
 }
 
@@ -606,18 +600,8 @@ static void gln_fwd_go(const T* x, const uint8_t* gid, const float* gamma, const
   const int warps = 8 * 8 * num_sms();
   const int tpw = std::max(1, ceil_div(ntok, warps));
   const int blocks = ceil_div(ceil_div(ntok, tpw), 8);
-  // depth: 4 tokens for the one-row (GLN1) bf16 form up to d = 768, else 2 (two rows per token,
-  // or fp32 / wide rows whose registers would spill)
-  constexpr bool deep = std::is_same<T, __nv_bfloat16>::value && NC <= 3;
-  if constexpr (deep) {
-    if (gate == nullptr) {
-      gln_fwd_kernel<T, NC, 4><<<blocks, 256, 0, st>>>(x, gid, gamma, beta, y, mean, rstd, ntok, d, eps,
-                                                       gate, ld_gate, tpw);
-      return;
-    }
-  }
-  gln_fwd_kernel<T, NC, 2><<<blocks, 256, 0, st>>>(x, gid, gamma, beta, y, mean, rstd, ntok, d, eps,
-                                                   gate, ld_gate, tpw);
+  gln_fwd_kernel<T, NC><<<blocks, 256, 0, st>>>(x, gid, gamma, beta, y, mean, rstd, ntok, d, eps,
+                                                gate, ld_gate, tpw);
 }
 
 template <class T>
