@@ -674,14 +674,16 @@ def main():
     if args.impl == "reference":
         run_reference(args, cfg, rank, world)
         return
+    if world > 1:
+        # communicator INIT lines (nranks, transport) go to stderr; stdout carries one JSON line.
+        # Set before torch is imported: NCCL reads its debug settings once, at its first call
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     import torch
     import torch.distributed as dist
     if world > 1:
         torch.cuda.set_device(local_rank)
-        # communicator INIT lines (nranks, transport) go to stderr; stdout carries one JSON line
-        os.environ.setdefault("NCCL_DEBUG", "INFO")
-        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
-        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         dist.init_process_group(args.backend, device_id=torch.device("cuda", local_rank))
     try:
         run_mtgr(args, cfg, rank, world, local_rank)

@@ -51,6 +51,9 @@
 namespace mtgr {
 namespace tca {
 
+#ifndef KV_NS
+#define KV_NS 2
+#endif
 constexpr int KV_NG_MAX = 32;       // G ring depth (tiles) per CTA: ks.ng <= this (MTGR_KV_NG)
 constexpr int KV_THREADS = 384;     // 12 warps (13 would round the register budget to 16 warps')
 constexpr int KV_EXIT = 1 << 30;    // per-warp counter flag: the warp has left its item loop
@@ -133,14 +136,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KV_THREADS, 1)
   // its head dims 128..255 resident for the item as the SS half of the score MMA [128,160) KB,
   // the epilogue tile [160,224) KB
   constexpr int OFF_C1 = 0, OFF_X = 48 * KB, OFF_R1STAGE = 96 * KB, OFF_R1U = 128 * KB, OFF_EPI = 160 * KB;
-  constexpr int NS = 3;  // score tiles in flight
+  // KV_NS score tiles in flight.  2 (default): the whole row operand in TMEM (TS score MMA);
+  // 3: head dims 128..255 of the row operand resident in smem as the SS half of the score MMA,
+  // freeing 64 TMEM columns for a third tile (measured ~3 % slower at `small`: the SS half is
+  // shared-memory bound, and the two-tile chain is not what limits the loop)
+  constexpr int NS = KV_NS;
+  constexpr bool SPLIT_R1 = NS == 3;
   // TMEM: row operand [0,128), accumulator [128,384), score tiles S[b] = [384 + 64b, +64), b = tile & 1;
   // the bf16 T tile is written in place: warp half h's 32 values into columns [32h, 32h + 16) of
   // its own S[b] half, so the next tile's score MMA never waits for the softmax
   // TMEM: row operand head dims 0..127 [0,64), accumulator [64,320), score tiles S[b] =
   // [320 + 64b, +64), b = tile % 3 (triple-buffered: the score MMA runs two tiles ahead of the
   // softmax)
-  constexpr uint32_t T_R1 = 0, T_ACC = 64, T_S = 320;
+  constexpr uint32_t T_R1 = 0, T_ACC = SPLIT_R1 ? 64 : 128, T_S = SPLIT_R1 ? 320 : 384;
 
   const uint32_t crank = cluster_ctarank();
   const bool leader = crank == 0;
@@ -334,15 +342,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KV_THREADS, 1)
         decode_item<TRANS>(a, k, crank, it);
         if (it.ntiles > 0) {
           if (mi > 0) mbar_wait(r1_copied, (mi - 1) & 1);  // staging free again
-          if (leader) mbar_expect_tx(r1_full, RT_BYTES);
+          constexpr int NSTAGED = SPLIT_R1 ? 2 : 4;  // 64-column boxes staged for TMEM
+          if (leader) mbar_expect_tx(r1_full, NSTAGED * (RT_BYTES / 2));
 #pragma unroll
-          for (int c = 0; c < 2; ++c)  // head dims 0..127 -> staging (then TMEM)
+          for (int c = 0; c < NSTAGED; ++c)  // head dims -> staging (then TMEM)
             tma_load_2d_2sm(smem + OFF_R1STAGE + c * (RT_BYTES / 4), mR1, r1_full, it.hcol + c * 64, it.us.off + it.r0);
-          if (mi > 0) mbar_wait(r1u_free, (mi - 1) & 1);  // the previous item's score MMAs are done
-          if (leader) mbar_expect_tx(r1u_full, RT_BYTES);
+          if constexpr (SPLIT_R1) {
+            if (mi > 0) mbar_wait(r1u_free, (mi - 1) & 1);  // the previous item's score MMAs are done
+            if (leader) mbar_expect_tx(r1u_full, RT_BYTES);
 #pragma unroll
-          for (int c = 2; c < 4; ++c)  // head dims 128..255 -> resident (SS half of the score MMA)
-            tma_load_2d_2sm(smem + OFF_R1U + (c - 2) * (RT_BYTES / 4), mR1, r1u_full, it.hcol + c * 64, it.us.off + it.r0);
+            for (int c = 2; c < 4; ++c)  // head dims 128..255 -> resident (SS half of the score MMA)
+              tma_load_2d_2sm(smem + OFF_R1U + (c - 2) * (RT_BYTES / 4), mR1, r1u_full, it.hcol + c * 64, it.us.off + it.r0);
+          }
           ++mi;
         }
         if (a.uu != nullptr) {
@@ -394,7 +405,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KV_THREADS, 1)
         tc_fence_after();
         if (elect_one()) {
 #pragma unroll
-          for (int kk = 0; kk < DH / 32; ++kk)  // head dims 0..127
+          for (int kk = 0; kk < (SPLIT_R1 ? DH / 32 : DH / 16); ++kk)  // the TMEM-resident head dims
             tmem_cp_128x256b_2sm(tm + T_R1 + kk * 8,
                                  desc_sw128(r1s_base + (kk >> 2) * (RT_BYTES / 4) + (kk & 3) * 32, 16, 1024));
           mma_commit_2sm_mc(r1_copied, 0x3);
@@ -412,7 +423,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KV_THREADS, 1)
         if (nt == 0) continue;
         if (cp_done == mi) copy_r1();  // not prefetched at the end of the previous item
         const int item_n = n;
-        mbar_wait(r1u_full, mi & 1);  // head dims 128..255 of this item's rows in smem
+        if constexpr (SPLIT_R1) mbar_wait(r1u_full, mi & 1);  // head dims 128..255 of the rows in smem
         const uint32_t r1u_base = smem_u32(smem + OFF_R1U);
         // acc += T_j X_j  (A = T from each CTA's TMEM, B = X: each CTA's half of the head dim)
         auto acc = [&](int j, int g) {
@@ -444,7 +455,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KV_THREADS, 1)
 #pragma unroll
             for (int kk = 0; kk < DH / 16; ++kk) {
               const uint64_t bd = desc_sw128(c1 + (kk >> 2) * (C1_BYTES / 4) + (kk & 3) * 32, 16, 1024);
-              if (kk < 8)
+              if (!SPLIT_R1 || kk < 8)
                 mma_bf16_ts_2sm(ts, tm + T_R1 + kk * 8, bd, idesc_s, kk > 0);
               else
                 mma_bf16_ss_2sm(ts, desc_sw128(r1u_base + ((kk >> 2) - 2) * (RT_BYTES / 4) + (kk & 3) * 32, 16, 1024),
@@ -452,15 +463,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KV_THREADS, 1)
             }
             mma_commit_2sm_mc(&s_full[g % NS], 0x3);
             mma_commit_2sm_mc(&c1_empty[g % NC1], 0x3);
-            if (t + 1 == nt) mma_commit_2sm_mc(r1u_free, 0x3);  // the resident half may be replaced
+            if (SPLIT_R1 && t + 1 == nt) mma_commit_2sm_mc(r1u_free, 0x3);  // the resident half may go
           }
           __syncwarp();
           if (lane == 0) { const long long tt = gtimer(); KV_TR(9, g, tt); if (t == 0) KV_TR(5, item_n, tt); }
         };
-        score(0);
-        if (nt > 1) score(1);
+        // score MMAs run NS - 1 tiles ahead of the T MMAs: a score tile's buffer was last read
+        // by the T MMA of tile g - NS, issued (in order) in an earlier iteration
+        for (int t = 0; t < NS - 1 && t < nt; ++t) score(t);
         for (int t = 0; t < nt; ++t) {
-          if (t + 2 < nt) score(t + 2);  // its buffer's T tile (t - 1) went to the pipe last iteration
+          if (t + NS - 1 < nt) score(t + NS - 1);
           acc(t, gt + t);
         }
         if (elect_one()) mma_commit_2sm_mc(o_full, 0x3);

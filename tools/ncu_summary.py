@@ -75,7 +75,7 @@ def full(path):
 # GEMM EPI enum: STORE 0, QKVU 1, RESID 2, F32 3)
 KIND = [(r"attn_tc_kernel<0>", "attn_fwd"), (r"attn_tc_kernel<1>", "attn_bwd_dv"),
         (r"attn_tc_kernel<2>", "attn_bwd_dq"), (r"attn_tc_kernel<3>", "attn_bwd_dk_fused"),
-        (r"attn_sc_kernel", "attn_bwd_scores"),
+        (r"attn_sc_kernel", "attn_bwd_scores"), (r"attn_kv_kernel", "attn_bwd_kv"),
         (r"gemm_tc_kernel<1,", "gemm_qkvu"), (r"gemm_tc_kernel<2,", "gemm_out"),
         (r"gemm_tc_kernel<0,", "gemm_dgrad"), (r"gemm_tc_kernel<3,", "gemm_wgrad"),
         (r"gln_fwd_kernel", "gln_fwd"), (r"gln_bwd", "gln_bwd"),
