@@ -231,7 +231,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KV_THREADS, 1)
   int* items = ks.items + (size_t)couple * ks.item_cap;
   // this CTA's G ring: [KV_NG slots][8 warps][4 chunks][32 lanes] x 16 B
   uint4* gring = ks.gbuf + (size_t)(couple * 2 + (int)crank) * KV_NG_MAX * NSM * 128;
-  long long* tr = (ks.trace != nullptr && couple == 0 && crank == 0) ? ks.trace + (size_t)role * 18 * 1024 : nullptr;
+  long long* tr = (ks.trace != nullptr && couple == 0) ? ks.trace + ((size_t)role * 2 + crank) * 26 * 1024 : nullptr;
 
   auto q_read = [&](int n) -> int {
     mbar_wait_cluster(&q_full[n & 3], (n >> 2) & 1);
@@ -591,6 +591,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KV_THREADS, 1)
             tc_fence_before();
             arrive_leader(&t_full[tb]);
             if (trw) KV_TR(8, gt, gtimer());
+            if (lane == 0) KV_TR(18 + sw, gt, gtimer());
             // publish the PREVIOUS tile's G piece: its stores were issued a tile ago, so this
             // release (which waits for them) does not stall; this tile's follow below
             __syncwarp();
@@ -641,6 +642,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KV_THREADS, 1)
             tc_fence_before();
             arrive_leader(&t_full[tb]);
             if (trw) KV_TR(8, gt, gtimer());
+            if (lane == 0) KV_TR(18 + sw, gt, gtimer());
             // this tile's G is consumed
             __syncwarp();
             if (lane == 0) *reinterpret_cast<volatile int*>(&wcnt[sw]) = gt + 1;
@@ -889,7 +891,7 @@ mtgr_status_t attn_kv_launch(const AttnIO& io, const tca::Args& ax_in, const tca
     ks.ng = ng;
   }
   static const bool trace = getenv("MTGR_KV_TRACE") != nullptr;
-  const size_t trn = 2 * 18 * 1024;
+  const size_t trn = 2 * 2 * 26 * 1024;
   if (trace) {  // debug only
     cudaMalloc(&ks.trace, trn * sizeof(long long));
     cudaMemsetAsync(ks.trace, 0, trn * sizeof(long long), st);

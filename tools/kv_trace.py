@@ -43,7 +43,7 @@ def parse(path):
     for line in open(path):
         if line.startswith("KV_TRACE"):
             last = line
-    v = np.array([int(t) for t in last.split()[1:]], dtype=np.int64).reshape(2, 18, 1024)
+    v = np.array([int(t) for t in last.split()[1:]], dtype=np.int64).reshape(2, 2, 26, 1024)[:, 0]
     base = min(int(x[x > 0].min()) for x in (v[0], v[1]))
     for role in (0, 1):
         w = v[role]
@@ -84,7 +84,7 @@ def summary(path):
     for line in open(path):
         if line.startswith("KV_TRACE"):
             last = line
-    v = np.array([int(t) for t in last.split()[1:]], dtype=np.int64).reshape(2, 18, 1024)
+    v = np.array([int(t) for t in last.split()[1:]], dtype=np.int64).reshape(2, 2, 26, 1024)[:, 0]
     for role in (0, 1):
         w = v[role]
         n = int((w[0] > 0).sum())
@@ -98,9 +98,27 @@ def summary(path):
               f"loop/tile {loop:.0f} softmax {np.median(sm[sm > 0]):.0f} epilogue {epi:.0f} ns")
 
 
+def warps(path):
+    """Per tile: each softmax warp's T-tile arrival relative to the earliest (both CTAs)."""
+    last = None
+    for line in open(path):
+        if line.startswith("KV_TRACE"):
+            last = line
+    v = np.array([int(t) for t in last.split()[1:]], dtype=np.int64).reshape(2, 2, 26, 1024)
+    for role in (0, 1):
+        a = v[role][:, 18:26, :]            # [crank][warp][tile]
+        ok = (a > 0).all(axis=(0, 1))
+        rel = a[:, :, ok] - a[:, :, ok].min(axis=(0, 1), keepdims=True)
+        print(f"role {'XY'[role]}: {ok.sum()} tiles; median lag (ns) behind the first warp, [crank][warp 4..11]:")
+        print(np.median(rel, axis=2).astype(int))
+        print("   last-warp lag median", int(np.median(rel.max(axis=(0, 1)))))
+
+
 if __name__ == "__main__":
     if sys.argv[1] == "run":
         run(*(sys.argv[2:3]))
+    elif sys.argv[1] == "warps":
+        warps(sys.argv[2])
     elif sys.argv[1] == "summary":
         for f in sys.argv[2:]:
             summary(f)
