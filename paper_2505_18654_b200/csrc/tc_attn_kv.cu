@@ -54,6 +54,14 @@ namespace tca {
 #ifndef KV_NS
 #define KV_NS 2
 #endif
+// timing experiments only (`make EXTRA=-DMTGR_KV_DEBUG_BUILD`, then MTGR_KV_DEBUG=bits; results
+// are wrong when set): 1 Y does not wait for G, 2 X writes no G, 4 Y stores no dS^T, 8 X ignores
+// ring reuse, 16 X skips the softmax math.  Compiled out otherwise (the branches cost registers)
+#ifdef MTGR_KV_DEBUG_BUILD
+#define KV_DBG(bit) (ks.dbg & (bit))
+#else
+#define KV_DBG(bit) false
+#endif
 constexpr int KV_NG_MAX = 32;       // G ring depth (tiles) per CTA: ks.ng <= this (MTGR_KV_NG)
 constexpr int KV_THREADS = 384;     // 12 warps (13 would round the register budget to 16 warps')
 constexpr int KV_EXIT = 1 << 30;    // per-warp counter flag: the warp has left its item loop
@@ -577,7 +585,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KV_THREADS, 1)
                 gw[(e0 + e) >> 1] = pack_h2(d2.x, d2.y);
               }
             };
-            if (ks.dbg & 16) {  // timing experiment: no softmax math
+            if (KV_DBG(16)) {  // timing experiment: no softmax math
               tmem_ld_wait();
 #pragma unroll
               for (int e = 0; e < 16; ++e) { pk[e] = sa[e]; gw[e] = sb[e]; }
@@ -597,9 +605,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KV_THREADS, 1)
             __syncwarp();
             if (lane == 0 && t > 0) st_release_cta_smem(&wcnt[sw], gt);
             // G piece -> ring slot gt % NG (free once Y consumed tile gt - NG)
-            if (gt >= ks.ng && !(ks.dbg & 8))
+            if (gt >= ks.ng && !KV_DBG(8))
               while (*reinterpret_cast<volatile int*>(cons_ok) < gt - ks.ng + 1) __nanosleep(32);
-            if (!(ks.dbg & 2)) {
+            if (!KV_DBG(2)) {
 #pragma unroll
               for (int c = 0; c < 4; ++c)
                 gp[c * 32 + lane] = make_uint4(gw[4 * c], gw[4 * c + 1], gw[4 * c + 2], gw[4 * c + 3]);
@@ -610,7 +618,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KV_THREADS, 1)
             }
           } else {
             // ---------------- Y: dS^T = dP^T (.) G for the dK MMA and the dQ GEMM
-            if (ready < gt + 1 && !(ks.dbg & 1)) {  // X's count, mirrored by the sync thread
+            if (ready < gt + 1 && !KV_DBG(1)) {  // X's count, mirrored by the sync thread
               int v;
               while ((v = ld_acquire_cta_smem(gready)) < gt + 1) __nanosleep(32);
               ready = v;
@@ -656,13 +664,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KV_THREADS, 1)
               oth.v[i] = __shfl_xor_sync(0xffffffffu, b ? pk[i] : pk[8 + i], 1);
             }
             __nv_bfloat16* p0 = a.st_ds + st_row + cb + 16 * b;
-            if (!(ks.dbg & 4)) {
+            if (!KV_DBG(4)) {
               stg256(p0 - (int64_t)b * a.st_pitch, b ? oth : own);
               stg256(p0 + (int64_t)(1 - b) * a.st_pitch, b ? own : oth);
             }
             // prefetch the next tile's G when it is already published (its L2 latency then hides
             // behind this tile's tail and the next score wait)
-            if (t + 1 < it.ntiles && !(ks.dbg & 1)) {
+            if (t + 1 < it.ntiles && !KV_DBG(1)) {
               if (ready < gt + 2) ready = ld_acquire_cta_smem(gready);
               if (ready >= gt + 2) {
                 const uint4* gn = gring + ((size_t)((gt + 1) & (ks.ng - 1)) * NSM + sw) * 128;
