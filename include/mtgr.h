@@ -185,9 +185,10 @@ mtgr_status_t mtgr_gln_bwd(const mtgr_layer_cfg_t* cfg, const mtgr_jagged_t* jag
  * q, k, v, u: [T] rows with leading dimension ld elements (ld % 8 == 0, 16-byte aligned
  * pointers); head h occupies columns [h*d_h, (h+1)*d_h).  o, y: [T][d] (ld d).
  * u == NULL: no gate, y ignored.  Otherwise y = o (.) u (Eq.6 gate).
- * bf16 path: the tcgen05 kernels only, d_h = 256 (Table 2's 512/2 and 768/3) and
- * rab off; any other bf16 configuration returns MTGR_E_UNSUPPORTED before launching anything
- * (there is no fallback).  fp32 path: SIMT kernels, d_h a multiple of 8 up to 256, rab allowed.
+ * bf16 path: the tcgen05 kernels only, d_h = 256 (Table 2's 512/2 and 768/3), rab
+ * on or off (the bias is added to the fp32 scores in TMEM before SiLU); any other bf16 head dim
+ * returns MTGR_E_UNSUPPORTED before launching anything (there is no fallback).  fp32 path: SIMT
+ * kernels, d_h a multiple of 8 up to 256.
  * Workspace: mtgr_attn_workspace_bytes(). */
 size_t mtgr_attn_workspace_bytes(const mtgr_layer_cfg_t* cfg, const mtgr_jagged_t* jag,
                                  mtgr_dtype_t dtype);

@@ -111,14 +111,13 @@ size_t attn_ws_bytes(int ntok, int H) { return 2 * align_up((size_t)ntok * H * s
 static size_t attn_diag_half(int ntok, int H) { return align_up((size_t)ntok * H * sizeof(float), 256); }
 
 static bool tc_attn_path(const mtgr_layer_cfg_t* c, mtgr_dtype_t dt) {
-  return dt == MTGR_BF16 && c->rab_buckets == 0 && c->n_heads > 0 && attn_tc_supported(c->d_model / c->n_heads);
+  return dt == MTGR_BF16 && c->n_heads > 0 && attn_tc_supported(c->d_model / c->n_heads);
 }
 
-// bf16 attention = the tcgen05 kernels only: head dim 256 (every MTGR config, Table 2)
-// and no rab term (R#4: optional, not part of Eq.5; built on the fp32 path only)
+// bf16 attention = the tcgen05 kernels only: head dim 256 (every MTGR config, Table 2);
+// the optional rab term (R#4) is added inside them (RAB instantiations)
 static mtgr_status_t check_attn_dtype(const mtgr_layer_cfg_t* c, mtgr_dtype_t dt) {
   if (dt != MTGR_BF16) return MTGR_OK;
-  MTGR_CHECK(c->rab_buckets == 0, MTGR_E_UNSUPPORTED, "bf16 attention: rab is supported on the fp32 path only");
   MTGR_CHECK(attn_tc_supported(c->d_model / c->n_heads), MTGR_E_UNSUPPORTED,
              "bf16 attention: head dim %d unsupported (the tensor-core kernels need d_h = 256)",
              c->d_model / c->n_heads);
@@ -158,7 +157,7 @@ static mtgr_status_t run_gemm(const GemmIO& g, int epi, void* ws, size_t wsb, cu
   else return gemm_simt_launch<float>(g, epi, st);
 }
 
-// The bf16 attention runs only on the tensor-core kernels (d_h = 256, no rab); the SIMT kernels
+// The bf16 attention runs only on the tensor-core kernels (d_h = 256); the SIMT kernels
 // are the fp32 parity path.  There is no dispatch between them: check_attn_dtype rejects every
 // other bf16 configuration with MTGR_E_UNSUPPORTED before anything is launched.
 template <class T>

@@ -24,7 +24,7 @@ static double g_ms[PROF_NKINDS];
 static const char* kNames[PROF_NKINDS] = {
     "gln_fwd", "gln_bwd", "gemm_qkvu", "gemm_out", "gemm_dgrad", "gemm_wgrad", "attn_diag",
     "attn_fwd", "attn_bwd_dv", "attn_bwd_dk", "attn_bwd_dq", "colsum", "other", "head", "token", "embed", "attn_bwd_scores",
-    "attn_bwd_dk_fused", "attn_bwd_kv"};
+    "attn_bwd_dk_fused", "attn_bwd_kv", "attn_bwd_drab"};
 
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 

@@ -50,7 +50,7 @@
 namespace mtgr {
 namespace tca {
 
-template <int MODE>
+template <int MODE, bool RAB>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tmC1, const __grid_constant__ CUtensorMap tmC2,
                    const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmR1,
@@ -113,6 +113,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
   uint8_t* smem = smem_raw + ((1024u - (sm100::smem_u32(smem_raw) & 1023u)) & 1023u);
   long long* sTs = reinterpret_cast<long long*>(smem + off_ts(TWO));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + off_bar(TWO));
+  float* sRab = reinterpret_cast<float*>(smem + off_rab(TWO));    // RAB: rab_w[h][0, nb)
+  float* sRacc = reinterpret_cast<float*>(smem + off_racc(TWO));  // RAB, DQ: drab bins of the item
   uint64_t* c1_full = bars;           // [3] leader
   uint64_t* c1_empty = bars + 3;      // [3]
   uint64_t* x_full = bars + 6;        // [3] leader
@@ -530,6 +532,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       ++copied;
     };
     int idx = 0;
+    // RAB, DQ recompute backward: drab bins.  Each thread sums its dS run by run (a run = equal
+    // buckets along its row; the time gaps change bucket rarely), a finished run goes into the
+    // CTA's shared bins, and the bins leave (x nu) to drab at the end of every item
+    const bool acc_drab = RAB && MODE == DQ && a.drab != nullptr;  // uniform
+    int rb = 0;
+    float racc = 0.f;
+    if (acc_drab && threadIdx.x - 128 < 64) sRacc[threadIdx.x - 128] = 0.f;  // ordered by tile 0's barriers
     for (int n = 0;; ++n) {
       const int k = q_read(n);
       __syncwarp();
@@ -550,12 +559,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
 #pragma unroll 1
         for (int t = 0; t < it.ntiles; ++t, ++gt) {
           const int c0 = it.c_begin + t * BC;
-          const bool need_ts = TRANS ? need_ts_rows : (!a.causal && !a.full && c0 + BC > us.ns && c0 < it.kv_end);
+          const bool need_ts = RAB || (TRANS ? need_ts_rows : (!a.causal && !a.full && c0 + BC > us.ns && c0 < it.kv_end));
           long long* tsb = sTs;
           if (need_ts) {  // uniform over the 8 softmax warps
             const int i = threadIdx.x - 128;
             named_bar_sync(1, 32 * NSM);  // everyone is done reading the previous tile's times
             if (i < BC) tsb[i] = (c0 + i < us.L && a.jag.ts) ? a.jag.ts[us.off + c0 + i] : 0;
+            if (RAB && t == 0 && i >= BC && i < BC + a.nb) sRab[i - BC] = a.rab_w[it.h * a.nb + i - BC];
             named_bar_sync(1, 32 * NSM);
           }
           const uint32_t t_s = TWO ? T_S : T_S + 64 * (gt & 1);
@@ -574,6 +584,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
             tc_fence_before();
             arrive_leader(s_free);
           }
+          if constexpr (RAB) add_rab<32>(s, my_ts, tsb + j_half, sRab, a.nb - 1);  // s_ij + rab (R#4)
           // visibility of this warp's 32 columns for this row (dynamic mask, R#8-R#12)
           const int cb = c0 + j_half;
           uint32_t vis;
@@ -657,6 +668,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
             v0 = ((vis >> e) & 1u) ? v0 : 0.f;  // selects, no branch (masked: exact zeros, R#2)
             v1 = ((vis >> (e + 1)) & 1u) ? v1 : 0.f;
             pk[e >> 1] = pack2(v0, v1);
+            if (acc_drab && my < us.L) {  // dS (before nu) of the two entries into this row's bucket runs
+              // (rows past L are the pair's padding: their values are discarded, never summed)
+#pragma unroll
+              for (int h2 = 0; h2 < 2; ++h2) {
+                const int bk = rab_bkt(my_ts - tsb[j_half + e + h2], a.nb - 1);
+                if (bk != rb) {
+                  if (racc != 0.f) atomicAdd(&sRacc[rb], racc);
+                  rb = bk;
+                  racc = 0.f;
+                }
+                racc += h2 ? v1 : v0;
+              }
+            }
           }
           }
           const int tb = gt & 1;
@@ -690,6 +714,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
           }
         }
         if (dbgw) DBG(1, idx);
+        if (acc_drab) {  // the item's bins (x nu: ds carries the user's 1/N, R#5) -> drab[h]
+          if (racc != 0.f) atomicAdd(&sRacc[rb], racc);
+          racc = 0.f;
+          named_bar_sync(1, 32 * NSM);
+          const int i = threadIdx.x - 128;
+          if (i < a.nb) {
+            const float v = sRacc[i];
+            if (v != 0.f) atomicAdd(&a.drab[it.h * a.nb + i], us.nu * v);
+            sRacc[i] = 0.f;  // the next item's first atomics follow its tile 0 barriers
+          }
+        }
         // !TWO: every S MMA of this item has completed: hand the next item's row operand (already
         // in the staging area) to the tensor pipe before draining this item's accumulator.
         // (TWO: the next item's rows are loaded only after this epilogue frees the region.)
@@ -867,9 +902,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
 constexpr int SC_OFF_R1 = 0, SC_OFF_R2 = 64 * KB, SC_OFF_C1 = 128 * KB, SC_OFF_C2 = 176 * KB;
 constexpr int SC_OFF_TS = 224 * KB;
 constexpr int SC_OFF_BAR = SC_OFF_TS + BC * 8;
-constexpr int SC_SMEM_BYTES = 227 * KB;
+constexpr int SC_SMEM_BYTES = SMEM_BYTES;  // the rab weights at off_rab(false) as in FWD / DV
 constexpr int SC_NC = 3;
 
+template <bool RAB>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     attn_sc_kernel(const __grid_constant__ CUtensorMap tmC1, const __grid_constant__ CUtensorMap tmC2,
                    const __grid_constant__ CUtensorMap tmR1, const __grid_constant__ CUtensorMap tmR2, Args a) {
@@ -883,6 +919,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
   uint8_t* smem = smem_raw + ((1024u - (sm100::smem_u32(smem_raw) & 1023u)) & 1023u);
   long long* sTs = reinterpret_cast<long long*>(smem + SC_OFF_TS);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SC_OFF_BAR);
+  float* sRab = reinterpret_cast<float*>(smem + off_rab(false));  // RAB: rab_w[h][0, nb)
   uint64_t* c1_full = bars;        // [3] leader
   uint64_t* c1_empty = bars + 3;   // [3]
   uint64_t* c2_full = bars + 6;    // [3] leader
@@ -1124,7 +1161,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       arrive_leader(r_done);
       }
       const long long my_ts = (my < us.L && a.jag.ts) ? a.jag.ts[(int64_t)us.off + my] : 0;
-      const bool need_ts = !a.causal && !a.full && (it.r0 + BR > us.ns) && (it.r0 < it.kv_end);  // uniform
+      const bool need_ts = RAB || (!a.causal && !a.full && (it.r0 + BR > us.ns) && (it.r0 < it.kv_end));  // uniform
       const int64_t st_row = ((int64_t)it.h * a.st_rows + a.koff[it.u] + my) * a.st_pitch;
 #pragma unroll 1
       for (int t = 0; t < it.ntiles; ++t, ++gt) {
@@ -1134,6 +1171,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
           const int i = threadIdx.x - 128;
           named_bar_sync(1, 32 * NSM);
           if (i < BC) sTs[i] = (c0 + i < us.L && a.jag.ts) ? a.jag.ts[us.off + c0 + i] : 0;
+          if (RAB && t == 0 && i >= BC && i < BC + a.nb) sRab[i - BC] = a.rab_w[it.h * a.nb + i - BC];
           named_bar_sync(1, 32 * NSM);
         }
         mbar_wait(&s_full[b], (gt >> 1) & 1);
@@ -1144,6 +1182,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
         tmem_ld_wait();
         tc_fence_before();
         arrive_leader(&s_free[b]);
+        if constexpr (RAB) add_rab<32>(s, my_ts, sTs + j_half, sRab, a.nb - 1);  // s_ij + rab (R#4)
         const int cb = c0 + j_half;  // this warp's 32 query columns
         uint32_t vis;
         if (a.causal) {  // queries i >= key j, i < L
@@ -1578,6 +1617,72 @@ __global__ void attn_koff_kernel(mtgr_jagged_t j, int causal, int* koff) {
   }
 }
 
+// drab[h][b] = sum over visible (i, j) with bucket(ts_i - ts_j) = b of ds_ij (R#4; the
+// oracle's attn_bwd_user), read back from the stored dS^T of the kv / stored-score backward:
+// one warp per (key token, head) walks the key's visible query range [lo, L) in bf16 pairs,
+// sums its entries run by run (equal buckets), and a finished run goes (x nu, the user's 1/N in
+// ds) into the block's shared bins; the bins leave to drab at the end.  Candidate keys have no
+// off-diagonal entries (their diagonal terms come from the diagonal kernel).
+__global__ void __launch_bounds__(256) attn_drab_kernel(mtgr_jagged_t j, int causal, int full, int nb,
+                                                        const int* koff, const __nv_bfloat16* ds,
+                                                        int64_t pitch, int64_t rows, float* drab) {
+  __shared__ float bins[64];
+  const int h = blockIdx.y, lane = threadIdx.x & 31;
+  if (threadIdx.x < 64) bins[threadIdx.x] = 0.f;
+  __syncthreads();
+  const int tok = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (tok < j.total_tokens) {
+    int lo_u = 0, hi_u = j.num_users - 1;  // the user owning token tok (warp-uniform search)
+    while (lo_u < hi_u) {
+      const int mid = (lo_u + hi_u + 1) >> 1;
+      if (j.offsets[mid] <= tok) lo_u = mid; else hi_u = mid - 1;
+    }
+    const UserSpan us = load_user(j, lo_u);
+    const int kj = tok - us.off;
+    const int kv_end = causal ? us.L : us.ns + us.nr;
+    if (kj < kv_end) {
+      const int64_t ts_j = j.ts ? j.ts[tok] : 0;
+      const int64_t* tsu = j.ts ? j.ts + us.off : nullptr;
+      // visible queries of key kj: causal i >= kj; full / static keys every i; real-time keys
+      // i == kj or (i >= ns and ts_j < ts_i)
+      const int lo = causal ? kj : ((full || kj < us.ns) ? 0 : us.ns);
+      const __nv_bfloat16* row = ds + ((int64_t)h * rows + koff[lo_u] + kj) * pitch;
+      int rb = 0;
+      float racc = 0.f;
+      for (int i0 = (lo & ~1) + 2 * lane; i0 < us.L; i0 += 64) {
+        const __nv_bfloat162 v2 = *reinterpret_cast<const __nv_bfloat162*>(row + i0);
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int i = i0 + e;
+          if (i < lo || i >= us.L) continue;
+          const int64_t ts_i = tsu ? tsu[i] : 0;
+          const bool vis = causal || full || kj < us.ns || i == kj || (i >= us.ns && ts_j < ts_i);
+          if (!vis) continue;
+          const int bk = rab_bkt(ts_i - ts_j, nb - 1);
+          if (bk != rb) {
+            if (racc != 0.f) atomicAdd(&bins[rb], us.nu * racc);
+            rb = bk;
+            racc = 0.f;
+          }
+          racc += __bfloat162float(e ? v2.y : v2.x);
+        }
+      }
+      if (racc != 0.f) atomicAdd(&bins[rb], us.nu * racc);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < nb && bins[threadIdx.x] != 0.f) atomicAdd(&drab[h * nb + threadIdx.x], bins[threadIdx.x]);
+}
+
+static mtgr_status_t launch_drab(const AttnIO& io, const int* koff, const __nv_bfloat16* ds, int64_t pitch,
+                                 int64_t rows, cudaStream_t st) {
+  if (io.nb <= 0 || io.drab == nullptr || io.rab_w == nullptr) return MTGR_OK;
+  ProfScope ps(PROF_ATTN_DRAB, st);
+  dim3 grid(ceil_div(io.jag.total_tokens, 8), io.H);
+  attn_drab_kernel<<<grid, 256, 0, st>>>(io.jag, io.causal, io.full, io.nb, koff, ds, pitch, rows, io.drab);
+  return check_launch("attn_drab");
+}
+
 static int num_sms_cached() {
   static int n = 0;
   if (n == 0) {
@@ -1619,6 +1724,8 @@ static mtgr_status_t launch_mode(const AttnIO& io, const void* c1, int64_t ld_c1
   Args a2 = args;
   a2.causal = io.causal;
   a2.full = io.full;
+  a2.nb = io.nb > 0 && io.rab_w != nullptr ? io.nb : 0;
+  a2.rab_w = io.rab_w;
   // row operand into TMEM by tcgen05.cp from the MMA warp (default) or through the softmax
   // warps' registers (MTGR_ROW_CP=0)
   { const char* x = getenv("MTGR_ROW_CP"); a2.row_cp = !(x != nullptr && x[0] == '0'); }
@@ -1633,13 +1740,15 @@ static mtgr_status_t launch_mode(const AttnIO& io, const void* c1, int64_t ld_c1
   const int pairs = std::max(1, std::min(num_sms_cached() / 2, a2.nitems));
   dim3 grid(2 * pairs, 1, 1);  // persistent CTA pairs
   ProfScope ps(MODE == FWD ? PROF_ATTN_FWD : MODE == DV ? PROF_ATTN_DV : MODE == DK ? PROF_ATTN_DK_FUSED : PROF_ATTN_DQ, st);
-  cudaFuncSetAttribute(attn_tc_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+  // rab on: the instantiation that adds the bias (and reads the timestamps of every tile)
+  auto kern = a2.nb > 0 ? attn_tc_kernel<MODE, true> : attn_tc_kernel<MODE, false>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
   static const bool trace = getenv("MTGR_ATTN_TRACE") != nullptr;
   if (trace) {  // debug only: time-stamp one CTA pair's pipeline events
     cudaMalloc(&a2.dbg, 2 * 20 * 64 * sizeof(long long));
     cudaMemsetAsync(a2.dbg, 0, 2 * 20 * 64 * sizeof(long long), st);
   }
-  attn_tc_kernel<MODE><<<grid, 384, SMEM_BYTES, st>>>(m.c1, m.c2, m.x, m.r1, m.r2, m.e, m.u, m.o, a2);
+  kern<<<grid, 384, SMEM_BYTES, st>>>(m.c1, m.c2, m.x, m.r1, m.r2, m.e, m.u, m.o, a2);
   if (trace) {
     long long hb[2 * 20 * 64];
     cudaMemcpyAsync(hb, a2.dbg, sizeof(hb), cudaMemcpyDeviceToHost, st);
@@ -1718,14 +1827,17 @@ static mtgr_status_t launch_sc(const AttnIO& io, const MmLayout& l, const Args& 
   a2.nitems = io.jag.num_users * a2.pmax * io.H;
   a2.st_pitch = l.pitch; a2.st_rows = l.rows;
   a2.c_align = 1;
+  a2.nb = io.nb > 0 && io.rab_w != nullptr ? io.nb : 0;
+  a2.rab_w = io.rab_w;
   { const char* x = getenv("MTGR_SC_CP"); a2.sc_cp = !(x != nullptr && x[0] == '0'); }  // as MTGR_ROW_CP
   MTGR_CHECK(io.ctr != nullptr, MTGR_E_ARG, "attention: work-queue counters (workspace) missing");
   a2.ctr = io.ctr + 6;
   cudaMemsetAsync(a2.ctr, 0, sizeof(int), st);
   const int pairs = std::max(1, std::min(num_sms_cached() / 2, a2.nitems));
   ProfScope ps(PROF_ATTN_SC, st);
-  cudaFuncSetAttribute(attn_sc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SC_SMEM_BYTES);
-  attn_sc_kernel<<<2 * pairs, 384, SC_SMEM_BYTES, st>>>(tc1, tc2, tr1, tr2, a2);
+  auto kern = a2.nb > 0 ? attn_sc_kernel<true> : attn_sc_kernel<false>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SC_SMEM_BYTES);
+  kern<<<2 * pairs, 384, SC_SMEM_BYTES, st>>>(tc1, tc2, tr1, tr2, a2);
   return check_launch("attn_sc");
 }
 
@@ -1810,7 +1922,8 @@ mtgr_status_t attn_tc_bwd_launch(const AttnIO& io, cudaStream_t st) {
       a.out = (bf*)io.dq; a.ld_out = io.ld_out; a.diag = io.diag_ds;
       a.dbias = io.dbias;
       a.koff = koff;
-      return launch_mm<MM_DQ>(io, kds, io.k, io.ld, io.k, io.ld, pre, io.ld_pre, l, a, PROF_ATTN_DQ, st);
+      MTGR_TRY(launch_mm<MM_DQ>(io, kds, io.k, io.ld, io.k, io.ld, pre, io.ld_pre, l, a, PROF_ATTN_DQ, st));
+      return launch_drab(io, koff, kds, l.pitch, l.rows, st);
     }
     if (path == 2) {  // dK = nu dS^T Q (+ diag), * silu'(p_K); also stores P^T, dS^T
       Args a{};
@@ -1855,7 +1968,7 @@ mtgr_status_t attn_tc_bwd_launch(const AttnIO& io, cudaStream_t st) {
       a.koff = koff;
       MTGR_TRY(launch_mm<MM_DQ>(io, sds, io.k, io.ld, io.k, io.ld, pre, io.ld_pre, l, a, PROF_ATTN_DQ, st));
     }
-    return MTGR_OK;
+    return launch_drab(io, koff, sds, l.pitch, l.rows, st);
   }
   {  // dV = nu P^T dO (+ diag a_jj dO_j), * silu'(p_V): C1 = Q, X = dO, R1 = K, E = dO, U = p_V
     Args a{};
@@ -1878,6 +1991,7 @@ mtgr_status_t attn_tc_bwd_launch(const AttnIO& io, cudaStream_t st) {
     a.jag = io.jag; a.H = io.H; a.d = io.d;
     a.out = (bf*)io.dq; a.ld_out = io.ld_out; a.diag = io.diag_ds;
     a.dbias = io.dbias;
+    a.drab = io.nb > 0 ? io.drab : nullptr;  // drab summed inside the DQ kernel (no stored dS)
     MTGR_TRY(launch_mode<DQ>(io, io.k, io.ld, io.v, io.ld, io.q, io.ld, io.dO, D, io.k, io.ld, pre,
                              io.ld_pre, a, st));
   }

@@ -20,7 +20,10 @@ constexpr int RT_BYTES = BR * DH * 2;   // 64 KB: 4 boxes {64 dh, 128 rows}
 // (!TWO) / after the dbias scratch [208,216) KB (TWO)
 constexpr int off_ts(bool two) { return (two ? 216 : 224) * KB; }
 constexpr int off_bar(bool two) { return off_ts(two) + BC * 8; }
-constexpr int SMEM_BYTES = off_bar(false) + 512 + 1024;
+// after the barriers: the item's rab weights rab_w[h][0, nb) and the drab bins (fp32 x 64 each)
+constexpr int off_rab(bool two) { return off_bar(two) + 512; }
+constexpr int off_racc(bool two) { return off_rab(two) + 256; }
+constexpr int SMEM_BYTES = off_racc(false) + 256 + 1024;
 constexpr int NSM = 8;  // softmax/epilogue warps
 
 enum { FWD = 0, DV = 1, DQ = 2, DK = 3 };
@@ -49,6 +52,9 @@ struct Args {
   int row_cp;                               // FWD / DV: row operand via tcgen05.cp
   int c_align;                              // TRANS items of real-time keys start their query
                                             // range at the 256-aligned pair holding n_static
+  // relative-attention bias (R#4; kernels instantiated with RAB): s_ij += rab_w[h][bucket(ts_i -
+  // ts_j)]; drab (DQ only, the recompute backward) accumulates nu * dS per bucket
+  const float* rab_w; float* drab; int nb;
 };
 
 // debug tracing (MTGR_ATTN_TRACE=1) of the CTA pair of cluster 1: slot layout [event][item]
@@ -58,6 +64,21 @@ struct Args {
 #define DBG_ON (a.dbg != nullptr && (blockIdx.x >> 1) == 1)
 #define DBGV(ev, i, val) do { if (DBG_ON && (i) < 64) a.dbg[(blockIdx.x & 1) * 20 * 64 + (ev) * 64 + (i)] = (val); } while (0)
 #define DBG(ev, i) DBGV(ev, i, clock64())
+
+// rab bucket (R#4): min(nb - 1, floor(log2(max(|dt|, 1)))); nb1 = nb - 1.  |dt| | 1 has the
+// same floor(log2) as max(|dt|, 1) for every |dt| (0 and 1 both map to bucket 0)
+__device__ __forceinline__ int rab_bkt(long long dt, int nb1) {
+  const unsigned long long x = (unsigned long long)(dt < 0 ? -dt : dt) | 1ull;
+  return min(63 - __clzll((long long)x), nb1);
+}
+// s[e] += w[bucket(ts_row - ts_col[e])] for n score values of one row (fp32 bit patterns)
+template <int N>
+__device__ __forceinline__ void add_rab(uint32_t* s, long long ts_row, const long long* ts_col,
+                                        const float* w, int nb1) {
+#pragma unroll
+  for (int e = 0; e < N; ++e)
+    s[e] = __float_as_uint(__uint_as_float(s[e]) + w[rab_bkt(ts_row - ts_col[e], nb1)]);
+}
 
 __device__ __forceinline__ float silu_fast(float s) {
   const float h = 0.5f * s;

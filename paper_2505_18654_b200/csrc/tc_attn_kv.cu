@@ -127,6 +127,7 @@ __device__ __forceinline__ uint32_t pack_h2(float a, float b) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
+template <bool RAB>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KV_THREADS, 1)
     attn_kv_kernel(const __grid_constant__ CUtensorMap xC1, const __grid_constant__ CUtensorMap xX,
                    const __grid_constant__ CUtensorMap xR1, const __grid_constant__ CUtensorMap xU,
@@ -164,6 +165,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KV_THREADS, 1)
   uint8_t* smem = smem_raw + ((1024u - (sm100::smem_u32(smem_raw) & 1023u)) & 1023u);
   long long* sTs = reinterpret_cast<long long*>(smem + off_ts(false));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + off_bar(false));
+  float* sRab = reinterpret_cast<float*>(smem + off_rab(false));  // RAB (X): rab_w[h][0, nb)
   uint64_t* c1_full = bars;           // [3] leader
   uint64_t* c1_empty = bars + 3;      // [3]
   uint64_t* x_full = bars + 6;        // [3] leader
@@ -523,7 +525,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KV_THREADS, 1)
         const long long my_ts = (role == 0 && my < us.L && a.jag.ts) ? a.jag.ts[g] : 0;
         // stored dS^T row of this key (Y): [h][koff[u] + my][query]
         const int64_t st_row = role ? ((int64_t)it.h * a.st_rows + a.koff[it.u] + my) * a.st_pitch : 0;
-        const bool need_ts = role == 0 && !a.causal && a.full == 0 && (it.r0 + BR > us.ns) && (it.r0 < it.kv_end);
+        const bool need_ts = role == 0 && (RAB || (!a.causal && a.full == 0 && (it.r0 + BR > us.ns) && (it.r0 < it.kv_end)));
 #pragma unroll 1
         for (int t = 0; t < it.ntiles; ++t, ++gt) {
           const int c0 = it.c_begin + t * BC;
@@ -536,6 +538,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KV_THREADS, 1)
               const int i = threadIdx.x - 128;
               named_bar_sync(1, 32 * NSM);
               if (i < BC) sTs[i] = (c0 + i < us.L && a.jag.ts) ? a.jag.ts[us.off + c0 + i] : 0;
+              if (RAB && t == 0 && i >= BC && i < BC + a.nb) sRab[i - BC] = a.rab_w[it.h * a.nb + i - BC];
               named_bar_sync(1, 32 * NSM);
             }
             const int tb = gt % NS;
@@ -590,8 +593,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KV_THREADS, 1)
 #pragma unroll
               for (int e = 0; e < 16; ++e) { pk[e] = sa[e]; gw[e] = sb[e]; }
             } else {
+              if constexpr (RAB) add_rab<16>(sa, my_ts, sTs + j_half, sRab, a.nb - 1);  // s + rab (R#4)
               half16(sa, 0);
               tmem_ld_wait();
+              if constexpr (RAB) add_rab<16>(sb, my_ts, sTs + j_half + 16, sRab, a.nb - 1);
               half16(sb, 16);
             }
             tmem_st16(tmem + T_S + 64 * tb + j_half + lane_off, pk);  // in place (this warp's S)
@@ -906,9 +911,13 @@ mtgr_status_t attn_kv_launch(const AttnIO& io, const tca::Args& ax_in, const tca
   }
   cudaMemsetAsync(w, 0, flag_bytes, st);
   cudaMemsetAsync(ax.ctr, 0, sizeof(int), st);
+  // rab on (X role adds the bias; drab: attn_drab_kernel over the stored dS^T afterwards)
+  ax.nb = io.nb > 0 && io.rab_w != nullptr ? io.nb : 0;
+  ax.rab_w = io.rab_w;
   ProfScope ps(PROF_ATTN_KV, st);
-  cudaFuncSetAttribute(attn_kv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, KV_SMEM_BYTES);
-  attn_kv_kernel<<<4 * nc, KV_THREADS, KV_SMEM_BYTES, st>>>(xc1, xx, xr1, xu, xo, yc1, yx, yr1, yu, yo, ax, ay, ks);
+  auto kern = ax.nb > 0 ? attn_kv_kernel<true> : attn_kv_kernel<false>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, KV_SMEM_BYTES);
+  kern<<<4 * nc, KV_THREADS, KV_SMEM_BYTES, st>>>(xc1, xx, xr1, xu, xo, yc1, yx, yr1, yu, yo, ax, ay, ks);
   if (trace) {
     std::vector<long long> hb(trn);
     cudaMemcpyAsync(hb.data(), ks.trace, trn * sizeof(long long), cudaMemcpyDeviceToHost, st);

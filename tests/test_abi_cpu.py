@@ -58,13 +58,13 @@ def test_host_side_argument_errors():
 
 
 def test_bf16_attention_unsupported_configs_rejected():
-    """The bf16 attention runs only on the tcgen05 kernels (d_h = 256, rab off): any other bf16
-    configuration is MTGR_E_UNSUPPORTED (7) at the host checks, before any launch (no SIMT
+    """The bf16 attention runs only on the tcgen05 kernels (d_h = 256; rab on or off): any other
+    bf16 head dim is MTGR_E_UNSUPPORTED (7) at the host checks, before any launch (no SIMT
     fallback); the same configurations are accepted on the fp32 path's checks."""
     L = lib()
     j = Jagged(0, 0, 0, None, None, None, None, None, None, None)
     for cfg in (LayerCfg(512, 4, 4, 0, 1e-6, 1),     # d_h 128
-                LayerCfg(512, 2, 4, 16, 1e-6, 1)):   # rab on
+                LayerCfg(256, 2, 4, 16, 1e-6, 1)):   # d_h 128, rab on
         st = L.mtgr_hstu_attn_fwd(ctypes.byref(cfg), ctypes.byref(j), 1, None, None, None, 512, None,
                                   None, None, None, None, 0, None)
         assert st == 7, st

@@ -252,6 +252,66 @@ def test_layer_rab_fp32(dev):
     _compare(z, dx, grads, Z, dX, G, 1e-4)
 
 
+@pytest.mark.parametrize("mask", ["dynamic", "causal", "full"])
+@pytest.mark.parametrize("name", ["parity", "parity768"])
+def test_attention_rab_bf16(dev, name, bwd_path, mask):
+    """The rab term (R#4) on the tcgen05 kernels: o, y, dq, dk, dv and drab against the oracle
+    (drab: the kv / stored paths sum the stored dS^T, the recompute path inside the DQ kernel).
+    rab_w ~ 8 N(0, 1) over 16 buckets (the synthetic time gaps, seconds within the real-time hour
+    up to months to the static items, fill buckets 0..11 and the capped 15), large enough that a
+    wrong bucket, sign or missing term moves the outputs far beyond the tolerance (checked: the
+    outputs without rab differ from the oracle's by > 10x the tolerance; 0.42 on "parity")."""
+    cfg, seg, ts, qkvu, dO = _attn_case(name)
+    dt = _dt(cfg)
+    d, H, NB = cfg["d"], cfg["H"], 16
+    rab = (8.0 * np.random.default_rng(5).standard_normal((H, NB))).astype(np.float32)
+    jb = m.JaggedBatch.build(seg, ts, dev)
+    lc = m.layer_cfg(d, H, rab_buckets=NB, mask_mode=mask)
+    a = _t(qkvu, dev, dt)
+    rw = torch.from_numpy(rab).to(dev)
+    o, y = m.attn_fwd(lc, jb, a[:, 0:], a[:, d:], a[:, 2 * d:], 4 * d, u=a[:, 3 * d:], rab_w=rw)
+    dq, dk, dv, drab = m.attn_bwd(lc, jb, _t(dO, dev, dt), a[:, 0:], a[:, d:], a[:, 2 * d:], 4 * d, rab_w=rw)
+    h = oracle.build_jagged(seg)
+    got = dict(o=o, y=y, dq=dq, dk=dk, dv=dv)
+    got = {k: v.float().cpu().numpy() for k, v in got.items()}
+    ref = {k: np.zeros_like(got[k], dtype=np.float64) for k in got}
+    ref_norab = np.zeros_like(got["o"], dtype=np.float64)
+    rdrab = np.zeros((H, NB))
+    for u in range(len(seg)):
+        s, e = h["offsets"][u], h["offsets"][u + 1]
+        if e == s:
+            continue
+        ns, nr, nc = int(h["n_static"][u]), int(h["n_rt"][u]), int(h["n_cand"][u])
+        q, k, v, uu = (qkvu[s:e, i * d:(i + 1) * d].astype(np.float64) for i in range(4))
+        nu = 1.0 / (e - s)
+        oo, S, M = oracle.attn_fwd_user(q, k, v, ns, nr, nc, ts[s:e], H, nu, rab_w=rab.astype(np.float64),
+                                        mask_mode=mask)
+        ref["o"][s:e] = oo
+        ref["y"][s:e] = oo * uu
+        ref_norab[s:e] = oracle.attn_fwd_user(q, k, v, ns, nr, nc, ts[s:e], H, nu, mask_mode=mask)[0]
+        dq_, dk_, dv_, dr = oracle.attn_bwd_user(dO[s:e].astype(np.float64), q, k, v, S, M, H, nu, ts[s:e],
+                                                 rab.astype(np.float64))
+        ref["dq"][s:e], ref["dk"][s:e], ref["dv"][s:e] = dq_, dk_, dv_
+        rdrab += dr
+    assert rel_err(ref_norab, ref["o"]) > 10 * TOL[dt]  # the rab term is not negligible here
+    errs = {k: rel_err(got[k], ref[k]) for k in got}
+    errs["drab"] = rel_err(drab.cpu().numpy(), rdrab)
+    bad = {k: e for k, e in errs.items() if not e <= TOL[dt]}
+    assert not bad, (bad, errs)
+
+
+@pytest.mark.parametrize("name", ["parity", "parity768"])
+def test_layer_rab_bf16(dev, name, bwd_path):
+    """A whole bf16 layer with rab on (R#4): z, dX and every parameter gradient incl. d rab_w."""
+    cfg, seg, ts, X, dZ, P = make_batch(name, rab_buckets=16)
+    P = dict(P, rab_w=(10.0 * P["rab_w"]).astype(np.float32))  # ~N(0, 1): a visible term
+    z, dx, grads = _run_layer(dev, cfg, seg, ts, X, dZ, P)
+    Z, dX, G = _oracle_stack(cfg, seg, ts, X, dZ, [P])
+    errs = _compare(z, dx, grads, Z, dX, G, TOL[_dt(cfg)])
+    assert "L0.drab_w" in errs
+    print(errs)
+
+
 def test_stack_three_layers_bf16(dev):
     import synth
     cfg, seg, ts, X, dZ, P = make_batch("parity")
