@@ -56,6 +56,8 @@ def parse():
                     help="step = stack fwd + candidate head/BCE (SURVEY f2) + stack bwd from the head's dZ")
     ap.add_argument("--balance", default="tokens", choices=["tokens", "flops"],
                     help="LPT cost: token count (R#19, default) or per-user FLOPs (SURVEY f3)")
+    ap.add_argument("--rab", type=int, default=0, metavar="NB",
+                    help="optional relative-time bias with NB buckets (R#4; 0 = Eq.5 exactly, MTGR)")
     ap.add_argument("--no-large-attn", action="store_true",
                     help="skip the MTGR-large attention sub-record (one large layer fwd+bwd, N=1 only)")
     return ap.parse_args()
@@ -225,7 +227,7 @@ def time_oracle(cfg, wl, n_users, start=0):
     import oracle
     ocfg = dict(d=cfg["d"], H=cfg["H"], mask_mode=cfg.get("mask_mode", "dynamic"),
                 post_mlp_layers=cfg.get("post_mlp_layers", 1))
-    Ps = [synth.gen_layer_params(cfg, li) for li in range(cfg["n_layers"])]
+    Ps = [synth.gen_layer_params(cfg, li, cfg.get("rab_buckets", 0)) for li in range(cfg["n_layers"])]
     tok, secs = 0, 0.0
     for k in range(n_users):
         idx = (start + k) % len(wl["users"])
@@ -262,6 +264,7 @@ def workload_desc(cfg, wl, world):
             "balancer": "FLOP-cost LPT" if wl.get("balance") == "flops" else "token-count LPT",
             "mask": cfg.get("mask_mode", "dynamic"),
             "post_mlp_layers": cfg.get("post_mlp_layers", 1),
+            "rab_buckets": cfg.get("rab_buckets", 0),
             "l2": "no flush: per-step activations are several GB (>> 126 MB L2)"}
 
 
@@ -309,9 +312,9 @@ def run_mtgr(args, cfg, rank, world, local_rank):
     X = np.concatenate([synth.gen_user_x(cfg, int(u), int(l)) for u, l in zip(users, Ls)])
     dZ = np.concatenate([synth.gen_user_dz(cfg, int(u), int(l)) for u, l in zip(users, Ls)])
     jb = m.JaggedBatch.build(wl["seg"], ts, dev, users=users)
-    lc = m.layer_cfg(cfg["d"], cfg["H"], cfg["groups"], mask_mode=cfg.get("mask_mode", "dynamic"),
-                     post_mlp_layers=cfg.get("post_mlp_layers", 1))
-    Ps = [m.params_to_device(synth.gen_layer_params(cfg, li), dt, dev) for li in range(cfg["n_layers"])]
+    lc = m.layer_cfg(cfg["d"], cfg["H"], cfg["groups"], cfg.get("rab_buckets", 0),
+                     mask_mode=cfg.get("mask_mode", "dynamic"), post_mlp_layers=cfg.get("post_mlp_layers", 1))
+    Ps = [m.params_to_device(synth.gen_layer_params(cfg, li, cfg.get("rab_buckets", 0)), dt, dev) for li in range(cfg["n_layers"])]
     stack = m.HstuStack(lc, Ps, dt, dev)
     stack.bind(jb)
     x_dev = torch.from_numpy(X).to(dev, dt)
@@ -358,7 +361,7 @@ def run_mtgr(args, cfg, rank, world, local_rank):
         lab = np.concatenate([synth.gen_user_labels(cfg, int(u), int(l)) for u, l in zip(users, Ls)])
         uids = np.concatenate([i["u"].reshape(-1) for i in ids])
         iids = np.concatenate([np.concatenate([i[t].reshape(-1) for i in ids]) for t in "src"])
-        model = m.MTGRModel(cfg, lc, [synth.gen_layer_params(cfg, li) for li in range(cfg["n_layers"])],
+        model = m.MTGRModel(cfg, lc, [synth.gen_layer_params(cfg, li, cfg.get("rab_buckets", 0)) for li in range(cfg["n_layers"])],
                             synth.gen_token_params(cfg), synth.gen_head_params(cfg), synth.token_widths(cfg),
                             synth.EMB_DIM, dt, dev, cap_user=1 << 20, cap_item=1 << 23,
                             n_users_global=wl["B_g"])
@@ -525,7 +528,7 @@ def run_large_attention(torch, m, dev, pk, layers=1, steps=3, warmup=2):
     dZ = np.concatenate([synth.gen_user_dz(cfg, int(u), int(l)) for u, l in zip(users, Ls)])
     jb = m.JaggedBatch.build(wl["seg"], ts, dev, users=users)
     lc = m.layer_cfg(cfg["d"], cfg["H"], cfg["groups"])
-    stack = m.HstuStack(lc, [m.params_to_device(synth.gen_layer_params(cfg, li), dt, dev)
+    stack = m.HstuStack(lc, [m.params_to_device(synth.gen_layer_params(cfg, li, cfg.get("rab_buckets", 0)), dt, dev)
                              for li in range(layers)], dt, dev)
     stack.bind(jb)
     x = torch.from_numpy(X).to(dev, dt)
@@ -670,7 +673,7 @@ def main():
         print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}: launch one rank per GPU "
               f"(torchrun --nproc-per-node {args.gpus}) or drop --gpus", file=sys.stderr)
         sys.exit(2)
-    cfg = synth.config(args.config, mask_mode=args.mask, post_mlp_layers=args.post_mlp)
+    cfg = synth.config(args.config, mask_mode=args.mask, post_mlp_layers=args.post_mlp, rab_buckets=args.rab)
     if args.impl == "reference":
         run_reference(args, cfg, rank, world)
         return

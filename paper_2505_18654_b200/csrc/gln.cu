@@ -72,12 +72,20 @@ __device__ __forceinline__ float warp_sum(float v) {
 }
 
 // One warp per token over a CONTIGUOUS token range per warp (tokens of a group are contiguous
-// within a user, so gamma / beta of the current group stay in registers and are reloaded only on
-// a group change: the per-token traffic is the token's own rows, not 2d fp32 parameters through
-// L1).  Software pipelined: the next token's rows (and group id) are in flight while this one is
-// reduced, normalised and stored.
-template <class T, int NC>
-__global__ void __launch_bounds__(256) gln_fwd_kernel(const T* __restrict__ x,
+// within a user, so gamma / beta of the current group are reloaded only on a group change: the
+// per-token traffic is the token's own rows, not 2d fp32 parameters through L1).  Software
+// pipelined: the next token's rows (and group id) are in flight while this one is reduced,
+// normalised and stored.  The current group's gamma / beta live in a per-warp shared-memory slot
+// (each lane reads back only the chunks it wrote, float4-interleaved: conflict-free) instead of
+// 16 registers per chunk, so the kernel fits MINB 256-thread blocks per SM: the resident warps,
+// each with two tokens in flight, are what keeps enough bytes in flight for HBM.
+template <class T, int NC, bool GATE> constexpr int gln_fwd_minb() {
+  return sizeof(T) == 2 ? (NC <= 2 ? (GATE ? 2 : 3) : (NC == 3 ? 2 : 1)) : (NC <= 1 ? 3 : (NC == 2 ? 2 : 1));
+}
+template <int NC> constexpr int gln_fwd_smem() { return 8 * NC * 2 * 2 * 32 * 16; }  // 8 warps
+
+template <class T, int NC, bool GATE>
+__global__ void __launch_bounds__(256, gln_fwd_minb<T, NC, GATE>()) gln_fwd_kernel(const T* __restrict__ x,
                                                       const uint8_t* __restrict__ gid,
                                                       const float* __restrict__ gamma,
                                                       const float* __restrict__ beta,
@@ -85,24 +93,27 @@ __global__ void __launch_bounds__(256) gln_fwd_kernel(const T* __restrict__ x,
                                                       float* __restrict__ rstd, int ntok, int d,
                                                       float eps, const T* __restrict__ gate,
                                                       int64_t ld_gate, int tok_per_warp) {
+  extern __shared__ float4 gln_sp[];
   const int lane = threadIdx.x & 31;
   const int nch = d >> 3;
   const float inv_d = 1.0f / (float)d;
   const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  // this warp's slot: [k][gamma lo, gamma hi, beta lo, beta hi][lane] float4
+  float4* gb = gln_sp + (threadIdx.x >> 5) * (NC * 4 * 32) + lane;
   const int t_begin = w * tok_per_warp;
   const int t_end = min(ntok, t_begin + tok_per_warp);
-  Raw8<T> cx[NC], cg[NC], nx[NC], ng[NC];
+  Raw8<T> cx[NC], nx[NC];
+  Raw8<T> cg[GATE ? NC : 1], ng[GATE ? NC : 1];
   auto issue = [&](int tt, Raw8<T>* xa, Raw8<T>* ga) {
 #pragma unroll
     for (int k = 0; k < NC; ++k) {
       const int c = lane + 32 * k;
       if (c < nch) {
         rload(x + (int64_t)tt * d + c * 8, xa[k]);
-        if (gate != nullptr) rload(gate + (int64_t)tt * ld_gate + c * 8, ga[k]);
+        if constexpr (GATE) rload(gate + (int64_t)tt * ld_gate + c * 8, ga[k]);
       }
     }
   };
-  float gg[NC][8], bb[NC][8];
   int g_loaded = -1;
   int t = t_begin;
   int g_cur = 0;
@@ -111,13 +122,15 @@ __global__ void __launch_bounds__(256) gln_fwd_kernel(const T* __restrict__ x,
     const int tn = t + 1;
     int g_next = 0;
     if (tn < t_end) { issue(tn, nx, ng); g_next = gid[tn]; }
-    if (g_cur != g_loaded) {  // group change: this group's affine parameters into registers
+    if (g_cur != g_loaded) {  // group change: this group's affine parameters into the slot
 #pragma unroll
       for (int k = 0; k < NC; ++k) {
         const int c = lane + 32 * k;
         if (c < nch) {
-          load8(gamma + (int64_t)g_cur * d + c * 8, gg[k]);
-          load8(beta + (int64_t)g_cur * d + c * 8, bb[k]);
+          const float4* gp = reinterpret_cast<const float4*>(gamma + (int64_t)g_cur * d + c * 8);
+          const float4* bp = reinterpret_cast<const float4*>(beta + (int64_t)g_cur * d + c * 8);
+          gb[(k * 4 + 0) * 32] = gp[0]; gb[(k * 4 + 1) * 32] = gp[1];
+          gb[(k * 4 + 2) * 32] = bp[0]; gb[(k * 4 + 3) * 32] = bp[1];
         }
       }
       g_loaded = g_cur;
@@ -129,7 +142,7 @@ __global__ void __launch_bounds__(256) gln_fwd_kernel(const T* __restrict__ x,
       int c = lane + 32 * k;
       if (c < nch) {
         unpack(cx[k], v[k]);
-        if (gate != nullptr) {  // input = x (.) gate (Eq.6 gate folded into the norm's load)
+        if constexpr (GATE) {  // input = x (.) gate (Eq.6 gate folded into the norm's load)
           float gv[8];
           unpack(cg[k], gv);
 #pragma unroll
@@ -157,9 +170,13 @@ __global__ void __launch_bounds__(256) gln_fwd_kernel(const T* __restrict__ x,
     for (int k = 0; k < NC; ++k) {
       int c = lane + 32 * k;
       if (c < nch) {
+        const float4 g0 = gb[(k * 4 + 0) * 32], g1 = gb[(k * 4 + 1) * 32];
+        const float4 b0 = gb[(k * 4 + 2) * 32], b1 = gb[(k * 4 + 3) * 32];
+        const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+        const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
         float o[8];
 #pragma unroll
-        for (int e = 0; e < 8; ++e) o[e] = gg[k][e] * ((v[k][e] - mu) * r) + bb[k][e];
+        for (int e = 0; e < 8; ++e) o[e] = gg[e] * ((v[k][e] - mu) * r) + bb[e];
         store8(yr + c * 8, o);
       }
     }
@@ -168,7 +185,10 @@ __global__ void __launch_bounds__(256) gln_fwd_kernel(const T* __restrict__ x,
       if (rstd) rstd[t] = r;
     }
 #pragma unroll
-    for (int k = 0; k < NC; ++k) { cx[k] = nx[k]; cg[k] = ng[k]; }
+    for (int k = 0; k < NC; ++k) {
+      cx[k] = nx[k];
+      if constexpr (GATE) cg[k] = ng[k];
+    }
     g_cur = g_next;
   }
 }
@@ -596,12 +616,15 @@ template <class T, int NC>
 static void gln_fwd_go(const T* x, const uint8_t* gid, const float* gamma, const float* beta, T* y,
                        float* mean, float* rstd, int ntok, int d, float eps, const T* gate,
                        int64_t ld_gate, cudaStream_t st) {
-  // ~8 resident 256-thread blocks per SM (64 warps), each warp a contiguous run of tokens
-  const int warps = 8 * 8 * num_sms();
+  // MINB resident 256-thread blocks per SM, each warp a contiguous run of tokens
+  constexpr int smem = gln_fwd_smem<NC>();
+  const int minb = gate != nullptr ? gln_fwd_minb<T, NC, true>() : gln_fwd_minb<T, NC, false>();
+  const int warps = 8 * minb * num_sms();
   const int tpw = std::max(1, ceil_div(ntok, warps));
   const int blocks = ceil_div(ceil_div(ntok, tpw), 8);
-  gln_fwd_kernel<T, NC><<<blocks, 256, 0, st>>>(x, gid, gamma, beta, y, mean, rstd, ntok, d, eps,
-                                                gate, ld_gate, tpw);
+  auto kern = gate != nullptr ? gln_fwd_kernel<T, NC, true> : gln_fwd_kernel<T, NC, false>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  kern<<<blocks, 256, smem, st>>>(x, gid, gamma, beta, y, mean, rstd, ntok, d, eps, gate, ld_gate, tpw);
 }
 
 template <class T>

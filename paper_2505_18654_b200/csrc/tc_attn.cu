@@ -1618,68 +1618,116 @@ __global__ void attn_koff_kernel(mtgr_jagged_t j, int causal, int* koff) {
 }
 
 // drab[h][b] = sum over visible (i, j) with bucket(ts_i - ts_j) = b of ds_ij (R#4; the
-// oracle's attn_bwd_user), read back from the stored dS^T of the kv / stored-score backward:
-// one warp per (key token, head) walks the key's visible query range [lo, L) in bf16 pairs,
-// sums its entries run by run (equal buckets), and a finished run goes (x nu, the user's 1/N in
-// ds) into the block's shared bins; the bins leave to drab at the end.  Candidate keys have no
-// off-diagonal entries (their diagonal terms come from the diagonal kernel).
+// oracle's attn_bwd_user), read back from the stored dS^T of the kv / stored-score backward.
+// A block owns 64 consecutive padded key rows [koff[u] + 64c, +64) of one head (a user's block
+// of rows is a multiple of 256, so a chunk never spans two users; one search for u per block,
+// the user's timestamps staged in shared memory), each warp 8 of them: the key's visible query
+// range [lo, L) in lane-interleaved bf16 pairs (coalesced; 8 pairs in flight), summed run by run (equal buckets: the time gaps along a row change
+// bucket rarely) and each finished run (x nu, the user's 1/N in ds) into the block's shared bins,
+// which leave to drab at the end.  Candidate keys have no off-diagonal entries (their diagonal
+// terms come from the diagonal kernel).
+constexpr int DRAB_TS_CAP = 8192;  // query chunk whose timestamps are staged in smem
+
 __global__ void __launch_bounds__(256) attn_drab_kernel(mtgr_jagged_t j, int causal, int full, int nb,
                                                         const int* koff, const __nv_bfloat16* ds,
                                                         int64_t pitch, int64_t rows, float* drab) {
-  __shared__ float bins[64];
-  const int h = blockIdx.y, lane = threadIdx.x & 31;
-  if (threadIdx.x < 64) bins[threadIdx.x] = 0.f;
-  __syncthreads();
-  const int tok = blockIdx.x * 8 + (threadIdx.x >> 5);
-  if (tok < j.total_tokens) {
-    int lo_u = 0, hi_u = j.num_users - 1;  // the user owning token tok (warp-uniform search)
-    while (lo_u < hi_u) {
-      const int mid = (lo_u + hi_u + 1) >> 1;
-      if (j.offsets[mid] <= tok) lo_u = mid; else hi_u = mid - 1;
+  // dynamic smem: the chunk's timestamps [min(max_len, CAP)], then per-lane private bins
+  // [8 warps][nb][32 lanes] (conflict-free, no atomics: a lane adds a finished run to its own)
+  extern __shared__ int64_t s_ts[];
+  __shared__ int s_u;
+  const int h = blockIdx.y, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int row0 = blockIdx.x * 64;
+  if (threadIdx.x == 0) {
+    int u = -1;
+    if (row0 < koff[j.num_users]) {  // the user whose padded rows hold row0
+      int lo_u = 0, hi_u = j.num_users - 1;
+      while (lo_u < hi_u) {
+        const int mid = (lo_u + hi_u + 1) >> 1;
+        if (koff[mid] <= row0) lo_u = mid; else hi_u = mid - 1;
+      }
+      u = lo_u;
     }
-    const UserSpan us = load_user(j, lo_u);
-    const int kj = tok - us.off;
-    const int kv_end = causal ? us.L : us.ns + us.nr;
-    if (kj < kv_end) {
-      const int64_t ts_j = j.ts ? j.ts[tok] : 0;
-      const int64_t* tsu = j.ts ? j.ts + us.off : nullptr;
+    s_u = u;
+  }
+  __syncthreads();
+  const int u = s_u;
+  if (u < 0) return;  // uniform: padded rows past the last user
+  const UserSpan us = load_user(j, u);
+  const int cap = min(max(j.max_len, 1), DRAB_TS_CAP);
+  float* bins = reinterpret_cast<float*>(s_ts + cap);
+  float* mine = bins + warp * nb * 32 + lane;  // bins of this lane: mine[b * 32]
+  for (int b = 0; b < nb; ++b) mine[b * 32] = 0.f;
+  const int64_t* tsg = j.ts + us.off;  // ts may be NULL: every timestamp 0
+  const int kv_end = causal ? us.L : us.ns + us.nr;
+  for (int c0 = 0; c0 < us.L; c0 += DRAB_TS_CAP) {  // query chunks (one up to CAP tokens)
+    const int c1 = min(us.L, c0 + DRAB_TS_CAP);
+    __syncthreads();
+    for (int i = c0 + threadIdx.x; i < c1; i += 256) s_ts[i - c0] = j.ts ? tsg[i] : 0;
+    __syncthreads();
+    for (int r = 0; r < 8; ++r) {
+      const int kj = row0 - koff[u] + warp * 8 + r;  // key (user-local)
+      if (kj >= kv_end) break;
+      const int64_t ts_j = j.ts ? tsg[kj] : 0;
       // visible queries of key kj: causal i >= kj; full / static keys every i; real-time keys
       // i == kj or (i >= ns and ts_j < ts_i)
       const int lo = causal ? kj : ((full || kj < us.ns) ? 0 : us.ns);
-      const __nv_bfloat16* row = ds + ((int64_t)h * rows + koff[lo_u] + kj) * pitch;
+      const bool all_vis = causal || full || kj < us.ns;  // uniform
+      const int qa = max(lo, c0);
+      const __nv_bfloat16* row = ds + ((int64_t)h * rows + row0 + warp * 8 + r) * pitch;
       int rb = 0;
       float racc = 0.f;
-      for (int i0 = (lo & ~1) + 2 * lane; i0 < us.L; i0 += 64) {
-        const __nv_bfloat162 v2 = *reinterpret_cast<const __nv_bfloat162*>(row + i0);
+      // lane-interleaved query pairs (coalesced dS^T and timestamp reads), 8 pairs in flight;
+      // a run of equal buckets is summed in a register and added to the lane's bin when it ends
+      for (int i0 = (qa & ~1) + 2 * lane; i0 < c1; i0 += 512) {
+        __nv_bfloat162 w[8];
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int i = i0 + e;
-          if (i < lo || i >= us.L) continue;
-          const int64_t ts_i = tsu ? tsu[i] : 0;
-          const bool vis = causal || full || kj < us.ns || i == kj || (i >= us.ns && ts_j < ts_i);
-          if (!vis) continue;
-          const int bk = rab_bkt(ts_i - ts_j, nb - 1);
-          if (bk != rb) {
-            if (racc != 0.f) atomicAdd(&bins[rb], us.nu * racc);
-            rb = bk;
-            racc = 0.f;
+        for (int e = 0; e < 8; ++e) {
+          const int i = i0 + 64 * e;
+          w[e] = i < c1 ? *reinterpret_cast<const __nv_bfloat162*>(row + i) : __nv_bfloat162{};
+        }
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const int i = i0 + 64 * e;
+          const float2 f = __bfloat1622float2(w[e]);
+          const longlong2 t2 = *reinterpret_cast<const longlong2*>(s_ts + ((min(i, c1 - 1) - c0) & ~1));  // pair (i, i+1)
+#pragma unroll
+          for (int h2 = 0; h2 < 2; ++h2) {
+            const int ii = i + h2;
+            const int64_t ts_i = h2 ? t2.y : t2.x;
+            const bool ok = ii >= qa && ii < c1 && (all_vis || ii == kj || (ii >= us.ns && ts_j < ts_i));
+            const int bk = rab_bkt(ts_i - ts_j, nb - 1);
+            const bool brk = ok && bk != rb;
+            if (brk) {  // predicated, not atomic: the lane's own bin
+              mine[rb * 32] += racc;
+              rb = bk;
+              racc = 0.f;
+            }
+            racc += ok ? (h2 ? f.y : f.x) : 0.f;
           }
-          racc += __bfloat162float(e ? v2.y : v2.x);
         }
       }
-      if (racc != 0.f) atomicAdd(&bins[rb], us.nu * racc);
+      mine[rb * 32] += racc;
     }
   }
   __syncthreads();
-  if (threadIdx.x < nb && bins[threadIdx.x] != 0.f) atomicAdd(&drab[h * nb + threadIdx.x], bins[threadIdx.x]);
+  for (int b = threadIdx.x >> 5; b < nb; b += 8) {  // warp per bucket: 8 x 32 lane bins
+    float v = 0.f;
+    for (int w2 = 0; w2 < 8; ++w2) v += bins[(w2 * nb + b) * 32 + lane];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0 && v != 0.f) atomicAdd(&drab[h * nb + b], us.nu * v);  // x nu (R#5's 1/N in ds)
+  }
 }
 
 static mtgr_status_t launch_drab(const AttnIO& io, const int* koff, const __nv_bfloat16* ds, int64_t pitch,
                                  int64_t rows, cudaStream_t st) {
   if (io.nb <= 0 || io.drab == nullptr || io.rab_w == nullptr) return MTGR_OK;
   ProfScope ps(PROF_ATTN_DRAB, st);
-  dim3 grid(ceil_div(io.jag.total_tokens, 8), io.H);
-  attn_drab_kernel<<<grid, 256, 0, st>>>(io.jag, io.causal, io.full, io.nb, koff, ds, pitch, rows, io.drab);
+  // padded rows koff[B] <= rows (= T + 256 B); chunks past koff[B] exit at once
+  dim3 grid((unsigned)ceil_div64(rows, 64), io.H);
+  const int smem = std::min(std::max(io.jag.max_len, 1), DRAB_TS_CAP) * 8 + 8 * io.nb * 32 * 4;
+  cudaFuncSetAttribute(attn_drab_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  attn_drab_kernel<<<grid, 256, smem, st>>>(io.jag, io.causal, io.full, io.nb, koff, ds, pitch, rows, io.drab);
   return check_launch("attn_drab");
 }
 
