@@ -389,6 +389,35 @@ struct GlnRing {
   uint32_t ring_off;  // byte offset of the first warp's ring in dynamic smem
 };
 
+// packed fp32 pairs (sm_100 FFMA2 / FMUL2 / FADD2) and bf16 pair conversions for the bulk backward
+__device__ __forceinline__ unsigned long long p2u(float2 v) { return *reinterpret_cast<unsigned long long*>(&v); }
+__device__ __forceinline__ float2 u2p(unsigned long long v) { return *reinterpret_cast<float2*>(&v); }
+__device__ __forceinline__ float2 p2fma(float2 a, float2 b, float2 c) {
+  unsigned long long d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(p2u(a)), "l"(p2u(b)), "l"(p2u(c)));
+  return u2p(d);
+}
+__device__ __forceinline__ float2 p2mul(float2 a, float2 b) {
+  unsigned long long d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(p2u(a)), "l"(p2u(b)));
+  return u2p(d);
+}
+__device__ __forceinline__ float2 p2add(float2 a, float2 b) {
+  unsigned long long d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(p2u(a)), "l"(p2u(b)));
+  return u2p(d);
+}
+__device__ __forceinline__ float2 bf2_to_f2(uint32_t w) {  // (lo, hi) bf16 -> fp32: shifts only
+  return make_float2(__uint_as_float(w << 16), __uint_as_float(w & 0xffff0000u));
+}
+__device__ __forceinline__ void store8p(__nv_bfloat16* p, const float2* v) {
+  uint4 a;
+  __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&a);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) h[i] = __float22bfloat162_rn(v[i]);
+  *reinterpret_cast<uint4*>(p) = a;
+}
+
 template <int MODE, int NC>
 __global__ void __launch_bounds__(512, 1) gln_bwd_bulk_kernel(GlnBwdArgs<__nv_bfloat16> a, GlnRing R) {
   using namespace sm100;
@@ -426,11 +455,12 @@ __global__ void __launch_bounds__(512, 1) gln_bwd_bulk_kernel(GlnBwdArgs<__nv_bf
   };
   if (lane == 0)
     for (int s = 0; s < R.S && w_begin + s < w_end; ++s) issue(w_begin + s, s);
-  float pg[NC][8], pb[NC][8], pc[NC][8];
+  // packed fp32 pairs (FFMA2 / FMUL2 / FADD2): the per-token math in half the issue slots
+  float2 pg[NC][4], pb[NC][4], pc[NC][4];
 #pragma unroll
   for (int k = 0; k < NC; ++k)
 #pragma unroll
-    for (int e = 0; e < 8; ++e) pg[k][e] = pb[k][e] = pc[k][e] = 0.f;
+    for (int e = 0; e < 4; ++e) pg[k][e] = pb[k][e] = pc[k][e] = make_float2(0.f, 0.f);
   int cur_g = w_begin < w_end ? a.gid[w_begin] : 0;
   auto flush = [&]() {
 #pragma unroll
@@ -438,10 +468,12 @@ __global__ void __launch_bounds__(512, 1) gln_bwd_bulk_kernel(GlnBwdArgs<__nv_bf
       const int c = lane + 32 * k;
       if (c < nch) {
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          atomicAdd(&sacc[(cur_g * 2 + 0) * d + c * 8 + e], pg[k][e]);
-          atomicAdd(&sacc[(cur_g * 2 + 1) * d + c * 8 + e], pb[k][e]);
-          pg[k][e] = pb[k][e] = 0.f;
+        for (int e = 0; e < 4; ++e) {
+          atomicAdd(&sacc[(cur_g * 2 + 0) * d + c * 8 + 2 * e], pg[k][e].x);
+          atomicAdd(&sacc[(cur_g * 2 + 0) * d + c * 8 + 2 * e + 1], pg[k][e].y);
+          atomicAdd(&sacc[(cur_g * 2 + 1) * d + c * 8 + 2 * e], pb[k][e].x);
+          atomicAdd(&sacc[(cur_g * 2 + 1) * d + c * 8 + 2 * e + 1], pb[k][e].y);
+          pg[k][e] = pb[k][e] = make_float2(0.f, 0.f);
         }
       }
     }
@@ -457,107 +489,111 @@ __global__ void __launch_bounds__(512, 1) gln_bwd_bulk_kernel(GlnBwdArgs<__nv_bf
     if (t + 1 < w_end) { g_n = a.gid[t + 1]; mu_n = a.mean[t + 1]; r_n = a.rstd[t + 1]; }
     mbar_wait(&bars[s], (i / R.S) & 1);
     const uint8_t* st = ring + (size_t)s * R.stage_bytes;
-    auto row8 = [&](int slot, int c, float* v) {  // 8 elements of an input row (16-byte lane)
-      Raw8<bf> rw;
+    auto row8 = [&](int slot, int c, float2* v) {  // 8 elements of an input row (16-byte lane)
+      uint32_t w0, w1, w2, w3;
       asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
-                   : "=r"(rw.v.x), "=r"(rw.v.y), "=r"(rw.v.z), "=r"(rw.v.w)
+                   : "=r"(w0), "=r"(w1), "=r"(w2), "=r"(w3)
                    : "r"(smem_u32(st + slot * row_bytes + c * 16)));
-      unpack(rw, v);
+      v[0] = bf2_to_f2(w0); v[1] = bf2_to_f2(w1); v[2] = bf2_to_f2(w2); v[3] = bf2_to_f2(w3);
     };
-    auto x_of = [&](int k, float* xv) {
-      const int c = lane + 32 * k;
-      if (MODE == GLN_GATE && R.r_x < 0) {  // gated norm input x = o (.) u
-        float uu[8], oo[8];
-        row8(R.r_u, c, uu);
-        row8(R.r_o, c, oo);
-#pragma unroll
-        for (int e = 0; e < 8; ++e) xv[e] = oo[e] * uu[e];
-      } else {
-        row8(R.r_x, c, xv);
-      }
+    auto gam = [&](const float* gr, float2* v) {
+      const float4 g0 = reinterpret_cast<const float4*>(gr)[0], g1 = reinterpret_cast<const float4*>(gr)[1];
+      v[0] = make_float2(g0.x, g0.y); v[1] = make_float2(g0.z, g0.w);
+      v[2] = make_float2(g1.x, g1.y); v[3] = make_float2(g1.z, g1.w);
     };
     if (g != cur_g) {
       flush();
       cur_g = g;
     }
     const float* gr = sgam + g * d;
-    float s1 = 0.f, s2 = 0.f;
+    const float2 r2 = make_float2(r, r), nmur2 = make_float2(-mu * r, -mu * r);
+    float2 s1 = make_float2(0.f, 0.f), s2 = make_float2(0.f, 0.f);
 #pragma unroll
     for (int k = 0; k < NC; ++k) {
       const int c = lane + 32 * k;
       if (c < nch) {
-        float xv[8], dyv[8], gg[8];
-        x_of(k, xv);
-        row8(0, c, dyv);
-        load8(gr + c * 8, gg);
+        float2 xv[4], dyv[4], gg[4];
+        if (MODE == GLN_GATE && R.r_x < 0) {  // gated norm input x = o (.) u
+          float2 uu[4];
+          row8(R.r_u, c, uu);
+          row8(R.r_o, c, xv);
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const float xh = fmaf(xv[e], r, -mu * r);
-          const float dxh = dyv[e] * gg[e];
-          pg[k][e] = fmaf(dyv[e], xh, pg[k][e]);
-          pb[k][e] += dyv[e];
-          s1 += dxh;
-          s2 = fmaf(dxh, xh, s2);
+          for (int e = 0; e < 4; ++e) xv[e] = p2mul(xv[e], uu[e]);
+        } else {
+          row8(R.r_x, c, xv);
+        }
+        row8(0, c, dyv);
+        gam(gr + c * 8, gg);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 xh = p2fma(xv[e], r2, nmur2);
+          const float2 dxh = p2mul(dyv[e], gg[e]);
+          pg[k][e] = p2fma(dyv[e], xh, pg[k][e]);
+          pb[k][e] = p2add(pb[k][e], dyv[e]);
+          s1 = p2add(s1, dxh);
+          s2 = p2fma(dxh, xh, s2);
         }
       }
     }
-    const float m1 = warp_sum(s1) * inv_d, m2 = warp_sum(s2) * inv_d;
-    const float mur = mu * r;
+    const float m1 = warp_sum(s1.x + s1.y) * inv_d, m2 = warp_sum(s2.x + s2.y) * inv_d;
+    const float2 nm1 = make_float2(-m1, -m1), nm2 = make_float2(-m2, -m2);
 #pragma unroll
     for (int k = 0; k < NC; ++k) {
       const int c = lane + 32 * k;
       if (c < nch) {
-        float xv[8], dyv[8], gg[8], o[8], uu[8], oo[8];
-        if (MODE == GLN_GATE && R.r_x < 0) {  // x = o (.) u, keeping o and u for the gate
+        float2 xv[4], dyv[4], gg[4], o[4], uu[4], oo[4];
+        if (MODE == GLN_GATE) {
           row8(R.r_u, c, uu);
           row8(R.r_o, c, oo);
+        }
+        if (MODE == GLN_GATE && R.r_x < 0) {  // x = o (.) u, keeping o and u for the gate
 #pragma unroll
-          for (int e = 0; e < 8; ++e) xv[e] = oo[e] * uu[e];
+          for (int e = 0; e < 4; ++e) xv[e] = p2mul(oo[e], uu[e]);
         } else {
-          x_of(k, xv);
-          if (MODE == GLN_GATE) {
-            row8(R.r_u, c, uu);
-            row8(R.r_o, c, oo);
-          }
+          row8(R.r_x, c, xv);
         }
         row8(0, c, dyv);
-        load8(gr + c * 8, gg);
+        gam(gr + c * 8, gg);
+        // dx = r (dy g - m1 - xhat m2)
 #pragma unroll
-        for (int e = 0; e < 8; ++e) o[e] = r * (dyv[e] * gg[e] - m1 - fmaf(xv[e], r, -mur) * m2);
+        for (int e = 0; e < 4; ++e) {
+          const float2 xh = p2fma(xv[e], r2, nmur2);
+          o[e] = p2mul(p2fma(xh, nm2, p2fma(dyv[e], gg[e], nm1)), r2);
+        }
         if (MODE == GLN_RESID) {
-          float z[8];
+          float2 z[4];
           row8(R.r_dz, c, z);
 #pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            o[e] += z[e];
-            pc[k][e] += z[e];
+          for (int e = 0; e < 4; ++e) {
+            o[e] = p2add(o[e], z[e]);
+            pc[k][e] = p2add(pc[k][e], z[e]);
           }
-          store8(a.dx + (int64_t)t * d + c * 8, o);
+          store8p(a.dx + (int64_t)t * d + c * 8, o);
         } else if (MODE == GLN_GATE) {
           // o[] = dY; dO = dY * U;  dp_U = dY * O * silu'(p_U)
-          float dO[8], du[8];
+          float2 dO[4], du[4];
 #pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            dO[e] = o[e] * uu[e];
-            du[e] = o[e] * oo[e];
+          for (int e = 0; e < 4; ++e) {
+            dO[e] = p2mul(o[e], uu[e]);
+            du[e] = p2mul(o[e], oo[e]);
           }
           if (R.r_pre >= 0) {
-            float pp[8];
+            float2 pp[4];
             row8(R.r_pre, c, pp);
             if (a.pre_dsilu) {
 #pragma unroll
-              for (int e = 0; e < 8; ++e) du[e] *= pp[e];
+              for (int e = 0; e < 4; ++e) du[e] = p2mul(du[e], pp[e]);
             } else {
 #pragma unroll
-              for (int e = 0; e < 8; ++e) du[e] *= dsilu_f(pp[e]);
+              for (int e = 0; e < 4; ++e) du[e] = make_float2(du[e].x * dsilu_f(pp[e].x), du[e].y * dsilu_f(pp[e].y));
             }
           }
 #pragma unroll
-          for (int e = 0; e < 8; ++e) pc[k][e] += du[e];
-          store8(a.dx + (int64_t)t * d + c * 8, dO);
-          store8(a.dpu + (int64_t)t * a.ld_dp + c * 8, du);
+          for (int e = 0; e < 4; ++e) pc[k][e] = p2add(pc[k][e], du[e]);
+          store8p(a.dx + (int64_t)t * d + c * 8, dO);
+          store8p(a.dpu + (int64_t)t * a.ld_dp + c * 8, du);
         } else {
-          store8(a.dx + (int64_t)t * d + c * 8, o);
+          store8p(a.dx + (int64_t)t * d + c * 8, o);
         }
       }
     }
@@ -571,7 +607,10 @@ __global__ void __launch_bounds__(512, 1) gln_bwd_bulk_kernel(GlnBwdArgs<__nv_bf
       const int c = lane + 32 * k;
       if (c < nch)
 #pragma unroll
-        for (int e = 0; e < 8; ++e) atomicAdd(&sacc[G * 2 * d + c * 8 + e], pc[k][e]);
+        for (int e = 0; e < 4; ++e) {
+          atomicAdd(&sacc[G * 2 * d + c * 8 + 2 * e], pc[k][e].x);
+          atomicAdd(&sacc[G * 2 * d + c * 8 + 2 * e + 1], pc[k][e].y);
+        }
     }
   }
   __syncthreads();
@@ -688,7 +727,7 @@ static mtgr_status_t gln_bwd_bulk_launch(GlnBwdArgs<__nv_bfloat16> a, int mode, 
   R.S = 3;
   const size_t acc_bytes = align_up(((size_t)a.G * 3 * a.d + a.d) * sizeof(float), 128);  // + gamma
   R.ring_off = (uint32_t)acc_bytes;
-  const size_t budget = 200 * 1024;
+  const size_t budget = 226 * 1024;  // of the 227 KB opt-in: 16 warps for the 4-row GLN2 stages at d = 512
   int warps = (int)((budget - acc_bytes) / ((size_t)R.S * R.stage_bytes + R.S * 8));
   warps = std::max(1, std::min(16, warps));
   const int threads = 32 * warps;
