@@ -679,8 +679,10 @@ def main():
         return
     if world > 1:
         # communicator INIT lines (nranks, transport) go to stderr; stdout carries one JSON line.
-        # Set before torch is imported: NCCL reads its debug settings once, at its first call
-        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        # Set before torch is imported: NCCL reads its debug settings once, at its first call.
+        # The GPU image presets NCCL_DEBUG=VERSION (version line only): raised to INFO here
+        if os.environ.get("NCCL_DEBUG", "").upper() not in ("INFO", "TRACE"):
+            os.environ["NCCL_DEBUG"] = "INFO"
         os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     import torch
