@@ -171,7 +171,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KV_THREADS, 1)
   uint64_t* x_full = bars + 6;        // [3] leader
   uint64_t* x_empty = bars + 9;       // [3]
   uint64_t* s_full = bars + 12;       // [3] score tile b complete (multicast commit)
-  uint64_t* t_full = bars + 16;       // [3] leader, both CTAs: T tile b written
+  uint64_t* t_full = bars + 16;       // [NS][2] leader: T tile b, warp half w written (both CTAs)
   uint64_t* r1_full = bars + 22;      // leader: both CTAs' row operand (dh 0..127) staged
   uint64_t* r1_copied = bars + 24;    // own (tcgen05.cp done: staging reusable)
   uint64_t* r1u_full = bars + 25;     // leader: both CTAs' row operand dh 128..255 resident
@@ -201,7 +201,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KV_THREADS, 1)
       mbar_init(&c1_full[s], 1); mbar_init(&c1_empty[s], 1);
       mbar_init(&x_full[s], 1); mbar_init(&x_empty[s], 1);
     }
-    for (int s = 0; s < NS; ++s) { mbar_init(&t_full[s], 2 * NSM); mbar_init(&s_full[s], 1); }
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&t_full[2 * s], NSM); mbar_init(&t_full[2 * s + 1], NSM); mbar_init(&s_full[s], 1);
+    }
     mbar_init(r1_full, 1);
     mbar_init(r1_copied, 1);
     mbar_init(r1u_full, 1);
@@ -436,21 +438,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KV_THREADS, 1)
         if constexpr (SPLIT_R1) mbar_wait(r1u_full, mi & 1);  // head dims 128..255 of the rows in smem
         const uint32_t r1u_base = smem_u32(smem + OFF_R1U);
         // acc += T_j X_j  (A = T from each CTA's TMEM, B = X: each CTA's half of the head dim)
+        // per warp half w (queries 32 w.., K chunks 2w, 2w + 1): its MMAs go as soon as the 8
+        // warps of that half (both CTAs) have written their T columns, not after all 16
         auto acc = [&](int j, int g) {
           const int tb = g % NS;
-          mbar_wait(&t_full[tb], (g / NS) & 1);
           mbar_wait(&x_full[g % NX], (g / NX) & 1);
-          if (lane == 0) KV_TR(13, g, gtimer());
           const uint32_t x = x_base + (g % NX) * X_BYTES;
-          tc_fence_after();
-          if (elect_one()) {
 #pragma unroll
-            for (int kk = 0; kk < BC / 16; ++kk)
-              mma_bf16_ts_2sm(tm + T_ACC, tm + T_S + 64 * tb + (kk >> 1) * 32 + (kk & 1) * 8,
-                              desc_sw128(x + kk * 2048, X_BYTES / 2, 1024), idesc_acc, (j > 0 || kk > 0));
-            mma_commit_2sm_mc(&x_empty[g % NX], 0x3);
+          for (int w = 0; w < 2; ++w) {
+            mbar_wait(&t_full[2 * tb + w], (g / NS) & 1);
+            if (lane == 0 && w == 1) KV_TR(13, g, gtimer());
+            tc_fence_after();
+            if (elect_one()) {
+#pragma unroll
+              for (int kk = 2 * w; kk < 2 * w + 2; ++kk)
+                mma_bf16_ts_2sm(tm + T_ACC, tm + T_S + 64 * tb + (kk >> 1) * 32 + (kk & 1) * 8,
+                                desc_sw128(x + kk * 2048, X_BYTES / 2, 1024), idesc_acc, (j > 0 || kk > 0));
+              if (w == 1) mma_commit_2sm_mc(&x_empty[g % NX], 0x3);
+            }
+            __syncwarp();
           }
-          __syncwarp();
         };
         // score tile g: head dims 0..127 with A from TMEM, 128..255 with A from smem.  Its buffer
         // (g % 3) was last read by the T MMA of tile g - 3, issued (in order) before this one
@@ -602,7 +609,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KV_THREADS, 1)
             tmem_st16(tmem + T_S + 64 * tb + j_half + lane_off, pk);  // in place (this warp's S)
             tmem_st_wait();
             tc_fence_before();
-            arrive_leader(&t_full[tb]);
+            arrive_leader(&t_full[2 * tb + half]);
             if (trw) KV_TR(8, gt, gtimer());
             if (lane == 0) KV_TR(18 + sw, gt, gtimer());
             // publish the PREVIOUS tile's G piece: its stores were issued a tile ago, so this
@@ -653,7 +660,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KV_THREADS, 1)
             tmem_st16(tmem + T_S + 64 * tb + j_half + lane_off, pk);  // in place (this warp's S)
             tmem_st_wait();
             tc_fence_before();
-            arrive_leader(&t_full[tb]);
+            arrive_leader(&t_full[2 * tb + half]);
             if (trw) KV_TR(8, gt, gtimer());
             if (lane == 0) KV_TR(18 + sw, gt, gtimer());
             // this tile's G is consumed
