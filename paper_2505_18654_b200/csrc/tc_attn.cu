@@ -122,13 +122,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
   uint64_t* c2_full = bars + 12;      // [2] leader
   uint64_t* c2_empty = bars + 14;     // [2]
   // !TWO: the score tile is double-buffered (S[b] = T_S + 64 b) and the P tile written in place,
-  // so s_full is [2] (bars 16 and 44), s_free is unused and t_free holds the T arrivals of warp
-  // half 1; TWO: single S / dP
+  // so s_full is [2] (bars 16 and 44) and neither s_free nor t_free is used; TWO: single S / dP
   uint64_t* s_full = bars + 16;
   uint64_t* s_free = bars + 17;       // leader, both CTAs' softmax warps (TWO)
   uint64_t* s_full1 = bars + 46;      // !TWO: score tile 1 (after q_item [43, 45))
-  uint64_t* t_full = bars + 18;       // [2] leader, both CTAs (!TWO: warp half 0 of each CTA)
-  uint64_t* t_free = bars + 20;       // [2] TWO: P buffer free; !TWO: T tile, warp half 1 written
+  uint64_t* t_full = bars + 18;       // [2] leader, both CTAs
+  uint64_t* t_free = bars + 20;       // [2]
   uint64_t* r1_full = bars + 22;
   uint64_t* r1_done = bars + 23;      // leader, both CTAs (R1 in TMEM)
   uint64_t* r1_copied = bars + 24;    // own (staging area reusable)
@@ -161,7 +160,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&c2_full[s], 1); mbar_init(&c2_empty[s], 1);
-      mbar_init(&t_full[s], TWO ? 2 * NSM : NSM); mbar_init(&t_free[s], TWO ? 1 : NSM);
+      mbar_init(&t_full[s], 2 * NSM); mbar_init(&t_free[s], 1);
     }
     mbar_init(s_full, 1);
     mbar_init(s_full1, 1);
@@ -421,28 +420,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
           mbar_wait(r1_done, mi & 1);  // R1 of both CTAs copied into TMEM
         }
         // acc += P_j X_j  (A = P from each CTA's TMEM, B = X: each CTA's half of the head dim)
-        // !TWO: per warp half w (queries 32 w.., K chunks 2w, 2w + 1): its MMAs go as soon as the
-        // 8 warps of that half (both CTAs) have written their T columns
         auto acc = [&](int j, int g) {
           const int tb = g & 1;
-          if (TWO) mbar_wait(&t_full[tb], (g >> 1) & 1);
+          mbar_wait(&t_full[tb], (g >> 1) & 1);
           mbar_wait(&x_full[g % NX], (g / NX) & 1);
           const uint32_t x = x_base + (g % NX) * X_BYTES;
+          tc_fence_after();
+          if (elect_one()) {
 #pragma unroll
-          for (int w = 0; w < (TWO ? 1 : 2); ++w) {
-            if (!TWO) mbar_wait(w ? &t_free[tb] : &t_full[tb], (g >> 1) & 1);
-            tc_fence_after();
-            if (elect_one()) {
-#pragma unroll
-              for (int kk = (TWO ? 0 : 2 * w); kk < (TWO ? BC / 16 : 2 * w + 2); ++kk)
-                mma_bf16_ts_2sm(tm + T_ACC, TWO ? tm + T_P + tb * 32 + kk * 8
-                                                  : tm + T_S + 64 * tb + (kk >> 1) * 32 + (kk & 1) * 8,
-                                desc_sw128(x + kk * 2048, X_BYTES / 2, 1024), idesc_acc, (j > 0 || kk > 0));
-              if (TWO) mma_commit_2sm_mc(&t_free[tb], 0x3);
-              if (TWO || w == 1) mma_commit_2sm_mc(&x_empty[g % NX], 0x3);
-            }
-            __syncwarp();
+            for (int kk = 0; kk < BC / 16; ++kk)
+              mma_bf16_ts_2sm(tm + T_ACC, TWO ? tm + T_P + tb * 32 + kk * 8
+                                                : tm + T_S + 64 * tb + (kk >> 1) * 32 + (kk & 1) * 8,
+                              desc_sw128(x + kk * 2048, X_BYTES / 2, 1024), idesc_acc, (j > 0 || kk > 0));
+            if (TWO) mma_commit_2sm_mc(&t_free[tb], 0x3);
+            mma_commit_2sm_mc(&x_empty[g % NX], 0x3);
           }
+          __syncwarp();
         };
         for (int t = 0; t < nt; ++t) {
           const int g = gt + t;
@@ -699,7 +692,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
           tmem_st16(tmem + (TWO ? T_P + tb * 32 + half * 16 : t_s + j_half) + lane_off, pk);
           tmem_st_wait();
           tc_fence_before();
-          arrive_leader(TWO || half == 0 ? &t_full[tb] : &t_free[tb]);
+          arrive_leader(&t_full[tb]);
           if (store_scores) {
             // this row's 32 query columns are 64 contiguous bytes per matrix.  Lane pairs swap
             // halves so that each 256-bit store instruction writes 16 whole 64-byte row pieces
