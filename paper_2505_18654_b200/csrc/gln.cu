@@ -724,10 +724,12 @@ static mtgr_status_t gln_bwd_bulk_launch(GlnBwdArgs<__nv_bfloat16> a, int mode, 
   R.r_pre = slot(mode == GLN_GATE && a.pre_u != nullptr);
   R.nrows = n;
   R.stage_bytes = (uint32_t)(n * a.d * 2);
-  R.S = 3;
   const size_t acc_bytes = align_up(((size_t)a.G * 3 * a.d + a.d) * sizeof(float), 128);  // + gamma
   R.ring_off = (uint32_t)acc_bytes;
   const size_t budget = 226 * 1024;  // of the 227 KB opt-in: 16 warps for the 4-row GLN2 stages at d = 512
+  // three stages per warp while that still fits 14 warps per SM, else two (d = 768: 10 -> 15 warps)
+  R.S = 3;
+  if ((budget - acc_bytes) / ((size_t)3 * R.stage_bytes + 24) < 14) R.S = 2;
   int warps = (int)((budget - acc_bytes) / ((size_t)R.S * R.stage_bytes + R.S * 8));
   warps = std::max(1, std::min(16, warps));
   const int threads = 32 * warps;
