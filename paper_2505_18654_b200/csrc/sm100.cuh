@@ -131,6 +131,23 @@ __device__ __forceinline__ void stg256(void* p, const U8& r) {
                "r"(r.v[2]), "r"(r.v[3]), "r"(r.v[4]), "r"(r.v[5]), "r"(r.v[6]), "r"(r.v[7])
                : "memory");
 }
+// streaming (evict-first) 256-bit store: data read back much later (after other traffic)
+__device__ __forceinline__ void stg256_cs(void* p, const U8& r) {
+  asm volatile("st.global.cs.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(r.v[0]), "r"(r.v[1]),
+               "r"(r.v[2]), "r"(r.v[3]), "r"(r.v[4]), "r"(r.v[5]), "r"(r.v[6]), "r"(r.v[7])
+               : "memory");
+}
+// L2 evict-last policy and a 128-bit store under it: data re-read soon by another SM
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void stg128_hint(void* p, uint4 v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v4.u32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w), "l"(pol)
+               : "memory");
+}
 // cluster-scope handoff of a 32-bit value: store into CTA `rank`'s shared memory at the same
 // offset, then arrive there with release.cluster semantics (pair with mbar_wait_cluster)
 __device__ __forceinline__ void st_cluster_u32(uint32_t* p, uint32_t rank, uint32_t v) {

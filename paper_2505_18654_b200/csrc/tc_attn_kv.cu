@@ -621,8 +621,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KV_THREADS, 1)
               while (*reinterpret_cast<volatile int*>(cons_ok) < gt - ks.ng + 1) __nanosleep(32);
             if (!KV_DBG(2)) {
 #pragma unroll
-              for (int c = 0; c < 4; ++c)
-                gp[c * 32 + lane] = make_uint4(gw[4 * c], gw[4 * c + 1], gw[4 * c + 2], gw[4 * c + 3]);
+              for (int c = 0; c < 4; ++c)  // L2 evict-last: Y reads the piece back within a few tiles
+                stg128_hint(&gp[c * 32 + lane], make_uint4(gw[4 * c], gw[4 * c + 1], gw[4 * c + 2], gw[4 * c + 3]),
+                            l2_policy_evict_last());
             }
             if (t + 1 == it.ntiles) {  // the item's last tile: publish now (before the epilogue)
               __syncwarp();
@@ -677,8 +678,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KV_THREADS, 1)
             }
             __nv_bfloat16* p0 = a.st_ds + st_row + cb + 16 * b;
             if (!KV_DBG(4)) {
-              stg256(p0 - (int64_t)b * a.st_pitch, b ? oth : own);
-              stg256(p0 + (int64_t)(1 - b) * a.st_pitch, b ? own : oth);
+              // streaming stores: dS^T is read back by the dQ GEMM only after the whole kernel
+              stg256_cs(p0 - (int64_t)b * a.st_pitch, b ? oth : own);
+              stg256_cs(p0 + (int64_t)(1 - b) * a.st_pitch, b ? own : oth);
             }
             // prefetch the next tile's G when it is already published (its L2 latency then hides
             // behind this tile's tail and the next score wait)
