@@ -1363,7 +1363,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
         for (int t = 0; t < it.ntiles; ++t, ++gt) {
           const int slot = gt % MM_STAGES;
           mbar_wait(&empty[slot], ((gt / MM_STAGES) & 1) ^ 1);
-          if (leader) mbar_expect_tx(&full[slot], 2 * MM_STAGE_BYTES);
+          // DQ: 64-query boxes wholly past the user's last query are not loaded (their D rows are
+          // never stored; MMA rows are independent), e.g. 3 of the 4 boxes of a last pair holding
+          // 6 queries.  The leader expects the bytes both CTAs actually load.
+          int nbox = 4;
+          if (M2 == MM_DQ) nbox = (it.pr0 < it.us.L) + (it.pr0 + 64 < it.us.L) + (it.pr0 + 128 < it.us.L) + (it.pr0 + 192 < it.us.L);
+          if (leader) mbar_expect_tx(&full[slot], 2 * MM_B_BYTES + (M2 == MM_DQ ? nbox * (MM_A_BYTES / 2) : 2 * MM_A_BYTES));
           uint8_t* sa = smem + slot * MM_STAGE_BYTES;
           uint8_t* sb = sa + MM_A_BYTES;
           const int c0 = it.c_begin + t * BC;
@@ -1372,7 +1377,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
           } else {            // dS^T rows = 64 keys, this CTA's 128 query columns (MN-major)
 #pragma unroll
             for (int c = 0; c < 2; ++c)
-              tma_load_2d_2sm(sa + c * (MM_A_BYTES / 2), &tmA, &full[slot], it.r0 + c * 64, (int)(krow + c0));
+              if (it.r0 + c * 64 < it.us.L)
+                tma_load_2d_2sm(sa + c * (MM_A_BYTES / 2), &tmA, &full[slot], it.r0 + c * 64, (int)(krow + c0));
           }
 #pragma unroll
           for (int c = 0; c < 2; ++c)  // B: 64 rows (dO for DV, K for DQ), this CTA's 128 head dims
