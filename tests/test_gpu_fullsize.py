@@ -32,7 +32,7 @@ def _batch(cfg, users=None):
 
 def _run(dev, cfg, seg, users, ts, X, dZ, Ps):
     jb = m.JaggedBatch.build(seg, ts, dev, users=users.astype(np.int32))
-    lc = m.layer_cfg(cfg["d"], cfg["H"], cfg["groups"])
+    lc = m.layer_cfg(cfg["d"], cfg["H"], cfg["groups"], cfg.get("rab_buckets", 0))
     stack = m.HstuStack(lc, [m.params_to_device(P, torch.bfloat16, dev) for P in Ps], torch.bfloat16, dev)
     stack.bind(jb)
     z = stack.forward(torch.from_numpy(X).to(dev, torch.bfloat16))
@@ -99,12 +99,12 @@ def _oracle_grads(cfg, seg, off, ts, X, dZ, Ps, users):
 
 
 def _grad_views(cfg, flat, dev):
-    lc = m.layer_cfg(cfg["d"], cfg["H"], cfg["groups"])
+    lc = m.layer_cfg(cfg["d"], cfg["H"], cfg["groups"], cfg.get("rab_buckets", 0))
     g = m.alloc_grads(lc, dev, flat.to(dev))
     return {k: v.cpu().numpy() for k, v in g.items() if not k.startswith("_")}
 
 
-def _check_all(name, cfg, z, dx, gflat, Z, dX, G, dev, rows=None):
+def _check_all(name, cfg, z, dx, gflat, Z, dX, G, dev, rows=None, tol=None):
     sel = slice(None) if rows is None else rows
     rep = {"Z": (rel_err(z[sel], Z[sel]), p999_rel_err(z[sel], Z[sel])),
            "dX": (rel_err(dx[sel], dX[sel]), p999_rel_err(dx[sel], dX[sel]))}
@@ -114,7 +114,8 @@ def _check_all(name, cfg, z, dx, gflat, Z, dX, G, dev, rows=None):
     report(name, rep)
     print(name, rep)
     # max-normalised <= 2e-2 (north_star); elementwise p99.9 <= 0.5 (measured <= 0.24)
-    bad = {k: v for k, v in rep.items() if not (v[0] <= 2e-2 and v[1] <= 0.5)}
+    tol = tol or {}
+    bad = {k: v for k, v in rep.items() if not (v[0] <= tol.get(k, 2e-2) and v[1] <= 0.5)}
     assert not bad, bad
 
 
@@ -129,6 +130,72 @@ def test_small_one_layer_all_users_gradients(dev):
     off = jb.host["offsets"]
     Z, dX, G = _oracle_grads(cfg, seg, off, ts, X, dZ, Ps, range(len(seg)))
     _check_all("small_one_layer_all_users", cfg, z, dx, grads[0], Z, dX, G, dev)
+
+
+def test_small_one_layer_all_users_rab(dev):
+    """The same full bench batch with the optional relative-time bias (R#4, 16 buckets, rab_w ~
+    N(0, 1)): the RAB kernel instantiations of the forward and the coupled backward, the d rab_w
+    pass over the stored dS^T and the candidate diagonals, at the bench's launch configuration:
+    Z, dX and every parameter gradient including d rab_w against the oracle."""
+    cfg = synth.config("small", rab_buckets=16)
+    P = synth.gen_layer_params(cfg, 0, 16)
+    P["rab_w"] = (10.0 * P["rab_w"]).astype(np.float32)
+    seg, users, ts, X, dZ = _batch(cfg)
+    jb, z, dx, grads = _run(dev, cfg, seg, users, ts, X, dZ, [P])
+    off = jb.host["offsets"]
+    Z, dX, G = _oracle_grads(cfg, seg, off, ts, X, dZ, [P], range(len(seg)))
+    assert "rab_w" in G
+    # d rab_w: 5e-2 here (DESIGN.md R#25: bf16 rounding of the attention's inputs against the
+    # float64 oracle, amplified by the cancelling 1e8-term bucket sums); the kernels' own d rab_w
+    # is held to 2e-2 by test_small_attention_rab_all_users with identical bf16 inputs
+    _check_all("small_one_layer_all_users_rab", cfg, z, dx, grads[0], Z, dX, G, dev, tol={"drab_w": 5e-2})
+
+
+def test_small_attention_rab_all_users(dev):
+    """The attention alone over the full bench batch with rab (R#4, 16 buckets, rab_w ~ 8 N(0,1))
+    on bf16-exact inputs the oracle sees exactly (q, k, v, u, dO drawn in bf16; scores spread
+    over SiLU's curved range): o, y, dq, dk, dv and d rab_w at the bench's launch configuration.
+    d rab_w sums ~10^8 visible pairs per head and bucket; with the oracle fed the same bf16
+    inputs, what remains is the kernels' own arithmetic (fp32 accumulation, tanh.approx, the
+    fp16 SiLU' hand-over, the bf16 dS^T the sum reads back)."""
+    cfg = synth.config("small")
+    seg = synth.gen_segments(cfg)
+    L = seg.astype(np.int64).sum(1)
+    ts = np.concatenate([synth.gen_user_ts(cfg, u, seg[u]) for u in range(len(seg))])
+    jb = m.JaggedBatch.build(seg, ts, dev)
+    d, H, NB = cfg["d"], cfg["H"], 16
+    T = int(L.sum())
+    rng = np.random.default_rng(3)
+    qkvu = synth.round_bf16((rng.standard_normal((T, 4 * d)) * 0.12).astype(np.float32))
+    dO = synth.round_bf16(rng.standard_normal((T, d)).astype(np.float32))
+    rab = (8.0 * np.random.default_rng(5).standard_normal((H, NB))).astype(np.float32)
+    lc = m.layer_cfg(d, H, rab_buckets=NB)
+    a_ = torch.from_numpy(qkvu).to(dev, torch.bfloat16)
+    rw = torch.from_numpy(rab).to(dev)
+    o, y = m.attn_fwd(lc, jb, a_[:, 0:], a_[:, d:], a_[:, 2 * d:], 4 * d, u=a_[:, 3 * d:], rab_w=rw)
+    dq, dk, dv, drab = m.attn_bwd(lc, jb, torch.from_numpy(dO).to(dev, torch.bfloat16), a_[:, 0:], a_[:, d:],
+                                  a_[:, 2 * d:], 4 * d, rab_w=rw)
+    got = {k: v.float().cpu().numpy() for k, v in dict(o=o, y=y, dq=dq, dk=dk, dv=dv).items()}
+    ref = {k: np.zeros_like(v, dtype=np.float64) for k, v in got.items()}
+    rdrab = np.zeros((H, NB))
+    h = oracle.build_jagged(seg)
+    for u in range(len(seg)):
+        s0, e0 = h["offsets"][u], h["offsets"][u + 1]
+        ns, nr, nc = int(h["n_static"][u]), int(h["n_rt"][u]), int(h["n_cand"][u])
+        q, k, v, uu = (qkvu[s0:e0, i * d:(i + 1) * d].astype(np.float64) for i in range(4))
+        nu = 1.0 / (e0 - s0)
+        oo, S, M = oracle.attn_fwd_user(q, k, v, ns, nr, nc, ts[s0:e0], H, nu, rab_w=rab.astype(np.float64))
+        ref["o"][s0:e0], ref["y"][s0:e0] = oo, oo * uu
+        dq_, dk_, dv_, dr = oracle.attn_bwd_user(dO[s0:e0].astype(np.float64), q, k, v, S, M, H, nu, ts[s0:e0],
+                                                 rab.astype(np.float64))
+        ref["dq"][s0:e0], ref["dk"][s0:e0], ref["dv"][s0:e0] = dq_, dk_, dv_
+        rdrab += dr
+    rep = {k: (rel_err(got[k], ref[k]), p999_rel_err(got[k], ref[k])) for k in got}
+    rep["drab"] = (rel_err(drab.cpu().numpy(), rdrab), p999_rel_err(drab.cpu().numpy(), rdrab))
+    report("small_attention_rab_all_users", rep)
+    print(rep)
+    bad = {k: v for k, v in rep.items() if not (v[0] <= 2e-2 and v[1] <= 0.5)}
+    assert not bad, bad
 
 
 def test_large_shape_one_layer(dev):
