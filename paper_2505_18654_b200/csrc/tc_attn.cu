@@ -550,6 +550,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       const int my = it.r0 + row;                    // user-local index of this thread's row
       const int64_t g = (int64_t)us.off + my;        // global token index
       if (dbgw) DBG(0, idx);
+      // the candidate-row diagonal scalar of the epilogue, loaded now: its latency hides behind the tiles
+      const float dg_pre = (my < us.L && my >= it.kv_end) ? a.diag[g * a.H + it.h] : 0.f;
       if (it.ntiles > 0) {
         if (copied == mi && !(!TWO && a.row_cp)) copy_rows();  // not prefetched by the previous item
         const long long my_ts = (my < us.L && a.jag.ts) ? a.jag.ts[g] : 0;
@@ -750,7 +752,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       // the diagonal of real-time rows is inside the iterated key range (added in the loop);
       // candidate rows' own column lies outside it: their diagonal term is added here
       const bool has_e = row_ok && my >= it.kv_end;
-      const float dg = has_e ? a.diag[g * a.H + it.h] : 0.f;
+      const float dg = dg_pre;
       const __nv_bfloat16* erow = a.e + g * a.ld_e + it.hcol + half * 128;
       const int nrows = min(BR, us.L - it.r0);
       const bool full_chunk = q * 32 + 32 <= nrows;

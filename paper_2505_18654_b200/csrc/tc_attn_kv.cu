@@ -528,6 +528,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KV_THREADS, 1)
       const int64_t g = (int64_t)us.off + my;        // global token index
       const bool trw = warp == 4 && lane == 0;
       if (trw) { KV_TR(0, n, gtimer()); KV_TR(4, n, it.ntiles); }
+      // the candidate-row diagonal scalar of the epilogue, loaded now: its latency hides behind the tiles
+      const float dg_pre = (my < us.L && my >= it.kv_end) ? a.diag[g * a.H + it.h] : 0.f;
       if (it.ntiles > 0) {
         const long long my_ts = (role == 0 && my < us.L && a.jag.ts) ? a.jag.ts[g] : 0;
         // stored dS^T row of this key (Y): [h][koff[u] + my][query]
@@ -708,7 +710,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KV_THREADS, 1)
       // SiLU' of the projection from the TMA-staged tile; outputs formed in place and stored by TMA
       const bool row_ok = my < us.L;
       const bool has_e = row_ok && my >= it.kv_end;
-      const float dg = has_e ? a.diag[g * a.H + it.h] : 0.f;
+      const float dg = dg_pre;
       const __nv_bfloat16* erow = a.e + g * a.ld_e + it.hcol + half * 128;
       const int nrows = min(BR, us.L - it.r0);
       const bool full_chunk = q * 32 + 32 <= nrows;
