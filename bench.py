@@ -157,13 +157,14 @@ class ClockSampler:
     def __init__(self, gpu_id: str):
         self.gpu_id = gpu_id
         self.proc = None
-        self.lines = []
+        self.lines = []  # (host time, csv line)
+        self.window = None
 
     def start(self):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", self.gpu_id, f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -172,7 +173,17 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.monotonic(), line.strip()))
+
+    def wait_first(self, timeout=5.0):
+        """Block until nvidia-smi has produced a sample (it takes a while to start)."""
+        t_end = time.monotonic() + timeout
+        while self.proc is not None and not self.lines and time.monotonic() < t_end:
+            time.sleep(0.01)
+
+    def mark(self, t0, t1):
+        """Host-time bounds of the timed region: only samples inside it are reported."""
+        self.window = (t0, t1)
 
     def stop(self):
         if self.proc is None:
@@ -185,7 +196,12 @@ class ClockSampler:
         self.t.join(timeout=2)
         sm, mx, reasons = [], 0.0, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        lines = self.lines
+        if self.window is not None:
+            t0, t1 = self.window
+            inside = [x for x in lines if t0 <= x[0] <= t1 + 0.03]  # + one sampling period
+            lines = inside if inside else [x for x in lines if x[0] <= t1][-2:]  # the nearest under load
+        for _, ln in lines:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 7:
                 continue
@@ -396,14 +412,16 @@ def run_mtgr(args, cfg, rank, world, local_rank):
         if world > 1:
             dist.barrier()
 
+    # the clock sampler runs from the warm-up on (nvidia-smi takes a while to start); only its
+    # samples inside the timed region are reported
+    sampler = ClockSampler(gpu_id_for(torch, dev))
+    sampler.start()
+    sampler.wait_first()
     for _ in range(max(args.warmup, 1)):
         step()
     torch.cuda.synchronize()
     barrier()
 
-    sampler = ClockSampler(gpu_id_for(torch, dev))
-    sampler.start()
-    time.sleep(0.3)
     st = torch.cuda.current_stream()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     m.prof_reset()
@@ -411,14 +429,17 @@ def run_mtgr(args, cfg, rank, world, local_rank):
     launches0 = m.launch_count()
     barrier()
     torch.cuda.synchronize()
+    t_host0 = time.monotonic()
     ev0.record(st)
     for _ in range(args.steps):
         step()
     ev1.record(st)
     torch.cuda.synchronize()
+    t_host1 = time.monotonic()
     barrier()
     launches = m.launch_count() - launches0
     m.prof_enable(False)
+    sampler.mark(t_host0, t_host1)
     clocks = sampler.stop()
     ms = ev0.elapsed_time(ev1)
     kern = m.prof_query()
