@@ -244,6 +244,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KV_THREADS, 1)
   // this CTA's G ring: [KV_NG slots][8 warps][4 chunks][32 lanes] x 16 B
   uint4* gring = ks.gbuf + (size_t)(couple * 2 + (int)crank) * KV_NG_MAX * NSM * 128;
   long long* tr = (ks.trace != nullptr && couple == 0) ? ks.trace + ((size_t)role * 2 + crank) * 26 * 1024 : nullptr;
+  (void)tr;  // used by the KV_TR stamps of trace builds only
 
   auto q_read = [&](int n) -> int {
     mbar_wait_cluster(&q_full[n & 3], (n >> 2) & 1);
@@ -435,6 +436,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KV_THREADS, 1)
         if (nt == 0) continue;
         if (cp_done == mi) copy_r1();  // not prefetched at the end of the previous item
         const int item_n = n;
+        (void)item_n;  // trace builds only
         if constexpr (SPLIT_R1) mbar_wait(r1u_full, mi & 1);  // head dims 128..255 of the rows in smem
         const uint32_t r1u_base = smem_u32(smem + OFF_R1U);
         // acc += T_j X_j  (A = T from each CTA's TMEM, B = X: each CTA's half of the head dim)
