@@ -5,7 +5,9 @@ libmtgr's CUDA kernels.  Tensors must live on the current CUDA device.
 """
 from __future__ import annotations
 
+import contextlib
 import ctypes
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -339,7 +341,8 @@ class HstuStack:
         assert x.is_contiguous() and x.dtype == self.dtype
         self.xs[0] = x  # layer-0 input is read in place (kept alive for the backward)
         for li, P in enumerate(self.params):
-            hstu_layer_fwd(self.cfg, jb, P, self.xs[li], self.xs[li + 1], self.saved[li], self.ws)
+            with _nvtx(f"layer{li}.fwd"):
+                hstu_layer_fwd(self.cfg, jb, P, self.xs[li], self.xs[li + 1], self.saved[li], self.ws)
         return self.xs[-1][:jb.total_tokens]
 
     def backward(self, dz: torch.Tensor, accumulate=False, on_layer_done=None) -> torch.Tensor:
@@ -349,8 +352,9 @@ class HstuStack:
         cur = dz
         for li in range(len(self.params) - 1, -1, -1):
             out = self.dbuf[li % 2]
-            hstu_layer_bwd(self.cfg, jb, self.params[li], self.xs[li], self.saved[li], cur,
-                           self.grads[li], dx=out, accumulate=accumulate, ws=self.ws)
+            with _nvtx(f"layer{li}.bwd"):
+                hstu_layer_bwd(self.cfg, jb, self.params[li], self.xs[li], self.saved[li], cur,
+                               self.grads[li], dx=out, accumulate=accumulate, ws=self.ws)
             if on_layer_done is not None:
                 on_layer_done(li, self.grads[li]["_flat"])
             cur = out
@@ -358,6 +362,22 @@ class HstuStack:
 
 
 # ------------------------------------------------------------------ tracing
+
+_NVTX = os.environ.get("MTGR_NVTX") == "1"
+
+
+@contextlib.contextmanager
+def _nvtx(name: str):
+    """NVTX range around a layer call when MTGR_NVTX=1 (the library wraps each kernel launch in
+    its own range under the same switch); a no-op otherwise."""
+    if not _NVTX:
+        yield
+        return
+    torch.cuda.nvtx.range_push(name)
+    try:
+        yield
+    finally:
+        torch.cuda.nvtx.range_pop()
 
 # ------------------------------------------------------------------ candidate head (SURVEY f2)
 

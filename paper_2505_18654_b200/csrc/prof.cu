@@ -1,8 +1,11 @@
 // Launch counting and per-kernel CUDA-event timing (tracing subsystem).
 // When enabled, every instrumented launcher records a start/stop event pair on the stream it
 // launches on; mtgr_prof_query() resolves them into per-kind launch counts and device time.
+#include <cstdlib>
 #include <mutex>
 #include <vector>
+
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: ranges reach nsys / ncu when a tool is attached
 
 #include "common.cuh"
 #include "prof.h"
@@ -39,7 +42,18 @@ static cudaEvent_t get_event() {
   return e;
 }
 
+// MTGR_NVTX=1: every instrumented launch is wrapped in an NVTX range named by its kind (host
+// timeline of the launches for nsys; ncu --nvtx filters by it)
+static bool nvtx_on() {
+  static const bool on = [] { const char* e = getenv("MTGR_NVTX"); return e != nullptr && e[0] == '1'; }();
+  return on;
+}
+
 ProfScope::ProfScope(int kind, cudaStream_t st) : kind_(kind), st_(st), on_(false) {
+  if (nvtx_on()) {
+    nvtxRangePushA(kNames[kind]);
+    nv_ = true;
+  }
   if (g_prof_on.load(std::memory_order_relaxed)) {
     std::lock_guard<std::mutex> lk(g_mu);
     a_ = get_event();
@@ -54,6 +68,7 @@ ProfScope::~ProfScope() {
     std::lock_guard<std::mutex> lk(g_mu);
     g_recs.push_back({kind_, a_, b_});
   }
+  if (nv_) nvtxRangePop();
 }
 
 static void resolve() {

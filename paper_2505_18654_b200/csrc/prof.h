@@ -23,6 +23,7 @@ class ProfScope {
   int kind_;
   cudaStream_t st_;
   bool on_;
+  bool nv_ = false;  // an NVTX range was pushed (MTGR_NVTX=1)
   cudaEvent_t a_{}, b_{};
 };
 
