@@ -28,8 +28,9 @@
  *    faults surface as MTGR_E_CUDA at a later call.  mtgr_last_error()
  *    returns a thread-local message for the last failing call.
  *
- * Environment switches (read once per process; none changes results beyond
- * the floating-point summation order; defaults are the measured-fastest):
+ * Environment switches (read once per process; in the default build none
+ * changes results beyond the floating-point summation order; defaults are the
+ * measured-fastest):
  *  - MTGR_ATTN_BWD=kv|stored|fused_dk   bf16 attention backward: the coupled
  *    dK/dV kernel + dQ GEMM (default), the stored-score kernels, or the DK
  *    kernel that writes the scores.  MTGR_ATTN_RECOMPUTE=1 forces the
@@ -41,8 +42,9 @@
  *    thread poll period): coupled-kernel tuning knobs.
  *  - MTGR_NVTX=1   an NVTX range around every instrumented kernel launch.
  *  - MTGR_ATTN_TRACE=1, MTGR_KV_TRACE=1 (trace builds), MTGR_KV_DEBUG=bits
- *    (debug builds): clock-stamp / timing-experiment hooks; they synchronise
- *    the stream and are not for production use.
+ *    (debug builds only: the timing experiments drop work): clock-stamp /
+ *    timing-experiment hooks; they synchronise the stream and are not for
+ *    production use.
  */
 #ifndef MTGR_H_
 #define MTGR_H_
